@@ -1,0 +1,54 @@
+"""Seeded input recipes shared by oracle/make_golden.py and the tests.
+
+Only outputs are stored under tests/golden/; inputs are regenerated here from
+numpy seeds (PCG64 streams are platform-stable)."""
+
+import numpy as np
+
+PARAM_COUNTS = {"g": 2, "s": 1, "e": 1024, "r": 768, "c": 4, "n": 4, "d": 880}
+KERNEL_LEN = {"g": 3000, "s": 3000, "e": 3000, "r": 3000, "c": 3000, "n": 3000, "d": 7000}
+KERNEL_B = 2
+
+
+def kernel_inputs(tag):
+    """u (B,2,L), p (B,N_t) and an upstream weight w (B,2,L) for one kernel type."""
+    rng = np.random.default_rng(1000 + "gsecndr".index(tag))
+    L, B = KERNEL_LEN[tag], KERNEL_B
+    u = 0.3 * rng.standard_normal((B, 2, L))
+    p = 0.1 * rng.standard_normal((B, PARAM_COUNTS[tag]))
+    if tag == "r":
+        for lo in (192, 576):
+            p[:, lo:lo + 192] = -np.abs(p[:, lo:lo + 192]) - 0.01
+    if tag in "cn":
+        p[:, 0] = [2.5, 5.0][:B]      # alpha_raw: short and long ballistics
+        p[:, 1] = [-2.0, -1.0][:B]    # thresholds inside the signal's log-envelope range
+        p[:, 2] = [0.3, -0.5][:B]
+        p[:, 3] = [0.8, 1.5][:B]
+    if tag == "d":
+        # taps 0..2 land inside the 7000-sample window
+        for b in range(B):
+            for c in range(2):
+                base = c * 440
+                for m in range(3):
+                    ang = rng.uniform(0, 2 * np.pi)
+                    r = rng.uniform(0.5, 0.95)
+                    p[b, base + m] = r * np.cos(ang)
+                    p[b, base + 20 + m] = r * np.sin(ang)
+    w = rng.standard_normal((B, 2, L))
+    return u, p, w
+
+
+def mrstft_inputs(length=40_000):
+    rng = np.random.default_rng(4242)
+    t = np.arange(length) / 30000.0
+    sig = 0.3 * np.sin(2 * np.pi * 220 * t) + 0.1 * np.sin(2 * np.pi * 931 * t)
+    sig = sig * (0.5 + 0.5 * np.sin(2 * np.pi * 3 * t) ** 2)
+    tgt = np.stack([sig, 0.8 * sig]) + 0.02 * rng.standard_normal((2, length))
+    y_hat = np.stack([0.9 * sig, 0.7 * sig + 0.05 * np.roll(sig, 13)]) \
+        + 0.03 * rng.standard_normal((2, length))
+    return y_hat, tgt
+
+
+def step_spec():
+    """K, S, L, stems seed, param seed, target-param seed for the train_step golden."""
+    return 2, 1, 33_000, 3, 0, 1
