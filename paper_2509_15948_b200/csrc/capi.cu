@@ -1,0 +1,94 @@
+// extern "C" entry points of libmixgraph_b200 (see include/mixgraph_b200.h).
+#include <stdio.h>
+
+#include "common.cuh"
+#include "mgb_internal.h"
+#include "tables.cuh"
+
+__device__ float2 g_rev_spec[2][MGB_REV_FRAMES][MGB_REV_BINS];
+__device__ float g_rev_inv_wss[MGB_REV_LEN];
+
+extern "C" int mgb_init(const double* reverb_spec_host, const double* reverb_wss_host, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = mgb_init_device(st);
+  if (rc) return rc;
+  if ((rc = mgb_conv_init())) return rc;
+  if ((rc = mgb_loss_init())) return rc;
+  if (reverb_spec_host && reverb_wss_host) {
+    static float2 spec[2][MGB_REV_FRAMES][MGB_REV_BINS];
+    static float inv[MGB_REV_LEN];
+    for (int c = 0; c < 2; ++c)
+      for (int m = 0; m < MGB_REV_FRAMES; ++m)
+        for (int k = 0; k < MGB_REV_BINS; ++k) {
+          const double* z = reverb_spec_host + 2 * (((size_t)c * MGB_REV_FRAMES + m) * MGB_REV_BINS + k);
+          spec[c][m][k] = make_float2((float)z[0], (float)z[1]);
+        }
+    for (int t = 0; t < MGB_REV_LEN; ++t) inv[t] = (float)(1.0 / reverb_wss_host[t]);
+    if (cudaMemcpyToSymbolAsync(g_rev_spec, spec, sizeof(spec), 0, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return 2;
+    if (cudaMemcpyToSymbolAsync(g_rev_inv_wss, inv, sizeof(inv), 0, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return 2;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return 2;
+  }
+  return 0;
+}
+
+extern "C" size_t mgb_level_workspace(char tag, int B, int L) {
+  switch (tag) {
+    case 'g':
+    case 's': return mgb_simple_workspace(tag, B, L);
+    case 'e':
+    case 'r':
+    case 'd': return mgb_conv_workspace(tag, B, L);
+    case 'c':
+    case 'n': return mgb_dyn_workspace(tag, B, L);
+    default: return 0;
+  }
+}
+
+static int check_level(const MgbLevel* lv) {
+  if (!lv || lv->B <= 0 || lv->L <= 0 || !lv->u_rows || !lv->bank || !lv->prow || !lv->y) return 1;
+  if (lv->ws_bytes < mgb_level_workspace(lv->tag, lv->B, lv->L)) return 1;
+  return 0;
+}
+
+extern "C" int mgb_level_forward(const MgbLevel* lv, void* stream) {
+  if (int rc = check_level(lv)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (lv->tag) {
+    case 'g':
+    case 's': return mgb_simple_forward(lv, st);
+    case 'e':
+    case 'r':
+    case 'd': return mgb_conv_forward(lv, st);
+    case 'c':
+    case 'n': return mgb_dyn_forward(lv, st);
+    default: return 1;
+  }
+}
+
+extern "C" int mgb_level_backward(const MgbLevel* lv, void* stream) {
+  if (int rc = check_level(lv)) return rc;
+  if (!lv->gy_rows || !lv->gu || !lv->gbank) return 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (lv->tag) {
+    case 'g':
+    case 's': return mgb_simple_backward(lv, st);
+    case 'e':
+    case 'r':
+    case 'd': return mgb_conv_backward(lv, st);
+    case 'c':
+    case 'n': return mgb_dyn_backward(lv, st);
+    default: return 1;
+  }
+}
+
+extern "C" int mgb_fft(const void* in, void* out, void* tmp, int batch, int log2n, int inverse, float scale,
+                       void* stream) {
+  if (batch <= 0) return 0;
+  if (log2n > 13 && !tmp) return 1;
+  return mgb_fft_c2c((const float2*)in, (float2*)out, (float2*)tmp, batch, log2n, inverse, scale,
+                     (cudaStream_t)stream);
+}
+
+extern "C" int mgb_abi_version(void) { return MGB_ABI_VERSION; }

@@ -1,0 +1,116 @@
+// Optimiser step on device (mg/optimizer.py:82-137), float64 throughout:
+//   1. raw dry/wet gradient: g_raw = dL/dw * mask * s(1-s) + alpha_p * s(1-s)
+//      (effective_weights + sparsity_loss, mg/scheduler.py:218-222, mg/losses.py:181-183)
+//   2. delay rule on the d-bank z gradients: sgn(raw) + 0.01(|z|-1) conj(z)/|z|
+//   3. AdamW over the flat vector (banks + raw weights), fresh-state semantics
+//      are the caller's (moments zeroed at each train() call)
+//   4. unit-disk projection of every delay z
+// The AdamW arithmetic is written with explicit round-to-nearest ops so nvcc
+// does not contract it into FMAs: it reproduces numpy's operation order.
+#include "common.cuh"
+#include "mgb_internal.h"
+
+namespace {
+
+__global__ void k_raw_grad(const double* __restrict__ p, double* __restrict__ g, long long w_off, int P,
+                           const double* __restrict__ gw, const double* __restrict__ mask,
+                           const double* __restrict__ sc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const double s = expit64(p[w_off + i]);
+  const double ds = s * (1.0 - s);
+  double v = gw[i] * (mask ? mask[i] : 1.0) * ds;
+  const double ap = sc[7];
+  if (ap > 0.0) v += ap * ds;
+  g[w_off + i] = v;
+}
+
+__global__ void k_delay_rule(const double* __restrict__ p, double* __restrict__ g, long long d_off, int rows) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (row, channel, tap)
+  if (i >= rows * 40) return;
+  const int row = i / 40, c = (i / 20) % 2, m = i % 20;
+  const long long base = d_off + (long long)row * 880 + c * 440;
+  const double zr = p[base + m], zi = p[base + 20 + m];
+  const double gr = g[base + m], gi = g[base + 20 + m];
+  const double mag = hypot(gr, gi);
+  double sr = 0.0, si = 0.0;
+  if (mag > 0.0) { sr = gr / mag; si = gi / mag; }
+  const double zm = hypot(zr, zi);
+  double cr = 0.0, ci = 0.0;
+  if (zm > 0.0) { cr = zr / zm; ci = -zi / zm; }
+  const double k = 0.01 * (zm - 1.0);
+  g[base + m] = sr + k * cr;
+  g[base + 20 + m] = si + k * ci;
+}
+
+__global__ void k_adamw(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
+                        double* __restrict__ v, long long n, const double* __restrict__ sc,
+                        const double* __restrict__ guard) {
+  if (guard && !isfinite(*guard)) return;  // NonFiniteLoss: the reference raises before updating
+  const double lr = sc[0], b1 = sc[1], b2 = sc[2], eps = sc[3], wd = sc[4], c1 = sc[5], c2 = sc[6];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double gi = g[i];
+    double mi = m[i], vi = v[i], pi = p[i];
+    mi = __dadd_rn(mi, __dmul_rn(__dsub_rn(1.0, b1), __dsub_rn(gi, mi)));
+    vi = __dadd_rn(vi, __dmul_rn(__dsub_rn(1.0, b2), __dsub_rn(__dmul_rn(gi, gi), vi)));
+    const double mh = __ddiv_rn(mi, c1);
+    const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps);
+    const double upd = __dadd_rn(__ddiv_rn(mh, den), __dmul_rn(wd, pi));
+    pi = __dsub_rn(pi, __dmul_rn(lr, upd));
+    m[i] = mi;
+    v[i] = vi;
+    p[i] = pi;
+  }
+}
+
+__global__ void k_project(double* __restrict__ p, long long d_off, int rows, const double* __restrict__ guard) {
+  if (guard && !isfinite(*guard)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * 40) return;
+  const int row = i / 40, c = (i / 20) % 2, mm = i % 20;
+  const long long base = d_off + (long long)row * 880 + c * 440;
+  const double re = p[base + mm], im = p[base + 20 + mm];
+  const double mag = __dsqrt_rn(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
+  const double s = mag > 1.0 ? 1.0 / mag : 1.0;
+  p[base + mm] = re * s;
+  p[base + 20 + mm] = im * s;
+}
+
+__global__ void k_sparsity(const double* __restrict__ raw, int P, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) s += expit64(raw[i]);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+}  // namespace
+
+extern "C" int mgb_adamw_step(double* p, double* g, double* m, double* v, long long n, long long d_off, int d_rows,
+                              long long w_off, int P, const double* gw, const double* mask,
+                              const double* step_scalars, const double* loss_guard, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0) return 0;
+  if (P > 0) {
+    k_raw_grad<<<(P + 255) / 256, 256, 0, st>>>(p, g, w_off, P, gw, mask, step_scalars);
+    MGB_CHECK_LAUNCH();
+  }
+  if (d_rows > 0) {
+    k_delay_rule<<<(d_rows * 40 + 255) / 256, 256, 0, st>>>(p, g, d_off, d_rows);
+    MGB_CHECK_LAUNCH();
+  }
+  const int blocks = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
+  k_adamw<<<blocks, 256, 0, st>>>(p, g, m, v, n, step_scalars, loss_guard);
+  MGB_CHECK_LAUNCH();
+  if (d_rows > 0) {
+    k_project<<<(d_rows * 40 + 255) / 256, 256, 0, st>>>(p, d_off, d_rows, loss_guard);
+    MGB_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
+extern "C" int mgb_sparsity(const double* raw, int P, double* out, void* stream) {
+  k_sparsity<<<1, 256, 0, (cudaStream_t)stream>>>(raw, P, out);
+  MGB_CHECK_LAUNCH();
+  return 0;
+}

@@ -1,0 +1,575 @@
+"""Device engine: one compiled plan per graph version, launched through the C ABI.
+
+A ``RenderPlan`` turns a schedule's ``StepPlan`` list (mg/scheduler.py:157-204)
+into device row-pointer tables, so every level kernel reads its inputs straight
+out of the producer level's output buffer (no gather copies):
+
+* processor level  ->  ``mgb_level_forward/backward`` over all B rows at once;
+* mix/output level ->  ``mgb_bus_sum`` (atomic-free segmented sum).
+
+Backward gradient routing mirrors the tape's ``gather_rows``/``segment_sum``
+adjoints (mg/engine.py:439-467) without copies: a node with exactly one
+consumer simply points its dL/dy row at the consumer's dL/du row (processor
+consumer) or at the consumer's own dL/dy row (mix/output consumer, whose
+adjoint is a broadcast).  Only nodes with fan-out > 1 get a summing kernel.
+
+``TrainEngine`` is ``train_step`` (mg/optimizer.py:140-186) on device: render,
+target spectra, MRSTFT, full backward, delay rule, AdamW and projection, all
+on one stream and captured once into a CUDA graph per graph version.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import MgbLevel, MgbLoss, check, lib
+from .graph import PARAM_COUNTS, PROCESSOR_TYPES, MixGraph
+from .schedule import KERNEL_TYPES, LengthMismatch, Schedule, plan_indices, schedule_for
+from .tables import projection_sparse, reverb_tables
+
+F32, F64, I32 = torch.float32, torch.float64, torch.int32
+WARMUP_DEFAULT = 30_000
+
+_inited_devices = set()
+
+
+def ensure_device(device) -> torch.device:
+    """Load the library and upload per-device tables once."""
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise RuntimeError("the mixgraph B200 engine runs on CUDA devices only (no CPU fallback)")
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    dev = torch.device("cuda", idx)
+    if idx in _inited_devices:
+        return dev
+    L = lib()
+    specs, wss, _ = reverb_tables()
+    spec_arr = np.ascontiguousarray(np.stack([specs.real, specs.imag], axis=-1))
+    wss_arr = np.ascontiguousarray(wss)
+    with torch.cuda.device(idx):
+        check(L.mgb_init(spec_arr.ctypes.data, wss_arr.ctypes.data, stream_ptr()), "mgb_init")
+        torch.cuda.synchronize()
+    _inited_devices.add(idx)
+    return dev
+
+
+def stream_ptr():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t: torch.Tensor, elem_offset: int = 0) -> int:
+    return t.data_ptr() + elem_offset * t.element_size()
+
+
+def dev_ptr_array(ptrs, device) -> torch.Tensor:
+    return torch.tensor(np.asarray(ptrs, dtype=np.int64), dtype=torch.int64, device=device)
+
+
+# ---------------------------------------------------------------------------
+# parameters: one flat float64 vector  [e | c | n | s | g | d | r | raw_w]
+
+
+class ParamLayout:
+    def __init__(self, graph: MixGraph):
+        self.rows = {t: len(graph.nodes_of_type(t)) for t in PROCESSOR_TYPES}
+        self.off = {}
+        o = 0
+        for t in PROCESSOR_TYPES:
+            self.off[t] = o
+            o += self.rows[t] * PARAM_COUNTS[t]
+        self.w_off = o
+        self.P = len(graph.processor_nodes())
+        self.n = o + self.P
+
+    def pack(self, params) -> np.ndarray:
+        flat = np.empty(self.n, dtype=np.float64)
+        for t in PROCESSOR_TYPES:
+            a = np.asarray(params.params[t], dtype=np.float64).reshape(-1)
+            flat[self.off[t]:self.off[t] + a.size] = a
+        flat[self.w_off:] = np.asarray(params.raw_weights, dtype=np.float64)
+        return flat
+
+    def unpack_into(self, flat: np.ndarray, params) -> None:
+        for t in PROCESSOR_TYPES:
+            n = self.rows[t] * PARAM_COUNTS[t]
+            params.params[t] = flat[self.off[t]:self.off[t] + n].reshape(self.rows[t], PARAM_COUNTS[t]).copy()
+        params.raw_weights = flat[self.w_off:].copy()
+
+    def split(self, flat: np.ndarray) -> dict:
+        out = {t: flat[self.off[t]:self.off[t] + self.rows[t] * PARAM_COUNTS[t]]
+               .reshape(self.rows[t], PARAM_COUNTS[t]) for t in PROCESSOR_TYPES}
+        out["w"] = flat[self.w_off:]
+        return out
+
+
+# ---------------------------------------------------------------------------
+# render plan
+
+
+class _Level:
+    __slots__ = ("step", "tag", "B", "struct", "keep", "bus", "fanouts")
+
+
+class RenderPlan:
+    """Device plan of ``execute_batched`` for one (graph, schedule, L)."""
+
+    def __init__(self, graph: MixGraph, schedule: Schedule | None, L: int, device,
+                 params_flat: torch.Tensor, grads_flat: torch.Tensor | None, layout: ParamLayout,
+                 backward: bool = True):
+        self.device = ensure_device(device)
+        dev = self.device
+        if schedule is None:
+            schedule = schedule_for(graph)
+        elif schedule.plans is None:
+            schedule = plan_indices(graph, schedule)
+        self.schedule = schedule
+        self.graph = graph
+        self.L = L = int(L)
+        self.layout = layout
+        self.params = params_flat
+        self.grads = grads_flat
+        self.K = len(schedule.subsets[0])
+        self.P = layout.P
+        Ld = lib()
+        inputs = graph.nodes_of_type("i")
+        in_row = {v: i for i, v in enumerate(inputs)}
+        self.input_rows = [in_row[v] for v in schedule.subsets[0]]
+        self.stems = torch.zeros((len(inputs), 2, L), dtype=F32, device=dev)
+        self.w = torch.zeros(max(self.P, 1), dtype=F64, device=dev)
+        self.mask = torch.ones(max(self.P, 1), dtype=F64, device=dev)
+        self.gw = torch.zeros(max(self.P, 1), dtype=F64, device=dev)
+        self.greg = torch.zeros((), dtype=F64, device=dev)
+        nsteps = len(schedule.subsets)
+        self.outs = [None] * nsteps
+        self.gus = [None] * nsteps
+        n_reg = sum(len(schedule.subsets[s]) for s in range(1, nsteps)
+                    if schedule.type_sequence[s] in "erd")
+        self.reg = torch.zeros(max(n_reg, 1), dtype=F64, device=dev)
+        self._keep = []  # device tensors referenced by raw pointers
+
+        def row_ptr(step, row):
+            if step == 0:
+                return ptr(self.stems, self.input_rows[row] * 2 * L)
+            return ptr(self.outs[step], row * 2 * L)
+
+        # ---- forward structures
+        self.levels = []
+        reg_off = 0
+        for s in range(1, nsteps):
+            plan = schedule.plans[s]
+            tag = schedule.type_sequence[s]
+            B = plan.batch
+            self.outs[s] = torch.empty((B, 2, L), dtype=F32, device=dev)
+            lv = _Level()
+            lv.step, lv.tag, lv.B, lv.fanouts = s, tag, B, []
+            lv.keep = []
+            srcs = [row_ptr(*g) for g in plan.gather]
+            if tag in KERNEL_TYPES:
+                u_rows = dev_ptr_array(srcs, dev)
+                prow = torch.tensor(np.asarray(schedule.type_perm[tag])[plan.pslice], dtype=I32, device=dev)
+                widx = torch.tensor(np.asarray(plan.weight_idx), dtype=I32, device=dev)
+                ws_bytes = int(Ld.mgb_level_workspace(tag.encode(), B, L))
+                ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
+                ybar = torch.empty((B, 2, L), dtype=F32, device=dev) if tag in "erd" else None
+                aux = torch.empty((B, L), dtype=F32, device=dev) if tag in "cn" else None
+                gu = torch.empty((B, 2, L), dtype=F32, device=dev) if backward else None
+                self.gus[s] = gu
+                st = MgbLevel()
+                st.tag = tag.encode()
+                st.B, st.L = B, L
+                st.u_rows = ptr(u_rows)
+                st.bank = ptr(self.params, layout.off[tag])
+                st.prow, st.widx = ptr(prow), ptr(widx)
+                st.w = ptr(self.w)
+                st.greg = ptr(self.greg)
+                st.y = ptr(self.outs[s])
+                st.ybar = ptr(ybar) if ybar is not None else None
+                st.aux = ptr(aux) if aux is not None else None
+                if tag in "erd":
+                    st.reg = ptr(self.reg, reg_off)
+                    reg_off += B
+                st.gu = ptr(gu) if gu is not None else None
+                st.gbank = ptr(self.grads, layout.off[tag]) if self.grads is not None else None
+                st.gw = ptr(self.gw)
+                st.ws, st.ws_bytes = ptr(ws), ws_bytes
+                lv.struct = st
+                lv.keep = [u_rows, prow, widx, ws, ybar, aux, gu]
+                lv.bus = None
+            else:
+                seg = plan.segments if plan.segments is not None else np.arange(B)
+                counts = np.bincount(np.asarray(seg), minlength=B)
+                seg_off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+                in_rows = dev_ptr_array(srcs, dev)
+                seg_t = torch.tensor(seg_off, dtype=I32, device=dev)
+                lv.bus = (in_rows, seg_t, B)
+                lv.struct = None
+                lv.keep = [in_rows, seg_t]
+            self.levels.append(lv)
+        self.y = self.outs[nsteps - 1][0]  # (2, L) output node
+
+        # ---- backward gradient routing
+        self.dY = torch.zeros((2, L), dtype=F32, device=dev) if backward else None
+        if backward:
+            consumers = {}
+            for s in range(1, nsteps):
+                plan = schedule.plans[s]
+                seg = plan.segments if plan.segments is not None else np.arange(len(plan.gather))
+                for i, g in enumerate(plan.gather):
+                    consumers.setdefault(tuple(g), []).append((s, int(seg[i])))
+            gptr = {(nsteps - 1, 0): ptr(self.dY)}
+            fan_bufs = {}
+            for s in range(nsteps - 2, 0, -1):
+                tag = schedule.type_sequence[s]
+                lv = self.levels[s - 1]
+                rows = []
+                for r in range(len(schedule.subsets[s])):
+                    contrib = []
+                    for (cs, cr) in consumers.get((s, r), []):
+                        if schedule.type_sequence[cs] in KERNEL_TYPES:
+                            contrib.append(ptr(self.gus[cs], cr * 2 * L))
+                        else:
+                            contrib.append(gptr[(cs, cr)])
+                    if len(contrib) == 1:
+                        gptr[(s, r)] = contrib[0]
+                    else:
+                        buf = torch.empty((2, L), dtype=F32, device=dev)
+                        fan_bufs[(s, r)] = buf
+                        src = dev_ptr_array(contrib, dev)
+                        off = torch.tensor([0, len(contrib)], dtype=I32, device=dev)
+                        lv.fanouts.append((src, off, buf))
+                        gptr[(s, r)] = ptr(buf)
+                    rows.append(gptr[(s, r)])
+                if tag in KERNEL_TYPES:
+                    gy = dev_ptr_array(rows, dev)
+                    lv.struct.gy_rows = ptr(gy)
+                    lv.keep.append(gy)
+            self._fan_bufs = fan_bufs
+
+    # -- launches ---------------------------------------------------------
+    def set_stems(self, stems):
+        """Copy (K, 2, L) stems (numpy / torch, any device) into the static input buffer."""
+        t = stems if torch.is_tensor(stems) else torch.from_numpy(np.ascontiguousarray(stems))
+        if t.shape[-1] != self.L:
+            raise LengthMismatch(f"plan is built for L={self.L}, got {t.shape[-1]}")
+        self.stems.copy_(t.to(dtype=F32), non_blocking=True)
+
+    def forward(self, use_mask: bool):
+        L = lib()
+        sp = stream_ptr()
+        if self.P:
+            check(L.mgb_weights(ptr(self.params, self.layout.w_off), ptr(self.mask) if use_mask else None,
+                                ptr(self.w), self.P, sp), "mgb_weights")
+        for lv in self.levels:
+            if lv.struct is not None:
+                check(L.mgb_level_forward(ctypes.byref(lv.struct), sp), f"level {lv.tag} forward")
+            else:
+                in_rows, seg, B = lv.bus
+                check(L.mgb_bus_sum(ptr(in_rows), ptr(seg), ptr(self.outs[lv.step]), B, self.L, sp),
+                      "mgb_bus_sum")
+
+    def reg_total(self) -> torch.Tensor:
+        return self.reg.sum()
+
+    def backward(self):
+        L = lib()
+        sp = stream_ptr()
+        for lv in reversed(self.levels):
+            for src, off, buf in lv.fanouts:
+                check(L.mgb_bus_sum(ptr(src), ptr(off), ptr(buf), 1, self.L, sp), "fan-out sum")
+            if lv.struct is not None:
+                check(L.mgb_level_backward(ctypes.byref(lv.struct), sp), f"level {lv.tag} backward")
+
+    def launches_forward(self) -> int:
+        return (1 if self.P else 0) + sum(_LAUNCHES_FWD.get(lv.tag, 1) for lv in self.levels)
+
+    def launches_backward(self) -> int:
+        return sum(_LAUNCHES_BWD.get(lv.tag, 0) + len(lv.fanouts) for lv in self.levels)
+
+
+# kernels each C-ABI level call launches (fft: 2 passes per transform when N > 8192)
+_LAUNCHES_FWD = {"g": 1, "s": 1, "c": 2, "n": 2, "e": 11, "r": 12, "d": 12, "m": 1, "o": 1}
+_LAUNCHES_BWD = {"g": 2, "s": 2, "c": 4, "n": 4, "e": 9, "r": 10, "d": 9}
+
+
+# ---------------------------------------------------------------------------
+# loss plan
+
+
+class LossPlan:
+    """Device MRSTFT (mg/losses.py:104-170) for a fixed scored length Ls."""
+
+    def __init__(self, cfg, Ls: int, device):
+        self.device = ensure_device(device)
+        dev = self.device
+        self.cfg = cfg
+        self.Ls = Ls = int(Ls)
+        sizes = tuple(cfg.fft_sizes)
+        if len(sizes) > 8:
+            raise ValueError("at most 8 resolutions")
+        for n in sizes:
+            if n & (n - 1) or not 256 <= n <= 8192:
+                raise NotImplementedError(f"fft size {n}: power of two in [256, 8192] required")
+            if n // 2 >= Ls:
+                raise NotImplementedError(f"scored length {Ls} too short for fft size {n}")
+        if cfg.mel_bins > 128:
+            raise NotImplementedError("mel_bins <= 128")
+        st = MgbLoss()
+        st.n_res = len(sizes)
+        st.Ls = Ls
+        gw = [cfg.weight_lr / 2, cfg.weight_lr / 2, cfg.weight_mid, cfg.weight_side]
+        for i, v in enumerate(gw):
+            st.group_w[i] = v
+        self._keep = []
+        self.stats = torch.zeros(len(sizes) * 16, dtype=F64, device=dev)
+        self.loss = torch.zeros((), dtype=F64, device=dev)
+        st.stats, st.loss = ptr(self.stats), ptr(self.loss)
+        for i, n in enumerate(sizes):
+            hop = n // 4
+            frames = 1 + Ls // hop
+            tabs = projection_sparse(n, cfg.sample_rate, cfg.mel_bins, float(cfg.mel_fmax),
+                                     bool(cfg.a_weighting))
+            dt = [torch.from_numpy(a).to(dev) for a in tabs]
+            nm = cfg.mel_bins
+            tmel = torch.zeros((4, frames, nm), dtype=F64, device=dev)
+            tlog = torch.zeros_like(tmel)
+            mel = torch.zeros_like(tmel)
+            part = torch.zeros((frames, 4, 3), dtype=F64, device=dev)
+            gfr = torch.zeros((frames, 2, n), dtype=F32, device=dev)
+            r = st.res[i]
+            r.n_fft, r.hop, r.frames, r.n_mels = n, hop, frames, nm
+            (r.band_start, r.band_len, r.band_off, r.band_w,
+             r.bin_start, r.bin_len, r.bin_band, r.bin_w) = [ptr(t) for t in dt]
+            r.tmel, r.tlog, r.mel, r.part, r.gframes = ptr(tmel), ptr(tlog), ptr(mel), ptr(part), ptr(gfr)
+            self._keep += dt + [tmel, tlog, mel, part, gfr]
+        self.struct = st
+
+    def target(self, tl_ptr, tr_ptr):
+        check(lib().mgb_mrstft_target(ctypes.byref(self.struct), tl_ptr, tr_ptr, stream_ptr()), "mrstft target")
+
+    def forward(self, yl_ptr, yr_ptr):
+        check(lib().mgb_mrstft_forward(ctypes.byref(self.struct), yl_ptr, yr_ptr, stream_ptr()),
+              "mrstft forward")
+
+    def backward(self, yl_ptr, yr_ptr, gl_ptr, gr_ptr):
+        check(lib().mgb_mrstft_backward(ctypes.byref(self.struct), yl_ptr, yr_ptr, gl_ptr, gr_ptr,
+                                        stream_ptr()), "mrstft backward")
+
+    def launches(self, which: str) -> int:
+        n = self.struct.n_res
+        return n + 1
+
+
+# ---------------------------------------------------------------------------
+# train-step engine
+
+
+class TrainEngine:
+    """train_step (mg/optimizer.py:140-186) as one device program per graph version."""
+
+    def __init__(self, graph: MixGraph, L: int, cfg, device="cuda", schedule=None, warmup_len=None,
+                 use_graph=True):
+        self.device = ensure_device(device)
+        dev = self.device
+        self.graph = graph
+        self.cfg = cfg
+        self.L = int(L)
+        self.ws = int(cfg.warmup_len if warmup_len is None else warmup_len)
+        if self.ws >= self.L:
+            raise ValueError("segment must be longer than the warm-up exclusion")
+        self.layout = lay = ParamLayout(graph)
+        self.params = torch.zeros(lay.n, dtype=F64, device=dev)
+        self.grads = torch.zeros(lay.n, dtype=F64, device=dev)
+        self.m = torch.zeros(lay.n, dtype=F64, device=dev)
+        self.v = torch.zeros(lay.n, dtype=F64, device=dev)
+        self.plan = RenderPlan(graph, schedule, self.L, dev, self.params, self.grads, lay, backward=True)
+        self.lossp = LossPlan(cfg.loss, self.L - self.ws, dev)
+        self.target = torch.zeros((2, self.L), dtype=F32, device=dev)
+        self.scalars = torch.zeros(8, dtype=F64, device=dev)
+        self.scalars_host = torch.zeros(8, dtype=F64).pin_memory()
+        self.vals = torch.zeros(4, dtype=F64, device=dev)        # loss, L_a, L_g, L_p
+        self.vals_host = torch.zeros(4, dtype=F64).pin_memory()
+        self.sparsity = torch.zeros((), dtype=F64, device=dev)
+        self.plan.greg.fill_(float(cfg.loss.gain_staging_weight))
+        self.t = 0
+        self.use_graph = use_graph
+        self._graph = None
+        self.d_rows = lay.rows["d"]
+
+    # -- state ------------------------------------------------------------
+    def load_params(self, params):
+        self.params.copy_(torch.from_numpy(self.layout.pack(params)))
+
+    def store_params(self, params):
+        self.layout.unpack_into(self.params.cpu().numpy(), params)
+
+    def reset_optimizer(self):
+        self.m.zero_()
+        self.v.zero_()
+        self.t = 0
+
+    # -- the device program --------------------------------------------------
+    def _body(self):
+        L, ws, P = self.L, self.ws, self.layout.P
+        plan, lp = self.plan, self.lossp
+        Ld = lib()
+        plan.forward(use_mask=False)
+        y = plan.y
+        lp.target(ptr(self.target, ws), ptr(self.target, L + ws))
+        lp.forward(ptr(y, ws), ptr(y, L + ws))
+        reg = plan.reg_total()
+        if P:
+            check(Ld.mgb_sparsity(ptr(self.params, self.layout.w_off), P, ptr(self.sparsity), stream_ptr()),
+                  "mgb_sparsity")
+        ap = self.scalars[7]
+        total = lp.loss + reg * float(self.cfg.loss.gain_staging_weight) + \
+            torch.where(ap > 0, ap * self.sparsity, torch.zeros_like(ap))
+        torch.stack([total, lp.loss, reg, self.sparsity], out=self.vals)
+        plan.dY[:, :ws].zero_()
+        lp.backward(ptr(y, ws), ptr(y, L + ws), ptr(plan.dY, ws), ptr(plan.dY, L + ws))
+        plan.backward()
+        lay = self.layout
+        check(Ld.mgb_adamw_step(ptr(self.params), ptr(self.grads), ptr(self.m), ptr(self.v), lay.n,
+                                lay.off["d"], self.d_rows, lay.w_off, P, ptr(plan.gw), None,
+                                ptr(self.scalars), ptr(self.vals), stream_ptr()), "mgb_adamw_step")
+
+    def grads_only(self, alpha_p=0.0):
+        """Eager forward + backward without the optimiser (test hook).
+
+        Returns (values, bank grads split by type (raw, before the delay rule), dL/dw)."""
+        self.scalars.copy_(torch.tensor([0, 0, 0, 0, 0, 1, 1, float(alpha_p)], dtype=F64))
+        L, ws, P = self.L, self.ws, self.layout.P
+        plan, lp = self.plan, self.lossp
+        self.grads.zero_()
+        plan.forward(use_mask=False)
+        y = plan.y
+        lp.target(ptr(self.target, ws), ptr(self.target, L + ws))
+        lp.forward(ptr(y, ws), ptr(y, L + ws))
+        reg = plan.reg_total()
+        plan.dY[:, :ws].zero_()
+        lp.backward(ptr(y, ws), ptr(y, L + ws), ptr(plan.dY, ws), ptr(plan.dY, L + ws))
+        plan.backward()
+        torch.cuda.synchronize(self.device)
+        values = {"L_a": float(lp.loss), "L_g": float(reg)}
+        g = self.layout.split(self.grads.cpu().numpy())
+        return values, g, plan.gw[:P].cpu().numpy().copy(), y.detach().cpu().numpy().copy()
+
+    def launches_per_step(self) -> int:
+        n = self.plan.launches_forward() + self.plan.launches_backward()
+        n += 2 * self.lossp.launches("fwd") + self.lossp.launches("bwd") + 1  # target, fwd, bwd(+ola)
+        n += 1  # sparsity
+        n += 2 + (2 if self.d_rows else 0)  # raw-grad, adamw, delay rule, projection
+        return n
+
+    def _set_scalars(self, alpha_p):
+        c = self.cfg
+        self.t += 1
+        b1, b2 = c.betas
+        self.scalars_host.copy_(torch.tensor([c.lr, b1, b2, c.eps, c.weight_decay, 1.0 - b1 ** self.t,
+                                              1.0 - b2 ** self.t, float(alpha_p)], dtype=F64))
+        self.scalars.copy_(self.scalars_host, non_blocking=True)
+
+    def step_async(self, alpha_p=0.0):
+        """Enqueue one full train step (inputs already in plan.stems / self.target)."""
+        self._set_scalars(alpha_p)
+        if not self.use_graph:
+            self._body()
+            return
+        if self._graph is None:
+            # warm-up run outside capture (sets function attributes, JIT, allocations)
+            s = torch.cuda.Stream(device=self.device)
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                snap = [self.params.clone(), self.m.clone(), self.v.clone()]
+                self._body()
+                self.params.copy_(snap[0])
+                self.m.copy_(snap[1])
+                self.v.copy_(snap[2])
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._body()
+            self._graph = g
+            torch.cuda.synchronize(self.device)
+        self._graph.replay()
+
+    def read_values(self):
+        self.vals_host.copy_(self.vals, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        v = self.vals_host.tolist()
+        return {"loss": v[0], "L_a": v[1], "L_g": v[2], "L_p": v[3]}
+
+
+class EvalEngine:
+    """Forward-only masked render + MRSTFT over a fixed eval set (mg/pruning.py:99-123)."""
+
+    def __init__(self, graph: MixGraph, segments, warmup_len, loss_cfg, device="cuda", params=None,
+                 use_graph=True):
+        self.device = ensure_device(device)
+        dev = self.device
+        self.graph = graph
+        self.layout = lay = ParamLayout(graph)
+        self.params = torch.zeros(lay.n, dtype=F64, device=dev)
+        if params is not None:
+            self.params.copy_(torch.from_numpy(lay.pack(params)))
+        L = segments[0][0].shape[-1]
+        self.L, self.ws = L, int(warmup_len)
+        self.plan = RenderPlan(graph, None, L, dev, self.params, None, lay, backward=False)
+        self.seg_stems = []
+        self.losses = []
+        for stems, target in segments:
+            self.seg_stems.append(torch.as_tensor(np.asarray(stems), dtype=F32).to(dev))
+            lp = LossPlan(loss_cfg, L - self.ws, dev)
+            t = torch.as_tensor(np.asarray(target), dtype=F32).to(dev).contiguous()
+            lp.target(ptr(t, 0), ptr(t, t.shape[-1]))
+            self.losses.append((lp, t))
+        self.acc = torch.zeros(len(segments), dtype=F64, device=dev)
+        self.mask_host = torch.ones(max(lay.P, 1), dtype=F64).pin_memory()
+        self.acc_host = torch.zeros(len(segments), dtype=F64).pin_memory()
+        self.use_graph = use_graph
+        self._graph = None
+
+    def load_params(self, params):
+        self.params.copy_(torch.from_numpy(self.layout.pack(params)))
+
+    def _body(self):
+        L, ws = self.L, self.ws
+        for i, stems in enumerate(self.seg_stems):
+            self.plan.stems.copy_(stems)
+            self.plan.forward(use_mask=True)
+            lp, _ = self.losses[i]
+            lp.forward(ptr(self.plan.y, ws), ptr(self.plan.y, L + ws))
+            self.acc[i].copy_(lp.loss)
+
+    def run_async(self, mask):
+        self.mask_host[: len(mask)].copy_(torch.as_tensor(np.asarray(mask, dtype=np.float64)))
+        self.plan.mask.copy_(self.mask_host, non_blocking=True)
+        if not self.use_graph:
+            self._body()
+            return
+        if self._graph is None:
+            s = torch.cuda.Stream(device=self.device)
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self._body()
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._body()
+            self._graph = g
+        self._graph.replay()
+
+    def loss(self, mask) -> float:
+        self.run_async(mask)
+        self.acc_host.copy_(self.acc, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        # per-segment float() then mean, as mg/pruning.py:120-123
+        total = 0.0
+        for v in self.acc_host.tolist():
+            total += float(v)
+        return total / len(self.seg_stems)

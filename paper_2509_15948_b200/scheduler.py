@@ -1,0 +1,66 @@
+"""``execute_batched`` on the device (mg/scheduler.py:225-263).
+
+Planning (schedules, index plans) is host Python in ``schedule.py``; the
+render itself runs as one ``RenderPlan`` of level kernels.  Returns device
+tensors: ``y`` (2, L) float32 and the gain-staging sum ``reg`` (float64).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .engine import F32, F64, ParamLayout, RenderPlan, ensure_device
+from .schedule import (CONSOLE_SEQUENCE, GREEDY_TIE_ORDER, LengthMismatch, NotAConsole, Schedule,  # noqa: F401
+                       SchedulerError, StepPlan, console_chains, plan_indices, schedule_console,
+                       schedule_for, schedule_greedy)
+
+
+def _check_sources(graph, sources):
+    if torch.is_tensor(sources):
+        src = sources
+    elif isinstance(sources, (list, tuple)):
+        lengths = {np.asarray(s).shape[-1] if not torch.is_tensor(s) else s.shape[-1] for s in sources}
+        if len(lengths) > 1:
+            raise LengthMismatch(f"sources have mixed lengths {sorted(lengths)}")
+        src = torch.stack([torch.as_tensor(np.asarray(s)) if not torch.is_tensor(s) else s for s in sources])
+    else:
+        src = torch.as_tensor(np.asarray(sources))
+    k = len(graph.nodes_of_type("i"))
+    if src.shape[0] != k:
+        raise LengthMismatch(f"graph has {k} inputs, got {src.shape[0]} sources")
+    return src
+
+
+def execute_batched(graph, params, sources, schedule=None, mask=None, device="cuda"):
+    """Render the graph through its schedule; returns (y (2, L), reg) on the device."""
+    dev = ensure_device(device)
+    src = _check_sources(graph, sources)
+    L = src.shape[-1]
+    if schedule is None:
+        schedule = schedule_greedy(graph)
+    if schedule.plans is None:
+        schedule = plan_indices(graph, schedule)
+    lay = ParamLayout(graph)
+    flat = torch.from_numpy(lay.pack(params)).to(dev)
+    plan = RenderPlan(graph, schedule, L, dev, flat, None, lay, backward=False)
+    plan.set_stems(src)
+    if mask is not None:
+        plan.mask[: lay.P].copy_(torch.as_tensor(np.asarray(mask, dtype=np.float64)))
+    plan.forward(use_mask=mask is not None)
+    return plan.y.clone(), plan.reg_total()
+
+
+def execute_reference(graph, params, sources, device="cuda"):
+    """Same contract; in this implementation the batched device path IS the executor."""
+    return execute_batched(graph, params, sources, schedule_greedy(graph), device=device)
+
+
+def effective_weights(params, mask=None):
+    w = params.effective_weights()
+    return w * np.asarray(mask, dtype=np.float64) if mask is not None else w
+
+
+__all__ = ["execute_batched", "execute_reference", "effective_weights", "Schedule", "StepPlan",
+           "schedule_greedy", "schedule_console", "plan_indices", "console_chains", "NotAConsole",
+           "LengthMismatch", "SchedulerError", "F32", "F64"]

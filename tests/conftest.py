@@ -21,8 +21,13 @@ def golden(name):
 def normrel(a, b, floor=1e-12):
     """Norm-relative error of a against reference b, ignoring entries of b below
     floor * max|b| (FFT-noise-level oracle entries are excluded)."""
-    a = np.asarray(a, dtype=np.float64)
-    b = np.asarray(b, dtype=np.float64)
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if np.iscomplexobj(a) or np.iscomplexobj(b):
+        a = np.stack([np.real(a), np.imag(a)], -1).astype(np.float64)
+        b = np.stack([np.real(b), np.imag(b)], -1).astype(np.float64)
+    a = a.astype(np.float64)
+    b = b.astype(np.float64)
     scale = np.max(np.abs(b)) if b.size else 0.0
     if scale == 0.0:
         return float(np.max(np.abs(a))) if a.size else 0.0

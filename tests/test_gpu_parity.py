@@ -1,0 +1,228 @@
+"""Device parity: the CUDA path through the C ABI vs the reference's golden
+fixtures and the float64 oracle.  Tolerances (north_star): rendered mix and
+gradients 1e-4 norm-relative (fp32), loss 1e-5 relative."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden, normrel
+from golden_inputs import kernel_inputs, mrstft_inputs, step_spec
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2509_15948_b200.engine import ensure_device
+    return ensure_device("cuda")
+
+
+@pytest.mark.parametrize("log2n", [5, 8, 10, 11, 13, 14, 16, 18, 19, 21])
+def test_fft_matches_numpy(dev, log2n):
+    from paper_2509_15948_b200 import _lib
+    from paper_2509_15948_b200.engine import ptr, stream_ptr
+    n, B = 1 << log2n, 3
+    rng = np.random.default_rng(log2n)
+    x = (rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))).astype(np.complex64)
+    xt = torch.from_numpy(x).to(dev)
+    out = torch.empty_like(xt)
+    tmp = torch.empty_like(xt)
+    L = _lib.lib()
+    _lib.check(L.mgb_fft(ptr(xt), ptr(out), ptr(tmp), B, log2n, 0, 1.0, stream_ptr()), "fft")
+    ref = np.fft.fft(x.astype(np.complex128), axis=-1)
+    assert normrel(out.cpu().numpy(), ref) < 3e-6
+    _lib.check(L.mgb_fft(ptr(out), ptr(out), ptr(tmp), B, log2n, 1, 1.0 / n, stream_ptr()), "ifft")
+    assert normrel(out.cpu().numpy(), x) < 3e-6
+
+
+@pytest.mark.parametrize("tag", list("gsecndr"))
+def test_kernel_matches_reference_golden(dev, tag):
+    from paper_2509_15948_b200.processors import KERNELS
+    gk = golden("kernels.npz")
+    u, p, w = kernel_inputs(tag)
+    ut = torch.tensor(u, dtype=torch.float32, device=dev, requires_grad=True)
+    pt = torch.tensor(p, dtype=torch.float64, device=dev, requires_grad=True)
+    ybar, reg = KERNELS[tag](ut, pt)
+    loss = torch.sum(ybar.double() * torch.tensor(w, device=dev))
+    if reg is not None:
+        loss = loss + reg
+    loss.backward()
+    assert normrel(ybar.detach().cpu().numpy(), gk[f"{tag}_ybar"]) < 2e-6
+    if tag in "erd":
+        np.testing.assert_allclose(float(reg), float(gk[f"{tag}_reg"]), rtol=1e-5, atol=1e-7)
+    assert normrel(ut.grad.cpu().numpy(), gk[f"{tag}_gu"]) < 1e-4
+    # gradient banks: norm-relative, excluding FFT-noise-level reference entries
+    assert normrel(pt.grad.cpu().numpy(), gk[f"{tag}_gp"], floor=1e-6) < 1e-4
+
+
+@pytest.mark.parametrize("name,sizes", [("std", (512, 1024, 4096)),
+                                        ("six", (256, 512, 1024, 2048, 4096, 8192))])
+def test_mrstft_matches_reference_golden(dev, name, sizes):
+    from paper_2509_15948_b200.losses import LossConfig, mrstft
+    gm = golden("mrstft.npz")
+    y_hat, tgt = mrstft_inputs()
+    yt = torch.tensor(y_hat, dtype=torch.float32, device=dev, requires_grad=True)
+    val = mrstft(yt, tgt.astype(np.float32), LossConfig(fft_sizes=sizes))
+    val.backward()
+    # inputs are rounded to fp32 on the device: compare against the oracle on the same fp32 inputs
+    from oracle import mixgraph_oracle as O
+    yo = torch.tensor(y_hat.astype(np.float32).astype(np.float64), requires_grad=True)
+    ov = O.mrstft(yo, tgt.astype(np.float32).astype(np.float64), O.LossConfig(fft_sizes=sizes))
+    ov.backward()
+    np.testing.assert_allclose(float(val), float(ov), rtol=1e-5)
+    np.testing.assert_allclose(float(val), float(gm[f"{name}_loss"]), rtol=1e-3)
+    assert normrel(yt.grad.cpu().numpy(), yo.grad.numpy()) < 1e-4
+
+
+def _step_setup():
+    from paper_2509_15948_b200.console import build_console, init_params
+    from paper_2509_15948_b200.synth import SynthSpec, make_stems_f32, manifest_for
+    K, S, L, s_stems, s_p, s_t = step_spec()
+    spec = SynthSpec(tracks=K, subgroups=S, duration_seconds=L / 30000)
+    stems = make_stems_f32(spec, s_stems, L)
+    graph, zeros = build_console(manifest_for(spec))
+    return graph, init_params(zeros, s_p), stems, L
+
+
+def test_train_step_gradients_match_reference(dev):
+    from paper_2509_15948_b200.engine import TrainEngine
+    from paper_2509_15948_b200.optimizer import TrainConfig, _EngineCfg, make_optimizer
+    gs = golden("step.npz")
+    graph, params, stems, L = _step_setup()
+    cfg = TrainConfig(segment_seconds=L / 30000, steps=1)
+    eng = TrainEngine(graph, L, _EngineCfg(make_optimizer(params, cfg), cfg), device=dev, use_graph=False)
+    eng.load_params(params)
+    eng.plan.set_stems(stems)
+    eng.target.copy_(torch.as_tensor(gs["target"], dtype=torch.float32))
+    vals, grads, gw, y = eng.grads_only()
+    assert normrel(y, gs["y"]) < 1e-5
+    np.testing.assert_allclose(vals["L_a"], float(gs["v_L_a"]), rtol=1e-5)
+    np.testing.assert_allclose(vals["L_g"], float(gs["v_L_g"]), rtol=1e-5)
+    for t in "gsecnr":
+        assert normrel(grads[t], gs[f"grad_{t}"], floor=1e-6) < 1e-4, t
+    s = 1.0 / (1.0 + np.exp(-params.raw_weights))
+    assert normrel(gw * s * (1 - s), gs["grad_w"], floor=1e-6) < 1e-4
+    assert normrel(grads["d"], gs["d_raw"], floor=1e-4) < 1e-3
+
+
+def test_public_train_step_two_steps(dev):
+    from paper_2509_15948_b200.optimizer import TrainConfig, make_optimizer, train_step
+    gs = golden("step.npz")
+    graph, params, stems, L = _step_setup()
+    cfg = TrainConfig(segment_seconds=L / 30000, steps=1)
+    opt = make_optimizer(params, cfg)
+    v1 = train_step(graph, params, (stems, gs["target"]), cfg, opt)
+    v2 = train_step(graph, params, (stems, gs["target"]), cfg, opt)
+    np.testing.assert_allclose(v1["L_a"], float(gs["v_L_a"]), rtol=1e-5)
+    np.testing.assert_allclose(v2["L_a"], float(gs["v2_L_a"]), rtol=1e-3)
+    for t in "gsecnr":
+        np.testing.assert_allclose(params.params[t], gs[f"after2_{t}"], atol=5e-3)
+
+
+def _random_console(rng, kmax=4, prune=0.0):
+    from paper_2509_15948_b200.console import SessionManifest, TrackEntry, build_console
+    from paper_2509_15948_b200.graph import PARAM_COUNTS, ParamStore, bypass_remove
+    k = int(rng.integers(1, kmax + 1))
+    s = int(rng.integers(1, min(3, k) + 1))
+    tracks = [TrackEntry(f"t{i}", f"t{i}", f"bus{i % s}") for i in range(k)]
+    g, _ = build_console(SessionManifest(tracks, "m"))
+    P = {t: 0.1 * rng.standard_normal((len(g.nodes_of_type(t)), PARAM_COUNTS[t])) for t in PARAM_COUNTS}
+    for lo in (192, 576):
+        P["r"][:, lo:lo + 192] = -np.abs(P["r"][:, lo:lo + 192]) - 0.01
+    params = ParamStore(P, 0.1 * rng.standard_normal(len(g.processor_nodes())))
+    if prune > 0:
+        procs = g.processor_nodes()
+        drop = rng.choice(procs, size=int(round(prune * len(procs))), replace=False)
+        g, params = bypass_remove(g, params, set(int(v) for v in drop))
+    return g, params
+
+
+def _oracle_render(graph, params, src, mask=None):
+    from oracle import mixgraph_oracle as O
+    with torch.no_grad():
+        y, reg = O.execute(graph, {t: torch.tensor(v) for t, v in params.params.items()},
+                           torch.tensor(params.raw_weights), src.astype(np.float64), mask)
+    return y.numpy(), float(reg)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_execute_batched_matches_oracle_on_random_consoles(dev, seed):
+    from paper_2509_15948_b200.schedule import schedule_console
+    from paper_2509_15948_b200.scheduler import execute_batched
+    rng = np.random.default_rng(seed + 100)
+    graph, params = _random_console(rng, kmax=5, prune=rng.uniform(0, 0.8))
+    src = (0.3 * rng.standard_normal((len(graph.nodes_of_type("i")), 2, 5000))).astype(np.float32)
+    y, reg = execute_batched(graph, params, src, schedule_console(graph))
+    yo, rego = _oracle_render(graph, params, src)
+    assert normrel(y.cpu().numpy(), yo) < 1e-5
+    np.testing.assert_allclose(float(reg), rego, rtol=1e-5, atol=1e-9)
+
+
+def test_execute_batched_matches_oracle_on_random_dags(dev):
+    from paper_2509_15948_b200.graph import PARAM_COUNTS, PROCESSOR_TYPES, MixGraph, ParamStore
+    from paper_2509_15948_b200.scheduler import execute_batched
+    for seed in range(4):
+        rng = np.random.default_rng(seed + 500)
+        k = int(rng.integers(1, 5))
+        types, edges = list("i" * k), []
+        for _ in range(int(rng.integers(0, 13))):
+            nid = len(types)
+            if rng.random() < 0.7:
+                types.append(PROCESSOR_TYPES[int(rng.integers(0, 7))])
+                edges.append((int(rng.integers(0, nid)), nid))
+            else:
+                preds = rng.choice(nid, size=int(rng.integers(1, min(3, nid) + 1)), replace=False)
+                types.append("m")
+                edges.extend((int(p), nid) for p in preds)
+        sinks = [v for v in range(len(types)) if all(a != v for a, _ in edges)]
+        out = len(types)
+        types.append("o")
+        edges.extend((v, out) for v in sinks)
+        graph = MixGraph("".join(types), tuple(edges))
+        P = {t: 0.1 * rng.standard_normal((len(graph.nodes_of_type(t)), PARAM_COUNTS[t]))
+             for t in PARAM_COUNTS}
+        for lo in (192, 576):
+            P["r"][:, lo:lo + 192] = -np.abs(P["r"][:, lo:lo + 192]) - 0.01
+        params = ParamStore(P, 0.1 * rng.standard_normal(len(graph.processor_nodes())))
+        src = (0.3 * rng.standard_normal((k, 2, 3000))).astype(np.float32)
+        y, _ = execute_batched(graph, params, src)
+        yo, _ = _oracle_render(graph, params, src)
+        assert normrel(y.cpu().numpy(), yo) < 1e-5, seed
+
+
+def test_mask_matches_structural_bypass_and_all_masked_is_stem_sum(dev):
+    from paper_2509_15948_b200.graph import bypass_remove
+    from paper_2509_15948_b200.schedule import schedule_console
+    from paper_2509_15948_b200.scheduler import execute_batched
+    rng = np.random.default_rng(7)
+    graph, params = _random_console(rng, kmax=4)
+    src = (0.3 * rng.standard_normal((len(graph.nodes_of_type("i")), 2, 4000))).astype(np.float32)
+    procs = graph.processor_nodes()
+    drop = set(int(v) for v in rng.choice(procs, size=len(procs) // 2, replace=False))
+    mask = np.array([0.0 if v in drop else 1.0 for v in procs])
+    ym, _ = execute_batched(graph, params, src, schedule_console(graph), mask=mask)
+    g2, p2 = bypass_remove(graph, params, drop)
+    yc, _ = execute_batched(g2, p2, src, schedule_console(g2))
+    assert normrel(ym.cpu().numpy(), yc.cpu().numpy()) < 1e-6
+    y0, _ = execute_batched(graph, params, src, schedule_console(graph), mask=np.zeros(len(procs)))
+    np.testing.assert_allclose(y0.cpu().numpy(), src.astype(np.float64).sum(axis=0), atol=1e-6)
+
+
+def test_eval_loss_matches_oracle(dev):
+    from oracle import mixgraph_oracle as O
+    from paper_2509_15948_b200.losses import LossConfig
+    from paper_2509_15948_b200.pruning import EvalSet, eval_loss
+    gs = golden("step.npz")
+    graph, params, stems, L = _step_setup()
+    segs = [(stems, gs["target"][:, 30000:])]
+    es = EvalSet(segs, 30000, LossConfig(), device=dev)
+    mask = np.ones(len(graph.processor_nodes()))
+    mask[[1, 5, 9]] = 0.0
+    got = eval_loss(graph, params, mask, es)
+    prep = O.prepare_target(gs["target"][:, 30000:].astype(np.float32).astype(np.float64), O.LossConfig())
+    want = O.eval_loss(graph, params.params, params.raw_weights, mask,
+                       [(stems.astype(np.float64), prep)], 30000, O.LossConfig())
+    np.testing.assert_allclose(got, want, rtol=1e-5)
