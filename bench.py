@@ -1,0 +1,347 @@
+"""Benchmark: console fwd+bwd train steps/s on B200 (BASELINE.json metric).
+
+Workload: full console, 16 tracks + 4 subgroups
+(140 processors, 161 nodes), L = 441,000 samples per channel ("10 s @ 44.1 kHz"
+read as a sample count, processed with the reference's 30 kHz constants),
+warm-up 30,000 samples excluded from the loss.  One step = render fwd + MRSTFT
+fwd + full backward + delay rule + AdamW + projection (mg/optimizer.py:140-186).
+Synthetic stems (mg/synth.py recipe, seed = rank), params init_params(seed),
+target = the same console rendered at init_params(seed + 1).
+
+value: device-resident inputs, CUDA-graph replays, CUDA events, max over ranks.
+e2e:   the public ``train_step`` with pinned host stems/target in, loss out.
+--impl reference: the float64 CPU oracle port (the reference is pure
+numpy/scipy and cannot travel to the GPU box) timed on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "console fwd+bwd steps/s (16 trk, 10 s stereo); songs searched/hour at 1-8 B200"
+K_TRACKS, S_GROUPS, L_SAMPLES, WARMUP = 16, 4, 441_000, 30_000
+
+
+def b_step(L, K, S, P):
+    """Design-neutral compulsory HBM bytes per step."""
+    return 40 * L * P + 16 * L * (K + S) + 16 * L * (S + 1) + 32 * (L - WARMUP)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tracks", type=int, default=K_TRACKS)
+    ap.add_argument("--subgroups", type=int, default=S_GROUPS)
+    ap.add_argument("--length", type=int, default=L_SAMPLES)
+    ap.add_argument("--eager-profile", type=int, default=0,
+                    help="run N eager (non-graph) steps and exit: for ncu launch lists")
+    return ap.parse_args()
+
+
+def make_inputs(seed, K, S, L, render_target):
+    from paper_2509_15948_b200.console import build_console, init_params
+    from paper_2509_15948_b200.synth import SynthSpec, make_stems_f32, manifest_for
+    spec = SynthSpec(tracks=K, subgroups=S, duration_seconds=L / 30000)
+    stems = make_stems_f32(spec, seed, L)
+    graph, zeros = build_console(manifest_for(spec))
+    params = init_params(zeros, seed)
+    tparams = init_params(zeros, seed + 1)
+    target = render_target(graph, tparams, stems)
+    return graph, params, stems, np.ascontiguousarray(target, dtype=np.float32)
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.samples = []
+        if self.proc is None:
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7 and f[0].isdigit():
+                self.samples.append(f)
+
+    def summary(self):
+        if not getattr(self, "samples", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(f[0]) for f in self.samples]
+        reasons = set()
+        for f in self.samples:
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"),
+                               f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(self.samples[0][1]),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_step_time(seed, K, S, L):
+    """Time one float64 oracle train_step on the host (the CPU baseline)."""
+    import torch
+    from oracle import mixgraph_oracle as O
+
+    def render(graph, tparams, stems):
+        with torch.no_grad():
+            y, _ = O.execute(graph, {t: torch.tensor(v) for t, v in tparams.params.items()},
+                             torch.tensor(tparams.raw_weights), stems.astype(np.float64))
+        return y.numpy()
+
+    graph, params, stems, target = make_inputs(seed, K, S, L, render)
+    p = {t: v.copy() for t, v in params.params.items()}
+    raw = params.raw_weights.copy()
+    opt = O.AdamW({**p, "w": raw})
+    cfg = O.LossConfig()
+    t0 = time.perf_counter()
+    O.train_step(graph, p, raw, stems.astype(np.float64), target.astype(np.float64), WARMUP, cfg, opt)
+    dt = time.perf_counter() - t0
+    return dt, torch.get_num_threads()
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if (torch.cuda.is_available() and args.impl == "ours") else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend, device_id=torch.device("cuda", local) if backend == "nccl" else None)
+    return world, rank, local
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    dt, cores = cpu_oracle_step_time(0, args.tracks, args.subgroups, args.length)
+    # each timed "step" of the reference arm is one oracle train_step (bounded sample)
+    times = [dt]
+    for _ in range(max(0, min(args.steps, 2) - 1)):
+        t, _ = cpu_oracle_step_time(0, args.tracks, args.subgroups, args.length)
+        times.append(t)
+    v = 1.0 / statistics.mean(times)
+    line = {"metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": args.gpus, "steps": len(times),
+            "warmup": 0, "ms_per_step": 1000 * statistics.mean(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "config2: full console 16 trk + 4 sub, L=441000 (10 s @44.1k as samples)",
+                       "tracks": args.tracks, "subgroups": args.subgroups, "length": args.length},
+            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "port",
+                             "sample": f"{len(times)} oracle train_step(s) of the config-2 console "
+                                       "(float64 torch CPU restatement; the reference itself is "
+                                       "numpy and cannot run on the GPU box)"},
+            "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_15948_b200.engine import TrainEngine
+    from paper_2509_15948_b200.optimizer import TrainConfig, _EngineCfg, make_optimizer, train_step
+    from paper_2509_15948_b200.scheduler import execute_batched
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    K, S, L = args.tracks, args.subgroups, args.length
+
+    def render(graph, tparams, stems):
+        y, _ = execute_batched(graph, tparams, stems, device=dev)
+        return y.cpu().numpy()
+
+    graph, params, stems, target = make_inputs(rank, K, S, L, render)
+    cfg = TrainConfig(segment_seconds=L / 30000, steps=1)
+    opt = make_optimizer(params, cfg, device=dev)
+    eng = TrainEngine(graph, L, _EngineCfg(opt, cfg), device=dev, use_graph=not args.eager_profile)
+    eng.load_params(params)
+    if args.eager_profile:
+        eng.plan.set_stems(stems)
+        eng.target.copy_(torch.from_numpy(target))
+        for _ in range(args.eager_profile):
+            eng.step_async()
+        torch.cuda.synchronize()
+        print(json.dumps({"eager_profile_steps": args.eager_profile, "launches_per_step": eng.launches_per_step()}))
+        return
+    eng.plan.set_stems(stems)
+    eng.target.copy_(torch.from_numpy(target))
+    for _ in range(max(3, args.warmup)):
+        eng.step_async()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record()
+        for _ in range(args.steps):
+            eng.step_async()
+        stop.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(stop)
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    ms_step = ms_max / args.steps
+    value = world * args.steps / (ms_max / 1000.0)
+    vals = eng.read_values()
+
+    # per-level kernel-group timing (eager, CUDA events on the launching stream)
+    level_ms = time_levels(eng, reps=3)
+    # e2e through the public API with pinned host buffers
+    st_pin = torch.from_numpy(stems).pin_memory()
+    tg_pin = torch.from_numpy(target).pin_memory()
+    opt2 = make_optimizer(params, cfg, device=dev)
+    p2 = params.copy()
+    train_step(graph, p2, (st_pin, tg_pin), cfg, opt2)  # builds + captures
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        train_step(graph, p2, (st_pin, tg_pin), cfg, opt2)
+    e2e_s = time.perf_counter() - t0
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_val = world * args.e2e_steps / float(e2e_t.item())
+    lay = eng.layout
+    h2d = stems.nbytes + target.nbytes + lay.n * 8
+    d2h = 4 * 8 + lay.n * 8
+
+    P = lay.P
+    bytes_step = b_step(L, K, S, P)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    dom = max(level_ms.items(), key=lambda kv: kv[1]["ms"]) if level_ms else None
+    roof = None
+    if dom:
+        name, rec = dom
+        ach = rec["bytes"] / (rec["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": None, "kernel": name, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": rec["bytes"], "launch_ms": rec["ms"]}
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                dt, cores = cpu_oracle_step_time(0, K, S, L)
+                cpu = {"value": 1.0 / dt, "unit": "steps/s", "cores": cores, "kind": "port",
+                       "sample": "1 float64 oracle train_step of the same config-2 console on the host"}
+            except Exception as exc:  # pragma: no cover
+                cpu = {"value": None, "unit": "steps/s", "cores": 0, "kind": "port",
+                       "sample": f"failed: {exc}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 scans/loss/optimizer)",
+            "data": "synthetic",
+            "config": {"workload": "config2: full console 16 trk + 4 sub, L=441000 (10 s @44.1k as samples)",
+                       "tracks": K, "subgroups": S, "length": L, "processors": P, "seed": "rank",
+                       "l2": "working set per step >> 126 MB L2 (no flush needed)",
+                       "parallelism": f"song-sharded x{world} (no collective in the step)"},
+            "e2e": {"value": e2e_val, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "paper_2509_15948_b200.train_step (pinned host stems/target)"},
+            "gpu_launches": eng.launches_per_step() * args.steps,
+            "clocks": clk.summary(),
+            "roofline": roof,
+            "step_roofline": {"bound": "hbm", "algorithmic_bytes": bytes_step,
+                              "achieved": bytes_step / (ms_step / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                              "frac": bytes_step / (ms_step / 1e3) / 1e9 / hbm},
+            "levels_ms": {k: round(v["ms"], 4) for k, v in level_ms.items()},
+            "loss": vals,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def time_levels(eng, reps=3):
+    """CUDA-event time of each level's forward+backward (eager) and its algorithmic bytes."""
+    import ctypes
+
+    import torch
+
+    from paper_2509_15948_b200._lib import check, lib
+    from paper_2509_15948_b200.engine import stream_ptr
+    Ld = lib()
+    L = eng.L
+    out = {}
+    plan = eng.plan
+    # run one eager forward/backward so all buffers hold a consistent state
+    eng.grads_only()
+    for lv in plan.levels:
+        if lv.struct is None:
+            continue
+        key = f"{lv.tag}@step{lv.step}(B={lv.B})"
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        fwd, bwd = [], []
+        for _ in range(reps):
+            ev[0].record()
+            check(Ld.mgb_level_forward(ctypes.byref(lv.struct), stream_ptr()), "fwd")
+            ev[1].record()
+            check(Ld.mgb_level_backward(ctypes.byref(lv.struct), stream_ptr()), "bwd")
+            ev[2].record()
+            torch.cuda.synchronize()
+            fwd.append(ev[0].elapsed_time(ev[1]))
+            bwd.append(ev[1].elapsed_time(ev[2]))
+        # compulsory bytes of one processor: 40 * L per node (fwd 16 L + bwd 24 L)
+        out[key] = {"ms": min(fwd) + min(bwd), "fwd_ms": min(fwd), "bwd_ms": min(bwd),
+                    "bytes": 40 * L * lv.B}
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -77,7 +77,8 @@ __device__ __forceinline__ void smem_fft(typename Cplx<R>::T* s, bool inv) {
   typedef typename Cplx<R>::T V;
   static_assert((N & (N - 1)) == 0 && N >= 2, "pow2");
   static_assert(N <= MGB_TW_N, "twiddle table");
-  constexpr int NB4 = (N >= 4) ? NSEQ * (N / 4) : 0;       // radix-4 butterflies per pass
+  constexpr int N4 = (N >= 4) ? N / 4 : 1;
+  constexpr int NB4 = NSEQ * N4;                            // radix-4 butterflies per pass
   constexpr int BPT4 = (NB4 + NT - 1) / NT;
   constexpr int NB2 = NSEQ * (N / 2);
   constexpr int BPT2 = (NB2 + NT - 1) / NT;
@@ -85,7 +86,7 @@ __device__ __forceinline__ void smem_fft(typename Cplx<R>::T* s, bool inv) {
   int Ns = 1;
   __syncthreads();
   // radix-4 passes
-  for (; Ns * 4 <= N; Ns *= 4) {
+  if constexpr (N >= 4) for (; Ns * 4 <= N; Ns *= 4) {
     V v[BPT4][4];
 #pragma unroll
     for (int i = 0; i < BPT4; ++i) {

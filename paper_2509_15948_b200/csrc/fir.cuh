@@ -1,0 +1,418 @@
+// FIR synthesis and FIR adjoint kernels of the e / r / d levels (included by conv.cu).
+#pragma once
+// ---------------------------------------------------------------------------
+// EQ FIR: centred[t'] = hann_sym(2047)[t'] * irfft(exp(p), 2047)[(t'+1024) % 2047]
+
+// 32 outputs per CTA (lane), 8 warps split the 1023 cosine terms; compact (B, 2047) output
+__global__ void __launch_bounds__(256) k_eq_fir(const double* __restrict__ bank, const int* __restrict__ prow,
+                                                float2* __restrict__ H) {
+  __shared__ double X[MGB_EQ_BINS];
+  __shared__ double ct[MGB_EQ_LEN];
+  __shared__ double part[8][33];
+  const int b = blockIdx.y;
+  const double* p = bank + (size_t)prow[b] * MGB_EQ_BINS;
+  for (int k = threadIdx.x; k < MGB_EQ_BINS; k += 256) X[k] = exp(p[k]);
+  for (int j = threadIdx.x; j < MGB_EQ_LEN; j += 256) ct[j] = cospi(2.0 * j / (double)MGB_EQ_LEN);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tp = blockIdx.x * 32 + lane;
+  const int t = (tp + 1024) % MGB_EQ_LEN;
+  const int k0 = 1 + w * 128, k1 = min(MGB_EQ_BINS, k0 + 128);
+  double acc = 0.0;
+  int idx = (int)(((long long)k0 * t) % MGB_EQ_LEN);
+  for (int k = k0; k < k1; ++k) {
+    acc = fma(X[k], ct[idx], acc);
+    idx += t;
+    if (idx >= MGB_EQ_LEN) idx -= MGB_EQ_LEN;
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && tp < MGB_EQ_LEN) {
+    double s = 0.0;
+    for (int i = 0; i < 8; ++i) s += part[i][lane];
+    const double hv = (X[0] + 2.0 * s) / (double)MGB_EQ_LEN;
+    const double win = 0.5 - 0.5 * cospi(2.0 * tp / (double)(MGB_EQ_LEN - 1));
+    const float c = (float)(hv * win);
+    H[(size_t)b * MGB_EQ_LEN + tp] = make_float2(c, c);
+  }
+}
+
+// d p_k = X_k * (2/n) sum_t dh[t] cos(2 pi k t / n)   (k = 0: 1/n), dh summed over channels.
+// 32 bins per CTA (lane), 8 warps split t.
+__global__ void __launch_bounds__(256) k_eq_fir_bwd(const double* __restrict__ bank, const int* __restrict__ prow,
+                                                    const float2* __restrict__ GH, int M,
+                                                    double* __restrict__ gbank) {
+  __shared__ double dh[MGB_EQ_LEN];
+  __shared__ double ct[MGB_EQ_LEN];
+  __shared__ double part[8][33];
+  const int b = blockIdx.y;
+  const float2* g = GH + (size_t)b * M;
+  for (int tp = threadIdx.x; tp < MGB_EQ_LEN; tp += 256) {
+    const double win = 0.5 - 0.5 * cospi(2.0 * tp / (double)(MGB_EQ_LEN - 1));
+    const float2 v = g[tp];
+    dh[(tp + 1024) % MGB_EQ_LEN] = ((double)v.x + (double)v.y) * win;
+    ct[tp] = cospi(2.0 * tp / (double)MGB_EQ_LEN);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + lane;
+  const int t0 = w * 256, t1 = min(MGB_EQ_LEN, t0 + 256);
+  double acc = 0.0;
+  int idx = (int)(((long long)k * t0) % MGB_EQ_LEN);
+  for (int t = t0; t < t1; ++t) {
+    acc = fma(dh[t], ct[idx], acc);
+    idx += k;
+    if (idx >= MGB_EQ_LEN) idx -= MGB_EQ_LEN;
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && k < MGB_EQ_BINS) {
+    double s = 0.0;
+    for (int i = 0; i < 8; ++i) s += part[i][lane];
+    const double scale = (k == 0 ? 1.0 : 2.0) / (double)MGB_EQ_LEN;
+    const double* p = bank + (size_t)prow[b] * MGB_EQ_BINS;
+    gbank[(size_t)prow[b] * MGB_EQ_BINS + k] = s * scale * exp(p[k]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Reverb FIR synthesis
+
+__global__ void __launch_bounds__(MGB_REV_NFFT) k_rev_frames(const double* __restrict__ bank,
+                                                             const int* __restrict__ prow,
+                                                             float* __restrict__ frames) {
+  __shared__ float2 X[2][MGB_REV_BINS];
+  __shared__ float2 cs[MGB_REV_NFFT];
+  const int m = blockIdx.x, b = blockIdx.y;
+  const double* p = bank + (size_t)prow[b] * 768;
+  const int i = threadIdx.x;
+  {
+    double s, c;
+    sincospi(2.0 * i / (double)MGB_REV_NFFT, &s, &c);
+    cs[i] = make_float2((float)c, (float)s);
+  }
+  for (int q = threadIdx.x; q < 2 * MGB_REV_BINS; q += blockDim.x) {
+    const int ch = q / MGB_REV_BINS, k = q % MGB_REV_BINS;
+    const int kk = k < MGB_REV_PBINS ? k : MGB_REV_PBINS - 1;  // Nyquist repeats the last bin
+    const double h0 = p[ch * 384 + kk], hd = p[ch * 384 + 192 + kk];
+    const float mag = (float)exp(h0 + hd * (double)m);
+    const float2 s = g_rev_spec[ch][m][k];
+    X[ch][k] = make_float2(mag * s.x, mag * s.y);
+  }
+  __syncthreads();
+  float a0 = 0.f, a1 = 0.f;
+  int idx = i;
+  for (int k = 1; k < MGB_REV_PBINS; ++k) {
+    const float2 w = cs[idx];
+    a0 = fmaf(X[0][k].x, w.x, fmaf(-X[0][k].y, w.y, a0));
+    a1 = fmaf(X[1][k].x, w.x, fmaf(-X[1][k].y, w.y, a1));
+    idx += i;
+    if (idx >= MGB_REV_NFFT) idx -= MGB_REV_NFFT;
+  }
+  const float sgn = (i & 1) ? -1.f : 1.f;
+  const float win = 0.5f - 0.5f * cs[i].x;
+  const float inv = 1.0f / (float)MGB_REV_NFFT;
+  const float f0 = (X[0][0].x + sgn * X[0][MGB_REV_PBINS].x + 2.f * a0) * inv * win;
+  const float f1 = (X[1][0].x + sgn * X[1][MGB_REV_PBINS].x + 2.f * a1) * inv * win;
+  frames[(((size_t)b * 2 + 0) * MGB_REV_FRAMES + m) * MGB_REV_NFFT + i] = f0;
+  frames[(((size_t)b * 2 + 1) * MGB_REV_FRAMES + m) * MGB_REV_NFFT + i] = f1;
+}
+
+__global__ void __launch_bounds__(NT) k_rev_assemble(const float* __restrict__ frames, float2* __restrict__ H) {
+  const int b = blockIdx.y;
+  const long long N = MGB_REV_LEN;
+  float2* h = H + (size_t)b * N;
+  const float* fm = frames + (size_t)b * 2 * MGB_REV_FRAMES * MGB_REV_NFFT;
+  const float* fs = fm + (size_t)MGB_REV_FRAMES * MGB_REV_NFFT;
+  for (long long t = (long long)blockIdx.x * NT + threadIdx.x; t < N; t += (long long)gridDim.x * NT) {
+    if (t >= MGB_REV_LEN) { h[t] = make_float2(0.f, 0.f); continue; }
+    const int P = (int)t + MGB_REV_HOP;
+    const int j = P / MGB_REV_HOP;
+    float vm = 0.f, vs = 0.f;
+    if (j < MGB_REV_FRAMES) {
+      vm += fm[(size_t)j * MGB_REV_NFFT + (P - j * MGB_REV_HOP)];
+      vs += fs[(size_t)j * MGB_REV_NFFT + (P - j * MGB_REV_HOP)];
+    }
+    if (j >= 1) {
+      vm += fm[(size_t)(j - 1) * MGB_REV_NFFT + (P - (j - 1) * MGB_REV_HOP)];
+      vs += fs[(size_t)(j - 1) * MGB_REV_NFFT + (P - (j - 1) * MGB_REV_HOP)];
+    }
+    const float iw = g_rev_inv_wss[t];
+    vm *= iw;
+    vs *= iw;
+    h[t] = make_float2(0.5f * (vm + vs), 0.5f * (vm - vs));
+  }
+}
+
+// dexpo[c][m][k] = Re(dX_k conj(S_mk)) * M_mk, dX = irfft adjoint of the windowed frame grad
+__global__ void __launch_bounds__(MGB_REV_NFFT) k_rev_bwd_frames(const double* __restrict__ bank,
+                                                                 const int* __restrict__ prow,
+                                                                 const float2* __restrict__ GH, int N,
+                                                                 float* __restrict__ dexpo) {
+  __shared__ float fr[2][MGB_REV_NFFT];
+  __shared__ float2 cs[MGB_REV_NFFT];
+  const int m = blockIdx.x, b = blockIdx.y;
+  const float2* g = GH + (size_t)b * N;
+  const int i = threadIdx.x;
+  {
+    double s, c;
+    sincospi(2.0 * i / (double)MGB_REV_NFFT, &s, &c);
+    cs[i] = make_float2((float)c, (float)s);
+  }
+  {
+    const int t = m * MGB_REV_HOP + i - MGB_REV_HOP;  // position in the sliced FIR
+    float dm = 0.f, ds = 0.f;
+    if (t >= 0 && t < MGB_REV_LEN) {
+      const float2 v = g[t];
+      const float iw = g_rev_inv_wss[t];
+      dm = 0.5f * (v.x + v.y) * iw;
+      ds = 0.5f * (v.x - v.y) * iw;
+    }
+    const float win = 0.5f - 0.5f * (float)cospi(2.0 * i / (double)MGB_REV_NFFT);
+    fr[0][i] = dm * win;
+    fr[1][i] = ds * win;
+  }
+  __syncthreads();
+  const double* p = bank + (size_t)prow[b] * 768;
+  for (int q = threadIdx.x; q < 2 * MGB_REV_BINS; q += blockDim.x) {
+    const int ch = q / MGB_REV_BINS, k = q % MGB_REV_BINS;
+    float re = 0.f, im = 0.f;
+    int idx = 0;
+    for (int t = 0; t < MGB_REV_NFFT; ++t) {
+      const float2 w = cs[idx];
+      re = fmaf(fr[ch][t], w.x, re);
+      im = fmaf(-fr[ch][t], w.y, im);
+      idx += k;
+      if (idx >= MGB_REV_NFFT) idx -= MGB_REV_NFFT;
+    }
+    float sc = 2.f / (float)MGB_REV_NFFT;
+    if (k == 0 || k == MGB_REV_PBINS) sc *= 0.5f;
+    re *= sc;
+    im *= sc;
+    const float2 s = g_rev_spec[ch][m][k];
+    const int kk = k < MGB_REV_PBINS ? k : MGB_REV_PBINS - 1;
+    const float mag = (float)exp(p[ch * 384 + kk] + p[ch * 384 + 192 + kk] * (double)m);
+    dexpo[(((size_t)b * 2 + ch) * MGB_REV_FRAMES + m) * MGB_REV_BINS + k] = (re * s.x + im * s.y) * mag;
+  }
+}
+
+__global__ void k_rev_bwd_reduce(const float* __restrict__ dexpo, const int* __restrict__ prow,
+                                 double* __restrict__ gbank) {
+  __shared__ double d0[2][MGB_REV_BINS], dd[2][MGB_REV_BINS];
+  const int b = blockIdx.x;
+  for (int q = threadIdx.x; q < 2 * MGB_REV_BINS; q += blockDim.x) {
+    const int ch = q / MGB_REV_BINS, k = q % MGB_REV_BINS;
+    const float* e = dexpo + ((size_t)b * 2 + ch) * MGB_REV_FRAMES * MGB_REV_BINS + k;
+    double s0 = 0.0, s1 = 0.0;
+    for (int m = 0; m < MGB_REV_FRAMES; ++m) {
+      const double v = e[(size_t)m * MGB_REV_BINS];
+      s0 += v;
+      s1 += v * m;
+    }
+    d0[ch][k] = s0;
+    dd[ch][k] = s1;
+  }
+  __syncthreads();
+  double* g = gbank + (size_t)prow[b] * 768;
+  for (int q = threadIdx.x; q < 2 * MGB_REV_PBINS; q += blockDim.x) {
+    const int ch = q / MGB_REV_PBINS, k = q % MGB_REV_PBINS;
+    double a = d0[ch][k], c = dd[ch][k];
+    if (k == MGB_REV_PBINS - 1) { a += d0[ch][MGB_REV_PBINS]; c += dd[ch][MGB_REV_PBINS]; }
+    g[ch * 384 + k] = a;
+    g[ch * 384 + 192 + k] = c;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Multitap delay
+
+// colour[t'] = hann_sym(39)[t'] * irfft(exp(bins), 39)[(t'+20) % 39] and the
+// quantised offset d = rint(((-angle z) mod 2pi) / 2pi * 3000) mod 3000 in fp64
+__global__ void k_dly_colour(const double* __restrict__ bank, const int* __restrict__ prow,
+                             float* __restrict__ colour, int* __restrict__ offs) {
+  const int tap = blockIdx.x, ch = blockIdx.y, b = blockIdx.z;
+  const double* p = bank + (size_t)prow[b] * 880 + ch * 440;
+  const int tp = threadIdx.x;
+  if (tp < MGB_COLOR_LEN) {
+    const double* bins = p + 40 + tap * MGB_COLOR_BINS;
+    const int t = (tp + 20) % MGB_COLOR_LEN;
+    double acc = 0.0;
+    for (int k = 1; k < MGB_COLOR_BINS; ++k) acc += exp(bins[k]) * cospi(2.0 * ((k * t) % MGB_COLOR_LEN) / 39.0);
+    const double hv = (exp(bins[0]) + 2.0 * acc) / 39.0;
+    const double win = 0.5 - 0.5 * cospi(2.0 * tp / 38.0);
+    colour[(((size_t)b * 2 + ch) * MGB_DLY_TAPS + tap) * MGB_COLOR_LEN + tp] = (float)(hv * win);
+  }
+  if (tp == 0) {
+    const double re = p[tap], im = p[20 + tap];
+    const double theta = atan2(im, re);
+    const double two_pi = 2.0 * PI;
+    double r = fmod(-theta, two_pi);
+    if (r != 0.0 && r < 0.0) r += two_pi;
+    const double pos = r / two_pi * (double)MGB_DLY_WIN;
+    int d = (int)rint(pos);
+    d %= MGB_DLY_WIN;
+    offs[((size_t)b * 2 + ch) * MGB_DLY_TAPS + tap] = d;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_dly_place(const float* __restrict__ colour, const int* __restrict__ offs,
+                                                  float2* __restrict__ H) {
+  const long long N = MGB_DLY_FIR;
+  __shared__ float col[2][MGB_DLY_TAPS][MGB_COLOR_LEN];
+  __shared__ int dd[2][MGB_DLY_TAPS];
+  const int b = blockIdx.y;
+  for (int i = threadIdx.x; i < 2 * MGB_DLY_TAPS * MGB_COLOR_LEN; i += NT)
+    (&col[0][0][0])[i] = colour[(size_t)b * 2 * MGB_DLY_TAPS * MGB_COLOR_LEN + i];
+  for (int i = threadIdx.x; i < 2 * MGB_DLY_TAPS; i += NT) (&dd[0][0])[i] = offs[(size_t)b * 2 * MGB_DLY_TAPS + i];
+  __syncthreads();
+  float2* h = H + (size_t)b * N;
+  for (long long k = (long long)blockIdx.x * NT + threadIdx.x; k < N; k += (long long)gridDim.x * NT) {
+    float v[2] = {0.f, 0.f};
+    if (k < MGB_DLY_FIR) {
+      const int m1 = (int)(k / MGB_DLY_WIN);
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        float acc = 0.f;
+        for (int m = m1 - 1; m <= m1; ++m) {
+          if (m < 0 || m >= MGB_DLY_TAPS) continue;
+          const int j = (int)k - m * MGB_DLY_WIN - dd[ch][m];
+          if (j >= 0 && j < MGB_COLOR_LEN) acc += col[ch][m][j];
+        }
+        v[ch] = acc;
+      }
+    }
+    h[k] = make_float2(v[0], v[1]);
+  }
+}
+
+// One CTA per (tap, channel, row): colour gradient (gather + zero-phase FIR
+// adjoint) and the damped-sinusoid surrogate z-gradient
+// graw = conj( (1/n) sum_k k z^{k-1} E_k ),  E_k = sum_t e_t e^{+2 pi i k t / n},
+// e_t = sum_j dh[m*3000 + t + j] colour[j]   (mg/processors.py:274-300).
+// E is a 3000-point DFT done as 60 x 50 (t = t1 + 50 t2, k = k2 + 60 k1).
+__global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank, const int* __restrict__ prow,
+                                                const float* __restrict__ colour, const int* __restrict__ offs,
+                                                const float2* __restrict__ GH, int N,
+                                                double* __restrict__ gbank) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float2* A = reinterpret_cast<float2*>(dsm);                  // 3000
+  float2* E = A + MGB_DLY_WIN;                                 // 3000
+  float* seg = reinterpret_cast<float*>(E + MGB_DLY_WIN);      // 3040
+  float* et = seg + 3040;                                      // 3000
+  __shared__ float col[MGB_COLOR_LEN];
+  __shared__ double dhz[MGB_COLOR_LEN];
+  __shared__ float2 w60[60], w50[50];
+  __shared__ double red[32];
+  const int tap = blockIdx.x, ch = blockIdx.y, b = blockIdx.z;
+  const float2* g = GH + (size_t)b * N;
+  const int base = tap * MGB_DLY_WIN;
+  for (int i = threadIdx.x; i < MGB_DLY_WIN + MGB_COLOR_LEN - 1; i += NT) {
+    const float2 v = g[base + i];
+    seg[i] = ch == 0 ? v.x : v.y;
+  }
+  if (threadIdx.x < MGB_COLOR_LEN)
+    col[threadIdx.x] = colour[(((size_t)b * 2 + ch) * MGB_DLY_TAPS + tap) * MGB_COLOR_LEN + threadIdx.x];
+  if (threadIdx.x < 60) {
+    float s, c;
+    sincospif(2.0f * threadIdx.x / 60.0f, &s, &c);
+    w60[threadIdx.x] = make_float2(c, s);
+  }
+  if (threadIdx.x < 50) {
+    float s, c;
+    sincospif(2.0f * threadIdx.x / 50.0f, &s, &c);
+    w50[threadIdx.x] = make_float2(c, s);
+  }
+  const int d = offs[((size_t)b * 2 + ch) * MGB_DLY_TAPS + tap];
+  const double* p = bank + (size_t)prow[b] * 880 + ch * 440;
+  double* gp = gbank + (size_t)prow[b] * 880 + ch * 440;
+  __syncthreads();
+  // colour gradient -> bins
+  if (threadIdx.x < MGB_COLOR_LEN) {
+    const int tp = threadIdx.x;
+    const double win = 0.5 - 0.5 * cospi(2.0 * tp / 38.0);
+    dhz[(tp + 20) % MGB_COLOR_LEN] = (double)seg[d + tp] * win;
+  }
+  // e_t
+  for (int t = threadIdx.x; t < MGB_DLY_WIN; t += NT) {
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < MGB_COLOR_LEN; ++j) acc = fmaf(seg[t + j], col[j], acc);
+    et[t] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < MGB_COLOR_BINS) {
+    const int k = threadIdx.x;
+    double acc = 0.0;
+    for (int t = 0; t < MGB_COLOR_LEN; ++t) acc += dhz[t] * cospi(2.0 * ((k * t) % MGB_COLOR_LEN) / 39.0);
+    const double sc = (k == 0 ? 1.0 : 2.0) / 39.0;
+    gp[40 + tap * MGB_COLOR_BINS + k] = acc * sc * exp(p[40 + tap * MGB_COLOR_BINS + k]);
+  }
+  // step A: A[t1][k2] = w_3000^{k2 t1} * sum_{t2} e[t1 + 50 t2] w_60^{k2 t2}
+  for (int o = threadIdx.x; o < MGB_DLY_WIN; o += NT) {
+    const int t1 = o / 60, k2 = o % 60;
+    float re = 0.f, im = 0.f;
+    int idx = 0;
+    for (int t2 = 0; t2 < 60; ++t2) {
+      const float e = et[t1 + 50 * t2];
+      re = fmaf(e, w60[idx].x, re);
+      im = fmaf(e, w60[idx].y, im);
+      idx += k2;
+      if (idx >= 60) idx -= 60;
+    }
+    float s, c;
+    sincospif(2.0f * (float)(k2 * t1) / 3000.0f, &s, &c);
+    A[o] = make_float2(re * c - im * s, re * s + im * c);
+  }
+  __syncthreads();
+  // step B: E[k2 + 60 k1] = sum_{t1} A[t1][k2] w_50^{k1 t1}
+  for (int o = threadIdx.x; o < MGB_DLY_WIN; o += NT) {
+    const int k1 = o / 60, k2 = o % 60;
+    float re = 0.f, im = 0.f;
+    int idx = 0;
+    for (int t1 = 0; t1 < 50; ++t1) {
+      const float2 a = A[t1 * 60 + k2];
+      const float2 w = w50[idx];
+      re += a.x * w.x - a.y * w.y;
+      im += a.x * w.y + a.y * w.x;
+      idx += k1;
+      if (idx >= 50) idx -= 50;
+    }
+    E[k2 + 60 * k1] = make_float2(re, im);
+  }
+  __syncthreads();
+  // S = (1/n) sum_{k>=1} k z^{k-1} E_k   (z projected into the unit disk)
+  double zr = p[tap], zi = p[20 + tap];
+  const double mag = sqrt(zr * zr + zi * zi);
+  if (mag > 1.0) { zr /= mag; zi /= mag; }
+  const bool zero = (zr == 0.0 && zi == 0.0);
+  const double lmag = zero ? 0.0 : log(zero ? 1.0 : fmin(mag, 1.0));
+  const double th = atan2(zi, zr);
+  double sre = 0.0, sim = 0.0;
+  for (int k = 1 + threadIdx.x; k < MGB_DLY_WIN; k += NT) {
+    double pr, pi;
+    if (zero) {
+      pr = (k == 1) ? 1.0 : 0.0;
+      pi = 0.0;
+    } else {
+      const double a = exp((double)(k - 1) * lmag);
+      double s, c;
+      sincos((double)(k - 1) * th, &s, &c);
+      pr = a * c;
+      pi = a * s;
+    }
+    const double er = E[k].x, ei = E[k].y;
+    sre += (double)k * (pr * er - pi * ei);
+    sim += (double)k * (pr * ei + pi * er);
+  }
+  sre = block_sum(sre, red);
+  __syncthreads();
+  sim = block_sum(sim, red);
+  if (threadIdx.x == 0) {
+    gp[tap] = sre / (double)MGB_DLY_WIN;
+    gp[20 + tap] = -sim / (double)MGB_DLY_WIN;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// conv epilogue / prologue with dry/wet and gain staging
+

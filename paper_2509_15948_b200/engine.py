@@ -464,13 +464,26 @@ class TrainEngine:
         n += 2 + (2 if self.d_rows else 0)  # raw-grad, adamw, delay rule, projection
         return n
 
+    _RING = 64
+
     def _set_scalars(self, alpha_p):
+        """Per-step [lr, b1, b2, eps, wd, c1, c2, alpha_p] -> device, from a ring of pinned
+        slots: a slot is rewritten only after its previous async copy has executed."""
         c = self.cfg
         self.t += 1
         b1, b2 = c.betas
-        self.scalars_host.copy_(torch.tensor([c.lr, b1, b2, c.eps, c.weight_decay, 1.0 - b1 ** self.t,
-                                              1.0 - b2 ** self.t, float(alpha_p)], dtype=F64))
-        self.scalars.copy_(self.scalars_host, non_blocking=True)
+        if not hasattr(self, "_ring"):
+            self._ring = torch.zeros((self._RING, 8), dtype=F64).pin_memory()
+            self._ring_ev = [None] * self._RING
+        i = self.t % self._RING
+        if self._ring_ev[i] is not None:
+            self._ring_ev[i].synchronize()
+        self._ring[i].copy_(torch.tensor([c.lr, b1, b2, c.eps, c.weight_decay, 1.0 - b1 ** self.t,
+                                          1.0 - b2 ** self.t, float(alpha_p)], dtype=F64))
+        self.scalars.copy_(self._ring[i], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ring_ev[i] = ev
 
     def step_async(self, alpha_p=0.0):
         """Enqueue one full train step (inputs already in plan.stems / self.target)."""
