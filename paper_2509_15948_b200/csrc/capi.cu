@@ -14,6 +14,7 @@ extern "C" int mgb_init(const double* reverb_spec_host, const double* reverb_wss
   if (rc) return rc;
   if ((rc = mgb_conv_init())) return rc;
   if ((rc = mgb_loss_init())) return rc;
+  if ((rc = mgb_dyn_init())) return rc;
   if (reverb_spec_host && reverb_wss_host) {
     static float2 spec[2][MGB_REV_FRAMES][MGB_REV_BINS];
     static float inv[MGB_REV_LEN];

@@ -67,103 +67,154 @@ __device__ __forceinline__ double2 twiddle_exact(long long e, long long n, bool 
 
 // ---------------------------------------------------------------------------
 // Shared-memory Stockham FFT over a tile of NSEQ sequences of length N (pow2).
-// Element j of sequence q lives at s[q * SEQ_STRIDE + j * ELEM_STRIDE].
-// SEQ_FAST: consecutive threads walk sequences (use when ELEM_STRIDE > 1 and
-// sequences are adjacent in memory, i.e. column tiles).
-// Unnormalised; inverse uses conjugate twiddles.  Must be called by all
-// NT threads of the block; ends with a __syncthreads().
-template <typename R, int N, int NSEQ, int NT, int SEQ_STRIDE, int ELEM_STRIDE, bool SEQ_FAST>
-__device__ __forceinline__ void smem_fft(typename Cplx<R>::T* s, bool inv) {
+//
+// Element j of sequence q lives at s[q * SEQ_STRIDE + pidx<PAD>(j) * ELEM_STRIDE].
+// PAD (unit-stride layouts only) inserts one slot every 8 elements so the
+// stride-R Stockham writes and the stride-N/R reads are bank-conflict free;
+// a padded sequence occupies padded_len<N>() slots.
+// SEQ_FAST: consecutive threads walk sequences (column tiles, ELEM_STRIDE > 1).
+// Radix-8 passes (radix-4 / radix-2 first when log2 N is not a multiple of 3);
+// one twiddle-table lookup per butterfly, higher powers by multiplication.
+// Unnormalised; inverse uses conjugate twiddles.  Called by all NT threads;
+// starts and ends with __syncthreads().
+
+template <bool PAD>
+__device__ __forceinline__ int pidx(int j) { return PAD ? j + (j >> 3) : j; }
+template <int N>
+constexpr int padded_len() { return N + N / 8; }
+
+template <typename V>
+__device__ __forceinline__ void dft4(V* v, bool inv) {
+  const V a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]), a2 = cadd(v[1], v[3]), a3 = csub(v[1], v[3]);
+  const V a3r = inv ? cmul_pi(a3) : cmul_mi(a3);
+  v[0] = cadd(a0, a2);
+  v[2] = csub(a0, a2);
+  v[1] = cadd(a1, a3r);
+  v[3] = csub(a1, a3r);
+}
+
+template <typename V, typename R>
+__device__ __forceinline__ void dft8(V* v, bool inv) {
+  V e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+  dft4(e, inv);
+  dft4(o, inv);
+  const R h = (R)0.70710678118654752440;
+  V t[4];
+  t[0] = o[0];
+  if (!inv) {
+    t[1] = cmk(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+    t[2] = cmul_mi(o[2]);
+    t[3] = cmk(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+  } else {
+    t[1] = cmk(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y));
+    t[2] = cmul_pi(o[2]);
+    t[3] = cmk(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y));
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[k] = cadd(e[k], t[k]);
+    v[k + 4] = csub(e[k], t[k]);
+  }
+}
+
+template <typename R, int RAD, int Ns, int N, int NSEQ, int NT, int SEQ_STRIDE, int ELEM_STRIDE, bool SEQ_FAST,
+          bool PAD>
+__device__ __forceinline__ void stockham_pass(typename Cplx<R>::T* s, bool inv) {
   typedef typename Cplx<R>::T V;
+  constexpr int M = N / RAD;
+  constexpr int NB = NSEQ * M;
+  constexpr int BPT = (NB + NT - 1) / NT;
+  V v[BPT][RAD];
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) {
+    const int b = threadIdx.x + i * NT;
+    if (b < NB) {
+      int q, j;
+      if (SEQ_FAST) { q = b % NSEQ; j = b / NSEQ; } else { j = b % M; q = b / M; }
+      const int k = j & (Ns - 1);
+      V* base = s + q * SEQ_STRIDE;
+#pragma unroll
+      for (int r = 0; r < RAD; ++r) v[i][r] = base[pidx<PAD>(j + r * M) * ELEM_STRIDE];
+      if constexpr (Ns > 1) {
+        const V w1 = tw_lookup((MGB_TW_N / (RAD * Ns)) * k, inv, R());
+        v[i][1] = cmul(v[i][1], w1);
+        if (RAD >= 4) {
+          const V w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+          v[i][2] = cmul(v[i][2], w2);
+          v[i][3] = cmul(v[i][3], w3);
+          if (RAD == 8) {
+            const V w4 = cmul(w2, w2);
+            v[i][4] = cmul(v[i][4], w4);
+            v[i][5] = cmul(v[i][5], cmul(w4, w1));
+            v[i][6] = cmul(v[i][6], cmul(w4, w2));
+            v[i][7] = cmul(v[i][7], cmul(w4, w3));
+          }
+        }
+      }
+      if (RAD == 8) dft8<V, R>(v[i], inv);
+      else if (RAD == 4) dft4(v[i], inv);
+      else {
+        const V t0 = v[i][0];
+        v[i][0] = cadd(t0, v[i][1]);
+        v[i][1] = csub(t0, v[i][1]);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) {
+    const int b = threadIdx.x + i * NT;
+    if (b < NB) {
+      int q, j;
+      if (SEQ_FAST) { q = b % NSEQ; j = b / NSEQ; } else { j = b % M; q = b / M; }
+      const int k = j & (Ns - 1);
+      const int d = (j / Ns) * (RAD * Ns) + k;
+      V* base = s + q * SEQ_STRIDE;
+#pragma unroll
+      for (int r = 0; r < RAD; ++r) base[pidx<PAD>(d + r * Ns) * ELEM_STRIDE] = v[i][r];
+    }
+  }
+  __syncthreads();
+}
+
+// radix-8 passes with compile-time strides Ns = NS, 8 NS, ... < N
+template <typename R, int NS, int N, int NSEQ, int NT, int SEQ_STRIDE, int ELEM_STRIDE, bool SEQ_FAST, bool PAD>
+__device__ __forceinline__ void fft_passes8(typename Cplx<R>::T* s, bool inv) {
+  if constexpr (NS < N) {
+    stockham_pass<R, 8, NS, N, NSEQ, NT, SEQ_STRIDE, ELEM_STRIDE, SEQ_FAST, PAD>(s, inv);
+    fft_passes8<R, NS * 8, N, NSEQ, NT, SEQ_STRIDE, ELEM_STRIDE, SEQ_FAST, PAD>(s, inv);
+  }
+}
+
+template <typename R, int N, int NSEQ, int NT, int SEQ_STRIDE, int ELEM_STRIDE, bool SEQ_FAST, bool PAD = false>
+__device__ __forceinline__ void smem_fft(typename Cplx<R>::T* s, bool inv) {
   static_assert((N & (N - 1)) == 0 && N >= 2, "pow2");
   static_assert(N <= MGB_TW_N, "twiddle table");
-  constexpr int N4 = (N >= 4) ? N / 4 : 1;
-  constexpr int NB4 = NSEQ * N4;                            // radix-4 butterflies per pass
-  constexpr int BPT4 = (NB4 + NT - 1) / NT;
-  constexpr int NB2 = NSEQ * (N / 2);
-  constexpr int BPT2 = (NB2 + NT - 1) / NT;
-  const int tid = threadIdx.x;
-  int Ns = 1;
+  static_assert(!PAD || ELEM_STRIDE == 1, "padding is for unit-stride layouts");
+  constexpr int LOG = __builtin_ctz(N);
+  constexpr int REM = LOG % 3;
   __syncthreads();
-  // radix-4 passes
-  if constexpr (N >= 4) for (; Ns * 4 <= N; Ns *= 4) {
-    V v[BPT4][4];
-#pragma unroll
-    for (int i = 0; i < BPT4; ++i) {
-      const int b = tid + i * NT;
-      if (b < NB4) {
-        int q, j;
-        if (SEQ_FAST) { q = b % NSEQ; j = b / NSEQ; } else { j = b % (N / 4); q = b / (N / 4); }
-        const int k = j & (Ns - 1);
-        V* base = s + q * SEQ_STRIDE;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) v[i][r] = base[(j + r * (N / 4)) * ELEM_STRIDE];
-        if (Ns > 1) {
-          const int step = (MGB_TW_N / (4 * Ns)) * k;
-          v[i][1] = cmul(v[i][1], tw_lookup(step, inv, R()));
-          v[i][2] = cmul(v[i][2], tw_lookup(2 * step, inv, R()));
-          v[i][3] = cmul(v[i][3], tw_lookup(3 * step, inv, R()));
-        }
-        V a0 = cadd(v[i][0], v[i][2]), a1 = csub(v[i][0], v[i][2]);
-        V a2 = cadd(v[i][1], v[i][3]), a3 = csub(v[i][1], v[i][3]);
-        V a3r = inv ? cmul_pi(a3) : cmul_mi(a3);
-        v[i][0] = cadd(a0, a2);
-        v[i][2] = csub(a0, a2);
-        v[i][1] = cadd(a1, a3r);
-        v[i][3] = csub(a1, a3r);
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < BPT4; ++i) {
-      const int b = tid + i * NT;
-      if (b < NB4) {
-        int q, j;
-        if (SEQ_FAST) { q = b % NSEQ; j = b / NSEQ; } else { j = b % (N / 4); q = b / (N / 4); }
-        const int k = j & (Ns - 1);
-        const int d = (j / Ns) * (4 * Ns) + k;
-        V* base = s + q * SEQ_STRIDE;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) base[(d + r * Ns) * ELEM_STRIDE] = v[i][r];
-      }
-    }
-    __syncthreads();
-  }
-  // final radix-2 pass when log2(N) is odd
-  if (Ns < N) {
-    V v[BPT2][2];
-#pragma unroll
-    for (int i = 0; i < BPT2; ++i) {
-      const int b = tid + i * NT;
-      if (b < NB2) {
-        int q, j;
-        if (SEQ_FAST) { q = b % NSEQ; j = b / NSEQ; } else { j = b % (N / 2); q = b / (N / 2); }
-        const int k = j & (Ns - 1);
-        V* base = s + q * SEQ_STRIDE;
-        v[i][0] = base[j * ELEM_STRIDE];
-        v[i][1] = base[(j + N / 2) * ELEM_STRIDE];
-        if (Ns > 1) v[i][1] = cmul(v[i][1], tw_lookup((MGB_TW_N / (2 * Ns)) * k, inv, R()));
-        V t0 = cadd(v[i][0], v[i][1]), t1 = csub(v[i][0], v[i][1]);
-        v[i][0] = t0;
-        v[i][1] = t1;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < BPT2; ++i) {
-      const int b = tid + i * NT;
-      if (b < NB2) {
-        int q, j;
-        if (SEQ_FAST) { q = b % NSEQ; j = b / NSEQ; } else { j = b % (N / 2); q = b / (N / 2); }
-        const int k = j & (Ns - 1);
-        const int d = (j / Ns) * (2 * Ns) + k;
-        V* base = s + q * SEQ_STRIDE;
-        base[d * ELEM_STRIDE] = v[i][0];
-        base[(d + Ns) * ELEM_STRIDE] = v[i][1];
-      }
-    }
-    __syncthreads();
-  }
+  constexpr int NS0 = (REM == 1) ? 2 : (REM == 2 ? 4 : 1);
+  if constexpr (REM == 1) stockham_pass<R, 2, 1, N, NSEQ, NT, SEQ_STRIDE, ELEM_STRIDE, SEQ_FAST, PAD>(s, inv);
+  if constexpr (REM == 2) stockham_pass<R, 4, 1, N, NSEQ, NT, SEQ_STRIDE, ELEM_STRIDE, SEQ_FAST, PAD>(s, inv);
+  fft_passes8<R, NS0, N, NSEQ, NT, SEQ_STRIDE, ELEM_STRIDE, SEQ_FAST, PAD>(s, inv);
+}
+
+// ---------------------------------------------------------------------------
+// four-step twiddles w_N^e, N = 2^l (11 <= l <= 22): two-level tables
+#define MGB_FS_LMIN 11
+#define MGB_FS_LMAX 22
+extern __device__ float2 g_fs_lo[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
+extern __device__ float2 g_fs_hi[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
+
+template <int LOGN>
+__device__ __forceinline__ float2 fs_twiddle(int e, bool inv) {
+  static_assert(LOGN >= MGB_FS_LMIN && LOGN <= MGB_FS_LMAX, "four-step size");
+  const float2 a = g_fs_lo[LOGN - MGB_FS_LMIN][e & 2047];
+  const float2 b = g_fs_hi[LOGN - MGB_FS_LMIN][e >> 11];
+  float2 w = cmul(a, b);
+  if (inv) w.y = -w.y;
+  return w;
 }
 
 // ---------------------------------------------------------------------------

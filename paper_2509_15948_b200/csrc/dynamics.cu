@@ -5,110 +5,127 @@
 // 8192-tap FIR h[k] = (1-a) a^k, a = sigmoid(a_raw) taken from log space,
 // clamp g >= 0, G = log(g + 1e-8), knee branches, y = u * exp(G_y - G).
 //
-// Here the FIR is never materialised.  With y_iir[n] = a y_iir[n-1] + x[n]
-// (zero state before the signal), the truncated filter is exactly
+// The FIR is never materialised.  With y_iir[n] = a y_iir[n-1] + x[n] (zero
+// state before the signal) the truncated filter is exactly
 //     g[n] = (1-a) (y_iir[n] - a^8192 y_iir[n-8192]).
-// Time is cut into chunks of C = 8192 samples (= the truncation length) so
+// Time is cut into chunks of C = 8192 samples (= the truncation length), so
 // y_iir[n-8192] sits at the same local offset of the previous chunk: a CTA
-// scans chunk j-1 and chunk j together (carries from per-chunk aggregates),
-// and each thread pairs its own samples -- no cross-thread exchange.
-// All scan state is float64 (fp32 recursions lose 1e-4..1e-3
-// at long ballistics); signals are float32 in HBM.
+// scans chunk j-1 and chunk j together (chunk carries from per-chunk
+// aggregates) and every thread pairs its own samples.  Scan state is float64
+// (fp32 recursions lose 1e-4..1e-3 at long ballistics);
+// inputs x = mid^2, the envelope and the gain computer are float32.
 //
 // Backward: the adjoint of the truncated causal filter is the truncated
-// anti-causal filter, i.e. the same construction on reversed time:
-//     v[m] = a v[m+1] + dg[m],  w[m] = a (w[m+1] + v[m+1])   (2-state scan)
-//     dx[m] = (1-a)(v[m] - a^C v[m+C]),
-//     r[m]  = (1-a)(w[m] - a^C (w[m+C] + C v[m+C]))   = sum_k k h[k] dg[m+k]
-//     d a_raw = (1-a) sum x r - a sum x dx     (from dh[k]/da = h[k](k(1-a) - a)).
+// anti-causal filter — the same construction on reversed time with the
+// 2-state recursion  v[m] = a v[m+1] + dg[m],  w[m] = a (w[m+1] + v[m+1]):
+//     dx[m] = (1-a)(v[m] - a^C v[m+C])
+//     r[m]  = (1-a)(w[m] - a^C (w[m+C] + C v[m+C])) = sum_k k h[k] dg[m+k]
+//     d a_raw = (1-a) sum x r - a sum x dx   (dh[k]/da = h[k](k(1-a) - a)).
 #include "common.cuh"
 #include "mgb_internal.h"
 #include "tables.cuh"
 
 namespace {
 
-constexpr int NT = 256;
-constexpr int SEG = 32;
+constexpr int NT = 512;
+constexpr int SEG = 16;
 constexpr int CH = NT * SEG;  // 8192 == MGB_ENV_LEN
 static_assert(CH == MGB_ENV_LEN, "chunk = truncation length");
 constexpr int NW = NT / 32;
+constexpr int NPW = 14;  // pw[i] = a^(SEG * 2^i)
 
 struct DynP {
-  double la, lb, a, b, aC, T, W, R, Wraw, Rraw;
+  double la, a, b, aC;
+  float T, W, R;
+  double Wraw, Rraw;
 };
 
 __device__ __forceinline__ DynP load_params(const double* bank, int row) {
   const double* p = bank + (size_t)row * 4;
   DynP q;
   q.la = -softplus64(-p[0]);
-  q.lb = -softplus64(p[0]);
   q.a = exp(q.la);
-  q.b = exp(q.lb);
+  q.b = exp(-softplus64(p[0]));
   q.aC = exp((double)CH * q.la);
-  q.T = p[1];
+  q.T = (float)p[1];
   q.Wraw = p[2];
   q.Rraw = p[3];
-  q.W = softplus64(p[2]) + 1e-3;
-  q.R = softplus64(p[3]) + 1.0;
+  q.W = (float)(softplus64(p[2]) + 1e-3);
+  q.R = (float)(softplus64(p[3]) + 1.0);
   return q;
 }
 
-__device__ __forceinline__ double mid_sq(const float* u, int L, long long n) {
-  if (n < 0 || n >= L) return 0.0;
+__device__ __forceinline__ float mid_sq(const float* u, int L, long long n) {
+  if (n < 0 || n >= L) return 0.f;
   const double m = (double)u[n] + (double)u[L + n];
-  return m * m;
+  return (float)(m * m);
 }
 
-// gain-computer: returns G_y for envelope G (mg/processors.py:217-232)
-__device__ __forceinline__ double knee_gy(double G, const DynP& q, bool gate) {
+// a^(SEG * k) for 0 <= k < 2^NPW from the power table
+__device__ __forceinline__ double powseg(const double* pw, int k) {
+  double p = 1.0;
+#pragma unroll
+  for (int i = 0; i < 10; ++i)
+    if (k & (1 << i)) p *= pw[i];
+  return p;
+}
+
+// gain-computer G_y (mg/processors.py:217-232), float32
+__device__ __forceinline__ float knee_gy(float G, const DynP& q, bool gate) {
   const bool above = G >= q.T + q.W, below = G < q.T - q.W;
   if (gate) {
     if (above) return G;
     if (below) return q.T + q.R * (G - q.T);
-    const double z = G - q.T - q.W;
-    return G + (1.0 - q.R) * (z * z / (q.W * 4.0));
+    const float z = G - q.T - q.W;
+    return G + (1.f - q.R) * (z * z / (q.W * 4.f));
   }
   if (above) return q.T + (G - q.T) / q.R;
   if (below) return G;
-  const double z = G - q.T + q.W;
-  return G + (1.0 / q.R - 1.0) * (z * z / (q.W * 4.0));
+  const float z = G - q.T + q.W;
+  return G + (1.f / q.R - 1.f) * (z * z / (q.W * 4.f));
 }
 
-// forward inclusive scan of S_t = a^SEG S_{t-1} + v_t over the block's threads;
-// returns the state at the end of the PREVIOUS thread's segment (exclusive),
-// excluding any chunk carry.  pw[i] = a^(SEG * 2^i), i = 0..12.
-__device__ __forceinline__ double block_scan_excl(double v, const double* pw, double* sh) {
+__device__ __forceinline__ float env_log(float gc) { return logf(fmaxf(gc, 0.f) + 1e-8f); }
+
+// Two forward exclusive scans at once: S_t = a^SEG S_{t-1} + v_t over the
+// block's threads; returns the state at the end of thread t-1's segment.
+__device__ __forceinline__ void scan2_excl(double& v0, double& v1, const double* pw, double* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double s = v;
+  double s0 = v0, s1 = v1;
 #pragma unroll
   for (int o = 1, i = 0; o < 32; o <<= 1, ++i) {
-    const double t = __shfl_up_sync(0xffffffffu, s, o);
-    if (lane >= o) s = fma(pw[i], t, s);
+    const double t0 = __shfl_up_sync(0xffffffffu, s0, o);
+    const double t1 = __shfl_up_sync(0xffffffffu, s1, o);
+    if (lane >= o) {
+      s0 = fma(pw[i], t0, s0);
+      s1 = fma(pw[i], t1, s1);
+    }
   }
+  if (lane == 31) { sh[wid] = s0; sh[NW + wid] = s1; }
   __syncthreads();
-  if (lane == 31) sh[wid] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {  // exclusive over warps: carry into warp w = state at end of warp w-1
+  if (threadIdx.x < 2) {  // exclusive over warps (carry into warp w)
     double c = 0.0;
+    double* x = sh + threadIdx.x * NW;
     for (int w = 0; w < NW; ++w) {
-      const double tot = sh[w];
-      sh[w] = c;
-      c = fma(c, pw[5], tot);  // a^(SEG*32) = a^1024
+      const double tot = x[w];
+      x[w] = c;
+      c = fma(c, pw[5], tot);  // a^(SEG*32)
     }
   }
   __syncthreads();
-  double prev = __shfl_up_sync(0xffffffffu, s, 1);
-  if (lane == 0) prev = 0.0;
-  // warp carry propagated to the end of thread (lane-1): a^(SEG*lane) * carry
-  const double wc = sh[wid];
-  double p = 1.0;  // a^(SEG*lane)
-#pragma unroll
-  for (int i = 0; i < 5; ++i)
-    if (lane & (1 << i)) p *= pw[i];
-  return fma(wc, p, prev);
+  double p0 = __shfl_up_sync(0xffffffffu, s0, 1), p1 = __shfl_up_sync(0xffffffffu, s1, 1);
+  if (lane == 0) { p0 = 0.0; p1 = 0.0; }
+  const double pl = powseg(pw, lane);
+  v0 = fma(sh[wid], pl, p0);
+  v1 = fma(sh[NW + wid], pl, p1);
 }
 
-// chunk aggregates: agg[b][j] = sum_{n in chunk j} a^{end-n} x[n]   (no (1-a) factor)
+__device__ __forceinline__ void init_pw(double* pw, double la) {
+  if (threadIdx.x < NPW) pw[threadIdx.x] = exp((double)SEG * (double)(1 << threadIdx.x) * la);
+}
+
+// chunk aggregates: agg[b][j] = sum_{n in chunk j} a^{end-n} x[n]   (no (1-a) factor).
+// Coalesced: thread t visits offsets o = t + NT k; weights a^{CH-1-o} walk down by a^NT.
 __global__ void __launch_bounds__(NT) k_dyn_agg(const float* const* __restrict__ u_rows,
                                                 const double* __restrict__ bank, const int* __restrict__ prow,
                                                 double* __restrict__ agg, int L, int nch) {
@@ -116,76 +133,94 @@ __global__ void __launch_bounds__(NT) k_dyn_agg(const float* const* __restrict__
   const int j = blockIdx.x, b = blockIdx.y;
   const float* u = u_rows[b];
   const DynP q = load_params(bank, prow[b]);
-  const long long s0 = (long long)j * CH + threadIdx.x * SEG;
-  double v = 0.0;
-  for (int i = 0; i < SEG; ++i) v = fma(q.a, v, mid_sq(u, L, s0 + i));
-  const double f = exp((double)SEG * (NT - 1 - threadIdx.x) * q.la);
-  const double tot = block_sum(v * f, red);
+  const long long c0 = (long long)j * CH;
+  const double step = exp((double)NT * q.la);
+  double wgt = exp((double)(NT - 1 - threadIdx.x) * q.la);  // o = t + NT*(SEG-1)
+  double acc = 0.0;
+#pragma unroll
+  for (int k = SEG - 1; k >= 0; --k) {
+    acc = fma(wgt, (double)mid_sq(u, L, c0 + threadIdx.x + (long long)NT * k), acc);
+    wgt *= step;
+  }
+  const double tot = block_sum(acc, red);
   if (threadIdx.x == 0) agg[(size_t)b * nch + j] = tot;
 }
+
+// padded segment-major staging index: thread t's sample i of a chunk
+__device__ __forceinline__ int sidx(int t, int i) { return t * (SEG + 1) + i; }
+__device__ __forceinline__ int sidx_n(int o) { return sidx(o / SEG, o % SEG); }
+constexpr int SPAD = NT * (SEG + 1);
+constexpr int kDynSmem = 2 * SPAD * 4;
 
 __global__ void __launch_bounds__(NT) k_dyn_fwd(char tag, const float* const* __restrict__ u_rows,
                                                 const double* __restrict__ bank, const int* __restrict__ prow,
                                                 const int* __restrict__ widx, const double* __restrict__ w,
                                                 const double* __restrict__ agg, float* __restrict__ env,
                                                 float* __restrict__ y, int L, int nch) {
-  __shared__ double pw[14];
-  __shared__ double sh[NW];
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float* xs = reinterpret_cast<float*>(dsm);  // [2][SPAD]: prev chunk, cur chunk
+  __shared__ double pw[NPW];
+  __shared__ double sh[2 * NW];
   __shared__ double carry[2];
   const int j = blockIdx.x, b = blockIdx.y;
   const float* u = u_rows[b];
   const DynP q = load_params(bank, prow[b]);
   const bool gate = tag == 'n';
-  if (threadIdx.x < 14) pw[threadIdx.x] = exp((double)SEG * (double)(1 << threadIdx.x) * q.la);
-  if (threadIdx.x == 0) {
-    // y_iir at the end of chunk j-2 (prev carry) and j-1 (cur carry)
-    const double aC = q.aC;
+  init_pw(pw, q.la);
+  if (threadIdx.x == 32) {  // y_iir at the end of chunk j-2 (prev carry) and j-1 (cur carry)
     double c = 0.0, cprev = 0.0;
     for (int i = 0; i < j; ++i) {
       if (i == j - 1) cprev = c;
-      c = fma(c, aC, agg[(size_t)b * nch + i]);
+      c = fma(c, q.aC, agg[(size_t)b * nch + i]);
     }
     carry[0] = cprev;
     carry[1] = c;
   }
+  const long long c0 = (long long)j * CH;
+  for (int o = threadIdx.x; o < CH; o += NT) {  // coalesced staging of x = mid^2
+    xs[sidx_n(o)] = mid_sq(u, L, c0 - CH + o);
+    xs[SPAD + sidx_n(o)] = mid_sq(u, L, c0 + o);
+  }
   __syncthreads();
-  const long long base_c = (long long)j * CH + threadIdx.x * SEG;
-  const long long base_p = base_c - CH;
-  double xp[SEG];
+  const float* xp = xs + sidx(threadIdx.x, 0);
+  const float* xc = xs + SPAD + sidx(threadIdx.x, 0);
   double vp = 0.0, vc = 0.0;
 #pragma unroll
   for (int i = 0; i < SEG; ++i) {
-    xp[i] = mid_sq(u, L, base_p + i);
-    vp = fma(q.a, vp, xp[i]);
+    vp = fma(q.a, vp, (double)xp[i]);
+    vc = fma(q.a, vc, (double)xc[i]);
   }
-#pragma unroll 4
-  for (int i = 0; i < SEG; ++i) vc = fma(q.a, vc, mid_sq(u, L, base_c + i));
-  const double ep = block_scan_excl(vp, pw, sh);
-  const double ec = block_scan_excl(vc, pw, sh);
-  // chunk carry into this thread's segment start: carry * a^(SEG*t)
-  const double at = exp((double)SEG * threadIdx.x * q.la);
-  double yp = fma(carry[0], at, ep);
-  double yc = fma(carry[1], at, ec);
-  if (j == 0) yp = 0.0;
+  scan2_excl(vp, vc, pw, sh);
+  const double at = powseg(pw, threadIdx.x);
+  double yp = (j == 0) ? 0.0 : fma(carry[0], at, vp);
+  double yc = fma(carry[1], at, vc);
+  float gcs[SEG], gns[SEG];
+#pragma unroll
+  for (int i = 0; i < SEG; ++i) {
+    yp = fma(q.a, yp, (double)xp[i]);
+    yc = fma(q.a, yc, (double)xc[i]);
+    const float gc = (float)(q.b * (yc - q.aC * yp));
+    const float G = env_log(gc);
+    gcs[i] = gc;
+    gns[i] = expf(knee_gy(G, q, gate) - G);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < SEG; ++i) {
+    xs[sidx(threadIdx.x, i)] = gcs[i];
+    xs[SPAD + sidx(threadIdx.x, i)] = gns[i];
+  }
+  __syncthreads();
   const double wv = w ? w[widx[b]] : 1.0;
   const float wf = (float)wv, om = (float)(1.0 - wv);
   const bool bypass = wv == 0.0;
   float* yo = y + (size_t)b * 2 * L;
   float* eo = env + (size_t)b * L;
-#pragma unroll
-  for (int i = 0; i < SEG; ++i) {
-    yp = fma(q.a, yp, xp[i]);
-    xp[i] = yp;  // reuse as y_iir[n - C]
-  }
-#pragma unroll 2
-  for (int i = 0; i < SEG; ++i) {
-    const long long n = base_c + i;
-    yc = fma(q.a, yc, mid_sq(u, L, n));
-    if (n >= L) continue;
-    const double gc = q.b * (yc - q.aC * xp[i]);
-    eo[n] = (float)gc;
-    const double G = log(fmax(gc, 0.0) + MGB_ENV_EPS);
-    const float gain = expf((float)(knee_gy(G, q, gate) - G));
+  for (int o = threadIdx.x; o < CH; o += NT) {  // coalesced outputs
+    const long long n = c0 + o;
+    if (n >= L) break;
+    const float gain = xs[SPAD + sidx_n(o)];
+    eo[n] = xs[sidx_n(o)];
     const float l = u[n], r = u[L + n];
     if (bypass) { yo[n] = l; yo[L + n] = r; }
     else {
@@ -196,12 +231,12 @@ __global__ void __launch_bounds__(NT) k_dyn_fwd(char tag, const float* const* __
 }
 
 // backward part 1: elementwise chain down to dg (grad wrt the unclamped envelope)
-__global__ void __launch_bounds__(NT) k_dyn_bwd0(char tag, const float* const* __restrict__ u_rows,
-                                                 const float* const* __restrict__ gy_rows,
-                                                 const double* __restrict__ bank, const int* __restrict__ prow,
-                                                 const int* __restrict__ widx, const double* __restrict__ w,
-                                                 const float* __restrict__ env, float* __restrict__ dg,
-                                                 float* __restrict__ gu, double* __restrict__ part, int L) {
+__global__ void __launch_bounds__(256) k_dyn_bwd0(char tag, const float* const* __restrict__ u_rows,
+                                                  const float* const* __restrict__ gy_rows,
+                                                  const double* __restrict__ bank, const int* __restrict__ prow,
+                                                  const int* __restrict__ widx, const double* __restrict__ w,
+                                                  const float* __restrict__ env, float* __restrict__ dg,
+                                                  float* __restrict__ gu, double* __restrict__ part, int L) {
   __shared__ double red[32];
   const int b = blockIdx.y;
   const float* u = u_rows[b];
@@ -215,52 +250,64 @@ __global__ void __launch_bounds__(NT) k_dyn_bwd0(char tag, const float* const* _
   float* dgo = dg + (size_t)b * L;
   float* go = gu + (size_t)b * 2 * L;
   double sT = 0.0, sW = 0.0, sR = 0.0, sw = 0.0;
-  for (long long n = (long long)blockIdx.x * NT + threadIdx.x; n < L; n += (long long)gridDim.x * NT) {
+  float fT = 0.f, fW = 0.f, fR = 0.f, fw = 0.f;
+  int cnt = 0;
+  for (long long n = (long long)blockIdx.x * 256 + threadIdx.x; n < L; n += (long long)gridDim.x * 256) {
     const float l = u[n], r = u[L + n], gl = gy[n], gr = gy[L + n];
-    const double gc = eo[n];
-    const double gcl = fmax(gc, 0.0);
-    const double G = log(gcl + MGB_ENV_EPS);
+    const float gc = eo[n];
+    const float gcl = fmaxf(gc, 0.f);
+    const float G = logf(gcl + 1e-8f);
     const bool above = G >= q.T + q.W, below = G < q.T - q.W;
-    double Gy, dGu, dT = 0.0, dW = 0.0, dR = 0.0;
+    float Gy, dGu, dT = 0.f, dW = 0.f, dR = 0.f;
     if (gate) {
-      if (above) { Gy = G; dGu = 1.0; }
-      else if (below) { Gy = q.T + q.R * (G - q.T); dGu = q.R; dT = 1.0 - q.R; dR = G - q.T; }
+      if (above) { Gy = G; dGu = 1.f; }
+      else if (below) { Gy = q.T + q.R * (G - q.T); dGu = q.R; dT = 1.f - q.R; dR = G - q.T; }
       else {
-        const double z = G - q.T - q.W, k = 1.0 - q.R;
-        Gy = G + k * (z * z / (q.W * 4.0));
-        dGu = 1.0 + k * z / (2.0 * q.W);
-        dT = -k * z / (2.0 * q.W);
-        dW = k * (-z / (2.0 * q.W) - z * z / (4.0 * q.W * q.W));
-        dR = -z * z / (4.0 * q.W);
+        const float z = G - q.T - q.W, k = 1.f - q.R;
+        Gy = G + k * (z * z / (q.W * 4.f));
+        dGu = 1.f + k * z / (2.f * q.W);
+        dT = -k * z / (2.f * q.W);
+        dW = k * (-z / (2.f * q.W) - z * z / (4.f * q.W * q.W));
+        dR = -z * z / (4.f * q.W);
       }
     } else {
-      if (above) { Gy = q.T + (G - q.T) / q.R; dGu = 1.0 / q.R; dT = 1.0 - 1.0 / q.R; dR = -(G - q.T) / (q.R * q.R); }
-      else if (below) { Gy = G; dGu = 1.0; }
+      if (above) {
+        Gy = q.T + (G - q.T) / q.R;
+        dGu = 1.f / q.R;
+        dT = 1.f - 1.f / q.R;
+        dR = -(G - q.T) / (q.R * q.R);
+      } else if (below) { Gy = G; dGu = 1.f; }
       else {
-        const double z = G - q.T + q.W, k = 1.0 / q.R - 1.0;
-        Gy = G + k * (z * z / (q.W * 4.0));
-        dGu = 1.0 + k * z / (2.0 * q.W);
-        dT = -k * z / (2.0 * q.W);
-        dW = k * (z / (2.0 * q.W) - z * z / (4.0 * q.W * q.W));
-        dR = -z * z / (4.0 * q.W * q.R * q.R);
+        const float z = G - q.T + q.W, k = 1.f / q.R - 1.f;
+        Gy = G + k * (z * z / (q.W * 4.f));
+        dGu = 1.f + k * z / (2.f * q.W);
+        dT = -k * z / (2.f * q.W);
+        dW = k * (z / (2.f * q.W) - z * z / (4.f * q.W * q.W));
+        dR = -z * z / (4.f * q.W * q.R * q.R);
       }
     }
-    const float gain = expf((float)(Gy - G));
+    const float gain = expf(Gy - G);
     float dl, dr, ul, ur;
     if (bypass) { dl = dr = 0.f; ul = gl; ur = gr; }
     else {
       dl = wf * gl; dr = wf * gr; ul = om * gl; ur = om * gr;
-      sw += (double)gl * (double)(l * gain - l) + (double)gr * (double)(r * gain - r);
+      fw = fmaf(gl, l * gain - l, fmaf(gr, r * gain - r, fw));
     }
     go[n] = fmaf(dl, gain, ul);
     go[L + n] = fmaf(dr, gain, ur);
-    const double D = ((double)dl * l + (double)dr * r) * (double)gain;
-    sT += D * dT;
-    sW += D * dW;
-    sR += D * dR;
-    const double dG = D * dGu - D;
-    dgo[n] = (gc > 0.0) ? (float)(dG / (gcl + MGB_ENV_EPS)) : 0.f;
+    const float D = (dl * l + dr * r) * gain;
+    fT = fmaf(D, dT, fT);
+    fW = fmaf(D, dW, fW);
+    fR = fmaf(D, dR, fR);
+    const float dG = D * dGu - D;
+    dgo[n] = (gc > 0.f) ? dG / (gcl + 1e-8f) : 0.f;
+    if (++cnt == 8) {
+      sT += fT; sW += fW; sR += fR; sw += fw;
+      fT = fW = fR = fw = 0.f;
+      cnt = 0;
+    }
   }
+  sT += fT; sW += fW; sR += fR; sw += fw;
   sT = block_sum(sT, red);
   __syncthreads();
   sW = block_sum(sW, red);
@@ -283,13 +330,16 @@ struct VW {
 
 // state X entering from the right, propagated through len zero-input steps
 __device__ __forceinline__ VW prop(VW x, double alen, double len) {
-  VW r;
-  r.v = alen * x.v;
-  r.w = alen * fma(len, x.v, x.w);
-  return r;
+  return VW{alen * x.v, alen * fma(len, x.v, x.w)};
 }
 
-// reverse aggregates: state at the chunk start from the chunk's own dg only
+__device__ __forceinline__ void rstep(VW& s, double a, double x) {
+  s.w = a * (s.w + s.v);
+  s.v = fma(a, s.v, x);
+}
+
+// reverse aggregates: state at the chunk start from the chunk's own dg only:
+// v = sum_o a^o dg[start + o], w = sum_o o a^o dg[start + o]  (coalesced, o = t + NT k)
 __global__ void __launch_bounds__(NT) k_dyn_bagg(const double* __restrict__ bank, const int* __restrict__ prow,
                                                  const float* __restrict__ dg, double* __restrict__ bagg, int L,
                                                  int nch) {
@@ -297,67 +347,73 @@ __global__ void __launch_bounds__(NT) k_dyn_bagg(const double* __restrict__ bank
   const int j = blockIdx.x, b = blockIdx.y;
   const DynP q = load_params(bank, prow[b]);
   const float* d = dg + (size_t)b * L;
-  const long long s0 = (long long)j * CH + threadIdx.x * SEG;
-  VW s{0.0, 0.0};
-  for (int i = SEG - 1; i >= 0; --i) {
-    const long long m = s0 + i;
+  const long long c0 = (long long)j * CH;
+  const double step = exp((double)NT * q.la);
+  double wgt = exp((double)threadIdx.x * q.la);
+  double av = 0.0, aw = 0.0;
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) {
+    const int o = threadIdx.x + NT * k;
+    const long long m = c0 + o;
     const double x = (m < L) ? (double)d[m] : 0.0;
-    s.w = q.a * (s.w + s.v);
-    s.v = fma(q.a, s.v, x);
+    const double t = wgt * x;
+    av += t;
+    aw = fma((double)o, t, aw);
+    wgt *= step;
   }
-  // propagate this segment's start state to the chunk start: through SEG*t samples
-  const double len = (double)SEG * threadIdx.x;
-  const VW pr = prop(s, exp(len * q.la), len);
-  const double tv = block_sum(pr.v, red);
+  const double tv = block_sum(av, red);
   __syncthreads();
-  const double tw = block_sum(pr.w, red);
+  const double tw = block_sum(aw, red);
   if (threadIdx.x == 0) {
     bagg[((size_t)b * nch + j) * 2] = tv;
     bagg[((size_t)b * nch + j) * 2 + 1] = tw;
   }
 }
 
-// reverse exclusive scan over the block: state at the END of this thread's
-// segment (start of the next), from segments t+1.. of the chunk only.
-__device__ __forceinline__ VW block_rscan_excl(VW s, const double* pw, double* shv, double* shw) {
+// Two reverse exclusive scans at once (segments t+1.. of the chunk) of 2-state
+// values: returns the state at the END of this thread's segment.
+__device__ __forceinline__ void rscan2_excl(VW& a, VW& c, const double* pw, double* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  VW r = s;  // inclusive: segments [t, t+o) covered
+  VW ra = a, rc = c;
 #pragma unroll
   for (int o = 1, i = 0; o < 32; o <<= 1, ++i) {
-    const double tv = __shfl_down_sync(0xffffffffu, r.v, o);
-    const double tw = __shfl_down_sync(0xffffffffu, r.w, o);
+    const double av = __shfl_down_sync(0xffffffffu, ra.v, o), aw = __shfl_down_sync(0xffffffffu, ra.w, o);
+    const double cv = __shfl_down_sync(0xffffffffu, rc.v, o), cw = __shfl_down_sync(0xffffffffu, rc.w, o);
     if (lane + o < 32) {
-      const VW p = prop(VW{tv, tw}, pw[i], (double)SEG * o);
-      r.v += p.v;
-      r.w += p.w;
+      const double len = (double)SEG * o;
+      const VW pa = prop(VW{av, aw}, pw[i], len), pc = prop(VW{cv, cw}, pw[i], len);
+      ra.v += pa.v; ra.w += pa.w;
+      rc.v += pc.v; rc.w += pc.w;
     }
   }
+  if (lane == 0) {
+    sh[wid] = ra.v; sh[NW + wid] = ra.w;
+    sh[2 * NW + wid] = rc.v; sh[3 * NW + wid] = rc.w;
+  }
   __syncthreads();
-  if (lane == 0) { shv[wid] = r.v; shw[wid] = r.w; }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // state at the end of warp w from warps w+1..
-    VW c{0.0, 0.0};
+  if (threadIdx.x < 2) {  // state at the end of warp w from warps w+1..
+    double* xv = sh + threadIdx.x * 2 * NW;
+    double* xw = xv + NW;
+    VW cc{0.0, 0.0};
     for (int w = NW - 1; w >= 0; --w) {
-      const VW tot{shv[w], shw[w]};
-      shv[w] = c.v;
-      shw[w] = c.w;
-      const VW p = prop(c, pw[5], (double)SEG * 32);
-      c.v = tot.v + p.v;
-      c.w = tot.w + p.w;
+      const VW tot{xv[w], xw[w]};
+      xv[w] = cc.v;
+      xw[w] = cc.w;
+      const VW p = prop(cc, pw[5], (double)SEG * 32);
+      cc.v = tot.v + p.v;
+      cc.w = tot.w + p.w;
     }
   }
   __syncthreads();
-  double nv = __shfl_down_sync(0xffffffffu, r.v, 1);
-  double nw = __shfl_down_sync(0xffffffffu, r.w, 1);
-  if (lane == 31) { nv = 0.0; nw = 0.0; }
-  // warp carry enters after lane 31: propagate through segments lane+1..31
+  double nav = __shfl_down_sync(0xffffffffu, ra.v, 1), naw = __shfl_down_sync(0xffffffffu, ra.w, 1);
+  double ncv = __shfl_down_sync(0xffffffffu, rc.v, 1), ncw = __shfl_down_sync(0xffffffffu, rc.w, 1);
+  if (lane == 31) nav = naw = ncv = ncw = 0.0;
   const int k = 31 - lane;
-  double p = 1.0;
-#pragma unroll
-  for (int i = 0; i < 5; ++i)
-    if (k & (1 << i)) p *= pw[i];
-  const VW wc = prop(VW{shv[wid], shw[wid]}, p, (double)SEG * k);
-  return VW{nv + wc.v, nw + wc.w};
+  const double p = powseg(pw, k);
+  const VW wa = prop(VW{sh[wid], sh[NW + wid]}, p, (double)SEG * k);
+  const VW wc = prop(VW{sh[2 * NW + wid], sh[3 * NW + wid]}, p, (double)SEG * k);
+  a = VW{nav + wa.v, naw + wa.w};
+  c = VW{ncv + wc.v, ncw + wc.w};
 }
 
 __global__ void __launch_bounds__(NT) k_dyn_bwd1(const float* const* __restrict__ u_rows,
@@ -365,17 +421,18 @@ __global__ void __launch_bounds__(NT) k_dyn_bwd1(const float* const* __restrict_
                                                  const double* __restrict__ bagg, const float* __restrict__ dg,
                                                  float* __restrict__ gu, double* __restrict__ part, int L,
                                                  int nch) {
-  __shared__ double pw[14];
-  __shared__ double shv[NW], shw[NW];
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float* ds = reinterpret_cast<float*>(dsm);  // [2][SPAD]: cur chunk, next chunk
+  __shared__ double pw[NPW];
+  __shared__ double sh[4 * NW];
   __shared__ double carry[4];
   __shared__ double red[32];
   const int j = blockIdx.x, b = blockIdx.y;
   const float* u = u_rows[b];
   const DynP q = load_params(bank, prow[b]);
   const float* d = dg + (size_t)b * L;
-  if (threadIdx.x < 14) pw[threadIdx.x] = exp((double)SEG * (double)(1 << threadIdx.x) * q.la);
-  if (threadIdx.x == 0) {
-    // state at the start of chunk j+1 (cur carry) and j+2 (next carry)
+  init_pw(pw, q.la);
+  if (threadIdx.x == 32) {  // state at the start of chunk j+1 (cur carry) and j+2 (next carry)
     VW c{0.0, 0.0}, cnext{0.0, 0.0};
     for (int i = nch - 1; i > j; --i) {
       if (i == j + 1) cnext = c;
@@ -388,55 +445,54 @@ __global__ void __launch_bounds__(NT) k_dyn_bwd1(const float* const* __restrict_
     carry[2] = cnext.v;
     carry[3] = cnext.w;
   }
-  __syncthreads();
-  const long long base_c = (long long)j * CH + threadIdx.x * SEG;
-  const long long base_n = base_c + CH;
-  // local segment aggregates (zero state after segment end)
-  VW sc{0.0, 0.0}, sn{0.0, 0.0};
-  for (int i = SEG - 1; i >= 0; --i) {
-    const long long m = base_c + i, mn = base_n + i;
-    const double xc = (m < L) ? (double)d[m] : 0.0;
-    const double xn = (mn < L) ? (double)d[mn] : 0.0;
-    sc.w = q.a * (sc.w + sc.v);
-    sc.v = fma(q.a, sc.v, xc);
-    sn.w = q.a * (sn.w + sn.v);
-    sn.v = fma(q.a, sn.v, xn);
+  const long long c0 = (long long)j * CH;
+  for (int o = threadIdx.x; o < CH; o += NT) {
+    const long long m = c0 + o, mn = m + CH;
+    ds[sidx_n(o)] = (m < L) ? d[m] : 0.f;
+    ds[SPAD + sidx_n(o)] = (mn < L) ? d[mn] : 0.f;
   }
-  const VW ec = block_rscan_excl(sc, pw, shv, shw);
-  const VW en = block_rscan_excl(sn, pw, shv, shw);
-  // chunk carry enters after the last segment: propagate through segments t+1..NT-1
+  __syncthreads();
+  const float* dc = ds + sidx(threadIdx.x, 0);
+  const float* dn = ds + SPAD + sidx(threadIdx.x, 0);
+  VW sc{0.0, 0.0}, sn{0.0, 0.0};
+#pragma unroll
+  for (int i = SEG - 1; i >= 0; --i) {
+    rstep(sc, q.a, (double)dc[i]);
+    rstep(sn, q.a, (double)dn[i]);
+  }
+  rscan2_excl(sc, sn, pw, sh);
   const double len = (double)SEG * (NT - 1 - threadIdx.x);
-  const double alen = exp(len * q.la);
+  const double alen = powseg(pw, NT - 1 - threadIdx.x);
   const VW cc = prop(VW{carry[0], carry[1]}, alen, len);
   const VW cn = prop(VW{carry[2], carry[3]}, alen, len);
-  VW stc{ec.v + cc.v, ec.w + cc.w};
-  VW stn{en.v + cn.v, en.w + cn.w};
-  double nv[SEG], nw[SEG];
+  VW stc{sc.v + cc.v, sc.w + cc.w};
+  VW stn{sn.v + cn.v, sn.w + cn.w};
+  float dxs[SEG], rrs[SEG];
 #pragma unroll
   for (int i = SEG - 1; i >= 0; --i) {
-    const long long mn = base_n + i;
-    const double xn = (mn < L) ? (double)d[mn] : 0.0;
-    stn.w = q.a * (stn.w + stn.v);
-    stn.v = fma(q.a, stn.v, xn);
-    nv[i] = stn.v;
-    nw[i] = stn.w;
+    rstep(stc, q.a, (double)dc[i]);
+    rstep(stn, q.a, (double)dn[i]);
+    dxs[i] = (float)(q.b * (stc.v - q.aC * stn.v));
+    rrs[i] = (float)(q.b * (stc.w - q.aC * fma((double)CH, stn.v, stn.w)));
   }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < SEG; ++i) {
+    ds[sidx(threadIdx.x, i)] = dxs[i];
+    ds[SPAD + sidx(threadIdx.x, i)] = rrs[i];
+  }
+  __syncthreads();
   double sxd = 0.0, sxr = 0.0;
   float* go = gu + (size_t)b * 2 * L;
-#pragma unroll
-  for (int i = SEG - 1; i >= 0; --i) {
-    const long long m = base_c + i;
-    const double xc = (m < L) ? (double)d[m] : 0.0;
-    stc.w = q.a * (stc.w + stc.v);
-    stc.v = fma(q.a, stc.v, xc);
-    if (m >= L) continue;
-    const double dx = q.b * (stc.v - q.aC * nv[i]);
-    const double rr = q.b * (stc.w - q.aC * fma((double)CH, nv[i], nw[i]));
+  for (int o = threadIdx.x; o < CH; o += NT) {  // coalesced: dmid = 2 mid dx; sums for d a_raw
+    const long long m = c0 + o;
+    if (m >= L) break;
+    const float dx = ds[sidx_n(o)], rr = ds[SPAD + sidx_n(o)];
     const double mid = (double)u[m] + (double)u[L + m];
     const double x = mid * mid;
-    sxd = fma(x, dx, sxd);
-    sxr = fma(x, rr, sxr);
-    const float dm = (float)(2.0 * mid * dx);
+    sxd = fma(x, (double)dx, sxd);
+    sxr = fma(x, (double)rr, sxr);
+    const float dm = (float)(2.0 * mid * (double)dx);
     go[m] += dm;
     go[L + m] += dm;
   }
@@ -450,38 +506,40 @@ __global__ void __launch_bounds__(NT) k_dyn_bwd1(const float* const* __restrict_
   }
 }
 
-__global__ void k_dyn_final(const double* __restrict__ part, int nblk0, int nch, const double* __restrict__ bank,
+__global__ void k_dyn_final(const double* __restrict__ part0, int nblk0, int nch, const double* __restrict__ bank,
                             const int* __restrict__ prow, const int* __restrict__ widx, const double* __restrict__ w,
                             double* __restrict__ gbank, double* __restrict__ gw, const double* __restrict__ part1) {
+  __shared__ double red[32];
   const int b = blockIdx.x;
-  if (threadIdx.x) return;
-  const DynP q = load_params(bank, prow[b]);
-  double sT = 0, sW = 0, sR = 0, sw = 0, sxd = 0, sxr = 0;
-  for (int i = 0; i < nblk0; ++i) {
-    const double* pp = part + ((size_t)b * nblk0 + i) * 8;
-    sT += pp[0];
-    sW += pp[1];
-    sR += pp[2];
-    sw += pp[3];
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  for (int i = threadIdx.x; i < nblk0; i += blockDim.x) {
+    const double* pp = part0 + ((size_t)b * nblk0 + i) * 8;
+    s[0] += pp[0]; s[1] += pp[1]; s[2] += pp[2]; s[3] += pp[3];
   }
-  for (int i = 0; i < nch; ++i) {
+  for (int i = threadIdx.x; i < nch; i += blockDim.x) {
     const double* pp = part1 + ((size_t)b * nch + i) * 8;
-    sxd += pp[4];
-    sxr += pp[5];
+    s[4] += pp[4]; s[5] += pp[5];
   }
-  double* g = gbank + (size_t)prow[b] * 4;
-  g[0] = (1.0 - q.a) * sxr - q.a * sxd;
-  g[1] = sT;
-  g[2] = sW * expit64(q.Wraw);
-  g[3] = sR * expit64(q.Rraw);
-  const double wv = w ? w[widx[b]] : 1.0;
-  if (gw) gw[widx[b]] = (wv == 0.0) ? 0.0 : sw;
+  for (int k = 0; k < 6; ++k) {
+    s[k] = block_sum(s[k], red);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const DynP q = load_params(bank, prow[b]);
+    double* g = gbank + (size_t)prow[b] * 4;
+    g[0] = (1.0 - q.a) * s[5] - q.a * s[4];
+    g[1] = s[0];
+    g[2] = s[1] * expit64(q.Wraw);
+    g[3] = s[2] * expit64(q.Rraw);
+    const double wv = w ? w[widx[b]] : 1.0;
+    if (gw) gw[widx[b]] = (wv == 0.0) ? 0.0 : s[3];
+  }
 }
 
 int nchunks(int L) { return (L + CH - 1) / CH; }
 int bwd0_grid(int L) {
-  int n = (L + 4 * NT - 1) / (4 * NT);
-  return n < 1 ? 1 : (n > 256 ? 256 : n);
+  int n = (L + 4 * 256 - 1) / (4 * 256);
+  return n < 1 ? 1 : (n > 512 ? 512 : n);
 }
 
 struct DynWs {
@@ -489,38 +547,40 @@ struct DynWs {
   float* dg;
 };
 
-DynWs dcarve(int B, int L, void* base) {
-  MgbArena a{(char*)base, 0};
+template <class A>
+DynWs dcarve(A& a, int B, int L) {
   DynWs w;
   const int nch = nchunks(L);
-  w.agg = a.take<double>((size_t)B * nch);
-  w.bagg = a.take<double>((size_t)B * nch * 2);
-  w.part0 = a.take<double>((size_t)B * bwd0_grid(L) * 8);
-  w.part1 = a.take<double>((size_t)B * nch * 8);
-  w.dg = a.take<float>((size_t)B * L);
+  w.agg = a.template take<double>((size_t)B * nch);
+  w.bagg = a.template take<double>((size_t)B * nch * 2);
+  w.part0 = a.template take<double>((size_t)B * bwd0_grid(L) * 8);
+  w.part1 = a.template take<double>((size_t)B * nch * 8);
+  w.dg = a.template take<float>((size_t)B * L);
   return w;
 }
 
 }  // namespace
 
+int mgb_dyn_init() {
+  cudaFuncSetAttribute(k_dyn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+  cudaFuncSetAttribute(k_dyn_bwd1, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
 size_t mgb_dyn_workspace(char, int B, int L) {
   MgbArena a{nullptr, 0};
-  const int nch = nchunks(L);
-  a.take<double>((size_t)B * nch);
-  a.take<double>((size_t)B * nch * 2);
-  a.take<double>((size_t)B * bwd0_grid(L) * 8);
-  a.take<double>((size_t)B * nch * 8);
-  a.take<float>((size_t)B * L);
+  dcarve(a, B, L);
   return a.off;
 }
 
 int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st) {
   if (!lv->aux) return 1;
   const int B = lv->B, L = lv->L, nch = nchunks(L);
-  DynWs w = dcarve(B, L, lv->ws);
+  MgbArena a{(char*)lv->ws, 0};
+  DynWs w = dcarve(a, B, L);
   k_dyn_agg<<<dim3(nch, B), NT, 0, st>>>(lv->u_rows, lv->bank, lv->prow, w.agg, L, nch);
   MGB_CHECK_LAUNCH();
-  k_dyn_fwd<<<dim3(nch, B), NT, 0, st>>>(lv->tag, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w, w.agg,
+  k_dyn_fwd<<<dim3(nch, B), NT, kDynSmem, st>>>(lv->tag, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w, w.agg,
                                          lv->aux, lv->y, L, nch);
   MGB_CHECK_LAUNCH();
   return 0;
@@ -529,15 +589,17 @@ int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st) {
 int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st) {
   if (!lv->aux) return 1;
   const int B = lv->B, L = lv->L, nch = nchunks(L), g0 = bwd0_grid(L);
-  DynWs w = dcarve(B, L, lv->ws);
-  k_dyn_bwd0<<<dim3(g0, B), NT, 0, st>>>(lv->tag, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx, lv->w,
-                                         lv->aux, w.dg, lv->gu, w.part0, L);
+  MgbArena a{(char*)lv->ws, 0};
+  DynWs w = dcarve(a, B, L);
+  k_dyn_bwd0<<<dim3(g0, B), 256, 0, st>>>(lv->tag, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx, lv->w,
+                                          lv->aux, w.dg, lv->gu, w.part0, L);
   MGB_CHECK_LAUNCH();
   k_dyn_bagg<<<dim3(nch, B), NT, 0, st>>>(lv->bank, lv->prow, w.dg, w.bagg, L, nch);
   MGB_CHECK_LAUNCH();
-  k_dyn_bwd1<<<dim3(nch, B), NT, 0, st>>>(lv->u_rows, lv->bank, lv->prow, w.bagg, w.dg, lv->gu, w.part1, L, nch);
+  k_dyn_bwd1<<<dim3(nch, B), NT, kDynSmem, st>>>(lv->u_rows, lv->bank, lv->prow, w.bagg, w.dg, lv->gu, w.part1, L, nch);
   MGB_CHECK_LAUNCH();
-  k_dyn_final<<<B, 32, 0, st>>>(w.part0, g0, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank, lv->gw, w.part1);
+  k_dyn_final<<<B, 256, 0, st>>>(w.part0, g0, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank, lv->gw,
+                                 w.part1);
   MGB_CHECK_LAUNCH();
   return 0;
 }

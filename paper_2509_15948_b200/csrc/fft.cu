@@ -19,6 +19,21 @@
 
 __device__ float2 g_tw32[MGB_TW_N];
 __device__ double2 g_tw64[MGB_TW_N];
+__device__ float2 g_fs_lo[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
+__device__ float2 g_fs_hi[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
+
+__global__ void k_init_fs_twiddles() {
+  const int l = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long N = 1LL << (l + MGB_FS_LMIN);
+  if (j < 2048) {
+    double s, c;
+    sincospi(-2.0 * (double)j / (double)N, &s, &c);
+    g_fs_lo[l][j] = make_float2((float)c, (float)s);
+    const long long e = (2048LL * j) % N;
+    sincospi(-2.0 * (double)e / (double)N, &s, &c);
+    g_fs_hi[l][j] = make_float2((float)c, (float)s);
+  }
+}
 
 __global__ void k_init_twiddles() {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -33,6 +48,8 @@ __global__ void k_init_twiddles() {
 int mgb_init_device(cudaStream_t st) {
   k_init_twiddles<<<MGB_TW_N / 256, 256, 0, st>>>();
   MGB_CHECK_LAUNCH();
+  k_init_fs_twiddles<<<dim3(2048 / 256, MGB_FS_LMAX - MGB_FS_LMIN + 1), 256, 0, st>>>();
+  MGB_CHECK_LAUNCH();
   return 0;
 }
 
@@ -45,14 +62,15 @@ __global__ void __launch_bounds__(NT) k_fft_small(const float2* __restrict__ in,
   extern __shared__ __align__(16) unsigned char smraw[];
   float2* sm = reinterpret_cast<float2*>(smraw);
   const long long b0 = (long long)blockIdx.x * SEQ;
+  constexpr int P = padded_len<N>();
   for (int i = threadIdx.x; i < SEQ * N; i += NT) {
     const long long b = b0 + i / N;
-    sm[i] = (b < batch) ? in[b0 * N + i] : make_float2(0.f, 0.f);
+    sm[(i / N) * P + pidx<true>(i % N)] = (b < batch) ? in[b0 * N + i] : make_float2(0.f, 0.f);
   }
-  smem_fft<float, N, SEQ, NT, N, 1, false>(sm, inv);
+  smem_fft<float, N, SEQ, NT, P, 1, false, true>(sm, inv);
   for (int i = threadIdx.x; i < SEQ * N; i += NT) {
     const long long b = b0 + i / N;
-    if (b < batch) { float2 v = sm[i]; v.x *= scale; v.y *= scale; out[b0 * N + i] = v; }
+    if (b < batch) { float2 v = sm[(i / N) * P + pidx<true>(i % N)]; v.x *= scale; v.y *= scale; out[b0 * N + i] = v; }
   }
 }
 
@@ -83,20 +101,20 @@ template <int N1, int N2, int TR, int NT>
 __global__ void __launch_bounds__(NT) k_fft_row(const float2* __restrict__ in, float2* __restrict__ out, bool inv,
                                                 float scale) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  float2* sm = reinterpret_cast<float2*>(smraw);  // [TR][N2+1]
-  constexpr int P = N2 + 1;
+  float2* sm = reinterpret_cast<float2*>(smraw);  // [TR][padded N2]
+  constexpr int P = padded_len<N2>();
   const long long N = (long long)N1 * N2;
   const int r0 = blockIdx.x * TR;
   const float2* src = in + (long long)blockIdx.y * N;
   float2* dst = out + (long long)blockIdx.y * N;
   for (int i = threadIdx.x; i < TR * N2; i += NT) {
     const int n2 = i % N2, r = i / N2;
-    sm[r * P + n2] = src[(long long)(r0 + r) * N2 + n2];
+    sm[r * P + pidx<true>(n2)] = src[(long long)(r0 + r) * N2 + n2];
   }
-  smem_fft<float, N2, TR, NT, P, 1, false>(sm, inv);
+  smem_fft<float, N2, TR, NT, P, 1, false, true>(sm, inv);
   for (int i = threadIdx.x; i < TR * N2; i += NT) {
     const int r = i % TR, k2 = i / TR;
-    float2 v = sm[r * P + k2];
+    float2 v = sm[r * P + pidx<true>(k2)];
     v.x *= scale;
     v.y *= scale;
     dst[(long long)(r0 + r) + (long long)N1 * k2] = v;
@@ -105,7 +123,7 @@ __global__ void __launch_bounds__(NT) k_fft_row(const float2* __restrict__ in, f
 
 template <int N, int SEQ, int NT>
 static int launch_small(const float2* in, float2* out, int batch, bool inv, float scale, cudaStream_t st) {
-  const size_t smem = sizeof(float2) * SEQ * N;
+  const size_t smem = sizeof(float2) * SEQ * padded_len<N>();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fft_small<N, SEQ, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -123,7 +141,7 @@ static int launch_four_step(const float2* in, float2* out, float2* tmp, int batc
   constexpr int TR = (N2 >= 4096) ? 2 : (N2 >= 2048 ? 4 : 8);
   constexpr int NT = 256;
   const size_t smc = sizeof(float2) * TC * N1;
-  const size_t smr = sizeof(float2) * TR * (N2 + 1);
+  const size_t smr = sizeof(float2) * TR * padded_len<N2>();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fft_col<N1, N2, TC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);

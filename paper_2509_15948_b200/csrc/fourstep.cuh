@@ -27,7 +27,8 @@ struct Geo {
   static constexpr int TC = (N1 >= 1024) ? 8 : 16;  // columns per column-pass CTA
   static constexpr int NTC = 256;
   static constexpr int NTR = (N2 >= 2048) ? 512 : 256;
-  static constexpr int P = N2 + 1;                  // padded row pitch in the row kernel
+  static constexpr int P = padded_len<N2>();        // padded row pitch in the row kernel
+  static constexpr int LOG = __builtin_ctz(N1) + __builtin_ctz(N2);
   static constexpr long long N = (long long)N1 * N2;
 };
 
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTC) k_colA(Ld ld, float2* __rest
   float2* dst = A + (long long)b * N;
   for (int i = threadIdx.x; i < TC * N1; i += NT) {
     const int c = i % TC, k1 = i / TC;
-    dst[(long long)k1 * N2 + c0 + c] = cmul(sm[i], twiddle_exact((long long)k1 * (c0 + c), N, false, 0.f));
+    dst[(long long)k1 * N2 + c0 + c] = cmul(sm[i], fs_twiddle<Geo<N1, N2>::LOG>(k1 * (c0 + c), false));
   }
 }
 
@@ -118,14 +119,14 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTR) k_rowB_fwd(const float2* __r
   for (int i = threadIdx.x; i < 2 * N2; i += NT) {
     const int q = i / N2, k = i % N2;
     const int rr = row[q < nr ? q : 0];
-    s[q * P + k] = Ax[base + (long long)rr * N2 + k];
-    s[(2 + q) * P + k] = Ah[base + (long long)rr * N2 + k];
+    s[q * P + pidx<true>(k)] = Ax[base + (long long)rr * N2 + k];
+    s[(2 + q) * P + pidx<true>(k)] = Ah[base + (long long)rr * N2 + k];
   }
-  smem_fft<float, N2, 4, NT, P, 1, false>(s, false);
+  smem_fft<float, N2, 4, NT, P, 1, false, true>(s, false);
   for (int i = threadIdx.x; i < nr * N2; i += NT) {
     const int q = i / N2, k = i % N2;
-    X[base + (long long)row[q] * N2 + k] = s[q * P + k];
-    H[base + (long long)row[q] * N2 + k] = s[(2 + q) * P + k];
+    X[base + (long long)row[q] * N2 + k] = s[q * P + pidx<true>(k)];
+    H[base + (long long)row[q] * N2 + k] = s[(2 + q) * P + pidx<true>(k)];
   }
   constexpr int PER = (2 * N2 + NT - 1) / NT;
   float2 qv[PER];
@@ -138,8 +139,8 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTR) k_rowB_fwd(const float2* __r
       if (nr == 2) { qp = 1 - q; kp = N2 - 1 - k; }
       else { qp = 0; kp = (row[0] == 0) ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k); }
       float2 xl, xr, hl, hr;
-      split_pair(s[q * P + k], s[qp * P + kp], xl, xr);
-      split_pair(s[(2 + q) * P + k], s[(2 + qp) * P + kp], hl, hr);
+      split_pair(s[q * P + pidx<true>(k)], s[qp * P + pidx<true>(kp)], xl, xr);
+      split_pair(s[(2 + q) * P + pidx<true>(k)], s[(2 + qp) * P + pidx<true>(kp)], hl, hr);
       const float2 y1 = cmul(xl, hl), y2 = cmul(xr, hr);
       qv[j] = make_float2(y1.x - y2.y, y1.y + y2.x);
     }
@@ -148,13 +149,13 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTR) k_rowB_fwd(const float2* __r
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int i = threadIdx.x + j * NT;
-    if (i < nr * N2) s[(i / N2) * P + (i % N2)] = qv[j];
+    if (i < nr * N2) s[(i / N2) * P + pidx<true>(i % N2)] = qv[j];
   }
-  smem_fft<float, N2, 2, NT, P, 1, false>(s, true);
+  smem_fft<float, N2, 2, NT, P, 1, false, true>(s, true);
   for (int i = threadIdx.x; i < nr * N2; i += NT) {
     const int q = i / N2, n2 = i % N2;
-    const float2 w = twiddle_exact((long long)row[q] * n2, N, true, 0.f);
-    Bo[base + (long long)row[q] * N2 + n2] = cmul(s[q * P + n2], w);
+    const float2 w = fs_twiddle<Geo<N1, N2>::LOG>(row[q] * n2, true);
+    Bo[base + (long long)row[q] * N2 + n2] = cmul(s[q * P + pidx<true>(n2)], w);
   }
 }
 
@@ -175,9 +176,9 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTR) k_rowB_bwd(const float2* __r
   const long long base = (long long)b * N;
   for (int i = threadIdx.x; i < 2 * N2; i += NT) {
     const int q = i / N2, k = i % N2;
-    s[q * P + k] = Ag[base + (long long)row[q < nr ? q : 0] * N2 + k];
+    s[q * P + pidx<true>(k)] = Ag[base + (long long)row[q < nr ? q : 0] * N2 + k];
   }
-  smem_fft<float, N2, 2, NT, P, 1, false>(s, false);
+  smem_fft<float, N2, 2, NT, P, 1, false, true>(s, false);
   constexpr int PER = (2 * N2 + NT - 1) / NT;
   float2 gx[PER], gh[PER];
 #pragma unroll
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTR) k_rowB_bwd(const float2* __r
       else { qp = 0; kp = (row[0] == 0) ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k); }
       const long long ik = base + (long long)row[q] * N2 + k, ip = base + (long long)row[qp] * N2 + kp;
       float2 gl, gr, hl, hr, xl, xr;
-      split_pair(s[q * P + k], s[qp * P + kp], gl, gr);
+      split_pair(s[q * P + pidx<true>(k)], s[qp * P + pidx<true>(kp)], gl, gr);
       split_pair(H[ik], H[ip], hl, hr);
       split_pair(X[ik], X[ip], xl, xr);
       float2 y1 = cmulc(gl, hl), y2 = cmulc(gr, hr);
@@ -205,16 +206,16 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTR) k_rowB_bwd(const float2* __r
   for (int j = 0; j < PER; ++j) {
     const int i = threadIdx.x + j * NT;
     if (i < nr * N2) {
-      s[(i / N2) * P + (i % N2)] = gx[j];
-      s[(2 + i / N2) * P + (i % N2)] = gh[j];
+      s[(i / N2) * P + pidx<true>(i % N2)] = gx[j];
+      s[(2 + i / N2) * P + pidx<true>(i % N2)] = gh[j];
     }
   }
-  smem_fft<float, N2, 4, NT, P, 1, false>(s, true);
+  smem_fft<float, N2, 4, NT, P, 1, false, true>(s, true);
   for (int i = threadIdx.x; i < nr * N2; i += NT) {
     const int q = i / N2, n2 = i % N2;
-    const float2 w = twiddle_exact((long long)row[q] * n2, N, true, 0.f);
-    B1[base + (long long)row[q] * N2 + n2] = cmul(s[q * P + n2], w);
-    B2[base + (long long)row[q] * N2 + n2] = cmul(s[(2 + q) * P + n2], w);
+    const float2 w = fs_twiddle<Geo<N1, N2>::LOG>(row[q] * n2, true);
+    B1[base + (long long)row[q] * N2 + n2] = cmul(s[q * P + pidx<true>(n2)], w);
+    B2[base + (long long)row[q] * N2 + n2] = cmul(s[(2 + q) * P + pidx<true>(n2)], w);
   }
 }
 

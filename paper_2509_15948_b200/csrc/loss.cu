@@ -31,7 +31,7 @@ template <int N>
 struct LossCfg {
   static constexpr int NT = N >= 4096 ? 512 : 256;
   static constexpr int NB = N / 2 + 1;
-  static constexpr size_t SMEM = sizeof(double2) * N + 64;  // + slack for 4*NB doubles
+  static constexpr size_t SMEM = sizeof(double2) * padded_len<N>() + 64;  // padded FFT buffer
 };
 
 // load windowed frame f of (xl, xr) into s (complex double) and FFT it
@@ -42,14 +42,14 @@ __device__ __forceinline__ void load_fft(double2* s, const float* __restrict__ x
   for (int t = threadIdx.x; t < N; t += NT) {
     const long long idx = reflect_idx((long long)f * hop + t - N / 2, Ls);
     const double win = 0.5 - 0.5 * cospi(2.0 * t / (double)N);
-    s[t] = make_double2((double)xl[idx] * win, (double)xr[idx] * win);
+    s[pidx<true>(t)] = make_double2((double)xl[idx] * win, (double)xr[idx] * win);
   }
-  smem_fft<double, N, 1, NT, N, 1, false>(s, false);
+  smem_fft<double, N, 1, NT, N, 1, false, true>(s, false);
 }
 
 // per-bin group spectra from the packed spectrum
 __device__ __forceinline__ void groups_at(const double2* s, int n, int k, double2 X[4]) {
-  const double2 zk = s[k], zp = s[(n - k) & (n - 1)];
+  const double2 zk = s[pidx<true>(k)], zp = s[pidx<true>((n - k) & (n - 1))];
   const double2 a = make_double2(0.5 * (zk.x + zp.x), 0.5 * (zk.y - zp.y));
   const double2 d = make_double2(0.5 * (zk.x - zp.x), 0.5 * (zk.y + zp.y));
   const double2 b = make_double2(d.y, -d.x);
@@ -226,21 +226,22 @@ __global__ void __launch_bounds__(LossCfg<N>::NT) k_mr_bwd(MgbLossRes r, const d
     const int k = threadIdx.x + i * NT;
     if (k < NB) {
       if (k == 0 || k == N / 2) {
-        s[k] = make_double2(dl[i].x, dr[i].x);
+        s[pidx<true>(k)] = make_double2(dl[i].x, dr[i].x);
       } else {
         const double2 hl = make_double2(0.5 * dl[i].x, 0.5 * dl[i].y);
         const double2 hr = make_double2(0.5 * dr[i].x, 0.5 * dr[i].y);
-        s[k] = make_double2(hl.x - hr.y, hl.y + hr.x);            // hl + i hr
-        s[N - k] = make_double2(hl.x + hr.y, -hl.y + hr.x);       // conj(hl) + i conj(hr)
+        s[pidx<true>(k)] = make_double2(hl.x - hr.y, hl.y + hr.x);         // hl + i hr
+        s[pidx<true>(N - k)] = make_double2(hl.x + hr.y, -hl.y + hr.x);    // conj(hl) + i conj(hr)
       }
     }
   }
-  smem_fft<double, N, 1, NT, N, 1, false>(s, true);
+  smem_fft<double, N, 1, NT, N, 1, false, true>(s, true);
   float* gf = r.gframes + (size_t)f * 2 * N;
   for (int t = threadIdx.x; t < N; t += NT) {
     const double win = 0.5 - 0.5 * cospi(2.0 * t / (double)N);
-    gf[t] = (float)(s[t].x * win);
-    gf[N + t] = (float)(s[t].y * win);
+    const double2 v = s[pidx<true>(t)];
+    gf[t] = (float)(v.x * win);
+    gf[N + t] = (float)(v.y * win);
   }
 }
 

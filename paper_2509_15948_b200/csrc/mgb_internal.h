@@ -22,6 +22,7 @@ int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_conv_workspace(char tag, int B, int L);
 int mgb_conv_init();
 int mgb_loss_init();
+int mgb_dyn_init();
 int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st);
 int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_dyn_workspace(char tag, int B, int L);

@@ -52,7 +52,9 @@ def test_kernel_matches_reference_golden(dev, tag):
     loss.backward()
     assert normrel(ybar.detach().cpu().numpy(), gk[f"{tag}_ybar"]) < 2e-6
     if tag in "erd":
-        np.testing.assert_allclose(float(reg), float(gk[f"{tag}_reg"]), rtol=1e-5, atol=1e-7)
+        # reg = sum_b |log||ybar_mid|| - log||u_mid|||: near-identity rows make it a difference of
+        # nearly equal logs, so the fp32 bound is absolute on the log scale (~1e-6 per row)
+        np.testing.assert_allclose(float(reg.detach()), float(gk[f"{tag}_reg"]), rtol=1e-5, atol=2e-6)
     assert normrel(ut.grad.cpu().numpy(), gk[f"{tag}_gu"]) < 1e-4
     # gradient banks: norm-relative, excluding FFT-noise-level reference entries
     assert normrel(pt.grad.cpu().numpy(), gk[f"{tag}_gp"], floor=1e-6) < 1e-4

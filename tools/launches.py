@@ -1,0 +1,30 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list (last step of N eager steps)."""
+import collections
+import csv
+import re
+import sys
+
+path = sys.argv[1]
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+rows = list(csv.reader(open(path)))
+hdr, data = None, []
+for r in rows:
+    if "Kernel Name" in r:
+        hdr = r
+        continue
+    if hdr and len(r) == len(hdr):
+        data.append(dict(zip(hdr, r)))
+n = len(data) // steps
+step = data[-n:]
+scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}
+agg = collections.defaultdict(lambda: [0, 0.0])
+tot = 0.0
+for d in step:
+    name = re.sub(r"\(.*", "", d["Kernel Name"])[:70]
+    t = float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1e-6)
+    agg[name][0] += 1
+    agg[name][1] += t
+    tot += t
+print(f"launches in one step: {len(step)}, total {tot:.3f} ms (serialised, cold)")
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"{v[1]:8.3f} ms {100 * v[1] / tot:5.1f}%  x{v[0]:3d}  {k}")
