@@ -35,6 +35,7 @@ constexpr int kMaxParts = 1024;  // partial-sum slots per row
 constexpr double PI = 3.141592653589793238462643383279502884;
 
 #include "fir.cuh"
+#include "rev_fft.cuh"
 
 struct ConvGeom {
   int M, off, logN;
@@ -369,7 +370,8 @@ int mgb_conv_forward(const MgbLevel* lv, cudaStream_t st) {
   if (tag == 'e') {
     k_eq_fir<<<dim3((MGB_EQ_LEN + 31) / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.hbuf);
   } else if (tag == 'r') {
-    k_rev_frames<<<dim3(MGB_REV_FRAMES, B), MGB_REV_NFFT, 0, st>>>(lv->bank, lv->prow, w.aux);
+    k_rev_frames_fft<<<dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B), RV_NT, kRevFftSmem, st>>>(lv->bank, lv->prow,
+                                                                                              w.aux);
     MGB_CHECK_LAUNCH();
     k_rev_assemble<<<dim3((MGB_REV_LEN + NT - 1) / NT, B), NT, 0, st>>>(w.aux, w.hbuf);
   } else {
@@ -392,7 +394,8 @@ int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st) {
   if (tag == 'e') {
     k_eq_fir_bwd<<<dim3(MGB_EQ_BINS / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.ghbuf, g.M, lv->gbank);
   } else if (tag == 'r') {
-    k_rev_bwd_frames<<<dim3(MGB_REV_FRAMES, B), MGB_REV_NFFT, 0, st>>>(lv->bank, lv->prow, w.ghbuf, g.M, w.aux2);
+    k_rev_bwd_frames_fft<<<dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B), RV_NT, kRevFftSmem, st>>>(
+        lv->bank, lv->prow, w.ghbuf, g.M, w.aux2);
     MGB_CHECK_LAUNCH();
     k_rev_bwd_reduce<<<B, 256, 0, st>>>(w.aux2, lv->prow, lv->gbank);
   } else {

@@ -167,14 +167,19 @@ __global__ void __launch_bounds__(NT) k_dyn_fwd(char tag, const float* const* __
   const DynP q = load_params(bank, prow[b]);
   const bool gate = tag == 'n';
   init_pw(pw, q.la);
-  if (threadIdx.x == 32) {  // y_iir at the end of chunk j-2 (prev carry) and j-1 (cur carry)
+  if ((threadIdx.x >> 5) == 1) {  // warp 1: y_iir at the end of chunk j-2 (prev) and j-1 (cur)
     double c = 0.0, cprev = 0.0;
-    for (int i = 0; i < j; ++i) {
-      if (i == j - 1) cprev = c;
-      c = fma(c, q.aC, agg[(size_t)b * nch + i]);
+    for (int i = threadIdx.x - 32; i < j; i += 32) {
+      const double a = agg[(size_t)b * nch + i];
+      c = fma(exp((double)CH * (double)(j - 1 - i) * q.la), a, c);
+      if (i < j - 1) cprev = fma(exp((double)CH * (double)(j - 2 - i) * q.la), a, cprev);
     }
-    carry[0] = cprev;
-    carry[1] = c;
+    c = warp_sum(c);
+    cprev = warp_sum(cprev);
+    if (threadIdx.x == 32) {
+      carry[0] = cprev;
+      carry[1] = c;
+    }
   }
   const long long c0 = (long long)j * CH;
   for (int o = threadIdx.x; o < CH; o += NT) {  // coalesced staging of x = mid^2
@@ -432,18 +437,31 @@ __global__ void __launch_bounds__(NT) k_dyn_bwd1(const float* const* __restrict_
   const DynP q = load_params(bank, prow[b]);
   const float* d = dg + (size_t)b * L;
   init_pw(pw, q.la);
-  if (threadIdx.x == 32) {  // state at the start of chunk j+1 (cur carry) and j+2 (next carry)
-    VW c{0.0, 0.0}, cnext{0.0, 0.0};
-    for (int i = nch - 1; i > j; --i) {
-      if (i == j + 1) cnext = c;
-      const VW p = prop(c, q.aC, (double)CH);
-      c.v = bagg[((size_t)b * nch + i) * 2] + p.v;
-      c.w = bagg[((size_t)b * nch + i) * 2 + 1] + p.w;
+  if ((threadIdx.x >> 5) == 1) {  // warp 1: state at the start of chunk j+1 (cur) and j+2 (next)
+    VW c{0.0, 0.0}, cn{0.0, 0.0};
+    for (int i = j + 1 + (threadIdx.x - 32); i < nch; i += 32) {
+      const VW a{bagg[((size_t)b * nch + i) * 2], bagg[((size_t)b * nch + i) * 2 + 1]};
+      const double len = (double)CH * (double)(i - j - 1);
+      const VW p = prop(a, exp(len * q.la), len);
+      c.v += p.v;
+      c.w += p.w;
+      if (i > j + 1) {
+        const double l2 = len - (double)CH;
+        const VW p2 = prop(a, exp(l2 * q.la), l2);
+        cn.v += p2.v;
+        cn.w += p2.w;
+      }
     }
-    carry[0] = c.v;
-    carry[1] = c.w;
-    carry[2] = cnext.v;
-    carry[3] = cnext.w;
+    c.v = warp_sum(c.v);
+    c.w = warp_sum(c.w);
+    cn.v = warp_sum(cn.v);
+    cn.w = warp_sum(cn.w);
+    if (threadIdx.x == 32) {
+      carry[0] = c.v;
+      carry[1] = c.w;
+      carry[2] = cn.v;
+      carry[3] = cn.w;
+    }
   }
   const long long c0 = (long long)j * CH;
   for (int o = threadIdx.x; o < CH; o += NT) {

@@ -138,37 +138,41 @@ __global__ void __launch_bounds__(LossCfg<N>::NT) k_mr_fwd(MgbLossRes r, const f
 }
 
 // stats layout per (res, group): [tnorm, slog, sdiff2, dn]
+// one CTA per (resolution, group)
 __global__ void k_mr_finalize(MgbLoss L, int mode) {
   __shared__ double red[32];
-  __shared__ double tot;
-  if (threadIdx.x == 0) tot = 0.0;
+  const int ri = blockIdx.x >> 2, g = blockIdx.x & 3;
+  const MgbLossRes& r = L.res[ri];
+  double s0 = 0.0, s1 = 0.0;
+  for (int f = threadIdx.x; f < r.frames; f += blockDim.x) {
+    s0 += r.part[((size_t)f * 4 + g) * 3 + 0];
+    s1 += r.part[((size_t)f * 4 + g) * 3 + 1];
+  }
+  s0 = block_sum(s0, red);
   __syncthreads();
-  for (int ri = 0; ri < L.n_res; ++ri) {
-    const MgbLossRes& r = L.res[ri];
-    for (int g = 0; g < 4; ++g) {
-      double s0 = 0.0, s1 = 0.0;
-      for (int f = threadIdx.x; f < r.frames; f += blockDim.x) {
-        s0 += r.part[((size_t)f * 4 + g) * 3 + 0];
-        s1 += r.part[((size_t)f * 4 + g) * 3 + 1];
-      }
-      s0 = block_sum(s0, red);
-      __syncthreads();
-      s1 = block_sum(s1, red);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double* st = L.stats + ((size_t)ri * 4 + g) * 4;
-        if (mode == 0) {
-          st[0] = fmax(sqrt(s0), 1e-12);
-        } else {
-          st[1] = s0;
-          st[2] = s1;
-          st[3] = sqrt(s1);
-          tot += L.group_w[g] * (s0 / (double)r.frames + st[3] / st[0]);
-        }
-      }
+  s1 = block_sum(s1, red);
+  if (threadIdx.x == 0) {
+    double* st = L.stats + ((size_t)ri * 4 + g) * 4;
+    if (mode == 0) {
+      st[0] = fmax(sqrt(s0), 1e-12);
+    } else {
+      st[1] = s0;
+      st[2] = s1;
+      st[3] = sqrt(s1);
     }
   }
-  if (threadIdx.x == 0 && mode == 1) *L.loss = tot;
+}
+
+// L_a = sum over (res, group) of w_g (slog / frames + dn / tnorm), in a fixed order
+__global__ void k_mr_total(MgbLoss L) {
+  if (threadIdx.x) return;
+  double tot = 0.0;
+  for (int ri = 0; ri < L.n_res; ++ri)
+    for (int g = 0; g < 4; ++g) {
+      const double* st = L.stats + ((size_t)ri * 4 + g) * 4;
+      tot += L.group_w[g] * (st[1] / (double)L.res[ri].frames + st[3] / st[0]);
+    }
+  *L.loss = tot;
 }
 
 template <int N>
@@ -352,7 +356,7 @@ extern "C" int mgb_mrstft_target(const MgbLoss* L, const float* tl, const float*
   cudaStream_t st = (cudaStream_t)stream;
   for (int i = 0; i < L->n_res; ++i)
     if (int rc = dispatch_fwd(L->res[i], tl, tr, L->Ls, 0, st)) return rc;
-  k_mr_finalize<<<1, 256, 0, st>>>(*L, 0);
+  k_mr_finalize<<<4 * L->n_res, 256, 0, st>>>(*L, 0);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -362,7 +366,9 @@ extern "C" int mgb_mrstft_forward(const MgbLoss* L, const float* yl, const float
   cudaStream_t st = (cudaStream_t)stream;
   for (int i = 0; i < L->n_res; ++i)
     if (int rc = dispatch_fwd(L->res[i], yl, yr, L->Ls, 1, st)) return rc;
-  k_mr_finalize<<<1, 256, 0, st>>>(*L, 1);
+  k_mr_finalize<<<4 * L->n_res, 256, 0, st>>>(*L, 1);
+  MGB_CHECK_LAUNCH();
+  k_mr_total<<<1, 32, 0, st>>>(*L);
   MGB_CHECK_LAUNCH();
   return 0;
 }

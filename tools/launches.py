@@ -28,3 +28,10 @@ for d in step:
 print(f"launches in one step: {len(step)}, total {tot:.3f} ms (serialised, cold)")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     print(f"{v[1]:8.3f} ms {100 * v[1] / tot:5.1f}%  x{v[0]:3d}  {k}")
+
+if len(sys.argv) > 3 and sys.argv[3] == "seq":
+    print("--- launch sequence of the last step")
+    for d in step:
+        name = re.sub(r"\(.*", "", d["Kernel Name"])[:60]
+        t = float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1e-6)
+        print(f"{1000 * t:9.1f} us  grid={d.get('Grid Size', '?'):>16}  {name}")
