@@ -47,7 +47,7 @@ ConvGeom geom(char tag, int L) {
   g.M = tag == 'e' ? MGB_EQ_LEN : (tag == 'r' ? MGB_REV_LEN : MGB_DLY_FIR);
   g.off = tag == 'e' ? (MGB_EQ_LEN - 1) / 2 : (tag == 'r' ? 0 : (MGB_COLOR_LEN - 1) / 2);
   g.logN = mgb_log2_ceil((long long)L + g.M - 1);
-  if (g.logN < 11) g.logN = 11;
+  if (g.logN < 12) g.logN = 12;
   g.N = 1LL << g.logN;
   return g;
 }
@@ -91,31 +91,53 @@ ConvWs carve_into(A& a, char tag, int B, int L) {
 // ---------------------------------------------------------------------------
 // loaders (column pass inputs) and epilogues (column pass outputs)
 
+struct NoCtx {};
+
 struct LdRows {
   static constexpr bool kAccum = false;
+  typedef NoCtx Ctx;
+  typedef float2 Raw;
   const float* const* rows;
   int L;
-  __device__ __forceinline__ float2 load(int b, long long n, float&) const {
-    if (n >= L) return make_float2(0.f, 0.f);
+  __device__ __forceinline__ Ctx prepare(int) const { return Ctx{}; }
+  __device__ __forceinline__ Raw fetch(const Ctx&, int b, long long n, bool ok) const {
+    if (!ok || n >= L) return make_float2(0.f, 0.f);
     const float* u = rows[b];
-    return make_float2(u[n], u[L + n]);
+    return make_float2(__ldg(u + n), __ldg(u + L + n));
   }
+  __device__ __forceinline__ float2 finish(const Ctx&, int, long long, const Raw& r, float&) const { return r; }
   __device__ __forceinline__ void commit(int, int, double) const {}
 };
 
 struct LdFir {
   static constexpr bool kAccum = false;
+  typedef NoCtx Ctx;
+  typedef float2 Raw;
   const float2* h;
   int M;
-  __device__ __forceinline__ float2 load(int b, long long n, float&) const {
-    return n < M ? h[(size_t)b * M + n] : make_float2(0.f, 0.f);
+  __device__ __forceinline__ Ctx prepare(int) const { return Ctx{}; }
+  __device__ __forceinline__ Raw fetch(const Ctx&, int b, long long n, bool ok) const {
+    return (ok && n < M) ? __ldg(h + (size_t)b * M + n) : make_float2(0.f, 0.f);
   }
+  __device__ __forceinline__ float2 finish(const Ctx&, int, long long, const Raw& r, float&) const { return r; }
   __device__ __forceinline__ void commit(int, int, double) const {}
 };
 
 // Backward prologue (dry/wet + gain-staging adjoints) as the G loader.
 struct LdBwdPro {
   static constexpr bool kAccum = true;
+  struct Ctx {
+    const float* u;
+    const float* gy;
+    const float* yb;
+    float* go;
+    float wf, om, cy, cu;
+    bool bypass;
+  };
+  struct Raw {
+    float l, r, gl, gr, yl, yr;
+    bool in;
+  };
   const float* const* u_rows;
   const float* const* gy_rows;
   const float* ybar;
@@ -126,43 +148,69 @@ struct LdBwdPro {
   float* gu;
   double* part;
   int L, off;
-  __device__ __forceinline__ float2 load(int b, long long n, float& acc) const {
-    const long long m = n - off;
-    if (m < 0 || m >= L) return make_float2(0.f, 0.f);
+  __device__ __forceinline__ Ctx prepare(int b) const {
+    Ctx c;
     const double wv = w ? w[widx[b]] : 1.0;
     const double sg = stats[b * 4 + 2] * (greg ? *greg : 0.0);
     const double nu = stats[b * 4], ny = stats[b * 4 + 1];
-    const float cy = (ny > 0.0) ? (float)(sg / ((ny + MGB_GS_EPS) * ny)) : 0.f;
-    const float cu = (nu > 0.0) ? (float)(-sg / ((nu + MGB_GS_EPS) * nu)) : 0.f;
-    const float* u = u_rows[b];
-    const float* gy = gy_rows[b];
-    const float* yb = ybar + (size_t)b * 2 * L;
-    const float l = u[m], r = u[L + m], gl = gy[m], gr = gy[L + m];
-    const float yl = yb[m], yr = yb[L + m];
-    const float my = yl + yr, mu = l + r;
-    float dl, dr, ul, ur;
-    if (wv == 0.0) {
-      dl = dr = 0.f;
-      ul = gl;
-      ur = gr;
-    } else {
-      const float wf = (float)wv, om = (float)(1.0 - wv);
-      dl = wf * gl;
-      dr = wf * gr;
-      ul = om * gl;
-      ur = om * gr;
-      acc = fmaf(gl, yl - l, fmaf(gr, yr - r, acc));
+    c.cy = (ny > 0.0) ? (float)(sg / ((ny + MGB_GS_EPS) * ny)) : 0.f;
+    c.cu = (nu > 0.0) ? (float)(-sg / ((nu + MGB_GS_EPS) * nu)) : 0.f;
+    c.bypass = (wv == 0.0);
+    c.wf = (float)wv;
+    c.om = (float)(1.0 - wv);
+    c.u = u_rows[b];
+    c.gy = gy_rows[b];
+    c.yb = ybar + (size_t)b * 2 * L;
+    c.go = gu + (size_t)b * 2 * L;
+    return c;
+  }
+  __device__ __forceinline__ Raw fetch(const Ctx& c, int, long long n, bool ok) const {
+    Raw r;
+    const long long m = n - off;
+    r.in = ok && m >= 0 && m < L;
+    if (r.in) {
+      r.l = __ldg(c.u + m);
+      r.r = __ldg(c.u + L + m);
+      r.gl = __ldg(c.gy + m);
+      r.gr = __ldg(c.gy + L + m);
+      r.yl = __ldg(c.yb + m);
+      r.yr = __ldg(c.yb + L + m);
     }
-    float* go = gu + (size_t)b * 2 * L;
-    go[m] = fmaf(cu, mu, ul);
-    go[L + m] = fmaf(cu, mu, ur);
-    return make_float2(fmaf(cy, my, dl), fmaf(cy, my, dr));
+    return r;
+  }
+  __device__ __forceinline__ float2 finish(const Ctx& c, int, long long n, const Raw& r, float& acc) const {
+    if (!r.in) return make_float2(0.f, 0.f);
+    const long long m = n - off;
+    const float my = r.yl + r.yr, mu = r.l + r.r;
+    float dl, dr, ul, ur;
+    if (c.bypass) {
+      dl = dr = 0.f;
+      ul = r.gl;
+      ur = r.gr;
+    } else {
+      dl = c.wf * r.gl;
+      dr = c.wf * r.gr;
+      ul = c.om * r.gl;
+      ur = c.om * r.gr;
+      acc = fmaf(r.gl, r.yl - r.l, fmaf(r.gr, r.yr - r.r, acc));
+    }
+    c.go[m] = fmaf(c.cu, mu, ul);
+    c.go[L + m] = fmaf(c.cu, mu, ur);
+    return make_float2(fmaf(c.cy, my, dl), fmaf(c.cy, my, dr));
   }
   __device__ __forceinline__ void commit(int b, int blk, double t) const { part[((size_t)b * kMaxParts + blk) * 4 + 2] = t; }
 };
 
 struct EpFwd {
   static constexpr bool kAccum = true;
+  struct Ctx {
+    const float* u;
+    float* yo;
+    float* yb;
+    float wf, om;
+    bool bypass;
+  };
+  typedef float2 Raw;
   const float* const* u_rows;
   const int* widx;
   const double* w;
@@ -170,25 +218,36 @@ struct EpFwd {
   float* ybar;
   double* part;
   int L, off;
-  __device__ __forceinline__ void store(int b, long long n, float2 v, float& a0, float& a1) const {
+  __device__ __forceinline__ Ctx prepare(int b) const {
+    Ctx c;
+    const double wv = w ? w[widx[b]] : 1.0;
+    c.bypass = (wv == 0.0);
+    c.wf = (float)wv;
+    c.om = (float)(1.0 - wv);
+    c.u = u_rows[b];
+    c.yo = y + (size_t)b * 2 * L;
+    c.yb = ybar + (size_t)b * 2 * L;
+    return c;
+  }
+  __device__ __forceinline__ Raw fetch(const Ctx& c, int, long long n, bool ok) const {
+    const long long m = n - off;
+    if (!ok || m < 0 || m >= L) return make_float2(0.f, 0.f);
+    return make_float2(__ldg(c.u + m), __ldg(c.u + L + m));
+  }
+  __device__ __forceinline__ void finish(const Ctx& c, int, long long n, float2 v, const Raw& u, float& a0,
+                                         float& a1) const {
     const long long m = n - off;
     if (m < 0 || m >= L) return;
-    const float* u = u_rows[b];
-    const float l = u[m], r = u[L + m];
-    float* yb = ybar + (size_t)b * 2 * L;
-    float* yo = y + (size_t)b * 2 * L;
-    yb[m] = v.x;
-    yb[L + m] = v.y;
-    const double wv = w ? w[widx[b]] : 1.0;
-    if (wv == 0.0) {
-      yo[m] = l;
-      yo[L + m] = r;
+    c.yb[m] = v.x;
+    c.yb[L + m] = v.y;
+    if (c.bypass) {
+      c.yo[m] = u.x;
+      c.yo[L + m] = u.y;
     } else {
-      const float wf = (float)wv, om = (float)(1.0 - wv);
-      yo[m] = wf * v.x + om * l;
-      yo[L + m] = wf * v.y + om * r;
+      c.yo[m] = c.wf * v.x + c.om * u.x;
+      c.yo[L + m] = c.wf * v.y + c.om * u.y;
     }
-    const float mu = l + r, my = v.x + v.y;
+    const float mu = u.x + u.y, my = v.x + v.y;
     a0 = fmaf(mu, mu, a0);
     a1 = fmaf(my, my, a1);
   }
@@ -201,22 +260,36 @@ struct EpFwd {
 
 struct EpGx {
   static constexpr bool kAccum = false;
+  typedef NoCtx Ctx;
+  typedef float2 Raw;
   float* gu;
   int L;
-  __device__ __forceinline__ void store(int b, long long n, float2 v, float&, float&) const {
+  __device__ __forceinline__ Ctx prepare(int) const { return Ctx{}; }
+  __device__ __forceinline__ Raw fetch(const Ctx&, int b, long long n, bool ok) const {
+    if (!ok || n >= L) return make_float2(0.f, 0.f);
+    const float* go = gu + (size_t)b * 2 * L;
+    return make_float2(go[n], go[L + n]);
+  }
+  __device__ __forceinline__ void finish(const Ctx&, int b, long long n, float2 v, const Raw& g, float&,
+                                         float&) const {
     if (n >= L) return;
     float* go = gu + (size_t)b * 2 * L;
-    go[n] += v.x;
-    go[L + n] += v.y;
+    go[n] = g.x + v.x;
+    go[L + n] = g.y + v.y;
   }
   __device__ __forceinline__ void commit(int, int, double, double) const {}
 };
 
 struct EpGh {
   static constexpr bool kAccum = false;
+  typedef NoCtx Ctx;
+  typedef int Raw;
   float2* gh;
   int M;
-  __device__ __forceinline__ void store(int b, long long n, float2 v, float&, float&) const {
+  __device__ __forceinline__ Ctx prepare(int) const { return Ctx{}; }
+  __device__ __forceinline__ Raw fetch(const Ctx&, int, long long, bool) const { return 0; }
+  __device__ __forceinline__ void finish(const Ctx&, int b, long long n, float2 v, const Raw&, float&,
+                                         float&) const {
     if (n < M) gh[(size_t)b * M + n] = v;
   }
   __device__ __forceinline__ void commit(int, int, double, double) const {}
@@ -275,7 +348,8 @@ struct Conv {
     cudaFuncSetAttribute(fs::k_colC<N1, N2, EpGx>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
     cudaFuncSetAttribute(fs::k_colC<N1, N2, EpGh>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
     cudaFuncSetAttribute(fs::k_rowB_fwd<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sr);
-    cudaFuncSetAttribute(fs::k_rowB_bwd<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sr);
+    cudaFuncSetAttribute(fs::k_rowB_bwd<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fs::rowbwd_smem<N1, N2>());
   }
 
   static int fwd(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
@@ -308,7 +382,7 @@ struct Conv {
     MGB_CHECK_LAUNCH();
     k_dw_finalize<<<B, 256, 0, st>>>(w.part, N2 / G::TC, lv->widx, lv->w, lv->gw);
     MGB_CHECK_LAUNCH();
-    fs::k_rowB_bwd<N1, N2><<<gr, G::NTR, sr, st>>>(w.Ax, w.X, w.H, w.Bo, w.Ah);
+    fs::k_rowB_bwd<N1, N2><<<gr, G::NTR, fs::rowbwd_smem<N1, N2>(), st>>>(w.Ax, w.X, w.H, w.Bo, w.Ah);
     MGB_CHECK_LAUNCH();
     fs::k_colC<N1, N2><<<gc, G::NTC, sc, st>>>(w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1);
     MGB_CHECK_LAUNCH();
@@ -321,7 +395,7 @@ struct Conv {
 };
 
 #define MGB_CONV_SIZES(X) \
-  X(11, 2, 1024) X(12, 4, 1024) X(13, 8, 1024) X(14, 16, 1024) X(15, 32, 1024) X(16, 64, 1024) \
+  X(12, 4, 1024) X(13, 8, 1024) X(14, 16, 1024) X(15, 32, 1024) X(16, 64, 1024) \
   X(17, 128, 1024) X(18, 256, 1024) X(19, 512, 1024) X(20, 1024, 1024) X(21, 1024, 2048) X(22, 1024, 4096)
 
 int conv_fwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {

@@ -151,6 +151,76 @@ __device__ __forceinline__ int sidx(int t, int i) { return t * (SEG + 1) + i; }
 __device__ __forceinline__ int sidx_n(int o) { return sidx(o / SEG, o % SEG); }
 constexpr int SPAD = NT * (SEG + 1);
 constexpr int kDynSmem = 2 * SPAD * 4;
+constexpr int Q4 = CH / (4 * NT);  // float4 groups per thread per chunk
+
+// 16-byte vector access is used when both channel rows are 16-byte aligned
+__device__ __forceinline__ bool vec_ok(const void* p, int L) {
+  return (L & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
+// samples n..n+3 of both channels of a (2, L) row, zeros outside [0, L)
+__device__ __forceinline__ void load4(const float* u, int L, long long n, bool vec, float4& l, float4& r) {
+  if (vec) {
+    if (n >= 0 && n < L) {
+      l = __ldg(reinterpret_cast<const float4*>(u + n));
+      r = __ldg(reinterpret_cast<const float4*>(u + L + n));
+    } else {
+      l = r = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return;
+  }
+  float a[4], c[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const bool in = n + e >= 0 && n + e < L;
+    a[e] = in ? u[n + e] : 0.f;
+    c[e] = in ? u[L + n + e] : 0.f;
+  }
+  l = make_float4(a[0], a[1], a[2], a[3]);
+  r = make_float4(c[0], c[1], c[2], c[3]);
+}
+
+__device__ __forceinline__ float msq(float l, float r) {
+  const double m = (double)l + (double)r;
+  return (float)(m * m);
+}
+
+__device__ __forceinline__ void stage_msq(float* dst, float4 l, float4 r) {
+  dst[0] = msq(l.x, r.x);
+  dst[1] = msq(l.y, r.y);
+  dst[2] = msq(l.z, r.z);
+  dst[3] = msq(l.w, r.w);
+}
+
+// y rows (2 channels) and one mono row at samples n..n+3 (bounds-checked when !vec)
+__device__ __forceinline__ void store4(float* yo, int L, long long n, bool vec, float4 yl, float4 yr, float* mono,
+                                       float4 m) {
+  if (vec) {
+    if (n < L) {
+      *reinterpret_cast<float4*>(yo + n) = yl;
+      *reinterpret_cast<float4*>(yo + L + n) = yr;
+      if (mono) *reinterpret_cast<float4*>(mono + n) = m;
+    }
+    return;
+  }
+  const float a[4] = {yl.x, yl.y, yl.z, yl.w}, c[4] = {yr.x, yr.y, yr.z, yr.w}, d[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (n + e < L) {
+      yo[n + e] = a[e];
+      yo[L + n + e] = c[e];
+      if (mono) mono[n + e] = d[e];
+    }
+}
+
+// samples n..n+3 of a mono row, zeros outside [0, L)
+__device__ __forceinline__ float4 load4m(const float* d, int L, long long n, bool vec) {
+  if (vec) return (n >= 0 && n < L) ? __ldg(reinterpret_cast<const float4*>(d + n)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float a[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) a[e] = (n + e >= 0 && n + e < L) ? d[n + e] : 0.f;
+  return make_float4(a[0], a[1], a[2], a[3]);
+}
 
 __global__ void __launch_bounds__(NT) k_dyn_fwd(char tag, const float* const* __restrict__ u_rows,
                                                 const double* __restrict__ bank, const int* __restrict__ prow,
@@ -182,9 +252,21 @@ __global__ void __launch_bounds__(NT) k_dyn_fwd(char tag, const float* const* __
     }
   }
   const long long c0 = (long long)j * CH;
-  for (int o = threadIdx.x; o < CH; o += NT) {  // coalesced staging of x = mid^2
-    xs[sidx_n(o)] = mid_sq(u, L, c0 - CH + o);
-    xs[SPAD + sidx_n(o)] = mid_sq(u, L, c0 + o);
+  const bool vec = vec_ok(u, L);
+  {  // coalesced staging of x = mid^2: all 16 float4 loads of a thread in flight at once
+    float4 pl[Q4], pr[Q4], cl[Q4], cr[Q4];
+#pragma unroll
+    for (int k = 0; k < Q4; ++k) {
+      const int o = 4 * (threadIdx.x + NT * k);
+      load4(u, L, c0 - CH + o, vec, pl[k], pr[k]);
+      load4(u, L, c0 + o, vec, cl[k], cr[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < Q4; ++k) {
+      const int o = 4 * (threadIdx.x + NT * k);
+      stage_msq(xs + sidx_n(o), pl[k], pr[k]);
+      stage_msq(xs + SPAD + sidx_n(o), cl[k], cr[k]);
+    }
   }
   __syncthreads();
   const float* xp = xs + sidx(threadIdx.x, 0);
@@ -221,17 +303,27 @@ __global__ void __launch_bounds__(NT) k_dyn_fwd(char tag, const float* const* __
   const bool bypass = wv == 0.0;
   float* yo = y + (size_t)b * 2 * L;
   float* eo = env + (size_t)b * L;
-  for (int o = threadIdx.x; o < CH; o += NT) {  // coalesced outputs
+  float4 ul[Q4], ur[Q4];
+#pragma unroll
+  for (int k = 0; k < Q4; ++k) load4(u, L, c0 + 4 * (threadIdx.x + NT * k), vec, ul[k], ur[k]);
+#pragma unroll
+  for (int k = 0; k < Q4; ++k) {  // coalesced outputs
+    const int o = 4 * (threadIdx.x + NT * k);
     const long long n = c0 + o;
-    if (n >= L) break;
-    const float gain = xs[SPAD + sidx_n(o)];
-    eo[n] = xs[sidx_n(o)];
-    const float l = u[n], r = u[L + n];
-    if (bypass) { yo[n] = l; yo[L + n] = r; }
-    else {
-      yo[n] = wf * (l * gain) + om * l;
-      yo[L + n] = wf * (r * gain) + om * r;
+    const float* gp = xs + SPAD + sidx_n(o);
+    const float* ep = xs + sidx_n(o);
+    float4 yl, yr;
+    const float4 g4 = make_float4(gp[0], gp[1], gp[2], gp[3]);
+    if (bypass) {
+      yl = ul[k];
+      yr = ur[k];
+    } else {
+      yl = make_float4(wf * (ul[k].x * g4.x) + om * ul[k].x, wf * (ul[k].y * g4.y) + om * ul[k].y,
+                       wf * (ul[k].z * g4.z) + om * ul[k].z, wf * (ul[k].w * g4.w) + om * ul[k].w);
+      yr = make_float4(wf * (ur[k].x * g4.x) + om * ur[k].x, wf * (ur[k].y * g4.y) + om * ur[k].y,
+                       wf * (ur[k].z * g4.z) + om * ur[k].z, wf * (ur[k].w * g4.w) + om * ur[k].w);
     }
+    store4(yo, L, n, vec, yl, yr, eo, make_float4(ep[0], ep[1], ep[2], ep[3]));
   }
 }
 
@@ -256,10 +348,20 @@ __global__ void __launch_bounds__(256) k_dyn_bwd0(char tag, const float* const* 
   float* go = gu + (size_t)b * 2 * L;
   double sT = 0.0, sW = 0.0, sR = 0.0, sw = 0.0;
   float fT = 0.f, fW = 0.f, fR = 0.f, fw = 0.f;
-  int cnt = 0;
-  for (long long n = (long long)blockIdx.x * 256 + threadIdx.x; n < L; n += (long long)gridDim.x * 256) {
-    const float l = u[n], r = u[L + n], gl = gy[n], gr = gy[L + n];
-    const float gc = eo[n];
+  const bool vec = vec_ok(u, L) && vec_ok(gy, L) && vec_ok(eo, L) && vec_ok(go, L) && vec_ok(dgo, L);
+  for (long long n4 = 4 * ((long long)blockIdx.x * 256 + threadIdx.x); n4 < L; n4 += 4LL * gridDim.x * 256) {
+   float4 ul4, ur4, gl4, gr4;
+   load4(u, L, n4, vec, ul4, ur4);
+   load4(gy, L, n4, vec, gl4, gr4);
+   const float4 ev4 = load4m(eo, L, n4, vec);
+   const float U[4] = {ul4.x, ul4.y, ul4.z, ul4.w}, V[4] = {ur4.x, ur4.y, ur4.z, ur4.w};
+   const float GL[4] = {gl4.x, gl4.y, gl4.z, gl4.w}, GR[4] = {gr4.x, gr4.y, gr4.z, gr4.w};
+   const float EV[4] = {ev4.x, ev4.y, ev4.z, ev4.w};
+   float OL[4], OR[4], OD[4];
+#pragma unroll
+   for (int e = 0; e < 4; ++e) {
+    const float l = U[e], r = V[e], gl = GL[e], gr = GR[e];
+    const float gc = EV[e];
     const float gcl = fmaxf(gc, 0.f);
     const float G = logf(gcl + 1e-8f);
     const bool above = G >= q.T + q.W, below = G < q.T - q.W;
@@ -298,19 +400,19 @@ __global__ void __launch_bounds__(256) k_dyn_bwd0(char tag, const float* const* 
       dl = wf * gl; dr = wf * gr; ul = om * gl; ur = om * gr;
       fw = fmaf(gl, l * gain - l, fmaf(gr, r * gain - r, fw));
     }
-    go[n] = fmaf(dl, gain, ul);
-    go[L + n] = fmaf(dr, gain, ur);
+    OL[e] = fmaf(dl, gain, ul);
+    OR[e] = fmaf(dr, gain, ur);
     const float D = (dl * l + dr * r) * gain;
     fT = fmaf(D, dT, fT);
     fW = fmaf(D, dW, fW);
     fR = fmaf(D, dR, fR);
     const float dG = D * dGu - D;
-    dgo[n] = (gc > 0.f) ? dG / (gcl + 1e-8f) : 0.f;
-    if (++cnt == 8) {
-      sT += fT; sW += fW; sR += fR; sw += fw;
-      fT = fW = fR = fw = 0.f;
-      cnt = 0;
-    }
+    OD[e] = (gc > 0.f) ? dG / (gcl + 1e-8f) : 0.f;
+   }
+   store4(go, L, n4, vec, make_float4(OL[0], OL[1], OL[2], OL[3]), make_float4(OR[0], OR[1], OR[2], OR[3]), dgo,
+          make_float4(OD[0], OD[1], OD[2], OD[3]));
+   sT += fT; sW += fW; sR += fR; sw += fw;
+   fT = fW = fR = fw = 0.f;
   }
   sT += fT; sW += fW; sR += fR; sw += fw;
   sT = block_sum(sT, red);
@@ -464,10 +566,23 @@ __global__ void __launch_bounds__(NT) k_dyn_bwd1(const float* const* __restrict_
     }
   }
   const long long c0 = (long long)j * CH;
-  for (int o = threadIdx.x; o < CH; o += NT) {
-    const long long m = c0 + o, mn = m + CH;
-    ds[sidx_n(o)] = (m < L) ? d[m] : 0.f;
-    ds[SPAD + sidx_n(o)] = (mn < L) ? d[mn] : 0.f;
+  const bool vec = vec_ok(u, L) && vec_ok(d, L);
+  {
+    float4 vc[Q4], vn[Q4];
+#pragma unroll
+    for (int k = 0; k < Q4; ++k) {
+      const int o = 4 * (threadIdx.x + NT * k);
+      vc[k] = load4m(d, L, c0 + o, vec);
+      vn[k] = load4m(d, L, c0 + CH + o, vec);
+    }
+#pragma unroll
+    for (int k = 0; k < Q4; ++k) {
+      const int o = 4 * (threadIdx.x + NT * k);
+      float* a = ds + sidx_n(o);
+      float* c = ds + SPAD + sidx_n(o);
+      a[0] = vc[k].x; a[1] = vc[k].y; a[2] = vc[k].z; a[3] = vc[k].w;
+      c[0] = vn[k].x; c[1] = vn[k].y; c[2] = vn[k].z; c[3] = vn[k].w;
+    }
   }
   __syncthreads();
   const float* dc = ds + sidx(threadIdx.x, 0);
@@ -502,17 +617,35 @@ __global__ void __launch_bounds__(NT) k_dyn_bwd1(const float* const* __restrict_
   __syncthreads();
   double sxd = 0.0, sxr = 0.0;
   float* go = gu + (size_t)b * 2 * L;
-  for (int o = threadIdx.x; o < CH; o += NT) {  // coalesced: dmid = 2 mid dx; sums for d a_raw
+  const bool vg = vec && vec_ok(go, L);
+  float4 ul[Q4], ur[Q4], gl[Q4], gr[Q4];
+#pragma unroll
+  for (int k = 0; k < Q4; ++k) {
+    const long long m = c0 + 4 * (threadIdx.x + NT * k);
+    load4(u, L, m, vg, ul[k], ur[k]);
+    load4(go, L, m, vg, gl[k], gr[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < Q4; ++k) {  // coalesced: dmid = 2 mid dx; sums for d a_raw
+    const int o = 4 * (threadIdx.x + NT * k);
     const long long m = c0 + o;
-    if (m >= L) break;
-    const float dx = ds[sidx_n(o)], rr = ds[SPAD + sidx_n(o)];
-    const double mid = (double)u[m] + (double)u[L + m];
-    const double x = mid * mid;
-    sxd = fma(x, (double)dx, sxd);
-    sxr = fma(x, (double)rr, sxr);
-    const float dm = (float)(2.0 * mid * (double)dx);
-    go[m] += dm;
-    go[L + m] += dm;
+    const float* dxp = ds + sidx_n(o);
+    const float* rrp = ds + SPAD + sidx_n(o);
+    const float lu[4] = {ul[k].x, ul[k].y, ul[k].z, ul[k].w}, ru[4] = {ur[k].x, ur[k].y, ur[k].z, ur[k].w};
+    float ol[4] = {gl[k].x, gl[k].y, gl[k].z, gl[k].w}, orr[4] = {gr[k].x, gr[k].y, gr[k].z, gr[k].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (m + e >= L) continue;
+      const double mid = (double)lu[e] + (double)ru[e];
+      const double x = mid * mid;
+      sxd = fma(x, (double)dxp[e], sxd);
+      sxr = fma(x, (double)rrp[e], sxr);
+      const float dm = (float)(2.0 * mid * (double)dxp[e]);
+      ol[e] += dm;
+      orr[e] += dm;
+    }
+    store4(go, L, m, vg, make_float4(ol[0], ol[1], ol[2], ol[3]), make_float4(orr[0], orr[1], orr[2], orr[3]),
+           nullptr, make_float4(0.f, 0.f, 0.f, 0.f));
   }
   sxd = block_sum(sxd, red);
   __syncthreads();
@@ -556,7 +689,7 @@ __global__ void k_dyn_final(const double* __restrict__ part0, int nblk0, int nch
 
 int nchunks(int L) { return (L + CH - 1) / CH; }
 int bwd0_grid(int L) {
-  int n = (L + 4 * 256 - 1) / (4 * 256);
+  int n = (L + 8 * 256 - 1) / (8 * 256);
   return n < 1 ? 1 : (n > 512 ? 512 : n);
 }
 
