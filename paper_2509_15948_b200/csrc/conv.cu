@@ -36,6 +36,7 @@ constexpr double PI = 3.141592653589793238462643383279502884;
 
 #include "fir.cuh"
 #include "rev_fft.cuh"
+#include "eq_os.cuh"
 
 struct ConvGeom {
   int M, off, logN;
@@ -60,12 +61,26 @@ struct ConvWs {
   float* aux;                  // r: frames (B,2,313,384) | d: colours (B,2,20,39)
   float* aux2;                 // r: dexpo (B,2,313,193)
   int* offs;                   // d: (B,2,20) quantised delays
+  float2 *Hs, *pspec;          // e (overlap-save): 8192-pt FIR spectra, per-block dh cross spectra
 };
 
 template <class A>
 ConvWs carve_into(A& a, char tag, int B, int L) {
   const ConvGeom g = geom(tag, L);
   ConvWs w;
+  w.Hs = w.pspec = nullptr;
+  if (tag == 'e') {  // overlap-save path: no four-step buffers
+    w.Ax = w.Ah = w.X = w.H = w.Bo = nullptr;
+    w.hbuf = a.template take<float2>((size_t)B * g.M);
+    w.ghbuf = a.template take<float2>((size_t)B * g.M);
+    w.stats = a.template take<double>((size_t)B * 4);
+    w.part = a.template take<double>((size_t)B * kMaxParts * 4);
+    w.aux = w.aux2 = nullptr;
+    w.offs = nullptr;
+    w.Hs = a.template take<float2>((size_t)B * EOS_N);
+    w.pspec = a.template take<float2>((size_t)B * eos_nblk(L) * (EOS_N / 2 + 1));
+    return w;
+  }
   const size_t BN = (size_t)B * g.N;
   w.Ax = a.template take<float2>(BN);
   w.Ah = a.template take<float2>(BN);
@@ -424,6 +439,10 @@ int mgb_conv_init() {
 #undef X
   if (cudaFuncSetAttribute(k_dly_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDlyBwdSmem) != cudaSuccess)
     return 2;
+  cudaFuncSetAttribute(k_eqos_hspec, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
+  cudaFuncSetAttribute(k_eqos_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
+  cudaFuncSetAttribute(k_eqos_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem2);
+  cudaFuncSetAttribute(k_eqos_gh, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -442,7 +461,17 @@ int mgb_conv_forward(const MgbLevel* lv, cudaStream_t st) {
   MgbArena a{(char*)lv->ws, 0};
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
+    const int nb = eos_nblk(L);
     k_eq_fir<<<dim3((MGB_EQ_LEN + 31) / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.hbuf);
+    MGB_CHECK_LAUNCH();
+    k_eqos_hspec<<<B, EOS_NT, kEosSmem1, st>>>(w.hbuf, w.Hs);
+    MGB_CHECK_LAUNCH();
+    k_eqos_fwd<<<dim3(nb, B), EOS_NT, kEosSmem1, st>>>(lv->u_rows, w.Hs, lv->widx, lv->w, lv->y, lv->ybar, w.part,
+                                                       L);
+    MGB_CHECK_LAUNCH();
+    k_gs_norms<<<B, 256, 0, st>>>(w.part, nb, w.stats, lv->reg);
+    MGB_CHECK_LAUNCH();
+    return 0;
   } else if (tag == 'r') {
     k_rev_frames_fft<<<dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B), RV_NT, kRevFftSmem, st>>>(lv->bank, lv->prow,
                                                                                               w.aux);
@@ -464,7 +493,18 @@ int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st) {
   const ConvGeom g = geom(tag, L);
   MgbArena a{(char*)lv->ws, 0};
   const ConvWs w = carve_into(a, tag, B, L);
-  if (int rc = conv_bwd_dispatch(lv, w, g, st)) return rc;
+  if (tag == 'e') {
+    const int nb = eos_nblk(L);
+    k_eqos_bwd<<<dim3(nb, B), EOS_NT, kEosSmem2, st>>>(lv->u_rows, lv->gy_rows, lv->ybar, w.Hs, lv->widx, lv->w,
+                                                       lv->greg, w.stats, lv->gu, w.part, w.pspec, L, nb);
+    MGB_CHECK_LAUNCH();
+    k_dw_finalize<<<B, 256, 0, st>>>(w.part, nb, lv->widx, lv->w, lv->gw);
+    MGB_CHECK_LAUNCH();
+    k_eqos_gh<<<B, EOS_NT, kEosSmem1, st>>>(w.pspec, nb, w.ghbuf);
+    MGB_CHECK_LAUNCH();
+  } else if (int rc = conv_bwd_dispatch(lv, w, g, st)) {
+    return rc;
+  }
   if (tag == 'e') {
     k_eq_fir_bwd<<<dim3(MGB_EQ_BINS / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.ghbuf, g.M, lv->gbank);
   } else if (tag == 'r') {
