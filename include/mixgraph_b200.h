@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define MGB_ABI_VERSION 1
+#define MGB_ABI_VERSION 2
 
 /* One homogeneous schedule level (Algorithm 1 step) of B same-type nodes.
  * Replaces processors.KERNELS[tag](u, p) + drywet_wrap(ybar, u, w)
@@ -73,6 +73,24 @@ int mgb_level_forward(const MgbLevel* level, void* stream);
 /* Backward of one level: consumes gy_rows (and greg), writes gu, gbank rows, gw
  * entries.  Must follow mgb_level_forward on the same workspace. */
 int mgb_level_backward(const MgbLevel* level, void* stream);
+
+/* The same two calls split in phases so a caller can overlap the
+ * parameter-only work with other levels on a second stream:
+ *   forward  phase 1: FIR synthesis and FIR spectra (e, r, d; depends on
+ *                     bank/prow only; no-op for g, s, c, n);
+ *            phase 2: the signal pass (everything else).
+ *   backward phase 1: the signal adjoint: gu, gw, and the FIR gradient kept in
+ *                     the workspace (all of the backward for g, s, c, n);
+ *            phase 2: the FIR adjoint into gbank (e, r, d; no-op otherwise).
+ * mgb_level_forward == phase 1 then 2 on one stream; likewise backward.
+ * Within one level the phases must be ordered (1 before 2, forward before
+ * backward); phase 2 of the backward may run concurrently with other levels. */
+int mgb_level_forward_phase(const MgbLevel* level, int phase, void* stream);
+int mgb_level_backward_phase(const MgbLevel* level, int phase, void* stream);
+
+/* Number of kernel launches this library has enqueued so far (host counter;
+ * a launch captured into a CUDA graph counts once, at capture). */
+long long mgb_launch_count(void);
 
 /* Effective dry/wet weights w = sigmoid(raw) * mask (mg/scheduler.py:218-222).
  * mask may be NULL. */

@@ -74,6 +74,10 @@ def lib():
     L.mgb_level_workspace.restype = c_size_t
     L.mgb_level_forward.argtypes = [ctypes.POINTER(MgbLevel), c_void_p]
     L.mgb_level_backward.argtypes = [ctypes.POINTER(MgbLevel), c_void_p]
+    L.mgb_level_forward_phase.argtypes = [ctypes.POINTER(MgbLevel), c_int, c_void_p]
+    L.mgb_level_backward_phase.argtypes = [ctypes.POINTER(MgbLevel), c_int, c_void_p]
+    L.mgb_launch_count.restype = c_longlong
+    L.mgb_launch_count.argtypes = []
     L.mgb_weights.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_void_p]
     L.mgb_bus_sum.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]
     L.mgb_fft.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_float, c_void_p]
@@ -84,7 +88,8 @@ def lib():
     L.mgb_adamw_step.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_longlong, c_int,
                                  c_longlong, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     L.mgb_sparsity.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
-    for name in ("mgb_init", "mgb_level_forward", "mgb_level_backward", "mgb_weights", "mgb_bus_sum",
+    for name in ("mgb_init", "mgb_level_forward", "mgb_level_backward", "mgb_level_forward_phase",
+                 "mgb_level_backward_phase", "mgb_weights", "mgb_bus_sum",
                  "mgb_fft", "mgb_mrstft_target", "mgb_mrstft_forward", "mgb_mrstft_backward",
                  "mgb_adamw_step", "mgb_sparsity"):
         getattr(L, name).restype = c_int
@@ -93,7 +98,7 @@ def lib():
 
 
 EXPORTED = ("mgb_abi_version", "mgb_init", "mgb_level_workspace", "mgb_level_forward",
-            "mgb_level_backward", "mgb_weights", "mgb_bus_sum", "mgb_fft", "mgb_mrstft_target",
+            "mgb_level_backward", "mgb_level_forward_phase", "mgb_level_backward_phase", "mgb_launch_count", "mgb_weights", "mgb_bus_sum", "mgb_fft", "mgb_mrstft_target",
             "mgb_mrstft_forward", "mgb_mrstft_backward", "mgb_adamw_step", "mgb_sparsity")
 
 

@@ -53,36 +53,51 @@ static int check_level(const MgbLevel* lv) {
   return 0;
 }
 
-extern "C" int mgb_level_forward(const MgbLevel* lv, void* stream) {
+extern "C" int mgb_level_forward_phase(const MgbLevel* lv, int phase, void* stream) {
   if (int rc = check_level(lv)) return rc;
+  if (phase != 1 && phase != 2) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   switch (lv->tag) {
     case 'g':
-    case 's': return mgb_simple_forward(lv, st);
+    case 's': return phase == 2 ? mgb_simple_forward(lv, st) : 0;
     case 'e':
     case 'r':
-    case 'd': return mgb_conv_forward(lv, st);
+    case 'd': return phase == 1 ? mgb_conv_prepare(lv, st) : mgb_conv_forward(lv, st);
     case 'c':
-    case 'n': return mgb_dyn_forward(lv, st);
+    case 'n': return phase == 2 ? mgb_dyn_forward(lv, st) : 0;
     default: return 1;
   }
 }
 
-extern "C" int mgb_level_backward(const MgbLevel* lv, void* stream) {
+extern "C" int mgb_level_backward_phase(const MgbLevel* lv, int phase, void* stream) {
   if (int rc = check_level(lv)) return rc;
   if (!lv->gy_rows || !lv->gu || !lv->gbank) return 1;
+  if (phase != 1 && phase != 2) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   switch (lv->tag) {
     case 'g':
-    case 's': return mgb_simple_backward(lv, st);
+    case 's': return phase == 1 ? mgb_simple_backward(lv, st) : 0;
     case 'e':
     case 'r':
-    case 'd': return mgb_conv_backward(lv, st);
+    case 'd': return phase == 1 ? mgb_conv_backward(lv, st) : mgb_conv_param_grad(lv, st);
     case 'c':
-    case 'n': return mgb_dyn_backward(lv, st);
+    case 'n': return phase == 1 ? mgb_dyn_backward(lv, st) : 0;
     default: return 1;
   }
 }
+
+extern "C" int mgb_level_forward(const MgbLevel* lv, void* stream) {
+  if (int rc = mgb_level_forward_phase(lv, 1, stream)) return rc;
+  return mgb_level_forward_phase(lv, 2, stream);
+}
+
+extern "C" int mgb_level_backward(const MgbLevel* lv, void* stream) {
+  if (int rc = mgb_level_backward_phase(lv, 1, stream)) return rc;
+  return mgb_level_backward_phase(lv, 2, stream);
+}
+
+long long g_mgb_launches = 0;
+extern "C" long long mgb_launch_count(void) { return g_mgb_launches; }
 
 extern "C" int mgb_fft(const void* in, void* out, void* tmp, int batch, int log2n, int inverse, float scale,
                        void* stream) {

@@ -252,5 +252,7 @@ __device__ __forceinline__ double softplus64(double x) {  // np.logaddexp(0, x)
   return fmax(x, 0.0) + log1p(exp(-fabs(x)));
 }
 
+// after EVERY kernel launch: error check + the host launch counter (mgb_launch_count)
+extern long long g_mgb_launches;
 #define MGB_CHECK_LAUNCH() \
-  do { cudaError_t e__ = cudaGetLastError(); if (e__ != cudaSuccess) return 2; } while (0)
+  do { ++g_mgb_launches; cudaError_t e__ = cudaGetLastError(); if (e__ != cudaSuccess) return 2; } while (0)

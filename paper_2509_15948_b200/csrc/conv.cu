@@ -367,13 +367,19 @@ struct Conv {
                          (int)fs::rowbwd_smem<N1, N2>());
   }
 
+  static int prep(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
+    const dim3 gc(N2 / G::TC, lv->B);
+    const int fir_rows = (int)((g.M + N2 - 1) / N2);
+    fs::k_colA<N1, N2><<<gc, G::NTC, fs::col_smem<N1, N2>(), st>>>(LdFir{w.hbuf, g.M}, w.Ah,
+                                                                  fir_rows < N1 ? fir_rows : N1);
+    MGB_CHECK_LAUNCH();
+    return 0;
+  }
+
   static int fwd(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
     const int B = lv->B, L = lv->L;
     const dim3 gc(N2 / G::TC, B), gr(N1 / 2 + 1, B);
     const size_t sc = fs::col_smem<N1, N2>(), sr = fs::row_smem<N1, N2>();
-    const int fir_rows = (int)((g.M + N2 - 1) / N2);
-    fs::k_colA<N1, N2><<<gc, G::NTC, sc, st>>>(LdFir{w.hbuf, g.M}, w.Ah, fir_rows < N1 ? fir_rows : N1);
-    MGB_CHECK_LAUNCH();
     const int x_rows = (int)((L + N2 - 1) / N2);
     fs::k_colA<N1, N2><<<gc, G::NTC, sc, st>>>(LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1);
     MGB_CHECK_LAUNCH();
@@ -422,6 +428,15 @@ int conv_fwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cu
   }
 }
 
+int conv_prep_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
+  switch (g.logN) {
+#define X(l, a, b) case l: return Conv<a, b>::prep(lv, w, g, st);
+    MGB_CONV_SIZES(X)
+#undef X
+    default: return 1;
+  }
+}
+
 int conv_bwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
   switch (g.logN) {
 #define X(l, a, b) case l: return Conv<a, b>::bwd(lv, w, g, st);
@@ -452,6 +467,37 @@ size_t mgb_conv_workspace(char tag, int B, int L) {
   return a.off;
 }
 
+// forward phase 1: FIR synthesis (+ the FIR column pass / 8192-point spectra), params only
+int mgb_conv_prepare(const MgbLevel* lv, cudaStream_t st) {
+  const char tag = lv->tag;
+  const int B = lv->B, L = lv->L;
+  const ConvGeom g = geom(tag, L);
+  if (g.logN > 22) return 1;
+  MgbArena a{(char*)lv->ws, 0};
+  const ConvWs w = carve_into(a, tag, B, L);
+  if (tag == 'e') {
+    k_eq_fir<<<dim3((MGB_EQ_LEN + 31) / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.hbuf);
+    MGB_CHECK_LAUNCH();
+    k_eqos_hspec<<<B, EOS_NT, kEosSmem1, st>>>(w.hbuf, w.Hs);
+    MGB_CHECK_LAUNCH();
+    return 0;
+  }
+  if (tag == 'r') {
+    k_rev_frames_fft<<<dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B), RV_NT, kRevFftSmem, st>>>(lv->bank, lv->prow,
+                                                                                              w.aux);
+    MGB_CHECK_LAUNCH();
+    k_rev_assemble<<<dim3((MGB_REV_LEN + NT - 1) / NT, B), NT, 0, st>>>(w.aux, w.hbuf);
+    MGB_CHECK_LAUNCH();
+  } else {
+    k_dly_colour<<<dim3(MGB_DLY_TAPS, 2, B), 64, 0, st>>>(lv->bank, lv->prow, w.aux, w.offs);
+    MGB_CHECK_LAUNCH();
+    k_dly_place<<<dim3((MGB_DLY_FIR + NT - 1) / NT, B), NT, 0, st>>>(w.aux, w.offs, w.hbuf);
+    MGB_CHECK_LAUNCH();
+  }
+  return conv_prep_dispatch(lv, w, g, st);
+}
+
+// forward phase 2: the signal pass
 int mgb_conv_forward(const MgbLevel* lv, cudaStream_t st) {
   const char tag = lv->tag;
   const int B = lv->B, L = lv->L;
@@ -462,30 +508,17 @@ int mgb_conv_forward(const MgbLevel* lv, cudaStream_t st) {
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
     const int nb = eos_nblk(L);
-    k_eq_fir<<<dim3((MGB_EQ_LEN + 31) / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.hbuf);
-    MGB_CHECK_LAUNCH();
-    k_eqos_hspec<<<B, EOS_NT, kEosSmem1, st>>>(w.hbuf, w.Hs);
-    MGB_CHECK_LAUNCH();
     k_eqos_fwd<<<dim3(nb, B), EOS_NT, kEosSmem1, st>>>(lv->u_rows, w.Hs, lv->widx, lv->w, lv->y, lv->ybar, w.part,
                                                        L);
     MGB_CHECK_LAUNCH();
     k_gs_norms<<<B, 256, 0, st>>>(w.part, nb, w.stats, lv->reg);
     MGB_CHECK_LAUNCH();
     return 0;
-  } else if (tag == 'r') {
-    k_rev_frames_fft<<<dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B), RV_NT, kRevFftSmem, st>>>(lv->bank, lv->prow,
-                                                                                              w.aux);
-    MGB_CHECK_LAUNCH();
-    k_rev_assemble<<<dim3((MGB_REV_LEN + NT - 1) / NT, B), NT, 0, st>>>(w.aux, w.hbuf);
-  } else {
-    k_dly_colour<<<dim3(MGB_DLY_TAPS, 2, B), 64, 0, st>>>(lv->bank, lv->prow, w.aux, w.offs);
-    MGB_CHECK_LAUNCH();
-    k_dly_place<<<dim3((MGB_DLY_FIR + NT - 1) / NT, B), NT, 0, st>>>(w.aux, w.offs, w.hbuf);
   }
-  MGB_CHECK_LAUNCH();
   return conv_fwd_dispatch(lv, w, g, st);
 }
 
+// backward phase 1: signal adjoint (gu, gw) and the FIR gradient in the workspace
 int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st) {
   const char tag = lv->tag;
   const int B = lv->B, L = lv->L;
@@ -500,18 +533,27 @@ int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st) {
     MGB_CHECK_LAUNCH();
     k_dw_finalize<<<B, 256, 0, st>>>(w.part, nb, lv->widx, lv->w, lv->gw);
     MGB_CHECK_LAUNCH();
-    k_eqos_gh<<<B, EOS_NT, kEosSmem1, st>>>(w.pspec, nb, w.ghbuf);
-    MGB_CHECK_LAUNCH();
-  } else if (int rc = conv_bwd_dispatch(lv, w, g, st)) {
-    return rc;
+    return 0;
   }
+  return conv_bwd_dispatch(lv, w, g, st);
+}
+
+// backward phase 2: FIR adjoint into the gradient bank
+int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st) {
+  const char tag = lv->tag;
+  const int B = lv->B, L = lv->L;
+  const ConvGeom g = geom(tag, L);
+  MgbArena a{(char*)lv->ws, 0};
+  const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
+    k_eqos_gh<<<B, EOS_NT, kEosSmem1, st>>>(w.pspec, eos_nblk(L), w.ghbuf);
+    MGB_CHECK_LAUNCH();
     k_eq_fir_bwd<<<dim3(MGB_EQ_BINS / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.ghbuf, g.M, lv->gbank);
   } else if (tag == 'r') {
     k_rev_bwd_frames_fft<<<dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B), RV_NT, kRevFftSmem, st>>>(
         lv->bank, lv->prow, w.ghbuf, g.M, w.aux2);
     MGB_CHECK_LAUNCH();
-    k_rev_bwd_reduce<<<B, 256, 0, st>>>(w.aux2, lv->prow, lv->gbank);
+    k_rev_bwd_reduce<<<dim3((MGB_REV_PBINS + 31) / 32, 2, B), 256, 0, st>>>(w.aux2, lv->prow, lv->gbank);
   } else {
     k_dly_bwd<<<dim3(MGB_DLY_TAPS, 2, B), NT, kDlyBwdSmem, st>>>(lv->bank, lv->prow, w.aux, w.offs, w.ghbuf, g.M,
                                                                  lv->gbank);

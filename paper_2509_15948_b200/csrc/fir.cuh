@@ -196,30 +196,57 @@ __global__ void __launch_bounds__(MGB_REV_NFFT) k_rev_bwd_frames(const double* _
   }
 }
 
-__global__ void k_rev_bwd_reduce(const float* __restrict__ dexpo, const int* __restrict__ prow,
-                                 double* __restrict__ gbank) {
-  __shared__ double d0[2][MGB_REV_BINS], dd[2][MGB_REV_BINS];
-  const int b = blockIdx.x;
-  for (int q = threadIdx.x; q < 2 * MGB_REV_BINS; q += blockDim.x) {
-    const int ch = q / MGB_REV_BINS, k = q % MGB_REV_BINS;
-    const float* e = dexpo + ((size_t)b * 2 + ch) * MGB_REV_FRAMES * MGB_REV_BINS + k;
-    double s0 = 0.0, s1 = 0.0;
-    for (int m = 0; m < MGB_REV_FRAMES; ++m) {
-      const double v = e[(size_t)m * MGB_REV_BINS];
-      s0 += v;
-      s1 += v * m;
+// d H0[c][k] = sum_m dexpo[c][m][k],  d HD[c][k] = sum_m m dexpo[c][m][k]; the Nyquist bin
+// folds into the last parameter bin.  Grid (bin groups of 32, 2 channels, B); 8 warps
+// split the frames, lanes walk consecutive bins; fixed-order float64 sums.
+__global__ void __launch_bounds__(256) k_rev_bwd_reduce(const float* __restrict__ dexpo,
+                                                        const int* __restrict__ prow,
+                                                        double* __restrict__ gbank) {
+  __shared__ double s0[8][33], s1[8][33];
+  const int ch = blockIdx.y, b = blockIdx.z;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + lane;
+  const float* e = dexpo + ((size_t)b * 2 + ch) * MGB_REV_FRAMES * MGB_REV_BINS;
+  double a0 = 0.0, a1 = 0.0, n0 = 0.0, n1 = 0.0;
+  const bool last = (k == MGB_REV_PBINS - 1);
+  for (int m = wp; m < MGB_REV_FRAMES; m += 8) {
+    if (k < MGB_REV_PBINS) {
+      const double v = e[(size_t)m * MGB_REV_BINS + k];
+      a0 += v;
+      a1 += v * m;
     }
-    d0[ch][k] = s0;
-    dd[ch][k] = s1;
+    if (last) {
+      const double v = e[(size_t)m * MGB_REV_BINS + MGB_REV_PBINS];
+      n0 += v;
+      n1 += v * m;
+    }
+  }
+  s0[wp][lane] = a0;
+  s1[wp][lane] = a1;
+  __syncthreads();
+  if (last) {  // the thread owning bin 191 of each warp slice pushes its Nyquist sums
+    s0[wp][32] = n0;
+    s1[wp][32] = n1;
   }
   __syncthreads();
-  double* g = gbank + (size_t)prow[b] * 768;
-  for (int q = threadIdx.x; q < 2 * MGB_REV_PBINS; q += blockDim.x) {
-    const int ch = q / MGB_REV_PBINS, k = q % MGB_REV_PBINS;
-    double a = d0[ch][k], c = dd[ch][k];
-    if (k == MGB_REV_PBINS - 1) { a += d0[ch][MGB_REV_PBINS]; c += dd[ch][MGB_REV_PBINS]; }
-    g[ch * 384 + k] = a;
-    g[ch * 384 + 192 + k] = c;
+  if (wp == 0 && k < MGB_REV_PBINS) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      t0 += s0[i][lane];
+      t1 += s1[i][lane];
+    }
+    if (last) {
+      double u0 = 0.0, u1 = 0.0;
+      for (int i = 0; i < 8; ++i) {
+        u0 += s0[i][32];
+        u1 += s1[i][32];
+      }
+      t0 += u0;
+      t1 += u1;
+    }
+    double* g = gbank + (size_t)prow[b] * 768 + ch * 384;
+    g[k] = t0;
+    g[192 + k] = t1;
   }
 }
 

@@ -13,14 +13,41 @@
 namespace {
 
 constexpr int NT = 256;
-constexpr int KP = 4;  // partial slots per CTA
+constexpr int KP = 4;      // partial slots per CTA
+constexpr int VPT = 4;     // float4 (or scalar groups of 4) per thread per channel
+constexpr int CHUNK = NT * VPT * 4;  // samples per channel per CTA
 
 __host__ __device__ inline int simple_nblk(int L) {
-  int n = (L + 4 * NT - 1) / (4 * NT);
-  return n < 1 ? 1 : (n > 64 ? 64 : n);
+  const int n = (L + CHUNK - 1) / CHUNK;
+  return n < 1 ? 1 : n;
 }
 
-__global__ void __launch_bounds__(NT) k_gs_fwd(char tag, const float* const* __restrict__ u_rows,
+// Four consecutive samples n..n+3 of both channels: float4 when the rows are
+// 16-byte aligned and L % 4 == 0 (VEC), else guarded scalars.
+template <bool VEC>
+__device__ __forceinline__ void ld4(const float* __restrict__ p, long long n, int L, float (&v)[4]) {
+  if (VEC) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p + n));
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = (n + i < L) ? __ldg(p + n + i) : 0.f;
+  }
+}
+template <bool VEC>
+__device__ __forceinline__ void st4(float* __restrict__ p, long long n, int L, const float (&v)[4]) {
+  if (VEC) {
+    *reinterpret_cast<float4*>(p + n) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (n + i < L) p[n + i] = v[i];
+  }
+}
+
+// forward: yo = w*ybar + (1-w)*u, exactly u when w == 0
+template <char TAG, bool VEC>
+__global__ void __launch_bounds__(NT) k_gs_fwd(const float* const* __restrict__ u_rows,
                                                const double* __restrict__ bank, const int* __restrict__ prow,
                                                const int* __restrict__ widx, const double* __restrict__ w,
                                                float* __restrict__ y, int L) {
@@ -28,36 +55,57 @@ __global__ void __launch_bounds__(NT) k_gs_fwd(char tag, const float* const* __r
   const float* u = u_rows[b];
   float* yo = y + (size_t)b * 2 * L;
   const double wv = w ? w[widx[b]] : 1.0;
-  const long long stride = (long long)gridDim.x * NT;
-  if (wv == 0.0) {  // exact bypass
-    for (long long n = (long long)blockIdx.x * NT + threadIdx.x; n < L; n += stride) {
-      yo[n] = u[n];
-      yo[L + n] = u[L + n];
-    }
-    return;
-  }
-  if (tag == 'g') {
-    const int P = 2;
-    const double g0 = exp(bank[(size_t)prow[b] * P]), g1 = exp(bank[(size_t)prow[b] * P + 1]);
-    const float c0 = (float)(wv * g0 + (1.0 - wv)), c1 = (float)(wv * g1 + (1.0 - wv));
-    for (long long n = (long long)blockIdx.x * NT + threadIdx.x; n < L; n += stride) {
-      yo[n] = c0 * u[n];
-      yo[L + n] = c1 * u[L + n];
-    }
+  const bool bypass = (wv == 0.0);
+  float c0, c1, k = 0.f, wf = 0.f, om = 0.f;
+  if (TAG == 'g') {
+    const double g0 = exp(bank[(size_t)prow[b] * 2]), g1 = exp(bank[(size_t)prow[b] * 2 + 1]);
+    c0 = bypass ? 1.f : (float)(wv * g0 + (1.0 - wv));
+    c1 = bypass ? 1.f : (float)(wv * g1 + (1.0 - wv));
   } else {
-    const float k = (float)exp(bank[prow[b]]);
-    const float wf = (float)wv, om = (float)(1.0 - wv);
-    for (long long n = (long long)blockIdx.x * NT + threadIdx.x; n < L; n += stride) {
-      const float l = u[n], r = u[L + n];
-      const float mid = l + r, side = k * (l - r);
-      const float yl = (mid + side) * 0.5f, yr = (mid - side) * 0.5f;
-      yo[n] = wf * yl + om * l;
-      yo[L + n] = wf * yr + om * r;
+    k = (float)exp(bank[prow[b]]);
+    wf = (float)wv;
+    om = (float)(1.0 - wv);
+    c0 = c1 = 1.f;
+  }
+  const long long base = (long long)blockIdx.x * CHUNK;
+  float l[VPT][4], r[VPT][4];
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const long long n = base + 4LL * (threadIdx.x + j * NT);
+    if (n < L) {
+      ld4<VEC>(u, n, L, l[j]);
+      ld4<VEC>(u + L, n, L, r[j]);
     }
+  }
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const long long n = base + 4LL * (threadIdx.x + j * NT);
+    if (n >= L) continue;
+    float ol[4], orr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (bypass) {
+        ol[i] = l[j][i];
+        orr[i] = r[j][i];
+      } else if (TAG == 'g') {
+        ol[i] = c0 * l[j][i];
+        orr[i] = c1 * r[j][i];
+      } else {
+        const float mid = l[j][i] + r[j][i], side = k * (l[j][i] - r[j][i]);
+        const float yl = (mid + side) * 0.5f, yr = (mid - side) * 0.5f;
+        ol[i] = wf * yl + om * l[j][i];
+        orr[i] = wf * yr + om * r[j][i];
+      }
+    }
+    st4<VEC>(yo, n, L, ol);
+    st4<VEC>(yo + L, n, L, orr);
   }
 }
 
-__global__ void __launch_bounds__(NT) k_gs_bwd(char tag, const float* const* __restrict__ u_rows,
+// backward: gu and the two per-row reductions (g: sum gy_c u_c per channel;
+// s: sum (l-r)(gl-gr) for dp and sum g.(ybar-u) for dw), float64 per CTA
+template <char TAG, bool VEC>
+__global__ void __launch_bounds__(NT) k_gs_bwd(const float* const* __restrict__ u_rows,
                                                const float* const* __restrict__ gy_rows,
                                                const double* __restrict__ bank, const int* __restrict__ prow,
                                                const int* __restrict__ widx, const double* __restrict__ w,
@@ -68,50 +116,68 @@ __global__ void __launch_bounds__(NT) k_gs_bwd(char tag, const float* const* __r
   const float* gy = gy_rows[b];
   float* go = gu + (size_t)b * 2 * L;
   const double wv = w ? w[widx[b]] : 1.0;
-  const long long stride = (long long)gridDim.x * NT;
-  double a0 = 0.0, a1 = 0.0;
-  if (wv == 0.0) {
-    for (long long n = (long long)blockIdx.x * NT + threadIdx.x; n < L; n += stride) {
-      go[n] = gy[n];
-      go[L + n] = gy[L + n];
-    }
-  } else if (tag == 'g') {
+  const bool bypass = (wv == 0.0);
+  float c0 = 1.f, c1 = 1.f, k = 0.f, wf = 0.f, om = 0.f;
+  if (TAG == 'g') {
     const double g0 = exp(bank[(size_t)prow[b] * 2]), g1 = exp(bank[(size_t)prow[b] * 2 + 1]);
-    const float c0 = (float)(wv * g0 + (1.0 - wv)), c1 = (float)(wv * g1 + (1.0 - wv));
-    float s0 = 0.f, s1 = 0.f;
-    int cnt = 0;
-    for (long long n = (long long)blockIdx.x * NT + threadIdx.x; n < L; n += stride) {
-      const float gl = gy[n], gr = gy[L + n];
-      go[n] = c0 * gl;
-      go[L + n] = c1 * gr;
-      s0 = fmaf(gl, u[n], s0);
-      s1 = fmaf(gr, u[L + n], s1);
-      if (++cnt == 16) { a0 += s0; a1 += s1; s0 = s1 = 0.f; cnt = 0; }
-    }
-    a0 += s0;
-    a1 += s1;
+    c0 = (float)(wv * g0 + (1.0 - wv));
+    c1 = (float)(wv * g1 + (1.0 - wv));
   } else {
-    const float k = (float)exp(bank[prow[b]]);
-    const float wf = (float)wv, om = (float)(1.0 - wv);
-    float s0 = 0.f, s1 = 0.f;
-    int cnt = 0;
-    for (long long n = (long long)blockIdx.x * NT + threadIdx.x; n < L; n += stride) {
-      const float l = u[n], r = u[L + n], gl = gy[n], gr = gy[L + n];
-      const float dl = wf * gl, dr = wf * gr;           // d ybar
-      const float sm = 0.5f * (dl + dr), sd = 0.5f * k * (dl - dr);
-      go[n] = om * gl + sm + sd;
-      go[L + n] = om * gr + sm - sd;
-      const float mid = l + r, side = k * (l - r);
-      const float yl = (mid + side) * 0.5f, yr = (mid - side) * 0.5f;
-      s0 = fmaf(l - r, gl - gr, s0);                   // for d p
-      s1 = fmaf(gl, yl - l, fmaf(gr, yr - r, s1));     // for d w
-      if (++cnt == 16) { a0 += s0; a1 += s1; s0 = s1 = 0.f; cnt = 0; }
-    }
-    a0 += s0;
-    a1 += s1;
+    k = (float)exp(bank[prow[b]]);
+    wf = (float)wv;
+    om = (float)(1.0 - wv);
   }
-  const double t0 = block_sum(a0, scratch);
-  const double t1 = block_sum(a1, scratch);
+  const long long base = (long long)blockIdx.x * CHUNK;
+  float gl[VPT][4], gr[VPT][4], l[VPT][4], r[VPT][4];
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const long long n = base + 4LL * (threadIdx.x + j * NT);
+    if (n < L) {
+      ld4<VEC>(gy, n, L, gl[j]);
+      ld4<VEC>(gy + L, n, L, gr[j]);
+      if (!bypass) {
+        ld4<VEC>(u, n, L, l[j]);
+        ld4<VEC>(u + L, n, L, r[j]);
+      }
+    }
+  }
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const long long n = base + 4LL * (threadIdx.x + j * NT);
+    if (n >= L) continue;
+    float ol[4], orr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool in = VEC || (n + i < L);
+      if (bypass) {
+        ol[i] = gl[j][i];
+        orr[i] = gr[j][i];
+      } else if (TAG == 'g') {
+        ol[i] = c0 * gl[j][i];
+        orr[i] = c1 * gr[j][i];
+        if (in) {
+          s0 = fmaf(gl[j][i], l[j][i], s0);
+          s1 = fmaf(gr[j][i], r[j][i], s1);
+        }
+      } else {
+        const float dl = wf * gl[j][i], dr = wf * gr[j][i];  // d ybar
+        const float sm = 0.5f * (dl + dr), sd = 0.5f * k * (dl - dr);
+        ol[i] = om * gl[j][i] + sm + sd;
+        orr[i] = om * gr[j][i] + sm - sd;
+        if (in) {
+          const float mid = l[j][i] + r[j][i], side = k * (l[j][i] - r[j][i]);
+          const float yl = (mid + side) * 0.5f, yr = (mid - side) * 0.5f;
+          s0 = fmaf(l[j][i] - r[j][i], gl[j][i] - gr[j][i], s0);
+          s1 = fmaf(gl[j][i], yl - l[j][i], fmaf(gr[j][i], yr - r[j][i], s1));
+        }
+      }
+    }
+    st4<VEC>(go, n, L, ol);
+    st4<VEC>(go + L, n, L, orr);
+  }
+  const double t0 = block_sum((double)s0, scratch);
+  const double t1 = block_sum((double)s1, scratch);
   if (threadIdx.x == 0) {
     double* pp = part + ((size_t)b * gridDim.x + blockIdx.x) * KP;
     pp[0] = t0;
@@ -119,16 +185,19 @@ __global__ void __launch_bounds__(NT) k_gs_bwd(char tag, const float* const* __r
   }
 }
 
+// one warp per row: deterministic fixed-order float64 sum of the CTA partials
 __global__ void k_gs_finalize(char tag, const double* __restrict__ part, int nblk, const double* __restrict__ bank,
                               const int* __restrict__ prow, const int* __restrict__ widx,
                               const double* __restrict__ w, double* __restrict__ gbank, double* __restrict__ gw) {
   const int b = blockIdx.x;
-  if (threadIdx.x != 0) return;
   double s0 = 0.0, s1 = 0.0;
-  for (int i = 0; i < nblk; ++i) {
+  for (int i = threadIdx.x; i < nblk; i += 32) {
     s0 += part[((size_t)b * nblk + i) * KP];
     s1 += part[((size_t)b * nblk + i) * KP + 1];
   }
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  if (threadIdx.x != 0) return;
   const double wv = w ? w[widx[b]] : 1.0;
   if (tag == 'g') {
     const double g0 = exp(bank[(size_t)prow[b] * 2]), g1 = exp(bank[(size_t)prow[b] * 2 + 1]);
@@ -152,16 +221,37 @@ __global__ void k_weights(const double* __restrict__ raw, const double* __restri
   }
 }
 
+// out[s] = sum of rows seg_off[s]..seg_off[s+1]-1 over 2L samples, fixed order
+template <bool VEC>
 __global__ void __launch_bounds__(NT) k_bus_sum(const float* const* __restrict__ in_rows,
                                                 const int* __restrict__ seg_off, float* __restrict__ out, int L) {
   const int s = blockIdx.y;
   const int i0 = seg_off[s], i1 = seg_off[s + 1];
   float* o = out + (size_t)s * 2 * L;
-  const long long twoL = 2LL * L;
-  for (long long n = (long long)blockIdx.x * NT + threadIdx.x; n < twoL; n += (long long)gridDim.x * NT) {
-    float acc = 0.f;
-    for (int i = i0; i < i1; ++i) acc += in_rows[i][n];
-    o[n] = acc;
+  const int twoL = 2 * L;
+  const long long base = (long long)blockIdx.x * CHUNK;
+  float acc[VPT][4];
+#pragma unroll
+  for (int j = 0; j < VPT; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[j][i] = 0.f;
+  for (int r = i0; r < i1; ++r) {
+    const float* p = in_rows[r];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const long long n = base + 4LL * (threadIdx.x + j * NT);
+      if (n < twoL) {
+        float v[4];
+        ld4<VEC>(p, n, twoL, v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[j][i] += v[i];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const long long n = base + 4LL * (threadIdx.x + j * NT);
+    if (n < twoL) st4<VEC>(o, n, twoL, acc[j]);
   }
 }
 
@@ -169,19 +259,29 @@ __global__ void __launch_bounds__(NT) k_bus_sum(const float* const* __restrict__
 
 size_t mgb_simple_workspace(char, int B, int L) { return mgb_align(sizeof(double) * KP * B * simple_nblk(L)); }
 
+static bool rows_vec_ok(int L) { return (L & 3) == 0; }  // row starts are then 16-byte aligned
+
 int mgb_simple_forward(const MgbLevel* lv, cudaStream_t st) {
-  const int nblk = simple_nblk(lv->L);
-  k_gs_fwd<<<dim3(nblk, lv->B), NT, 0, st>>>(lv->tag, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w, lv->y,
-                                             lv->L);
+  const dim3 grid(simple_nblk(lv->L), lv->B);
+  const bool vec = rows_vec_ok(lv->L);
+#define LAUNCH(T, V) k_gs_fwd<T, V><<<grid, NT, 0, st>>>(lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w, lv->y, lv->L)
+  if (lv->tag == 'g') { if (vec) LAUNCH('g', true); else LAUNCH('g', false); }
+  else { if (vec) LAUNCH('s', true); else LAUNCH('s', false); }
+#undef LAUNCH
   MGB_CHECK_LAUNCH();
   return 0;
 }
 
 int mgb_simple_backward(const MgbLevel* lv, cudaStream_t st) {
   const int nblk = simple_nblk(lv->L);
+  const dim3 grid(nblk, lv->B);
+  const bool vec = rows_vec_ok(lv->L);
   double* part = reinterpret_cast<double*>(lv->ws);
-  k_gs_bwd<<<dim3(nblk, lv->B), NT, 0, st>>>(lv->tag, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx,
-                                             lv->w, lv->gu, part, lv->L);
+#define LAUNCH(T, V) k_gs_bwd<T, V><<<grid, NT, 0, st>>>(lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx, \
+                                                          lv->w, lv->gu, part, lv->L)
+  if (lv->tag == 'g') { if (vec) LAUNCH('g', true); else LAUNCH('g', false); }
+  else { if (vec) LAUNCH('s', true); else LAUNCH('s', false); }
+#undef LAUNCH
   MGB_CHECK_LAUNCH();
   k_gs_finalize<<<lv->B, 32, 0, st>>>(lv->tag, part, nblk, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,
                                       lv->gw);
@@ -199,8 +299,9 @@ extern "C" int mgb_weights(const double* raw, const double* mask, double* w, int
 extern "C" int mgb_bus_sum(const float* const* in_rows, const int* seg_off, float* out, int S, int L,
                            void* stream) {
   if (S <= 0) return 0;
-  const int nblk = simple_nblk(2 * L);
-  k_bus_sum<<<dim3(nblk, S), NT, 0, (cudaStream_t)stream>>>(in_rows, seg_off, out, L);
+  const dim3 grid(simple_nblk(2 * L), S);
+  if (rows_vec_ok(L)) k_bus_sum<true><<<grid, NT, 0, (cudaStream_t)stream>>>(in_rows, seg_off, out, L);
+  else k_bus_sum<false><<<grid, NT, 0, (cudaStream_t)stream>>>(in_rows, seg_off, out, L);
   MGB_CHECK_LAUNCH();
   return 0;
 }

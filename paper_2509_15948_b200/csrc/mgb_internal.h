@@ -17,8 +17,10 @@ int mgb_spec_pair(const float2* Z, const float2* H, float2* Q, const float2* C, 
 int mgb_simple_forward(const MgbLevel* lv, cudaStream_t st);
 int mgb_simple_backward(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_simple_workspace(char tag, int B, int L);
+int mgb_conv_prepare(const MgbLevel* lv, cudaStream_t st);
 int mgb_conv_forward(const MgbLevel* lv, cudaStream_t st);
 int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st);
+int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_conv_workspace(char tag, int B, int L);
 int mgb_conv_init();
 int mgb_loss_init();
@@ -26,6 +28,9 @@ int mgb_dyn_init();
 int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st);
 int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_dyn_workspace(char tag, int B, int L);
+
+// host-side launch counter (mgb_launch_count); every launch site bumps it
+extern long long g_mgb_launches;
 
 static inline int mgb_log2_ceil(long long n) {
   int l = 0;

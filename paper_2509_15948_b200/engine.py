@@ -257,15 +257,47 @@ class RenderPlan:
             raise LengthMismatch(f"plan is built for L={self.L}, got {t.shape[-1]}")
         self.stems.copy_(t.to(dtype=F32), non_blocking=True)
 
-    def forward(self, use_mask: bool):
+    def prepare(self, side=None):
+        """Forward phase 1 of every e/r/d level (FIR synthesis; params only).
+
+        With ``side`` (a torch stream) the work is enqueued there and one event
+        per level is returned for ``forward`` to wait on; else it runs inline."""
+        L = lib()
+        events = {}
+        if side is None:
+            sp = stream_ptr()
+            for lv in self.levels:
+                if lv.struct is not None and lv.tag in "erd":
+                    check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 1, sp), f"level {lv.tag} prepare")
+            return events
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            sp = stream_ptr()
+            for lv in self.levels:
+                if lv.struct is not None and lv.tag in "erd":
+                    check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 1, sp), f"level {lv.tag} prepare")
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    events[lv.step] = ev
+        return events
+
+    def forward(self, use_mask: bool, prepared=None):
+        """The render.  ``prepared``: None => run the FIR syntheses inline; a dict of
+        events from ``prepare(side)`` => wait on them; True => already done."""
         L = lib()
         sp = stream_ptr()
+        if prepared is None:
+            self.prepare()
+            prepared = True
+        main = torch.cuda.current_stream()
         if self.P:
             check(L.mgb_weights(ptr(self.params, self.layout.w_off), ptr(self.mask) if use_mask else None,
                                 ptr(self.w), self.P, sp), "mgb_weights")
         for lv in self.levels:
             if lv.struct is not None:
-                check(L.mgb_level_forward(ctypes.byref(lv.struct), sp), f"level {lv.tag} forward")
+                if isinstance(prepared, dict) and lv.step in prepared:
+                    main.wait_event(prepared[lv.step])
+                check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 2, sp), f"level {lv.tag} forward")
             else:
                 in_rows, seg, B = lv.bus
                 check(L.mgb_bus_sum(ptr(in_rows), ptr(seg), ptr(self.outs[lv.step]), B, self.L, sp),
@@ -274,25 +306,27 @@ class RenderPlan:
     def reg_total(self) -> torch.Tensor:
         return self.reg.sum()
 
-    def backward(self):
+    def backward(self, side=None):
+        """Reverse level sweep.  With ``side`` the FIR adjoints (backward phase 2)
+        run there, overlapping the following levels; the caller must join
+        (``current_stream().wait_stream(side)``) before reading the e/r/d grads."""
         L = lib()
         sp = stream_ptr()
+        main = torch.cuda.current_stream()
         for lv in reversed(self.levels):
             for src, off, buf in lv.fanouts:
                 check(L.mgb_bus_sum(ptr(src), ptr(off), ptr(buf), 1, self.L, sp), "fan-out sum")
-            if lv.struct is not None:
+            if lv.struct is None:
+                continue
+            if side is None or lv.tag not in "erd":
                 check(L.mgb_level_backward(ctypes.byref(lv.struct), sp), f"level {lv.tag} backward")
+                continue
+            check(L.mgb_level_backward_phase(ctypes.byref(lv.struct), 1, sp), f"level {lv.tag} backward")
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                check(L.mgb_level_backward_phase(ctypes.byref(lv.struct), 2, stream_ptr()),
+                      f"level {lv.tag} FIR adjoint")
 
-    def launches_forward(self) -> int:
-        return (1 if self.P else 0) + sum(_LAUNCHES_FWD.get(lv.tag, 1) for lv in self.levels)
-
-    def launches_backward(self) -> int:
-        return sum(_LAUNCHES_BWD.get(lv.tag, 0) + len(lv.fanouts) for lv in self.levels)
-
-
-# kernels each C-ABI level call launches (fft: 2 passes per transform when N > 8192)
-_LAUNCHES_FWD = {"g": 1, "s": 1, "c": 2, "n": 2, "e": 11, "r": 12, "d": 12, "m": 1, "o": 1}
-_LAUNCHES_BWD = {"g": 2, "s": 2, "c": 4, "n": 4, "e": 9, "r": 10, "d": 9}
 
 
 # ---------------------------------------------------------------------------
@@ -398,6 +432,7 @@ class TrainEngine:
         self.use_graph = use_graph
         self._graph = None
         self.d_rows = lay.rows["d"]
+        self.side = torch.cuda.Stream(device=dev)
 
     # -- state ------------------------------------------------------------
     def load_params(self, params):
@@ -416,9 +451,16 @@ class TrainEngine:
         L, ws, P = self.L, self.ws, self.layout.P
         plan, lp = self.plan, self.lossp
         Ld = lib()
-        plan.forward(use_mask=False)
+        main, side = torch.cuda.current_stream(), self.side
+        # side stream: FIR syntheses (params only), then the target spectra
+        prepared = plan.prepare(side)
+        with torch.cuda.stream(side):
+            lp.target(ptr(self.target, ws), ptr(self.target, L + ws))
+            tev = torch.cuda.Event()
+            tev.record(side)
+        plan.forward(use_mask=False, prepared=prepared)
         y = plan.y
-        lp.target(ptr(self.target, ws), ptr(self.target, L + ws))
+        main.wait_event(tev)
         lp.forward(ptr(y, ws), ptr(y, L + ws))
         reg = plan.reg_total()
         if P:
@@ -430,7 +472,8 @@ class TrainEngine:
         torch.stack([total, lp.loss, reg, self.sparsity], out=self.vals)
         plan.dY[:, :ws].zero_()
         lp.backward(ptr(y, ws), ptr(y, L + ws), ptr(plan.dY, ws), ptr(plan.dY, L + ws))
-        plan.backward()
+        plan.backward(side)
+        main.wait_stream(side)
         lay = self.layout
         check(Ld.mgb_adamw_step(ptr(self.params), ptr(self.grads), ptr(self.m), ptr(self.v), lay.n,
                                 lay.off["d"], self.d_rows, lay.w_off, P, ptr(plan.gw), None,
@@ -458,11 +501,20 @@ class TrainEngine:
         return values, g, plan.gw[:P].cpu().numpy().copy(), y.detach().cpu().numpy().copy()
 
     def launches_per_step(self) -> int:
-        n = self.plan.launches_forward() + self.plan.launches_backward()
-        n += 2 * self.lossp.launches("fwd") + self.lossp.launches("bwd") + 1  # target, fwd, bwd(+ola)
-        n += 1  # sparsity
-        n += 2 + (2 if self.d_rows else 0)  # raw-grad, adamw, delay rule, projection
-        return n
+        """Library kernels one step enqueues (counted by the C ABI over one eager step)."""
+        if getattr(self, "_launches", None) is None:
+            Ld = lib()
+            snap = [self.params.clone(), self.m.clone(), self.v.clone(), self.t]
+            self._set_scalars(0.0)
+            n0 = Ld.mgb_launch_count()
+            self._body()
+            self._launches = int(Ld.mgb_launch_count() - n0)
+            torch.cuda.synchronize(self.device)
+            self.params.copy_(snap[0])
+            self.m.copy_(snap[1])
+            self.v.copy_(snap[2])
+            self.t = snap[3]
+        return self._launches
 
     _RING = 64
 
@@ -551,9 +603,10 @@ class EvalEngine:
 
     def _body(self):
         L, ws = self.L, self.ws
+        self.plan.prepare()  # FIR syntheses once per trial, shared by all segments
         for i, stems in enumerate(self.seg_stems):
             self.plan.stems.copy_(stems)
-            self.plan.forward(use_mask=True)
+            self.plan.forward(use_mask=True, prepared=True)
             lp, _ = self.losses[i]
             lp.forward(ptr(self.plan.y, ws), ptr(self.plan.y, L + ws))
             self.acc[i].copy_(lp.loss)

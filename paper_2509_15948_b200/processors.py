@@ -35,7 +35,10 @@ GAIN_STAGING_EPS = 1e-8
 def _as_u(u, device=None):
     t = u if torch.is_tensor(u) else torch.as_tensor(np.asarray(u))
     dev = ensure_device(device or (t.device if t.is_cuda else "cuda"))
-    return t.to(device=dev, dtype=F32).contiguous()
+    t = t.to(device=dev, dtype=F32).contiguous()
+    if t.data_ptr() % 16:  # the level kernels use 16-byte vector loads on rows when L % 4 == 0
+        t = t.clone()
+    return t
 
 
 class _Level:
@@ -87,6 +90,8 @@ class _KernelFn(torch.autograd.Function):
         lv = ctx.lv
         B, L = lv.B, lv.L
         gy = (gy if gy is not None else torch.zeros_like(lv.y)).to(F32).contiguous()
+        if gy.data_ptr() % 16:
+            gy = gy.clone()
         gyr = dev_ptr_array([ptr(gy, b * 2 * L) for b in range(B)], gy.device)
         greg_t = (greg if greg is not None else torch.zeros((), device=gy.device)).to(F64).reshape(())
         gu = torch.empty((B, 2, L), dtype=F32, device=gy.device)

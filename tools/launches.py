@@ -1,4 +1,4 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list (last step of N eager steps)."""
+"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list: the last full train step."""
 import collections
 import csv
 import re
@@ -14,8 +14,14 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         data.append(dict(zip(hdr, r)))
-n = len(data) // steps
-step = data[-n:]
+# one train step ends with the unit-disk projection (k_project, or k_adamw without delays)
+ends = [i for i, d in enumerate(data) if "k_project" in d["Kernel Name"]] or \
+    [i for i, d in enumerate(data) if "k_adamw" in d["Kernel Name"]]
+if len(ends) >= 2:
+    step = data[ends[-2] + 1: ends[-1] + 1]
+else:
+    n = len(data) // steps
+    step = data[-n:]
 scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}
 agg = collections.defaultdict(lambda: [0, 0.0])
 tot = 0.0

@@ -1,0 +1,19 @@
+#!/bin/bash
+# One `ncu --set full` capture per kernel name (one launch each) of an eager
+# config-2 step.  Exports the details page and raw metrics as text/CSV on the
+# box (gpurun_out/ncu_<name>.{txt,csv}); the .ncu-rep is kept only with KEEP=1.
+# usage: tools/ncu_full.sh name[:skip] ...   (skip = matching launches to skip)
+mkdir -p gpurun_out
+for spec in "$@"; do
+  k=${spec%%:*}; skip=0
+  [[ "$spec" == *:* ]] && skip=${spec##*:}
+  rep=/tmp/ncu_${k}_${skip}
+  timeout 600 ncu --set full --import-source on --clock-control none -k "regex:$k" --launch-skip "$skip" -c 1 \
+    -o "$rep" -f python bench.py --eager-profile 1 > "gpurun_out/ncu_${k}.log" 2>&1
+  echo "$k rc=$?"
+  ncu -i "$rep.ncu-rep" --page details > "gpurun_out/ncu_${k}_${skip}.txt" 2>&1
+  ncu -i "$rep.ncu-rep" --page raw --csv > "gpurun_out/ncu_${k}_${skip}_raw.csv" 2>&1
+  ncu -i "$rep.ncu-rep" --page source --csv 2>&1 | gzip > "gpurun_out/ncu_${k}_${skip}_src.csv.gz"
+  [ "${KEEP:-0}" = 1 ] && cp "$rep.ncu-rep" gpurun_out/
+done
+du -sh gpurun_out
