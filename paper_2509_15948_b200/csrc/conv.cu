@@ -25,6 +25,7 @@
 //           custom surrogate backward (mg/processors.py:250-318)
 #include "common.cuh"
 #include "fourstep.cuh"
+#include "fs2.cuh"
 #include "mgb_internal.h"
 #include "tables.cuh"
 
@@ -415,14 +416,85 @@ struct Conv {
   }
 };
 
+// register-FFT four-step (fs2.cuh), N = N1 x 1024 with N1 = 4..1024
+template <int N1>
+struct Conv2 {
+  using G = fs2::G<N1>;
+  static constexpr int N2 = fs2::N2;
+  static void attrs() {
+    const int sc = (int)G::COL_SMEM;
+    if (sc > 0) {
+      cudaFuncSetAttribute(fs2::k_colA<N1, LdRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
+      cudaFuncSetAttribute(fs2::k_colA<N1, LdFir>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
+      cudaFuncSetAttribute(fs2::k_colA<N1, LdBwdPro>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
+      cudaFuncSetAttribute(fs2::k_colC<N1, EpFwd>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
+      cudaFuncSetAttribute(fs2::k_colC<N1, EpGx>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
+      cudaFuncSetAttribute(fs2::k_colC<N1, EpGh>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
+    }
+    cudaFuncSetAttribute(fs2::k_rowH<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWF_SMEM);
+    cudaFuncSetAttribute(fs2::k_rowF<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWF_SMEM);
+    cudaFuncSetAttribute(fs2::k_rowG<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWG_SMEM);
+  }
+
+  static int prep(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
+    const dim3 gc(N2 / G::TC, lv->B), gr(G::ROW_CTAS, lv->B);
+    const int fir_rows = (int)((g.M + N2 - 1) / N2);
+    fs2::k_colA<N1><<<gc, G::NT, G::COL_SMEM, st>>>(LdFir{w.hbuf, g.M}, w.Ah, fir_rows < N1 ? fir_rows : N1);
+    MGB_CHECK_LAUNCH();
+    fs2::k_rowH<N1><<<gr, 2 * fs2::RP * 32, fs2::ROWF_SMEM, st>>>(w.Ah, w.H);
+    MGB_CHECK_LAUNCH();
+    return 0;
+  }
+
+  static int fwd(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
+    const int B = lv->B, L = lv->L;
+    const dim3 gc(N2 / G::TC, B), gr(G::ROW_CTAS, B);
+    const int x_rows = (int)((L + N2 - 1) / N2);
+    fs2::k_colA<N1><<<gc, G::NT, G::COL_SMEM, st>>>(LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1);
+    MGB_CHECK_LAUNCH();
+    fs2::k_rowF<N1><<<gr, 2 * fs2::RP * 32, fs2::ROWF_SMEM, st>>>(w.Ax, w.H, w.X, w.Bo);
+    MGB_CHECK_LAUNCH();
+    EpFwd ep{lv->u_rows, lv->widx, lv->w, lv->y, lv->ybar, w.part, L, g.off};
+    fs2::k_colC<N1><<<gc, G::NT, G::COL_SMEM, st>>>(w.Bo, ep, 1.f / (float)G::N, N1);
+    MGB_CHECK_LAUNCH();
+    k_gs_norms<<<B, 256, 0, st>>>(w.part, G::NBLK, w.stats, lv->reg);
+    MGB_CHECK_LAUNCH();
+    return 0;
+  }
+
+  static int bwd(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
+    const int B = lv->B, L = lv->L;
+    const dim3 gc(N2 / G::TC, B), gr(G::ROW_CTAS, B);
+    LdBwdPro ld{lv->u_rows, lv->gy_rows, lv->ybar, lv->widx, lv->w, lv->greg, w.stats, lv->gu, w.part, L, g.off};
+    const int g_rows = (int)((g.off + L + N2 - 1) / N2);
+    fs2::k_colA<N1><<<gc, G::NT, G::COL_SMEM, st>>>(ld, w.Ax, g_rows < N1 ? g_rows : N1);
+    MGB_CHECK_LAUNCH();
+    k_dw_finalize<<<B, 256, 0, st>>>(w.part, G::NBLK, lv->widx, lv->w, lv->gw);
+    MGB_CHECK_LAUNCH();
+    fs2::k_rowG<N1><<<gr, 2 * fs2::RP * 32, fs2::ROWG_SMEM, st>>>(w.Ax, w.X, w.H, w.Bo, w.Ah);
+    MGB_CHECK_LAUNCH();
+    fs2::k_colC<N1><<<gc, G::NT, G::COL_SMEM, st>>>(w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1);
+    MGB_CHECK_LAUNCH();
+    const int h_rows = (int)((g.M + N2 - 1) / N2);
+    fs2::k_colC<N1><<<gc, G::NT, G::COL_SMEM, st>>>(w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
+                                                   h_rows < N1 ? h_rows : N1);
+    MGB_CHECK_LAUNCH();
+    return 0;
+  }
+};
+
+// register path for N <= 2^20 (N1 <= 1024), Stockham four-step above
 #define MGB_CONV_SIZES(X) \
-  X(12, 4, 1024) X(13, 8, 1024) X(14, 16, 1024) X(15, 32, 1024) X(16, 64, 1024) \
-  X(17, 128, 1024) X(18, 256, 1024) X(19, 512, 1024) X(20, 1024, 1024) X(21, 1024, 2048) X(22, 1024, 4096)
+  X(12, 4) X(13, 8) X(14, 16) X(15, 32) X(16, 64) X(17, 128) X(18, 256) X(19, 512) X(20, 1024)
+#define MGB_CONV_SIZES_OLD(X) X(21, 1024, 2048) X(22, 1024, 4096)
 
 int conv_fwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
   switch (g.logN) {
-#define X(l, a, b) case l: return Conv<a, b>::fwd(lv, w, g, st);
+#define X(l, a) case l: return Conv2<a>::fwd(lv, w, g, st);
     MGB_CONV_SIZES(X)
+#undef X
+#define X(l, a, b) case l: return Conv<a, b>::fwd(lv, w, g, st);
+    MGB_CONV_SIZES_OLD(X)
 #undef X
     default: return 1;
   }
@@ -430,8 +502,11 @@ int conv_fwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cu
 
 int conv_prep_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
   switch (g.logN) {
-#define X(l, a, b) case l: return Conv<a, b>::prep(lv, w, g, st);
+#define X(l, a) case l: return Conv2<a>::prep(lv, w, g, st);
     MGB_CONV_SIZES(X)
+#undef X
+#define X(l, a, b) case l: return Conv<a, b>::prep(lv, w, g, st);
+    MGB_CONV_SIZES_OLD(X)
 #undef X
     default: return 1;
   }
@@ -439,8 +514,11 @@ int conv_prep_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, c
 
 int conv_bwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
   switch (g.logN) {
-#define X(l, a, b) case l: return Conv<a, b>::bwd(lv, w, g, st);
+#define X(l, a) case l: return Conv2<a>::bwd(lv, w, g, st);
     MGB_CONV_SIZES(X)
+#undef X
+#define X(l, a, b) case l: return Conv<a, b>::bwd(lv, w, g, st);
+    MGB_CONV_SIZES_OLD(X)
 #undef X
     default: return 1;
   }
@@ -449,8 +527,11 @@ int conv_bwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cu
 }  // namespace
 
 int mgb_conv_init() {
-#define X(l, a, b) Conv<a, b>::attrs();
+#define X(l, a) Conv2<a>::attrs();
   MGB_CONV_SIZES(X)
+#undef X
+#define X(l, a, b) Conv<a, b>::attrs();
+  MGB_CONV_SIZES_OLD(X)
 #undef X
   if (cudaFuncSetAttribute(k_dly_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDlyBwdSmem) != cudaSuccess)
     return 2;

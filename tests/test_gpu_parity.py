@@ -228,3 +228,29 @@ def test_eval_loss_matches_oracle(dev):
     want = O.eval_loss(graph, params.params, params.raw_weights, mask,
                        [(stems.astype(np.float64), prep)], 30000, O.LossConfig())
     np.testing.assert_allclose(got, want, rtol=1e-5)
+
+
+# FFT-size coverage of the convolution levels (N = next_pow2(L + M - 1)): the
+# register four-step at N1 = 128..1024 (2^17..2^20), the Stockham four-step at
+# 2^21, and the overlap-save EQ at the production length, against the oracle.
+@pytest.mark.parametrize("tag,L", [("d", 441_000), ("r", 441_000), ("e", 441_000), ("r", 132_300),
+                                   ("d", 600_000), ("r", 1_100_000), ("d", 33_000)])
+def test_conv_level_matches_oracle_at_length(dev, tag, L):
+    from oracle import mixgraph_oracle as O
+    from paper_2509_15948_b200.processors import KERNELS
+    _, p, _ = kernel_inputs(tag)
+    rng = np.random.default_rng(L + ord(tag))
+    u = (0.3 * rng.standard_normal((2, 2, L))).astype(np.float32)
+    w = rng.standard_normal((2, 2, L))
+    ut = torch.tensor(u, device=dev, requires_grad=True)
+    pt = torch.tensor(p, dtype=torch.float64, device=dev, requires_grad=True)
+    ybar, reg = KERNELS[tag](ut, pt)
+    (torch.sum(ybar.double() * torch.tensor(w, device=dev)) + reg).backward()
+    uo = torch.tensor(u.astype(np.float64), requires_grad=True)
+    po = torch.tensor(p, requires_grad=True)
+    yo, rego = O.KERNELS[tag](uo, po)
+    (torch.sum(yo * torch.tensor(w)) + rego).backward()
+    assert normrel(ybar.detach().cpu().numpy(), yo.detach().numpy()) < 1e-5
+    np.testing.assert_allclose(float(reg.detach()), float(rego.detach()), rtol=1e-5, atol=2e-6)
+    assert normrel(ut.grad.cpu().numpy(), uo.grad.numpy()) < 1e-4
+    assert normrel(pt.grad.cpu().numpy(), po.grad.numpy(), floor=1e-6) < 1e-4
