@@ -62,14 +62,14 @@ struct ConvWs {
   float* aux;                  // r: frames (B,2,313,384) | d: colours (B,2,20,39)
   float* aux2;                 // r: dexpo (B,2,313,193)
   int* offs;                   // d: (B,2,20) quantised delays
-  float2 *Hs, *pspec;          // e (overlap-save): 8192-pt FIR spectra, per-block dh cross spectra
+  float2 *Hs, *pspec, *csum;   // e (overlap-save): 8192-pt FIR spectra, per-block / summed dh cross spectra
 };
 
 template <class A>
 ConvWs carve_into(A& a, char tag, int B, int L) {
   const ConvGeom g = geom(tag, L);
   ConvWs w;
-  w.Hs = w.pspec = nullptr;
+  w.Hs = w.pspec = w.csum = nullptr;
   if (tag == 'e') {  // overlap-save path: no four-step buffers
     w.Ax = w.Ah = w.X = w.H = w.Bo = nullptr;
     w.hbuf = a.template take<float2>((size_t)B * g.M);
@@ -79,7 +79,8 @@ ConvWs carve_into(A& a, char tag, int B, int L) {
     w.aux = w.aux2 = nullptr;
     w.offs = nullptr;
     w.Hs = a.template take<float2>((size_t)B * EOS_N);
-    w.pspec = a.template take<float2>((size_t)B * eos_nblk(L) * (EOS_N / 2 + 1));
+    w.pspec = a.template take<float2>((size_t)B * eos_nblk(L) * EOS_N);
+    w.csum = a.template take<float2>((size_t)B * EOS_N);
     return w;
   }
   const size_t BN = (size_t)B * g.N;
@@ -537,7 +538,7 @@ int mgb_conv_init() {
     return 2;
   cudaFuncSetAttribute(k_eqos_hspec, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
   cudaFuncSetAttribute(k_eqos_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
-  cudaFuncSetAttribute(k_eqos_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem2);
+  cudaFuncSetAttribute(k_eqos_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
   cudaFuncSetAttribute(k_eqos_gh, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
@@ -609,7 +610,7 @@ int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st) {
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
     const int nb = eos_nblk(L);
-    k_eqos_bwd<<<dim3(nb, B), EOS_NT, kEosSmem2, st>>>(lv->u_rows, lv->gy_rows, lv->ybar, w.Hs, lv->widx, lv->w,
+    k_eqos_bwd<<<dim3(nb, B), EOS_NT, kEosSmem1, st>>>(lv->u_rows, lv->gy_rows, lv->ybar, w.Hs, lv->widx, lv->w,
                                                        lv->greg, w.stats, lv->gu, w.part, w.pspec, L, nb);
     MGB_CHECK_LAUNCH();
     k_dw_finalize<<<B, 256, 0, st>>>(w.part, nb, lv->widx, lv->w, lv->gw);
@@ -627,7 +628,9 @@ int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st) {
   MgbArena a{(char*)lv->ws, 0};
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
-    k_eqos_gh<<<B, EOS_NT, kEosSmem1, st>>>(w.pspec, eos_nblk(L), w.ghbuf);
+    k_eqos_csum<<<dim3(EOS_N / 256, B), 256, 0, st>>>(w.pspec, eos_nblk(L), w.csum);
+    MGB_CHECK_LAUNCH();
+    k_eqos_gh<<<B, EOS_NT, kEosSmem1, st>>>(w.csum, w.ghbuf);
     MGB_CHECK_LAUNCH();
     k_eq_fir_bwd<<<dim3(MGB_EQ_BINS / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.ghbuf, g.M, lv->gbank);
   } else if (tag == 'r') {

@@ -1,4 +1,5 @@
-// Equalizer level by overlap-save in shared memory (included by conv.cu).
+// Equalizer level by overlap-save with register-resident 8192-point FFTs
+// (included by conv.cu).
 //
 // ybar[n] = sum_t h[t] x[n + 1023 - t]  (2047-tap zero-phase FIR, offset 1023,
 // mg/processors.py:115-120 via mg/engine.py:549-585).  Output block
@@ -7,114 +8,206 @@
 // (8192-point circular convolution, no wrap).  Both channels ride one complex
 // transform (h is real and shared, so Y = Z H needs no pairing).
 //
-// Backward per block (one CTA, two 8192-point buffers):
-//   d window  dw[i] = dybar[n0 - 1023 + i] computed on the fly from
-//             (gy, ybar) = w gy + gain-staging term;
-//   gx[n0+j]  = (dw corr h)[j]           -> gu = (1-w) gy + gain-staging + gx, one write
-//   gh part   = sum_{n in block} dybar[n] x[n + 1023 - t]
-//             = IDFT( conj(FFT(dw masked to the block)) . FFT(xw) )[(1023 - t) mod 8192]
-//   the per-block cross spectra are summed per node by k_eqos_gh (float64) and
-//   one inverse FFT gives dh, consumed by the existing FIR adjoint k_eq_fir_bwd.
+// The 8192-point transform (eos_fft / eos_ifft) runs on 256 threads holding 32
+// values each: a 32-point register DFT, one exchange, 2 x 16-point register
+// DFTs, one exchange, 2 x 16-point register DFTs (8192 = 32 x 16 x 16).  The
+// forward leaves spectra in a fixed thread-private order (thread t, slot r),
+// which is exactly the input order of the inverse, so pointwise products
+// with a spectrum stored in the same order (Hs[r][t]) need no shuffling.
+//
+// Backward per block (one CTA):
+//   D   = FFT(d window), d = dybar = w gy + gain-staging term (on the fly)
+//   gx  = IDFT(D conj H)[j], j < HOP  -> gu = (1-w) gy + gain-staging + gx
+//   C   = conj(D) FFT(x masked to the block)      (packed: conj(d_l + i d_r)(x_l + i x_r))
+//   dh[t] = Re IDFT(sum_blocks C)[(1023 - t) mod 8192] = sum_c sum_n d_c[n] x_c[n + 1023 - t]
+//   (the real part of the packed cross-correlation is the channel sum; the
+//   per-block C are reduced in float64 by k_eqos_gh)
 #pragma once
+#include "regfft.cuh"
 
 constexpr int EOS_N = 8192;
 constexpr int EOS_OFF = (MGB_EQ_LEN - 1) / 2;        // 1023
 constexpr int EOS_HOP = EOS_N - (MGB_EQ_LEN - 1);    // 6146
-constexpr int EOS_NT = 512;
-constexpr int EOS_P = padded_len<EOS_N>();
-constexpr int kEosSmem1 = EOS_P * 8;
-constexpr int kEosSmem2 = 2 * EOS_P * 8;
-constexpr int EOS_PER = EOS_N / EOS_NT;              // 16 window elements per thread
-constexpr int EOS_OUT = (EOS_HOP + EOS_NT - 1) / EOS_NT;  // 13 outputs per thread
+constexpr int EOS_NT = 256;
+constexpr int EOS_S2P = 17;                          // stage-2 exchange row pitch
+constexpr int EOS_SM = 32 * 16 * EOS_S2P;            // 8704 float2 >= 8192
+constexpr int kEosSmem1 = EOS_SM * 8;
 
 int eos_nblk(int L) { return (L + EOS_HOP - 1) / EOS_HOP; }
 
-// H = FFT_8192(h) per node, natural order
-__global__ void __launch_bounds__(EOS_NT) k_eqos_hspec(const float2* __restrict__ hbuf, float2* __restrict__ Hs) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  float2* s = reinterpret_cast<float2*>(dsm);
-  const int b = blockIdx.x;
-  for (int i = threadIdx.x; i < EOS_N; i += EOS_NT)
-    s[pidx<true>(i)] = make_float2(i < MGB_EQ_LEN ? hbuf[(size_t)b * MGB_EQ_LEN + i].x : 0.f, 0.f);
-  smem_fft<float, EOS_N, 1, EOS_NT, EOS_P, 1, false, true>(s, false);
-  for (int i = threadIdx.x; i < EOS_N; i += EOS_NT) Hs[(size_t)b * EOS_N + i] = s[pidx<true>(i)];
+// natural order (thread t holds x[t + 256 m]) -> spectrum in (t, r) order:
+// v[s*16 + ka] = X[k1 + 32 kb + 512 ka], k1 = (t >> 4) + 16 s, kb = t & 15
+__device__ __forceinline__ void eos_fft(float2 (&v)[32], float2* S) {
+  const int t = threadIdx.x, lo = t & 15, kq = t >> 4;
+  rf::rdft<32, false>(v);
+  fs2::twiddle_run<13, 32, false>(v, 0, t);
+#pragma unroll
+  for (int k1 = 0; k1 < 32; ++k1) S[k1 * 256 + t] = v[k1];
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int k1 = kq + 16 * s;
+    float2 u[16];
+#pragma unroll
+    for (int tb = 0; tb < 16; ++tb) u[tb] = S[k1 * 256 + lo + 16 * tb];
+    rf::rdft<16, false>(u);
+    fs2::twiddle_run<8, 16, false>(u, 0, lo);
+#pragma unroll
+    for (int kb = 0; kb < 16; ++kb) v[s * 16 + kb] = u[kb];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int k1 = kq + 16 * s;
+#pragma unroll
+    for (int kb = 0; kb < 16; ++kb) S[k1 * 16 * EOS_S2P + kb * EOS_S2P + lo] = v[s * 16 + kb];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int k1 = kq + 16 * s;
+    float2 u[16];
+#pragma unroll
+    for (int ta = 0; ta < 16; ++ta) u[ta] = S[k1 * 16 * EOS_S2P + lo * EOS_S2P + ta];
+    rf::rdft<16, false>(u);
+#pragma unroll
+    for (int ka = 0; ka < 16; ++ka) v[s * 16 + ka] = u[ka];
+  }
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(EOS_NT) k_eqos_fwd(const float* const* __restrict__ u_rows,
+// (t, r) spectrum order -> natural order, unnormalised inverse
+__device__ __forceinline__ void eos_ifft(float2 (&v)[32], float2* S) {
+  const int t = threadIdx.x, lo = t & 15, kq = t >> 4;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int k1 = kq + 16 * s;
+    float2 u[16];
+#pragma unroll
+    for (int ka = 0; ka < 16; ++ka) u[ka] = v[s * 16 + ka];
+    rf::rdft<16, true>(u);
+#pragma unroll
+    for (int ta = 0; ta < 16; ++ta) S[k1 * 16 * EOS_S2P + lo * EOS_S2P + ta] = u[ta];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int k1 = kq + 16 * s;
+    float2 u[16];
+#pragma unroll
+    for (int kb = 0; kb < 16; ++kb) u[kb] = S[k1 * 16 * EOS_S2P + kb * EOS_S2P + lo];
+    fs2::twiddle_run<8, 16, true>(u, 0, lo);
+    rf::rdft<16, true>(u);
+#pragma unroll
+    for (int tb = 0; tb < 16; ++tb) v[s * 16 + tb] = u[tb];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int k1 = kq + 16 * s;
+#pragma unroll
+    for (int tb = 0; tb < 16; ++tb) S[k1 * 256 + lo + 16 * tb] = v[s * 16 + tb];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k1 = 0; k1 < 32; ++k1) v[k1] = S[k1 * 256 + t];
+  fs2::twiddle_run<13, 32, true>(v, 0, t);
+  rf::rdft<32, true>(v);
+  __syncthreads();
+}
+
+// H = FFT_8192(h) per node, (t, r) order: Hs[b][r * 256 + t]
+__global__ void __launch_bounds__(EOS_NT) k_eqos_hspec(const float2* __restrict__ hbuf, float2* __restrict__ Hs) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float2* S = reinterpret_cast<float2*>(dsm);
+  const int b = blockIdx.x, t = threadIdx.x;
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int i = t + 256 * m;
+    v[m] = make_float2(i < MGB_EQ_LEN ? hbuf[(size_t)b * MGB_EQ_LEN + i].x : 0.f, 0.f);
+  }
+  eos_fft(v, S);
+#pragma unroll
+  for (int r = 0; r < 32; ++r) Hs[(size_t)b * EOS_N + r * 256 + t] = v[r];
+}
+
+__global__ void __launch_bounds__(EOS_NT, 2) k_eqos_fwd(const float* const* __restrict__ u_rows,
                                                      const float2* __restrict__ Hs, const int* __restrict__ widx,
                                                      const double* __restrict__ w, float* __restrict__ y,
                                                      float* __restrict__ ybar, double* __restrict__ part, int L) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  float2* s = reinterpret_cast<float2*>(dsm);
+  float2* S = reinterpret_cast<float2*>(dsm);
   __shared__ double red[32];
-  const int blk = blockIdx.x, b = blockIdx.y;
+  const int blk = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
   const float* u = u_rows[b];
   const long long n0 = (long long)blk * EOS_HOP, w0 = n0 - EOS_OFF;
-  {
-    float2 v[EOS_PER];
+  float2 v[32];
 #pragma unroll
-    for (int k = 0; k < EOS_PER; ++k) {
-      const long long n = w0 + threadIdx.x + EOS_NT * k;
-      v[k] = (n >= 0 && n < L) ? make_float2(__ldg(u + n), __ldg(u + L + n)) : make_float2(0.f, 0.f);
-    }
-#pragma unroll
-    for (int k = 0; k < EOS_PER; ++k) s[pidx<true>(threadIdx.x + EOS_NT * k)] = v[k];
+  for (int m = 0; m < 32; ++m) {
+    const long long n = w0 + t + 256 * m;
+    v[m] = (n >= 0 && n < L) ? make_float2(__ldg(u + n), __ldg(u + L + n)) : make_float2(0.f, 0.f);
   }
-  smem_fft<float, EOS_N, 1, EOS_NT, EOS_P, 1, false, true>(s, false);
-  const float2* H = Hs + (size_t)b * EOS_N;
+  eos_fft(v, S);
+  const float2* H = Hs + (size_t)b * EOS_N + t;
   const float sc = 1.f / (float)EOS_N;
-#pragma unroll 4
-  for (int k = 0; k < EOS_PER; ++k) {
-    const int i = threadIdx.x + EOS_NT * k;
-    const float2 h = __ldg(H + i);
-    const float2 z = s[pidx<true>(i)];
-    s[pidx<true>(i)] = make_float2(sc * (z.x * h.x - z.y * h.y), sc * (z.x * h.y + z.y * h.x));
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const float2 h = __ldg(H + r * 256);
+    v[r] = make_float2(sc * (v[r].x * h.x - v[r].y * h.y), sc * (v[r].x * h.y + v[r].y * h.x));
   }
-  smem_fft<float, EOS_N, 1, EOS_NT, EOS_P, 1, false, true>(s, true);
+  eos_ifft(v, S);
+  // window index i = t + 256 m holds ybar[n0 + i - 2046] for i >= 2046
   const double wv = w ? w[widx[b]] : 1.0;
   const float wf = (float)wv, om = (float)(1.0 - wv);
   const bool bypass = wv == 0.0;
   float* yo = y + (size_t)b * 2 * L;
   float* yb = ybar + (size_t)b * 2 * L;
-  float2 uu[EOS_OUT];
-#pragma unroll
-  for (int k = 0; k < EOS_OUT; ++k) {
-    const int j = threadIdx.x + EOS_NT * k;
-    const long long n = n0 + j;
-    uu[k] = (j < EOS_HOP && n < L) ? make_float2(__ldg(u + n), __ldg(u + L + n)) : make_float2(0.f, 0.f);
-  }
   float su = 0.f, sy = 0.f;
 #pragma unroll
-  for (int k = 0; k < EOS_OUT; ++k) {
-    const int j = threadIdx.x + EOS_NT * k;
-    const long long n = n0 + j;
-    if (j < EOS_HOP && n < L) {
-      const float2 v = s[pidx<true>(EOS_N - EOS_HOP + j)];
-      yb[n] = v.x;
-      yb[L + n] = v.y;
-      if (bypass) {
-        yo[n] = uu[k].x;
-        yo[L + n] = uu[k].y;
-      } else {
-        yo[n] = wf * v.x + om * uu[k].x;
-        yo[L + n] = wf * v.y + om * uu[k].y;
+  for (int m0 = 7; m0 < 32; m0 += 5) {
+    float2 uu[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const int i = t + 256 * (m0 + q);
+      const long long n = n0 + i - (EOS_N - EOS_HOP);
+      uu[q] = (m0 + q < 32 && i >= EOS_N - EOS_HOP && n < L) ? make_float2(__ldg(u + n), __ldg(u + L + n))
+                                                              : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const int m = m0 + q;
+      if (m >= 32) break;
+      const int i = t + 256 * m;
+      const long long n = n0 + i - (EOS_N - EOS_HOP);
+      if (i >= EOS_N - EOS_HOP && n < L) {
+        const float2 vv = v[m];
+        yb[n] = vv.x;
+        yb[L + n] = vv.y;
+        if (bypass) {
+          yo[n] = uu[q].x;
+          yo[L + n] = uu[q].y;
+        } else {
+          yo[n] = wf * vv.x + om * uu[q].x;
+          yo[L + n] = wf * vv.y + om * uu[q].y;
+        }
+        const float mu = uu[q].x + uu[q].y, my = vv.x + vv.y;
+        su = fmaf(mu, mu, su);
+        sy = fmaf(my, my, sy);
       }
-      const float mu = uu[k].x + uu[k].y, my = v.x + v.y;
-      su = fmaf(mu, mu, su);
-      sy = fmaf(my, my, sy);
     }
   }
   const double tu = block_sum((double)su, red);
   __syncthreads();
   const double ty = block_sum((double)sy, red);
-  if (threadIdx.x == 0) {
+  if (t == 0) {
     double* pp = part + ((size_t)b * kMaxParts + blk) * 4;
     pp[0] = tu;
     pp[1] = ty;
   }
 }
 
-__global__ void __launch_bounds__(EOS_NT) k_eqos_bwd(const float* const* __restrict__ u_rows,
+__global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __restrict__ u_rows,
                                                      const float* const* __restrict__ gy_rows,
                                                      const float* __restrict__ ybar, const float2* __restrict__ Hs,
                                                      const int* __restrict__ widx, const double* __restrict__ w,
@@ -123,10 +216,9 @@ __global__ void __launch_bounds__(EOS_NT) k_eqos_bwd(const float* const* __restr
                                                      double* __restrict__ part, float2* __restrict__ pspec,
                                                      int L, int nblk) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  float2* A = reinterpret_cast<float2*>(dsm);  // full d window, then xw
-  float2* Bm = A + EOS_P;                       // d window masked to this block
+  float2* S = reinterpret_cast<float2*>(dsm);
   __shared__ double red[32];
-  const int blk = blockIdx.x, b = blockIdx.y;
+  const int blk = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
   const float* u = u_rows[b];
   const float* gy = gy_rows[b];
   const float* yb = ybar + (size_t)b * 2 * L;
@@ -138,115 +230,110 @@ __global__ void __launch_bounds__(EOS_NT) k_eqos_bwd(const float* const* __restr
   const double nu = stats[b * 4], ny = stats[b * 4 + 1];
   const float cy = (ny > 0.0) ? (float)(sg / ((ny + MGB_GS_EPS) * ny)) : 0.f;
   const float cu = (nu > 0.0) ? (float)(-sg / ((nu + MGB_GS_EPS) * nu)) : 0.f;
-  // 1. dybar window (full) and its block-masked copy
-#pragma unroll 1
-  for (int k0 = 0; k0 < EOS_PER; k0 += 8) {
-    float4 g[8];
+  float2 v[32];
+  // 1. d window (dybar) and D
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const long long n = w0 + threadIdx.x + EOS_NT * (k0 + k);
-      g[k] = (n >= 0 && n < L) ? make_float4(__ldg(gy + n), __ldg(gy + L + n), __ldg(yb + n), __ldg(yb + L + n))
+  for (int m0 = 0; m0 < 32; m0 += 4) {
+    float4 g[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long n = w0 + t + 256 * (m0 + q);
+      g[q] = (n >= 0 && n < L) ? make_float4(__ldg(gy + n), __ldg(gy + L + n), __ldg(yb + n), __ldg(yb + L + n))
                                : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int i = threadIdx.x + EOS_NT * (k0 + k);
-      const float my = g[k].z + g[k].w;
-      const float2 d = make_float2(fmaf(cy, my, wf * g[k].x), fmaf(cy, my, wf * g[k].y));
-      const long long n = w0 + i;
-      A[pidx<true>(i)] = d;
-      const bool inblk = i >= EOS_OFF && i < EOS_OFF + EOS_HOP && n < L;
-      Bm[pidx<true>(i)] = inblk ? d : make_float2(0.f, 0.f);
+    for (int q = 0; q < 4; ++q) {
+      const float my = g[q].z + g[q].w;
+      v[m0 + q] = make_float2(fmaf(cy, my, wf * g[q].x), fmaf(cy, my, wf * g[q].y));
     }
   }
-  smem_fft<float, EOS_N, 2, EOS_NT, EOS_P, 1, false, true>(A, false);
-  // 2. gx = IDFT(D conj(H)) over the block, fused with the dry/wet + gain-staging prologue
-  const float2* H = Hs + (size_t)b * EOS_N;
+  eos_fft(v, S);
+  // D parks in this block's pspec slot (thread-private [r][t] entries, L2-resident) until step 3
+  float2* ps = pspec + ((size_t)b * nblk + blk) * EOS_N + t;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) ps[r * 256] = v[r];
+  // 2. gx = IDFT(D conj H): window index i < HOP is gx[n0 + i]
+  const float2* H = Hs + (size_t)b * EOS_N + t;
   const float sc = 1.f / (float)EOS_N;
-#pragma unroll 4
-  for (int k = 0; k < EOS_PER; ++k) {
-    const int i = threadIdx.x + EOS_NT * k;
-    const float2 h = __ldg(H + i);
-    const float2 z = A[pidx<true>(i)];
-    A[pidx<true>(i)] = make_float2(sc * (z.x * h.x + z.y * h.y), sc * (z.y * h.x - z.x * h.y));
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const float2 h = __ldg(H + r * 256);
+    v[r] = make_float2(sc * (v[r].x * h.x + v[r].y * h.y), sc * (v[r].y * h.x - v[r].x * h.y));
   }
-  smem_fft<float, EOS_N, 1, EOS_NT, EOS_P, 1, false, true>(A, true);
+  eos_ifft(v, S);
   float* go = gu + (size_t)b * 2 * L;
   float fw = 0.f;
-  {
-    float4 gq[EOS_OUT];
-    float4 uq[EOS_OUT];
 #pragma unroll
-    for (int k = 0; k < EOS_OUT; ++k) {
-      const int j = threadIdx.x + EOS_NT * k;
-      const long long n = n0 + j;
-      const bool in = j < EOS_HOP && n < L;
-      gq[k] = in ? make_float4(__ldg(gy + n), __ldg(gy + L + n), __ldg(yb + n), __ldg(yb + L + n))
+  for (int m0 = 0; m0 < EOS_HOP / 256 + 1; m0 += 5) {  // window indices i < HOP: m <= 24
+    float4 gq[5];
+    float2 uq[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const int i = t + 256 * (m0 + q);
+      const long long n = n0 + i;
+      const bool in = i < EOS_HOP && n < L;
+      gq[q] = in ? make_float4(__ldg(gy + n), __ldg(gy + L + n), __ldg(yb + n), __ldg(yb + L + n))
                  : make_float4(0.f, 0.f, 0.f, 0.f);
-      uq[k] = in ? make_float4(__ldg(u + n), __ldg(u + L + n), 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+      uq[q] = in ? make_float2(__ldg(u + n), __ldg(u + L + n)) : make_float2(0.f, 0.f);
     }
 #pragma unroll
-    for (int k = 0; k < EOS_OUT; ++k) {
-      const int j = threadIdx.x + EOS_NT * k;
-      const long long n = n0 + j;
-      if (j < EOS_HOP && n < L) {
-        const float2 gx = A[pidx<true>(j)];
-        const float mu = uq[k].x + uq[k].y;
-        const float ul = bypass ? gq[k].x : om * gq[k].x, ur = bypass ? gq[k].y : om * gq[k].y;
+    for (int q = 0; q < 5; ++q) {
+      const int i = t + 256 * (m0 + q);
+      const long long n = n0 + i;
+      if (i < EOS_HOP && n < L) {
+        const float2 gx = v[m0 + q];
+        const float mu = uq[q].x + uq[q].y;
+        const float ul = bypass ? gq[q].x : om * gq[q].x, ur = bypass ? gq[q].y : om * gq[q].y;
         go[n] = fmaf(cu, mu, ul) + gx.x;
         go[L + n] = fmaf(cu, mu, ur) + gx.y;
-        if (!bypass) fw = fmaf(gq[k].x, gq[k].z - uq[k].x, fmaf(gq[k].y, gq[k].w - uq[k].y, fw));
+        if (!bypass) fw = fmaf(gq[q].x, gq[q].z - uq[q].x, fmaf(gq[q].y, gq[q].w - uq[q].y, fw));
       }
     }
   }
   const double tw = block_sum((double)fw, red);
-  if (threadIdx.x == 0) part[((size_t)b * kMaxParts + blk) * 4 + 2] = tw;
-  // 3. xw and the cross spectrum  sum_c conj(D'_c) XW_c  (Hermitian pairing on both)
-  {
-    float2 v[EOS_PER];
+  if (t == 0) part[((size_t)b * kMaxParts + blk) * 4 + 2] = tw;
+  // 3. x masked to the block, its spectrum, C = conj(D) Xm
 #pragma unroll
-    for (int k = 0; k < EOS_PER; ++k) {
-      const long long n = w0 + threadIdx.x + EOS_NT * k;
-      v[k] = (n >= 0 && n < L) ? make_float2(__ldg(u + n), __ldg(u + L + n)) : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
+  for (int m = 0; m < 32; ++m) {
+    const int i = t + 256 * m;
+    const long long n = w0 + i;
+    v[m] = (i >= EOS_OFF && i < EOS_OFF + EOS_HOP && n < L) ? make_float2(__ldg(u + n), __ldg(u + L + n))
+                                                              : make_float2(0.f, 0.f);
+  }
+  eos_fft(v, S);
 #pragma unroll
-    for (int k = 0; k < EOS_PER; ++k) A[pidx<true>(threadIdx.x + EOS_NT * k)] = v[k];
-  }
-  smem_fft<float, EOS_N, 1, EOS_NT, EOS_P, 1, false, true>(A, false);
-  float2* ps = pspec + ((size_t)b * nblk + blk) * (EOS_N / 2 + 1);
-  for (int k = threadIdx.x; k <= EOS_N / 2; k += EOS_NT) {
-    const int p = (EOS_N - k) & (EOS_N - 1);
-    float2 dl, dr, xl, xr;
-    fs::split_pair(Bm[pidx<true>(k)], Bm[pidx<true>(p)], dl, dr);
-    fs::split_pair(A[pidx<true>(k)], A[pidx<true>(p)], xl, xr);
-    const float2 c1 = cmulc(xl, dl), c2 = cmulc(xr, dr);  // X conj(D)
-    ps[k] = make_float2(c1.x + c2.x, c1.y + c2.y);
-  }
+  for (int r = 0; r < 32; ++r) ps[r * 256] = cmulc(v[r], ps[r * 256]);
 }
 
-// dh[t] = (1/N) IDFT( sum_blocks P )[(1023 - t) mod N], P Hermitian (real correlation)
-__global__ void __launch_bounds__(EOS_NT) k_eqos_gh(const float2* __restrict__ pspec, int nblk,
-                                                    float2* __restrict__ ghbuf) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  float2* s = reinterpret_cast<float2*>(dsm);
-  const int b = blockIdx.x;
-  const float2* ps = pspec + (size_t)b * nblk * (EOS_N / 2 + 1);
-  for (int k = threadIdx.x; k <= EOS_N / 2; k += EOS_NT) {
-    double re = 0.0, im = 0.0;
-    for (int q = 0; q < nblk; ++q) {
-      const float2 v = ps[(size_t)q * (EOS_N / 2 + 1) + k];
-      re += v.x;
-      im += v.y;
-    }
-    const float2 v = make_float2((float)re, (float)im);
-    s[pidx<true>(k)] = v;
-    if (k != 0 && k != EOS_N / 2) s[pidx<true>(EOS_N - k)] = make_float2(v.x, -v.y);
+// Csum[b][slot] = sum over blocks of C (float64, fixed order), one thread per slot
+__global__ void __launch_bounds__(256) k_eqos_csum(const float2* __restrict__ pspec, int nblk,
+                                                   float2* __restrict__ csum) {
+  const int b = blockIdx.y, slot = blockIdx.x * 256 + threadIdx.x;
+  const float2* ps = pspec + (size_t)b * nblk * EOS_N + slot;
+  double re = 0.0, im = 0.0;
+#pragma unroll 8
+  for (int q = 0; q < nblk; ++q) {
+    const float2 c = __ldg(ps + (size_t)q * EOS_N);
+    re += c.x;
+    im += c.y;
   }
-  smem_fft<float, EOS_N, 1, EOS_NT, EOS_P, 1, false, true>(s, true);
+  csum[(size_t)b * EOS_N + slot] = make_float2((float)re, (float)im);
+}
+
+// dh[t] = Re IDFT(Csum)[(1023 - t) mod N] / N
+__global__ void __launch_bounds__(EOS_NT) k_eqos_gh(const float2* __restrict__ csum, float2* __restrict__ ghbuf) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float2* S = reinterpret_cast<float2*>(dsm);
+  const int b = blockIdx.x, t = threadIdx.x;
+  float2 v[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) v[r] = csum[(size_t)b * EOS_N + r * 256 + t];
+  eos_ifft(v, S);
   const float sc = 1.f / (float)EOS_N;
-  for (int t = threadIdx.x; t < MGB_EQ_LEN; t += EOS_NT) {
-    const int sidx = (EOS_OFF - t) & (EOS_N - 1);
-    ghbuf[(size_t)b * MGB_EQ_LEN + t] = make_float2(sc * s[pidx<true>(sidx)].x, 0.f);
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int i = t + 256 * m;
+    const int tt = (EOS_OFF - i) & (EOS_N - 1);
+    if (tt < MGB_EQ_LEN) ghbuf[(size_t)b * MGB_EQ_LEN + tt] = make_float2(sc * v[m].x, 0.f);
   }
 }
