@@ -15,6 +15,13 @@
 // (fp32 recursions lose 1e-4..1e-3 at long ballistics);
 // inputs x = mid^2, the envelope and the gain computer are float32.
 //
+// Forward in one scan pass: by linearity the truncated filter is the plain
+// recursion driven by the differenced input x'[n] = x[n] - a^8192 x[n-8192]
+// (S[n] = sum_{k<8192} a^k x[n-k] = IIR(x')[n]), so a CTA scans only its own
+// chunk; x' is formed in float64 from the float32 mid^2 of this chunk and of
+// the previous one (same local offset).  The gain computer runs in float32
+// with MUFU exp/log (abs. error ~1e-6 in the log domain, far inside 1e-4).
+//
 // Backward: the adjoint of the truncated causal filter is the truncated
 // anti-causal filter — the same construction on reversed time with the
 // 2-state recursion  v[m] = a v[m+1] + dg[m],  w[m] = a (w[m+1] + v[m+1]):
@@ -37,6 +44,7 @@ constexpr int NPW = 14;  // pw[i] = a^(SEG * 2^i)
 struct DynP {
   double la, a, b, aC;
   float T, W, R;
+  float iR, i2W, i4W;  // 1/R, 1/(2W), 1/(4W)
   double Wraw, Rraw;
 };
 
@@ -52,13 +60,16 @@ __device__ __forceinline__ DynP load_params(const double* bank, int row) {
   q.Rraw = p[3];
   q.W = (float)(softplus64(p[2]) + 1e-3);
   q.R = (float)(softplus64(p[3]) + 1.0);
+  q.iR = 1.f / q.R;
+  q.i2W = 1.f / (2.f * q.W);
+  q.i4W = 1.f / (4.f * q.W);
   return q;
 }
 
 __device__ __forceinline__ float mid_sq(const float* u, int L, long long n) {
   if (n < 0 || n >= L) return 0.f;
-  const double m = (double)u[n] + (double)u[L + n];
-  return (float)(m * m);
+  const float m = __ldg(u + n) + __ldg(u + L + n);
+  return m * m;
 }
 
 // a^(SEG * k) for 0 <= k < 2^NPW from the power table
@@ -77,15 +88,15 @@ __device__ __forceinline__ float knee_gy(float G, const DynP& q, bool gate) {
     if (above) return G;
     if (below) return q.T + q.R * (G - q.T);
     const float z = G - q.T - q.W;
-    return G + (1.f - q.R) * (z * z / (q.W * 4.f));
+    return G + (1.f - q.R) * (z * z * q.i4W);
   }
-  if (above) return q.T + (G - q.T) / q.R;
+  if (above) return q.T + (G - q.T) * q.iR;
   if (below) return G;
   const float z = G - q.T + q.W;
-  return G + (1.f / q.R - 1.f) * (z * z / (q.W * 4.f));
+  return G + (q.iR - 1.f) * (z * z * q.i4W);
 }
 
-__device__ __forceinline__ float env_log(float gc) { return logf(fmaxf(gc, 0.f) + 1e-8f); }
+__device__ __forceinline__ float env_log(float gc) { return __logf(fmaxf(gc, 0.f) + 1e-8f); }
 
 // Two forward exclusive scans at once: S_t = a^SEG S_{t-1} + v_t over the
 // block's threads; returns the state at the end of thread t-1's segment.
@@ -120,37 +131,41 @@ __device__ __forceinline__ void scan2_excl(double& v0, double& v1, const double*
   v1 = fma(sh[NW + wid], pl, p1);
 }
 
-__device__ __forceinline__ void init_pw(double* pw, double la) {
-  if (threadIdx.x < NPW) pw[threadIdx.x] = exp((double)SEG * (double)(1 << threadIdx.x) * la);
+// one forward exclusive scan S_t = a^SEG S_{t-1} + v_t over the block's threads
+__device__ __forceinline__ void scan1_excl(double& v0, const double* pw, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double s0 = v0;
+#pragma unroll
+  for (int o = 1, i = 0; o < 32; o <<= 1, ++i) {
+    const double t0 = __shfl_up_sync(0xffffffffu, s0, o);
+    if (lane >= o) s0 = fma(pw[i], t0, s0);
+  }
+  if (lane == 31) sh[wid] = s0;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive over warps (carry into warp w)
+    double c = 0.0;
+    for (int w = 0; w < NW; ++w) {
+      const double tot = sh[w];
+      sh[w] = c;
+      c = fma(c, pw[5], tot);  // a^(SEG*32)
+    }
+  }
+  __syncthreads();
+  double p0 = __shfl_up_sync(0xffffffffu, s0, 1);
+  if (lane == 0) p0 = 0.0;
+  v0 = fma(sh[wid], powseg(pw, lane), p0);
 }
 
-// chunk aggregates: agg[b][j] = sum_{n in chunk j} a^{end-n} x[n]   (no (1-a) factor).
-// Coalesced: thread t visits offsets o = t + NT k; weights a^{CH-1-o} walk down by a^NT.
-__global__ void __launch_bounds__(NT) k_dyn_agg(const float* const* __restrict__ u_rows,
-                                                const double* __restrict__ bank, const int* __restrict__ prow,
-                                                double* __restrict__ agg, int L, int nch) {
-  __shared__ double red[32];
-  const int j = blockIdx.x, b = blockIdx.y;
-  const float* u = u_rows[b];
-  const DynP q = load_params(bank, prow[b]);
-  const long long c0 = (long long)j * CH;
-  const double step = exp((double)NT * q.la);
-  double wgt = exp((double)(NT - 1 - threadIdx.x) * q.la);  // o = t + NT*(SEG-1)
-  double acc = 0.0;
-#pragma unroll
-  for (int k = SEG - 1; k >= 0; --k) {
-    acc = fma(wgt, (double)mid_sq(u, L, c0 + threadIdx.x + (long long)NT * k), acc);
-    wgt *= step;
-  }
-  const double tot = block_sum(acc, red);
-  if (threadIdx.x == 0) agg[(size_t)b * nch + j] = tot;
+__device__ __forceinline__ void init_pw(double* pw, double la) {
+  if (threadIdx.x < NPW) pw[threadIdx.x] = exp((double)SEG * (double)(1 << threadIdx.x) * la);
 }
 
 // padded segment-major staging index: thread t's sample i of a chunk
 __device__ __forceinline__ int sidx(int t, int i) { return t * (SEG + 1) + i; }
 __device__ __forceinline__ int sidx_n(int o) { return sidx(o / SEG, o % SEG); }
 constexpr int SPAD = NT * (SEG + 1);
-constexpr int kDynSmem = 2 * SPAD * 4;
+constexpr int kDynSmem = 2 * SPAD * 4;                 // bwd1: two float chunks
+constexpr int kDynSmemF = SPAD * 8 + SPAD * 4;         // fwd: x' (double) + previous mid^2
 constexpr int Q4 = CH / (4 * NT);  // float4 groups per thread per chunk
 
 // 16-byte vector access is used when both channel rows are 16-byte aligned
@@ -181,8 +196,8 @@ __device__ __forceinline__ void load4(const float* u, int L, long long n, bool v
 }
 
 __device__ __forceinline__ float msq(float l, float r) {
-  const double m = (double)l + (double)r;
-  return (float)(m * m);
+  const float m = l + r;
+  return m * m;
 }
 
 __device__ __forceinline__ void stage_msq(float* dst, float4 l, float4 r) {
@@ -222,80 +237,68 @@ __device__ __forceinline__ float4 load4m(const float* d, int L, long long n, boo
   return make_float4(a[0], a[1], a[2], a[3]);
 }
 
-__global__ void __launch_bounds__(NT) k_dyn_fwd(char tag, const float* const* __restrict__ u_rows,
+__global__ void __launch_bounds__(NT, 2) k_dyn_fwd(char tag, const float* const* __restrict__ u_rows,
                                                 const double* __restrict__ bank, const int* __restrict__ prow,
                                                 const int* __restrict__ widx, const double* __restrict__ w,
-                                                const double* __restrict__ agg, float* __restrict__ env,
-                                                float* __restrict__ y, int L, int nch) {
+                                                float* __restrict__ env, float* __restrict__ y, int L) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  float* xs = reinterpret_cast<float*>(dsm);  // [2][SPAD]: prev chunk, cur chunk
+  double* xd = reinterpret_cast<double*>(dsm);        // [SPAD] x' of this chunk (segment-major)
+  float* xps = reinterpret_cast<float*>(xd + SPAD);   // [SPAD] mid^2 of the previous chunk
   __shared__ double pw[NPW];
   __shared__ double sh[2 * NW];
-  __shared__ double carry[2];
+  __shared__ double carry;
+  __shared__ double red[32];
   const int j = blockIdx.x, b = blockIdx.y;
   const float* u = u_rows[b];
   const DynP q = load_params(bank, prow[b]);
   const bool gate = tag == 'n';
   init_pw(pw, q.la);
-  if ((threadIdx.x >> 5) == 1) {  // warp 1: y_iir at the end of chunk j-2 (prev) and j-1 (cur)
-    double c = 0.0, cprev = 0.0;
-    for (int i = threadIdx.x - 32; i < j; i += 32) {
-      const double a = agg[(size_t)b * nch + i];
-      c = fma(exp((double)CH * (double)(j - 1 - i) * q.la), a, c);
-      if (i < j - 1) cprev = fma(exp((double)CH * (double)(j - 2 - i) * q.la), a, cprev);
-    }
-    c = warp_sum(c);
-    cprev = warp_sum(cprev);
-    if (threadIdx.x == 32) {
-      carry[0] = cprev;
-      carry[1] = c;
-    }
-  }
   const long long c0 = (long long)j * CH;
   const bool vec = vec_ok(u, L);
-  {  // coalesced staging of x = mid^2: all 16 float4 loads of a thread in flight at once
-    float4 pl[Q4], pr[Q4], cl[Q4], cr[Q4];
+  {  // coalesced staging of x' = mid^2 - a^C mid_prev^2 (float64), two float4 groups at a time
 #pragma unroll
-    for (int k = 0; k < Q4; ++k) {
-      const int o = 4 * (threadIdx.x + NT * k);
-      load4(u, L, c0 - CH + o, vec, pl[k], pr[k]);
-      load4(u, L, c0 + o, vec, cl[k], cr[k]);
-    }
+    for (int k0 = 0; k0 < Q4; k0 += 2) {
+      float4 pl[2], pr[2], cl[2], cr[2];
 #pragma unroll
-    for (int k = 0; k < Q4; ++k) {
-      const int o = 4 * (threadIdx.x + NT * k);
-      stage_msq(xs + sidx_n(o), pl[k], pr[k]);
-      stage_msq(xs + SPAD + sidx_n(o), cl[k], cr[k]);
+      for (int k = 0; k < 2; ++k) {
+        const int o = 4 * (threadIdx.x + NT * (k0 + k));
+        load4(u, L, c0 - CH + o, vec, pl[k], pr[k]);
+        load4(u, L, c0 + o, vec, cl[k], cr[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int o = 4 * (threadIdx.x + NT * (k0 + k));
+        stage_msq(xps + sidx_n(o), pl[k], pr[k]);
+        double* d = xd + sidx_n(o);
+        d[0] = fma(-q.aC, (double)msq(pl[k].x, pr[k].x), (double)msq(cl[k].x, cr[k].x));
+        d[1] = fma(-q.aC, (double)msq(pl[k].y, pr[k].y), (double)msq(cl[k].y, cr[k].y));
+        d[2] = fma(-q.aC, (double)msq(pl[k].z, pr[k].z), (double)msq(cl[k].z, cr[k].z));
+        d[3] = fma(-q.aC, (double)msq(pl[k].w, pr[k].w), (double)msq(cl[k].w, cr[k].w));
+      }
     }
   }
   __syncthreads();
-  const float* xp = xs + sidx(threadIdx.x, 0);
-  const float* xc = xs + SPAD + sidx(threadIdx.x, 0);
-  double vp = 0.0, vc = 0.0;
+  // local aggregates: x' over this thread's segment, and mid^2 of the previous chunk's
+  // segment (their weighted block sum is the state entering the chunk: the windowed
+  // sum S at the end of chunk j-1 spans exactly that chunk, as C = 8192 = chunk)
+  double v = 0.0, vp = 0.0;
 #pragma unroll
   for (int i = 0; i < SEG; ++i) {
-    vp = fma(q.a, vp, (double)xp[i]);
-    vc = fma(q.a, vc, (double)xc[i]);
+    v = fma(q.a, v, xd[sidx(threadIdx.x, i)]);
+    vp = fma(q.a, vp, (double)xps[sidx(threadIdx.x, i)]);
   }
-  scan2_excl(vp, vc, pw, sh);
-  const double at = powseg(pw, threadIdx.x);
-  double yp = (j == 0) ? 0.0 : fma(carry[0], at, vp);
-  double yc = fma(carry[1], at, vc);
-  float gcs[SEG], gns[SEG];
+  const double tot = block_sum(vp * powseg(pw, NT - 1 - threadIdx.x), red);
+  if (threadIdx.x == 0) carry = tot;
+  scan1_excl(v, pw, sh);  // (its barriers publish `carry`)
+  double yc = fma(carry, powseg(pw, threadIdx.x), v);
+  // second pass: each thread overwrites its own x' slots with (envelope, gain) pairs
+  float2* eg = reinterpret_cast<float2*>(dsm);
 #pragma unroll
   for (int i = 0; i < SEG; ++i) {
-    yp = fma(q.a, yp, (double)xp[i]);
-    yc = fma(q.a, yc, (double)xc[i]);
-    const float gc = (float)(q.b * (yc - q.aC * yp));
+    yc = fma(q.a, yc, xd[sidx(threadIdx.x, i)]);
+    const float gc = (float)(q.b * yc);
     const float G = env_log(gc);
-    gcs[i] = gc;
-    gns[i] = expf(knee_gy(G, q, gate) - G);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < SEG; ++i) {
-    xs[sidx(threadIdx.x, i)] = gcs[i];
-    xs[SPAD + sidx(threadIdx.x, i)] = gns[i];
+    eg[sidx(threadIdx.x, i)] = make_float2(gc, __expf(knee_gy(G, q, gate) - G));
   }
   __syncthreads();
   const double wv = w ? w[widx[b]] : 1.0;
@@ -310,10 +313,10 @@ __global__ void __launch_bounds__(NT) k_dyn_fwd(char tag, const float* const* __
   for (int k = 0; k < Q4; ++k) {  // coalesced outputs
     const int o = 4 * (threadIdx.x + NT * k);
     const long long n = c0 + o;
-    const float* gp = xs + SPAD + sidx_n(o);
-    const float* ep = xs + sidx_n(o);
+    const float2* p = eg + sidx_n(o);
+    const float2 e0 = p[0], e1 = p[1], e2 = p[2], e3 = p[3];
     float4 yl, yr;
-    const float4 g4 = make_float4(gp[0], gp[1], gp[2], gp[3]);
+    const float4 g4 = make_float4(e0.y, e1.y, e2.y, e3.y);
     if (bypass) {
       yl = ul[k];
       yr = ur[k];
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(NT) k_dyn_fwd(char tag, const float* const* __
       yr = make_float4(wf * (ur[k].x * g4.x) + om * ur[k].x, wf * (ur[k].y * g4.y) + om * ur[k].y,
                        wf * (ur[k].z * g4.z) + om * ur[k].z, wf * (ur[k].w * g4.w) + om * ur[k].w);
     }
-    store4(yo, L, n, vec, yl, yr, eo, make_float4(ep[0], ep[1], ep[2], ep[3]));
+    store4(yo, L, n, vec, yl, yr, eo, make_float4(e0.x, e1.x, e2.x, e3.x));
   }
 }
 
@@ -363,37 +366,37 @@ __global__ void __launch_bounds__(256) k_dyn_bwd0(char tag, const float* const* 
     const float l = U[e], r = V[e], gl = GL[e], gr = GR[e];
     const float gc = EV[e];
     const float gcl = fmaxf(gc, 0.f);
-    const float G = logf(gcl + 1e-8f);
+    const float G = __logf(gcl + 1e-8f);
     const bool above = G >= q.T + q.W, below = G < q.T - q.W;
     float Gy, dGu, dT = 0.f, dW = 0.f, dR = 0.f;
     if (gate) {
       if (above) { Gy = G; dGu = 1.f; }
       else if (below) { Gy = q.T + q.R * (G - q.T); dGu = q.R; dT = 1.f - q.R; dR = G - q.T; }
       else {
-        const float z = G - q.T - q.W, k = 1.f - q.R;
-        Gy = G + k * (z * z / (q.W * 4.f));
-        dGu = 1.f + k * z / (2.f * q.W);
-        dT = -k * z / (2.f * q.W);
-        dW = k * (-z / (2.f * q.W) - z * z / (4.f * q.W * q.W));
-        dR = -z * z / (4.f * q.W);
+        const float z = G - q.T - q.W, k = 1.f - q.R, zh = z * q.i2W, zq = z * z * q.i4W;
+        Gy = G + k * zq;
+        dGu = 1.f + k * zh;
+        dT = -k * zh;
+        dW = k * (-zh - zq * (4.f * q.i4W));
+        dR = -zq;
       }
     } else {
       if (above) {
-        Gy = q.T + (G - q.T) / q.R;
-        dGu = 1.f / q.R;
-        dT = 1.f - 1.f / q.R;
-        dR = -(G - q.T) / (q.R * q.R);
+        Gy = q.T + (G - q.T) * q.iR;
+        dGu = q.iR;
+        dT = 1.f - q.iR;
+        dR = -(G - q.T) * q.iR * q.iR;
       } else if (below) { Gy = G; dGu = 1.f; }
       else {
-        const float z = G - q.T + q.W, k = 1.f / q.R - 1.f;
-        Gy = G + k * (z * z / (q.W * 4.f));
-        dGu = 1.f + k * z / (2.f * q.W);
-        dT = -k * z / (2.f * q.W);
-        dW = k * (z / (2.f * q.W) - z * z / (4.f * q.W * q.W));
-        dR = -z * z / (4.f * q.W * q.R * q.R);
+        const float z = G - q.T + q.W, k = q.iR - 1.f, zh = z * q.i2W, zq = z * z * q.i4W;
+        Gy = G + k * zq;
+        dGu = 1.f + k * zh;
+        dT = -k * zh;
+        dW = k * (zh - zq * (4.f * q.i4W));
+        dR = -zq * q.iR * q.iR;
       }
     }
-    const float gain = expf(Gy - G);
+    const float gain = __expf(Gy - G);
     float dl, dr, ul, ur;
     if (bypass) { dl = dr = 0.f; ul = gl; ur = gr; }
     else {
@@ -407,7 +410,7 @@ __global__ void __launch_bounds__(256) k_dyn_bwd0(char tag, const float* const* 
     fW = fmaf(D, dW, fW);
     fR = fmaf(D, dR, fR);
     const float dG = D * dGu - D;
-    OD[e] = (gc > 0.f) ? dG / (gcl + 1e-8f) : 0.f;
+    OD[e] = (gc > 0.f) ? __fdividef(dG, gcl + 1e-8f) : 0.f;
    }
    store4(go, L, n4, vec, make_float4(OL[0], OL[1], OL[2], OL[3]), make_float4(OR[0], OR[1], OR[2], OR[3]), dgo,
           make_float4(OD[0], OD[1], OD[2], OD[3]));
@@ -443,38 +446,6 @@ __device__ __forceinline__ VW prop(VW x, double alen, double len) {
 __device__ __forceinline__ void rstep(VW& s, double a, double x) {
   s.w = a * (s.w + s.v);
   s.v = fma(a, s.v, x);
-}
-
-// reverse aggregates: state at the chunk start from the chunk's own dg only:
-// v = sum_o a^o dg[start + o], w = sum_o o a^o dg[start + o]  (coalesced, o = t + NT k)
-__global__ void __launch_bounds__(NT) k_dyn_bagg(const double* __restrict__ bank, const int* __restrict__ prow,
-                                                 const float* __restrict__ dg, double* __restrict__ bagg, int L,
-                                                 int nch) {
-  __shared__ double red[32];
-  const int j = blockIdx.x, b = blockIdx.y;
-  const DynP q = load_params(bank, prow[b]);
-  const float* d = dg + (size_t)b * L;
-  const long long c0 = (long long)j * CH;
-  const double step = exp((double)NT * q.la);
-  double wgt = exp((double)threadIdx.x * q.la);
-  double av = 0.0, aw = 0.0;
-#pragma unroll
-  for (int k = 0; k < SEG; ++k) {
-    const int o = threadIdx.x + NT * k;
-    const long long m = c0 + o;
-    const double x = (m < L) ? (double)d[m] : 0.0;
-    const double t = wgt * x;
-    av += t;
-    aw = fma((double)o, t, aw);
-    wgt *= step;
-  }
-  const double tv = block_sum(av, red);
-  __syncthreads();
-  const double tw = block_sum(aw, red);
-  if (threadIdx.x == 0) {
-    bagg[((size_t)b * nch + j) * 2] = tv;
-    bagg[((size_t)b * nch + j) * 2 + 1] = tw;
-  }
 }
 
 // Two reverse exclusive scans at once (segments t+1.. of the chunk) of 2-state
@@ -523,48 +494,21 @@ __device__ __forceinline__ void rscan2_excl(VW& a, VW& c, const double* pw, doub
   c = VW{ncv + wc.v, ncw + wc.w};
 }
 
-__global__ void __launch_bounds__(NT) k_dyn_bwd1(const float* const* __restrict__ u_rows,
+__global__ void __launch_bounds__(NT, 2) k_dyn_bwd1(const float* const* __restrict__ u_rows,
                                                  const double* __restrict__ bank, const int* __restrict__ prow,
-                                                 const double* __restrict__ bagg, const float* __restrict__ dg,
-                                                 float* __restrict__ gu, double* __restrict__ part, int L,
-                                                 int nch) {
+                                                 const float* __restrict__ dg, float* __restrict__ gu,
+                                                 double* __restrict__ part, int L, int nch) {
   extern __shared__ __align__(16) unsigned char dsm[];
   float* ds = reinterpret_cast<float*>(dsm);  // [2][SPAD]: cur chunk, next chunk
   __shared__ double pw[NPW];
   __shared__ double sh[4 * NW];
-  __shared__ double carry[4];
+  __shared__ double carry[2];
   __shared__ double red[32];
   const int j = blockIdx.x, b = blockIdx.y;
   const float* u = u_rows[b];
   const DynP q = load_params(bank, prow[b]);
   const float* d = dg + (size_t)b * L;
   init_pw(pw, q.la);
-  if ((threadIdx.x >> 5) == 1) {  // warp 1: state at the start of chunk j+1 (cur) and j+2 (next)
-    VW c{0.0, 0.0}, cn{0.0, 0.0};
-    for (int i = j + 1 + (threadIdx.x - 32); i < nch; i += 32) {
-      const VW a{bagg[((size_t)b * nch + i) * 2], bagg[((size_t)b * nch + i) * 2 + 1]};
-      const double len = (double)CH * (double)(i - j - 1);
-      const VW p = prop(a, exp(len * q.la), len);
-      c.v += p.v;
-      c.w += p.w;
-      if (i > j + 1) {
-        const double l2 = len - (double)CH;
-        const VW p2 = prop(a, exp(l2 * q.la), l2);
-        cn.v += p2.v;
-        cn.w += p2.w;
-      }
-    }
-    c.v = warp_sum(c.v);
-    c.w = warp_sum(c.w);
-    cn.v = warp_sum(cn.v);
-    cn.w = warp_sum(cn.w);
-    if (threadIdx.x == 32) {
-      carry[0] = c.v;
-      carry[1] = c.w;
-      carry[2] = cn.v;
-      carry[3] = cn.w;
-    }
-  }
   const long long c0 = (long long)j * CH;
   const bool vec = vec_ok(u, L) && vec_ok(d, L);
   {
@@ -593,59 +537,74 @@ __global__ void __launch_bounds__(NT) k_dyn_bwd1(const float* const* __restrict_
     rstep(sc, q.a, (double)dc[i]);
     rstep(sn, q.a, (double)dn[i]);
   }
-  rscan2_excl(sc, sn, pw, sh);
+  // The truncated windows of chunk j end inside chunk j+1, so both recursions start
+  // from zero at the end of chunk j+1: the state entering `cur` is the total of
+  // `next` (segment aggregates moved to the chunk start, block-summed).
+  {
+    const VW tn = prop(sn, powseg(pw, threadIdx.x), (double)SEG * threadIdx.x);
+    const double tv = block_sum(tn.v, red);
+    __syncthreads();
+    const double tw = block_sum(tn.w, red);
+    if (threadIdx.x == 0) {
+      carry[0] = tv;
+      carry[1] = tw;
+    }
+  }
+  rscan2_excl(sc, sn, pw, sh);  // (its barriers publish `carry`)
   const double len = (double)SEG * (NT - 1 - threadIdx.x);
   const double alen = powseg(pw, NT - 1 - threadIdx.x);
   const VW cc = prop(VW{carry[0], carry[1]}, alen, len);
-  const VW cn = prop(VW{carry[2], carry[3]}, alen, len);
   VW stc{sc.v + cc.v, sc.w + cc.w};
-  VW stn{sn.v + cn.v, sn.w + cn.w};
-  float dxs[SEG], rrs[SEG];
+  VW stn = sn;
+  // each thread overwrites its own dg slots: cur <- dx, next <- r (read before write, same slot)
+  float* dcw = ds + sidx(threadIdx.x, 0);
+  float* dnw = ds + SPAD + sidx(threadIdx.x, 0);
 #pragma unroll
   for (int i = SEG - 1; i >= 0; --i) {
-    rstep(stc, q.a, (double)dc[i]);
-    rstep(stn, q.a, (double)dn[i]);
-    dxs[i] = (float)(q.b * (stc.v - q.aC * stn.v));
-    rrs[i] = (float)(q.b * (stc.w - q.aC * fma((double)CH, stn.v, stn.w)));
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < SEG; ++i) {
-    ds[sidx(threadIdx.x, i)] = dxs[i];
-    ds[SPAD + sidx(threadIdx.x, i)] = rrs[i];
+    rstep(stc, q.a, (double)dcw[i]);
+    rstep(stn, q.a, (double)dnw[i]);
+    dcw[i] = (float)(q.b * (stc.v - q.aC * stn.v));
+    dnw[i] = (float)(q.b * (stc.w - q.aC * fma((double)CH, stn.v, stn.w)));
   }
   __syncthreads();
   double sxd = 0.0, sxr = 0.0;
   float* go = gu + (size_t)b * 2 * L;
   const bool vg = vec && vec_ok(go, L);
-  float4 ul[Q4], ur[Q4], gl[Q4], gr[Q4];
 #pragma unroll
-  for (int k = 0; k < Q4; ++k) {
-    const long long m = c0 + 4 * (threadIdx.x + NT * k);
-    load4(u, L, m, vg, ul[k], ur[k]);
-    load4(go, L, m, vg, gl[k], gr[k]);
+  for (int k0 = 0; k0 < Q4; k0 += 2) {  // coalesced: dmid = 2 mid dx; sums for d a_raw (2 groups at a time)
+  float4 ul[2], ur[2], gl[2], gr[2];
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) {
+    const long long m = c0 + 4 * (threadIdx.x + NT * (k0 + kk));
+    load4(u, L, m, vg, ul[kk], ur[kk]);
+    load4(go, L, m, vg, gl[kk], gr[kk]);
   }
 #pragma unroll
-  for (int k = 0; k < Q4; ++k) {  // coalesced: dmid = 2 mid dx; sums for d a_raw
-    const int o = 4 * (threadIdx.x + NT * k);
+  for (int kk = 0; kk < 2; ++kk) {
+    const int k = kk;
+    const int o = 4 * (threadIdx.x + NT * (k0 + kk));
     const long long m = c0 + o;
     const float* dxp = ds + sidx_n(o);
     const float* rrp = ds + SPAD + sidx_n(o);
     const float lu[4] = {ul[k].x, ul[k].y, ul[k].z, ul[k].w}, ru[4] = {ur[k].x, ur[k].y, ur[k].z, ur[k].w};
     float ol[4] = {gl[k].x, gl[k].y, gl[k].z, gl[k].w}, orr[4] = {gr[k].x, gr[k].y, gr[k].z, gr[k].w};
+    float fxd = 0.f, fxr = 0.f;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (m + e >= L) continue;
-      const double mid = (double)lu[e] + (double)ru[e];
-      const double x = mid * mid;
-      sxd = fma(x, (double)dxp[e], sxd);
-      sxr = fma(x, (double)rrp[e], sxr);
-      const float dm = (float)(2.0 * mid * (double)dxp[e]);
+      const float mid = lu[e] + ru[e];
+      const float x = mid * mid;
+      fxd = fmaf(x, dxp[e], fxd);
+      fxr = fmaf(x, rrp[e], fxr);
+      const float dm = 2.f * mid * dxp[e];
       ol[e] += dm;
       orr[e] += dm;
     }
+    sxd += (double)fxd;
+    sxr += (double)fxr;
     store4(go, L, m, vg, make_float4(ol[0], ol[1], ol[2], ol[3]), make_float4(orr[0], orr[1], orr[2], orr[3]),
            nullptr, make_float4(0.f, 0.f, 0.f, 0.f));
+  }
   }
   sxd = block_sum(sxd, red);
   __syncthreads();
@@ -694,7 +653,7 @@ int bwd0_grid(int L) {
 }
 
 struct DynWs {
-  double *agg, *bagg, *part0, *part1;
+  double *part0, *part1;
   float* dg;
 };
 
@@ -702,8 +661,6 @@ template <class A>
 DynWs dcarve(A& a, int B, int L) {
   DynWs w;
   const int nch = nchunks(L);
-  w.agg = a.template take<double>((size_t)B * nch);
-  w.bagg = a.template take<double>((size_t)B * nch * 2);
   w.part0 = a.template take<double>((size_t)B * bwd0_grid(L) * 8);
   w.part1 = a.template take<double>((size_t)B * nch * 8);
   w.dg = a.template take<float>((size_t)B * L);
@@ -713,7 +670,7 @@ DynWs dcarve(A& a, int B, int L) {
 }  // namespace
 
 int mgb_dyn_init() {
-  cudaFuncSetAttribute(k_dyn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+  cudaFuncSetAttribute(k_dyn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemF);
   cudaFuncSetAttribute(k_dyn_bwd1, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
@@ -729,10 +686,8 @@ int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st) {
   const int B = lv->B, L = lv->L, nch = nchunks(L);
   MgbArena a{(char*)lv->ws, 0};
   DynWs w = dcarve(a, B, L);
-  k_dyn_agg<<<dim3(nch, B), NT, 0, st>>>(lv->u_rows, lv->bank, lv->prow, w.agg, L, nch);
-  MGB_CHECK_LAUNCH();
-  k_dyn_fwd<<<dim3(nch, B), NT, kDynSmem, st>>>(lv->tag, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w, w.agg,
-                                         lv->aux, lv->y, L, nch);
+  k_dyn_fwd<<<dim3(nch, B), NT, kDynSmemF, st>>>(lv->tag, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w,
+                                                 lv->aux, lv->y, L);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -745,9 +700,7 @@ int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st) {
   k_dyn_bwd0<<<dim3(g0, B), 256, 0, st>>>(lv->tag, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx, lv->w,
                                           lv->aux, w.dg, lv->gu, w.part0, L);
   MGB_CHECK_LAUNCH();
-  k_dyn_bagg<<<dim3(nch, B), NT, 0, st>>>(lv->bank, lv->prow, w.dg, w.bagg, L, nch);
-  MGB_CHECK_LAUNCH();
-  k_dyn_bwd1<<<dim3(nch, B), NT, kDynSmem, st>>>(lv->u_rows, lv->bank, lv->prow, w.bagg, w.dg, lv->gu, w.part1, L, nch);
+  k_dyn_bwd1<<<dim3(nch, B), NT, kDynSmem, st>>>(lv->u_rows, lv->bank, lv->prow, w.dg, lv->gu, w.part1, L, nch);
   MGB_CHECK_LAUNCH();
   k_dyn_final<<<B, 256, 0, st>>>(w.part0, g0, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank, lv->gw,
                                  w.part1);
