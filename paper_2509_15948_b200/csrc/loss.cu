@@ -1,8 +1,8 @@
 // Multi-resolution STFT loss (mg/losses.py:104-170), forward and backward.
 //
-// Per resolution n (hop n/4, reflect pad n/2, periodic Hann), one CTA per
-// frame: both output channels ride one complex float64 FFT (left + i*right)
-// in shared memory; the four groups [L, R, L+R, L-R] are separated from the
+// Per resolution n (hop n/4, reflect pad n/2, periodic Hann), a few frames
+// per CTA: both output channels ride one complex float64 FFT (left + i*right),
+// done as register radix-8/16 Stockham stages with shared-memory exchanges; the four groups [L, R, L+R, L-R] are separated from the
 // spectrum by linearity; |X| x (A-weight * HTK mel) is applied as a banded
 // (CSR) product; log-mel L1 and spectral-convergence partial sums are reduced
 // per frame (float64) and combined by a one-CTA finalize.
@@ -27,59 +27,214 @@ __device__ __forceinline__ long long reflect_idx(long long i, long long n) {
   return a >= n ? period - a : a;
 }
 
-template <int N>
-struct LossCfg {
-  static constexpr int NT = N >= 4096 ? 512 : 256;
-  static constexpr int NB = N / 2 + 1;
-  static constexpr size_t SMEM = sizeof(double2) * padded_len<N>() + 64;  // padded FFT buffer
+// ---------------------------------------------------------------------------
+// float64 frame FFTs in registers: Stockham autosort, radix-R stages; a frame is
+// transformed by T threads holding V = N/T values each; stage inputs of the first
+// stage come straight from global memory (windowed, reflect-padded), every later
+// stage reads the previous stage's outputs from padded shared memory.
+
+__device__ __forceinline__ int pd16(int i) { return i + (i >> 4); }  // 16-byte slots, 1 pad per 16
+
+__device__ __forceinline__ double c16(int k) {
+  constexpr double t[16] = {1.0, 0.92387953251128674, 0.70710678118654757, 0.38268343236508984, 0.0,
+                            -0.38268343236508973, -0.70710678118654746, -0.92387953251128674, -1.0,
+                            -0.92387953251128685, -0.70710678118654768, -0.38268343236509034, 0.0,
+                            0.38268343236509, 0.70710678118654735, 0.92387953251128652};
+  return t[k & 15];
+}
+
+// x * W_R^e, R | 16, e constant after unrolling
+template <int R, bool INV>
+__device__ __forceinline__ double2 twc64(double2 x, int e) {
+  const int k = (e % R) * (16 / R);
+  if (k == 0) return x;
+  if (k == 8) return make_double2(-x.x, -x.y);
+  if (k == 4) return INV ? make_double2(-x.y, x.x) : make_double2(x.y, -x.x);
+  if (k == 12) return INV ? make_double2(x.y, -x.x) : make_double2(-x.y, x.x);
+  const double c = c16(k), sn = INV ? c16(k - 4) : -c16(k - 4);
+  return make_double2(x.x * c - x.y * sn, x.x * sn + x.y * c);
+}
+
+template <int R, bool INV>
+struct D64;
+template <bool INV>
+struct D64<1, INV> {
+  static __device__ __forceinline__ void run(double2*) {}
+};
+template <bool INV>
+struct D64<2, INV> {
+  static __device__ __forceinline__ void run(double2* v) {
+    const double2 a = v[0];
+    v[0] = make_double2(a.x + v[1].x, a.y + v[1].y);
+    v[1] = make_double2(a.x - v[1].x, a.y - v[1].y);
+  }
+};
+template <int A, int B, bool INV>
+__device__ __forceinline__ void d64_ab(double2* v) {
+  constexpr int N = A * B;
+  double2 t[A][B];
+#pragma unroll
+  for (int na = 0; na < A; ++na) {
+#pragma unroll
+    for (int nb = 0; nb < B; ++nb) t[na][nb] = v[na + A * nb];
+    D64<B, INV>::run(t[na]);
+#pragma unroll
+    for (int kb = 0; kb < B; ++kb) t[na][kb] = twc64<N, INV>(t[na][kb], na * kb);
+  }
+#pragma unroll
+  for (int kb = 0; kb < B; ++kb) {
+    double2 q[A];
+#pragma unroll
+    for (int na = 0; na < A; ++na) q[na] = t[na][kb];
+    D64<A, INV>::run(q);
+#pragma unroll
+    for (int ka = 0; ka < A; ++ka) v[kb + B * ka] = q[ka];
+  }
+}
+template <bool INV>
+struct D64<4, INV> {
+  static __device__ __forceinline__ void run(double2* v) { d64_ab<2, 2, INV>(v); }
+};
+template <bool INV>
+struct D64<8, INV> {
+  static __device__ __forceinline__ void run(double2* v) { d64_ab<2, 4, INV>(v); }
+};
+template <bool INV>
+struct D64<16, INV> {
+  static __device__ __forceinline__ void run(double2* v) { d64_ab<4, 4, INV>(v); }
 };
 
-// load windowed frame f of (xl, xr) into s (complex double) and FFT it
+// per-size plan: T threads per frame holding V = 8 values each (radix-8 stages, a
+// final radix-2/4 stage where log2 N is not a multiple of 3), frames per CTA
+template <int N> struct FP;
+template <> struct FP<256> { static constexpr int T = 32, R1 = 8, R2 = 8, R3 = 4, R4 = 1, R5 = 1; };
+template <> struct FP<512> { static constexpr int T = 64, R1 = 8, R2 = 8, R3 = 8, R4 = 1, R5 = 1; };
+template <> struct FP<1024> { static constexpr int T = 128, R1 = 8, R2 = 8, R3 = 8, R4 = 2, R5 = 1; };
+template <> struct FP<2048> { static constexpr int T = 256, R1 = 8, R2 = 8, R3 = 8, R4 = 4, R5 = 1; };
+template <> struct FP<4096> { static constexpr int T = 512, R1 = 8, R2 = 8, R3 = 8, R4 = 8, R5 = 1; };
+template <> struct FP<8192> { static constexpr int T = 1024, R1 = 8, R2 = 8, R3 = 8, R4 = 8, R5 = 2; };
+
 template <int N>
-__device__ __forceinline__ void load_fft(double2* s, const float* __restrict__ xl, const float* __restrict__ xr,
-                                         int Ls, int hop, int f) {
-  constexpr int NT = LossCfg<N>::NT;
-  for (int t = threadIdx.x; t < N; t += NT) {
-    const long long idx = reflect_idx((long long)f * hop + t - N / 2, Ls);
-    const double win = 0.5 - 0.5 * cospi(2.0 * t / (double)N);
-    s[pidx<true>(t)] = make_double2((double)xl[idx] * win, (double)xr[idx] * win);
+struct FC {
+  static constexpr int T = FP<N>::T, V = N / T;
+  static constexpr int FPC = T >= 256 ? 1 : 256 / T;  // frames per CTA (CTA = max(256, T) threads)
+  static constexpr int NT = T * FPC;
+  static constexpr int NB = N / 2 + 1;
+  static constexpr int PADN = N + N / 16;              // padded frame buffer (double2)
+  static constexpr size_t SMEM = sizeof(double2) * PADN * FPC;
+};
+
+// One Stockham stage over this thread's butterflies j = tt + T i (i < V/R):
+// inputs v[i*R + m] = x[j + m N/R]; outputs y[(j/NS) NS R + j%NS + m NS] -> S
+template <int N, int R, int NS, bool INV>
+__device__ __forceinline__ void st_stage(double2* v, double2* S, int tt) {
+  constexpr int T = FC<N>::T, V = FC<N>::V;
+#pragma unroll
+  for (int i = 0; i < V / R; ++i) {
+    const int j = tt + T * i, k = j % NS;
+    double2* a = v + i * R;
+    if (NS > 1) {
+#pragma unroll
+      for (int m = 1; m < R; ++m) {
+        double2 w = g_tw64[(k * m * (MGB_TW_N / (NS * R))) & (MGB_TW_N - 1)];
+        if (INV) w.y = -w.y;
+        a[m] = make_double2(a[m].x * w.x - a[m].y * w.y, a[m].x * w.y + a[m].y * w.x);
+      }
+    }
+    D64<R, INV>::run(a);
+    const int base = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int m = 0; m < R; ++m) S[pd16(base + m * NS)] = a[m];
   }
-  smem_fft<double, N, 1, NT, N, 1, false, true>(s, false);
 }
 
-// per-bin group spectra from the packed spectrum
-__device__ __forceinline__ void groups_at(const double2* s, int n, int k, double2 X[4]) {
-  const double2 zk = s[pidx<true>(k)], zp = s[pidx<true>((n - k) & (n - 1))];
-  const double2 a = make_double2(0.5 * (zk.x + zp.x), 0.5 * (zk.y - zp.y));
-  const double2 d = make_double2(0.5 * (zk.x - zp.x), 0.5 * (zk.y + zp.y));
-  const double2 b = make_double2(d.y, -d.x);
-  X[0] = a;
-  X[1] = b;
-  X[2] = make_double2(a.x + b.x, a.y + b.y);
-  X[3] = make_double2(a.x - b.x, a.y - b.y);
+// gather the inputs of a radix-R stage from S
+template <int N, int R>
+__device__ __forceinline__ void st_gather(double2* v, const double2* S, int tt) {
+  constexpr int T = FC<N>::T, V = FC<N>::V;
+#pragma unroll
+  for (int i = 0; i < V / R; ++i)
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[i * R + m] = S[pd16(tt + T * i + m * (N / R))];
 }
 
-// Replace the spectrum in s by the 4 group magnitudes mag[g*NB + k] (double view).
+// all stages after the first stage's inputs are in v; result (natural order) in S.
+// Contains __syncthreads: every thread of the CTA must call it.
+template <int N, bool INV>
+__device__ __forceinline__ void frame_fft(double2* v, double2* S, int tt) {
+  using P = FP<N>;
+  st_stage<N, P::R1, 1, INV>(v, S, tt);
+  __syncthreads();
+  st_gather<N, P::R2>(v, S, tt);
+  __syncthreads();
+  st_stage<N, P::R2, P::R1, INV>(v, S, tt);
+  __syncthreads();
+  if constexpr (P::R3 > 1) {
+    st_gather<N, P::R3>(v, S, tt);
+    __syncthreads();
+    st_stage<N, P::R3, P::R1 * P::R2, INV>(v, S, tt);
+    __syncthreads();
+  }
+  if constexpr (P::R4 > 1) {
+    st_gather<N, P::R4>(v, S, tt);
+    __syncthreads();
+    st_stage<N, P::R4, P::R1 * P::R2 * P::R3, INV>(v, S, tt);
+    __syncthreads();
+  }
+  if constexpr (P::R5 > 1) {
+    st_gather<N, P::R5>(v, S, tt);
+    __syncthreads();
+    st_stage<N, P::R5, P::R1 * P::R2 * P::R3 * P::R4, INV>(v, S, tt);
+    __syncthreads();
+  }
+}
+
+// windowed, reflect-padded frame f of (xl + i xr) into the first stage's inputs
 template <int N>
-__device__ __forceinline__ void spectrum_to_mags(double2* s) {
-  constexpr int NT = LossCfg<N>::NT, NB = LossCfg<N>::NB;
-  constexpr int PER = (NB + NT - 1) / NT;
-  double m[PER][4];
+__device__ __forceinline__ void load_frame(double2* v, const float* __restrict__ xl, const float* __restrict__ xr,
+                                           int Ls, int hop, int f, bool valid, int tt) {
+  constexpr int T = FC<N>::T, V = FC<N>::V, R = FP<N>::R1;
+#pragma unroll
+  for (int i = 0; i < V / R; ++i)
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      const int t = tt + T * i + m * (N / R);
+      double2 z = make_double2(0.0, 0.0);
+      if (valid) {
+        long long idx = (long long)f * hop + t - N / 2;
+        if (idx < 0 || idx >= Ls) idx = reflect_idx(idx, Ls);
+        const double win = 0.5 - 0.5 * g_tw64[t * (MGB_TW_N / N)].x;  // cos(2 pi t / N)
+        z = make_double2((double)__ldg(xl + idx) * win, (double)__ldg(xr + idx) * win);
+      }
+      v[i * R + m] = z;
+    }
+}
+
+// spectrum in S (natural, padded) -> the 4 group magnitudes as float32,
+// md[g*NB + k] over the start of the same buffer (all reads precede the barrier)
+template <int N>
+__device__ __forceinline__ void mags_inplace(double2* S, int tt) {
+  constexpr int T = FC<N>::T, NB = FC<N>::NB, PER = (NB + T - 1) / T;
+  float m[PER][4];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int k = threadIdx.x + i * NT;
+    const int k = tt + i * T;
     if (k < NB) {
-      double2 X[4];
-      groups_at(s, N, k, X);
-#pragma unroll
-      for (int g = 0; g < 4; ++g) m[i][g] = sqrt(X[g].x * X[g].x + X[g].y * X[g].y);
+      const double2 zk = S[pd16(k)], zp = S[pd16((N - k) & (N - 1))];
+      const double2 a = make_double2(0.5 * (zk.x + zp.x), 0.5 * (zk.y - zp.y));
+      const double2 d = make_double2(0.5 * (zk.x - zp.x), 0.5 * (zk.y + zp.y));
+      const double2 bb = make_double2(d.y, -d.x);
+      m[i][0] = (float)sqrt(a.x * a.x + a.y * a.y);
+      m[i][1] = (float)sqrt(bb.x * bb.x + bb.y * bb.y);
+      m[i][2] = (float)sqrt((a.x + bb.x) * (a.x + bb.x) + (a.y + bb.y) * (a.y + bb.y));
+      m[i][3] = (float)sqrt((a.x - bb.x) * (a.x - bb.x) + (a.y - bb.y) * (a.y - bb.y));
     }
   }
   __syncthreads();
-  double* md = reinterpret_cast<double*>(s);
+  float* md = reinterpret_cast<float*>(S);
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int k = threadIdx.x + i * NT;
+    const int k = tt + i * T;
     if (k < NB) {
 #pragma unroll
       for (int g = 0; g < 4; ++g) md[g * NB + k] = m[i][g];
@@ -90,50 +245,59 @@ __device__ __forceinline__ void spectrum_to_mags(double2* s) {
 
 // mode 0: target (write tmel, tlog, part[.,g,0] = sum mel^2)
 // mode 1: estimate (write mel, part[.,g,0] = sum |dlog|, part[.,g,1] = sum (mel - tmel)^2)
+// FPC frames per CTA; within a frame, T/4 threads per group g walk the mel bands.
 template <int N>
-__global__ void __launch_bounds__(LossCfg<N>::NT) k_mr_fwd(MgbLossRes r, const float* __restrict__ xl,
-                                                           const float* __restrict__ xr, int Ls, int mode) {
-  constexpr int NT = LossCfg<N>::NT, NB = LossCfg<N>::NB;
+__global__ void __launch_bounds__(FC<N>::NT) k_mr_fwd(MgbLossRes r, const float* __restrict__ xl,
+                                                      const float* __restrict__ xr, int Ls, int mode) {
+  using C = FC<N>;
+  constexpr int T = C::T, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smraw[];
-  double2* s = reinterpret_cast<double2*>(smraw);
-  __shared__ double red[32];
-  __shared__ double acc[4][2];
-  const int f = blockIdx.x;
-  load_fft<N>(s, xl, xr, Ls, r.hop, f);
-  spectrum_to_mags<N>(s);
-  const double* md = reinterpret_cast<const double*>(s);
-  if (threadIdx.x < 8) (&acc[0][0])[threadIdx.x] = 0.0;
-  __syncthreads();
+  __shared__ double red[2][C::NT];
+  const int q = threadIdx.x / T, tt = threadIdx.x % T;
+  const int f = blockIdx.x * C::FPC + q;
+  const bool valid = f < r.frames;
+  double2* S = reinterpret_cast<double2*>(smraw) + q * C::PADN;
+  double2 v[C::V];
+  load_frame<N>(v, xl, xr, Ls, r.hop, f, valid, tt);
+  frame_fft<N, false>(v, S, tt);
+  mags_inplace<N>(S, tt);
+  const float* md = reinterpret_cast<const float*>(S);
   const int nm = r.n_mels;
-  double a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
-  for (int q = threadIdx.x; q < 4 * nm; q += NT) {
-    const int g = q / nm, j = q % nm;
-    const int k0 = r.band_start[j], len = r.band_len[j], off = r.band_off[j];
-    double mel = 0.0;
-    for (int i = 0; i < len; ++i) mel = fma(md[g * NB + k0 + i], r.band_w[off + i], mel);
-    const size_t o = ((size_t)g * r.frames + f) * nm + j;
-    if (mode == 0) {
-      r.tmel[o] = mel;
-      r.tlog[o] = log(mel + LOG_EPS);
-      a0[g] += mel * mel;
-    } else {
-      r.mel[o] = mel;
-      const double dlog = log(mel + LOG_EPS) - r.tlog[o];
-      const double dm = mel - r.tmel[o];
-      a0[g] += fabs(dlog);
-      a1[g] += dm * dm;
+  const int g = tt & 3;  // items idx = tt + T i: group idx % 4 (fixed per thread), band idx / 4
+  double a0 = 0.0, a1 = 0.0;
+  if (valid) {
+    for (int idx = tt; idx < 4 * nm; idx += T) {
+      const int j = idx >> 2;
+      const int k0 = r.band_start[j], len = r.band_len[j], off = r.band_off[j];
+      const float* mg = md + g * NB + k0;
+      const double* bw = r.band_w + off;
+      double mel = 0.0;
+      for (int i = 0; i < len; ++i) mel = fma((double)mg[i], __ldg(bw + i), mel);
+      const size_t o = ((size_t)g * r.frames + f) * nm + j;
+      if (mode == 0) {
+        r.tmel[o] = mel;
+        r.tlog[o] = log(mel + LOG_EPS);
+        a0 += mel * mel;
+      } else {
+        r.mel[o] = mel;
+        const double dlog = log(mel + LOG_EPS) - r.tlog[o];
+        const double dm = mel - r.tmel[o];
+        a0 += fabs(dlog);
+        a1 += dm * dm;
+      }
     }
   }
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    const double t0 = block_sum(a0[g], red);
-    __syncthreads();
-    const double t1 = block_sum(a1[g], red);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      r.part[((size_t)f * 4 + g) * 3 + 0] = t0;
-      r.part[((size_t)f * 4 + g) * 3 + 1] = t1;
+  red[0][threadIdx.x] = a0;
+  red[1][threadIdx.x] = a1;
+  __syncthreads();
+  if (valid && tt < 4) {  // fixed-order sum over the T/4 threads of (frame, group)
+    double t0 = 0.0, t1 = 0.0;
+    for (int i = threadIdx.x; i < (q + 1) * T; i += 4) {
+      t0 += red[0][i];
+      t1 += red[1][i];
     }
+    r.part[((size_t)f * 4 + g) * 3 + 0] = t0;
+    r.part[((size_t)f * 4 + g) * 3 + 1] = t1;
   }
 }
 
@@ -175,120 +339,133 @@ __global__ void k_mr_total(MgbLoss L) {
   *L.loss = tot;
 }
 
+// backward: dmel, frame spectrum recomputed, d|X| through the CSC projection,
+// dX per group -> packed Hermitian adjoint of both channels, one inverse FFT,
+// windowed frame adjoints to gframes (float32) for the overlap-add gather.
 template <int N>
-__global__ void __launch_bounds__(LossCfg<N>::NT) k_mr_bwd(MgbLossRes r, const double* __restrict__ stats,
-                                                           MgbLoss L, const float* __restrict__ xl,
-                                                           const float* __restrict__ xr, int Ls) {
-  constexpr int NT = LossCfg<N>::NT, NB = LossCfg<N>::NB;
+__global__ void __launch_bounds__(FC<N>::NT, (FC<N>::NT <= 256 ? 2 : 1)) k_mr_bwd(MgbLossRes r, const double* __restrict__ stats, MgbLoss L,
+                                                      const float* __restrict__ xl, const float* __restrict__ xr,
+                                                      int Ls) {
+  using C = FC<N>;
+  constexpr int T = C::T, NB = C::NB, PER = (NB + T - 1) / T;
   extern __shared__ __align__(16) unsigned char smraw[];
-  double2* s = reinterpret_cast<double2*>(smraw);
-  __shared__ double dmel[4][128];
-  const int f = blockIdx.x;
+  __shared__ double dmel[C::FPC][4][128];
+  const int q = threadIdx.x / T, tt = threadIdx.x % T;
+  const int f = blockIdx.x * C::FPC + q;
+  const bool valid = f < r.frames;
+  double2* S = reinterpret_cast<double2*>(smraw) + q * C::PADN;
   const int nm = r.n_mels;
-  // dL/dmel
-  for (int q = threadIdx.x; q < 4 * nm; q += NT) {
-    const int g = q / nm, j = q % nm;
-    const size_t o = ((size_t)g * r.frames + f) * nm + j;
-    const double mel = r.mel[o];
-    const double dlog = log(mel + LOG_EPS) - r.tlog[o];
-    const double sg = (dlog > 0.0) ? 1.0 : (dlog < 0.0 ? -1.0 : 0.0);
-    const double* st = stats + (size_t)g * 4;
-    const double dn = st[3], tn = st[0];
-    double v = sg / ((double)r.frames * (mel + LOG_EPS));
-    if (dn > 0.0) v += (mel - r.tmel[o]) / (dn * tn);
-    dmel[g][j] = L.group_w[g] * v;
+  if (valid) {
+    for (int idx = tt; idx < 4 * nm; idx += T) {
+      const int g = idx / nm, j = idx % nm;
+      const size_t o = ((size_t)g * r.frames + f) * nm + j;
+      const double mel = r.mel[o];
+      const double dlog = log(mel + LOG_EPS) - r.tlog[o];
+      const double sg = (dlog > 0.0) ? 1.0 : (dlog < 0.0 ? -1.0 : 0.0);
+      const double* st = stats + (size_t)g * 4;
+      const double dn = st[3], tn = st[0];
+      double v = sg / ((double)r.frames * (mel + LOG_EPS));
+      if (dn > 0.0) v += (mel - r.tmel[o]) / (dn * tn);
+      dmel[q][g][j] = L.group_w[g] * v;
+    }
   }
-  load_fft<N>(s, xl, xr, Ls, r.hop, f);
-  // per bin: dX_l, dX_r from the four groups, stored as Hermitian packs
-  constexpr int PER = (NB + NT - 1) / NT;
-  double2 dl[PER], dr[PER];
+  double2 v[C::V];
+  load_frame<N>(v, xl, xr, Ls, r.hop, f, valid, tt);
+  frame_fft<N, false>(v, S, tt);  // (its barriers also publish dmel)
+  float2 dl[PER], dr[PER];  // (float32 stash of the per-bin adjoints across the barrier)
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int k = threadIdx.x + i * NT;
-    dl[i] = dr[i] = make_double2(0.0, 0.0);
-    if (k < NB) {
+    const int k = tt + i * T;
+    dl[i] = dr[i] = make_float2(0.f, 0.f);
+    if (k < NB && valid) {
+      const double2 zk = S[pd16(k)], zp = S[pd16((N - k) & (N - 1))];
       double2 X[4];
-      groups_at(s, N, k, X);
+      X[0] = make_double2(0.5 * (zk.x + zp.x), 0.5 * (zk.y - zp.y));
+      const double2 d = make_double2(0.5 * (zk.x - zp.x), 0.5 * (zk.y + zp.y));
+      X[1] = make_double2(d.y, -d.x);
+      X[2] = make_double2(X[0].x + X[1].x, X[0].y + X[1].y);
+      X[3] = make_double2(X[0].x - X[1].x, X[0].y - X[1].y);
+      const int b0 = r.bin_start[k], bl = r.bin_len[k];
       double2 dX[4];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         double dm = 0.0;
-        const int b0 = r.bin_start[k], bl = r.bin_len[k];
-        for (int e = 0; e < bl; ++e) dm = fma(dmel[g][r.bin_band[b0 + e]], r.bin_w[b0 + e], dm);
+        for (int e = 0; e < bl; ++e) dm = fma(dmel[q][g][r.bin_band[b0 + e]], r.bin_w[b0 + e], dm);
         const double mag = sqrt(X[g].x * X[g].x + X[g].y * X[g].y);
         const double den = mag == 0.0 ? 1.0 : mag;
         dX[g] = make_double2(dm * X[g].x / den, dm * X[g].y / den);
       }
-      dl[i] = make_double2(dX[0].x + dX[2].x + dX[3].x, dX[0].y + dX[2].y + dX[3].y);
-      dr[i] = make_double2(dX[1].x + dX[2].x - dX[3].x, dX[1].y + dX[2].y - dX[3].y);
+      dl[i] = make_float2((float)(dX[0].x + dX[2].x + dX[3].x), (float)(dX[0].y + dX[2].y + dX[3].y));
+      dr[i] = make_float2((float)(dX[1].x + dX[2].x - dX[3].x), (float)(dX[1].y + dX[2].y - dX[3].y));
     }
   }
   __syncthreads();
   // P[k] = Hl[k] + i Hr[k]; Hc[k] = dXc/2 (0<k<N/2), Hc[N-k] = conj(dXc)/2, Hc[0]/Hc[N/2] = Re dXc
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int k = threadIdx.x + i * NT;
+    const int k = tt + i * T;
     if (k < NB) {
       if (k == 0 || k == N / 2) {
-        s[pidx<true>(k)] = make_double2(dl[i].x, dr[i].x);
+        S[pd16(k)] = make_double2((double)dl[i].x, (double)dr[i].x);
       } else {
-        const double2 hl = make_double2(0.5 * dl[i].x, 0.5 * dl[i].y);
-        const double2 hr = make_double2(0.5 * dr[i].x, 0.5 * dr[i].y);
-        s[pidx<true>(k)] = make_double2(hl.x - hr.y, hl.y + hr.x);         // hl + i hr
-        s[pidx<true>(N - k)] = make_double2(hl.x + hr.y, -hl.y + hr.x);    // conj(hl) + i conj(hr)
+        const double2 hl = make_double2(0.5 * (double)dl[i].x, 0.5 * (double)dl[i].y);
+        const double2 hr = make_double2(0.5 * (double)dr[i].x, 0.5 * (double)dr[i].y);
+        S[pd16(k)] = make_double2(hl.x - hr.y, hl.y + hr.x);          // hl + i hr
+        S[pd16(N - k)] = make_double2(hl.x + hr.y, -hl.y + hr.x);     // conj(hl) + i conj(hr)
       }
     }
   }
-  smem_fft<double, N, 1, NT, N, 1, false, true>(s, true);
+  __syncthreads();
+  st_gather<N, FP<N>::R1>(v, S, tt);
+  __syncthreads();
+  frame_fft<N, true>(v, S, tt);
+  if (!valid) return;
   float* gf = r.gframes + (size_t)f * 2 * N;
-  for (int t = threadIdx.x; t < N; t += NT) {
-    const double win = 0.5 - 0.5 * cospi(2.0 * t / (double)N);
-    const double2 v = s[pidx<true>(t)];
-    gf[t] = (float)(v.x * win);
-    gf[N + t] = (float)(v.y * win);
+  for (int t = tt; t < N; t += T) {
+    const double win = 0.5 - 0.5 * g_tw64[t * (MGB_TW_N / N)].x;
+    const double2 z = S[pd16(t)];
+    gf[t] = (float)(z.x * win);
+    gf[N + t] = (float)(z.y * win);
   }
 }
 
-__global__ void k_mr_ola(MgbLoss L, float* __restrict__ gl, float* __restrict__ gr) {
+// dL/dy[t] = sum over resolutions of the frame adjoints covering the padded
+// position t + n/2, plus the reflect-pad adjoint near both ends (gather, no atomics)
+__global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ gl, float* __restrict__ gr) {
   const int Ls = L.Ls;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < Ls; t += (long long)gridDim.x * blockDim.x) {
-    double al = 0.0, ar = 0.0;
-    for (int ri = 0; ri < L.n_res; ++ri) {
-      const MgbLossRes& r = L.res[ri];
-      const int n = r.n_fft, hop = r.hop, pad = n / 2;
-      long long P[3];
-      int np = 0;
-      P[np++] = t + pad;
-      if (t >= 1 && t <= pad) P[np++] = pad - t;
-      if (t >= Ls - 1 - pad && t <= Ls - 2) P[np++] = 2LL * (Ls - 1) - t + pad;
-      for (int q = 0; q < np; ++q) {
-        const long long p = P[q];
-        long long fhi = p / hop;
-        if (fhi > r.frames - 1) fhi = r.frames - 1;
-        long long flo = (p - n + hop) / hop;  // ceil((p - n + 1) / hop) for p >= n - 1
-        if (p - n + 1 <= 0) flo = 0;
-        for (long long f = flo; f <= fhi; ++f) {
-          const long long o = p - f * hop;
-          if (o < 0 || o >= n) continue;
-          al += r.gframes[(size_t)f * 2 * n + o];
-          ar += r.gframes[(size_t)f * 2 * n + n + o];
-        }
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Ls) return;
+  double al = 0.0, ar = 0.0;
+  for (int ri = 0; ri < L.n_res; ++ri) {
+    const MgbLossRes& r = L.res[ri];
+    const int n = r.n_fft, pad = n / 2, lh = __ffs(r.hop) - 1, ln = __ffs(n) - 1;
+    int P[3];
+    int np = 0;
+    P[np++] = t + pad;
+    if (t >= 1 && t <= pad) P[np++] = pad - t;
+    if (t >= Ls - 1 - pad && t <= Ls - 2) P[np++] = 2 * (Ls - 1) - t + pad;
+    for (int qi = 0; qi < np; ++qi) {
+      const int p = P[qi];
+      int fhi = p >> lh;
+      if (fhi > r.frames - 1) fhi = r.frames - 1;
+      const int flo = (p - n + 1 <= 0) ? 0 : ((p - n + r.hop) >> lh);  // ceil((p - n + 1) / hop)
+      for (int f = flo; f <= fhi; ++f) {
+        const int o = p - (f << lh);
+        if (o < 0 || o >= n) continue;
+        const float* gfp = r.gframes + ((size_t)f << (ln + 1));
+        al += __ldg(gfp + o);
+        ar += __ldg(gfp + n + o);
       }
     }
-    gl[t] = (float)al;
-    gr[t] = (float)ar;
   }
+  gl[t] = (float)al;
+  gr[t] = (float)ar;
 }
 
 template <int N>
 int launch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, int mode, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_mr_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LossCfg<N>::SMEM);
-    cudaFuncSetAttribute(k_mr_bwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LossCfg<N>::SMEM);
-    attr = true;
-  }
-  k_mr_fwd<N><<<r.frames, LossCfg<N>::NT, LossCfg<N>::SMEM, st>>>(r, xl, xr, Ls, mode);
+  using C = FC<N>;
+  k_mr_fwd<N><<<(r.frames + C::FPC - 1) / C::FPC, C::NT, C::SMEM, st>>>(r, xl, xr, Ls, mode);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -296,7 +473,8 @@ int launch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, in
 template <int N>
 int launch_bwd(const MgbLossRes& r, const double* stats, const MgbLoss& L, const float* xl, const float* xr,
                int Ls, cudaStream_t st) {
-  k_mr_bwd<N><<<r.frames, LossCfg<N>::NT, LossCfg<N>::SMEM, st>>>(r, stats, L, xl, xr, Ls);
+  using C = FC<N>;
+  k_mr_bwd<N><<<(r.frames + C::FPC - 1) / C::FPC, C::NT, C::SMEM, st>>>(r, stats, L, xl, xr, Ls);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -335,19 +513,20 @@ int check_loss(const MgbLoss* L) {
   return 0;
 }
 
+template <int N>
+int loss_attrs() {
+  int rc = 0;
+  rc |= cudaFuncSetAttribute(k_mr_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC<N>::SMEM);
+  rc |= cudaFuncSetAttribute(k_mr_bwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC<N>::SMEM);
+  return rc;
+}
+
 }  // namespace
 
 int mgb_loss_init() {
-  // set smem attributes eagerly (outside any stream capture)
-  MgbLossRes r{};
-  (void)r;
-  int rc = 0;
-  rc |= cudaFuncSetAttribute(k_mr_fwd<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LossCfg<4096>::SMEM);
-  rc |= cudaFuncSetAttribute(k_mr_bwd<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LossCfg<4096>::SMEM);
-  rc |= cudaFuncSetAttribute(k_mr_fwd<8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LossCfg<8192>::SMEM);
-  rc |= cudaFuncSetAttribute(k_mr_bwd<8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LossCfg<8192>::SMEM);
-  rc |= cudaFuncSetAttribute(k_mr_fwd<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LossCfg<2048>::SMEM);
-  rc |= cudaFuncSetAttribute(k_mr_bwd<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LossCfg<2048>::SMEM);
+  // smem attributes set eagerly (outside any stream capture)
+  int rc = loss_attrs<256>() | loss_attrs<512>() | loss_attrs<1024>() | loss_attrs<2048>() | loss_attrs<4096>() |
+           loss_attrs<8192>();
   return rc ? 2 : 0;
 }
 
@@ -379,8 +558,7 @@ extern "C" int mgb_mrstft_backward(const MgbLoss* L, const float* yl, const floa
   cudaStream_t st = (cudaStream_t)stream;
   for (int i = 0; i < L->n_res; ++i)
     if (int rc = dispatch_bwd(L->res[i], L->stats + (size_t)i * 16, *L, yl, yr, L->Ls, st)) return rc;
-  const int blocks = (int)((L->Ls + 255) / 256 < 2048 ? (L->Ls + 255) / 256 : 2048);
-  k_mr_ola<<<blocks, 256, 0, st>>>(*L, gl, gr);
+  k_mr_ola<<<(L->Ls + 255) / 256, 256, 0, st>>>(*L, gl, gr);
   MGB_CHECK_LAUNCH();
   return 0;
 }
