@@ -432,7 +432,7 @@ struct Conv2 {
       cudaFuncSetAttribute(fs2::k_colC<N1, EpGx>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
       cudaFuncSetAttribute(fs2::k_colC<N1, EpGh>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
     }
-    cudaFuncSetAttribute(fs2::k_rowH<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWF_SMEM);
+    cudaFuncSetAttribute(fs2::k_rowH<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWH_SMEM);
     cudaFuncSetAttribute(fs2::k_rowF<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWF_SMEM);
     cudaFuncSetAttribute(fs2::k_rowG<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWG_SMEM);
   }
@@ -442,7 +442,7 @@ struct Conv2 {
     const int fir_rows = (int)((g.M + N2 - 1) / N2);
     fs2::k_colA<N1><<<gc, G::NT, G::COL_SMEM, st>>>(LdFir{w.hbuf, g.M}, w.Ah, fir_rows < N1 ? fir_rows : N1);
     MGB_CHECK_LAUNCH();
-    fs2::k_rowH<N1><<<gr, 2 * fs2::RP * 32, fs2::ROWF_SMEM, st>>>(w.Ah, w.H);
+    fs2::k_rowH<N1><<<gr, 2 * fs2::RP * 32, fs2::ROWH_SMEM, st>>>(w.Ah, w.H);
     MGB_CHECK_LAUNCH();
     return 0;
   }

@@ -28,7 +28,7 @@
 namespace fs2 {
 
 constexpr int N2 = 1024;
-constexpr int RP = 2;  // row pairs (4 warps) per row-kernel CTA
+constexpr int RP = 1;  // row pairs (2 warps) per row-kernel CTA
 
 template <int N1>
 struct G {
@@ -49,8 +49,26 @@ struct G {
 
 constexpr int TP = 33;                 // transpose pitch
 constexpr int TBUF = 32 * TP;          // per-warp transpose buffer (float2)
-constexpr size_t ROWF_SMEM = (size_t)2 * RP * TBUF * sizeof(float2);
-constexpr size_t ROWG_SMEM = (size_t)2 * RP * (TBUF + N2) * sizeof(float2);
+// per-warp shared memory of the row kernels: the transpose buffer plus NROW
+// staged rows of N2 float2 (cp.async prefetch of every operand row)
+template <int NROW>
+constexpr size_t row_smem() { return (size_t)2 * RP * (TBUF + NROW * N2) * sizeof(float2); }
+constexpr size_t ROWH_SMEM = row_smem<1>();
+constexpr size_t ROWF_SMEM = row_smem<2>();
+constexpr size_t ROWG_SMEM = row_smem<3>();
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+// one warp copies a row of N2 float2 (8 KB) into shared memory, 16 B per request
+__device__ __forceinline__ void row_prefetch(float2* dst, const float2* __restrict__ src, int lane) {
+#pragma unroll
+  for (int i = 0; i < N2 / 2 / 32; ++i) cp_async16(dst + 2 * (lane + 32 * i), src + 2 * (lane + 32 * i));
+}
 
 __device__ __forceinline__ void split_pair(float2 zk, float2 zp, float2& a, float2& b) {
   a = make_float2(0.5f * (zk.x + zp.x), 0.5f * (zk.y - zp.y));
@@ -115,6 +133,25 @@ __device__ __forceinline__ void row_fft(float2 (&v)[32], float2* T, int lane) {
   for (int j = 0; j < 32; ++j) v[j] = T[j * TP + lane];
   __syncwarp();
   rf::rdft<32, INV>(v);
+}
+
+// The same forward transform with ONE copy of the 32-point DFT code (run twice
+// in a non-unrolled loop): the row kernels run three transforms per warp and
+// were instruction-cache bound with fully unrolled copies.  Inverses use
+// IFFT(x) = conj(FFT(conj(x))).
+__device__ __forceinline__ void row_fft_compact(float2 (&v)[32], float2* T, int lane) {
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    rf::rdft<32, false>(v);
+    if (h == 1) break;
+    twiddle_run<10, 32, false>(v, 0, lane);
+#pragma unroll
+    for (int kb = 0; kb < 32; ++kb) T[lane * TP + kb] = v[kb];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = T[j * TP + lane];
+    __syncwarp();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -228,125 +265,150 @@ __device__ __forceinline__ RowMap row_map() {
 // Hermitian partner column of spectral column k in row `row` (partner row prow)
 __device__ __forceinline__ int partner_col(int row, int k) { return row == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k); }
 
+// warp-private regions of the row kernels: [T (TBUF) | row 0 | row 1 | ...]
+template <int NROW>
+__device__ __forceinline__ float2* warp_region(unsigned char* smraw, int w) {
+  return reinterpret_cast<float2*>(smraw) + (size_t)w * (TBUF + NROW * N2);
+}
+
 // prep: H[b][row][k] = FFT_{N2}(Ah[b][row][.])  (FIR spectrum, row layout)
 template <int N1>
 __global__ void __launch_bounds__(2 * RP * 32) k_rowH(const float2* __restrict__ Ah, float2* __restrict__ H) {
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
-  float2* T = reinterpret_cast<float2*>(smraw) + (threadIdx.x >> 5) * TBUF;
   const RowMap rm = row_map<N1>();
   if (!rm.active) return;
+  float2* T = warp_region<1>(smraw, threadIdx.x >> 5);
+  float2* sA = T + TBUF;
   const long long base = (long long)blockIdx.y * g::N + (long long)rm.row * N2;
+  row_prefetch(sA, Ah + base, rm.lane);
+  cp_async_wait_all();
+  __syncwarp();
   float2 v[32];
 #pragma unroll
-  for (int m = 0; m < 32; ++m) v[m] = Ah[base + rm.lane + 32 * m];
+  for (int m = 0; m < 32; ++m) v[m] = sA[rm.lane + 32 * m];
   row_fft<false>(v, T, rm.lane);
 #pragma unroll
   for (int ka = 0; ka < 32; ++ka) H[base + rm.lane + 32 * ka] = v[ka];
 }
 
 // forward convolution rows: X = FFT rows of Ax (stored for the backward);
-// Y = X_l H_l + i X_r H_r (paired split); Bo = w_N^{-row n2} IFFT rows of Y
+// Y = X_l H_l + i X_r H_r (paired split); Bo = w_N^{-row n2} IFFT rows of Y.
+// Both operand rows of the warp (Ax, H) are prefetched with cp.async; the
+// partner warp's staged H row and spectrum are read from its region.  The two
+// transforms share one code copy (pass loop); the duplicate warp of a
+// self-paired row computes along but stores nothing.
 template <int N1>
-__global__ void __launch_bounds__(2 * RP * 32, 3) k_rowF(const float2* __restrict__ Ax, const float2* __restrict__ H,
+__global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__ Ax, const float2* __restrict__ H,
                                                      float2* __restrict__ X, float2* __restrict__ Bo) {
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
-  float2* T = reinterpret_cast<float2*>(smraw) + (threadIdx.x >> 5) * TBUF;
-  float2* Tp = reinterpret_cast<float2*>(smraw) + ((threadIdx.x >> 5) ^ 1) * TBUF;
+  const int w = threadIdx.x >> 5;
+  float2* T = warp_region<2>(smraw, w);
+  float2* sA = T + TBUF;       // Ax row, then this row's spectrum (natural order)
+  float2* sH = sA + N2;        // H row
   const RowMap rm = row_map<N1>();
   const bool self = rm.row == rm.prow;
-  const long long bb = (long long)blockIdx.y * g::N;
-  const long long base = bb + (long long)rm.row * N2, pbase = bb + (long long)rm.prow * N2;
+  float2* pA = self ? sA : warp_region<2>(smraw, w ^ 1) + TBUF;
+  float2* pH = pA + N2;
+  const long long base = (long long)blockIdx.y * g::N + (long long)rm.row * N2;
+  const int lane = rm.lane;
+  row_prefetch(sA, Ax + base, lane);
+  row_prefetch(sH, H + base, lane);
+  cp_async_wait_all();
+  __syncwarp();
   float2 v[32];
-  if (rm.active) {
 #pragma unroll
-    for (int m = 0; m < 32; ++m) v[m] = Ax[base + rm.lane + 32 * m];
-    row_fft<false>(v, T, rm.lane);
+  for (int m = 0; m < 32; ++m) v[m] = sA[lane + 32 * m];
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    row_fft_compact(v, T, lane);
+    if (pass == 1) break;
 #pragma unroll
     for (int ka = 0; ka < 32; ++ka) {
-      X[base + rm.lane + 32 * ka] = v[ka];
-      T[rm.lane + 32 * ka] = v[ka];  // natural order for the partner warp
+      if (rm.active) X[base + lane + 32 * ka] = v[ka];
+      sA[lane + 32 * ka] = v[ka];  // natural order for the partner warp
     }
-  }
-  __syncthreads();
-  if (rm.active) {
-    const float2* ps = self ? T : Tp;
+    __syncthreads();
 #pragma unroll
     for (int ka = 0; ka < 32; ++ka) {
-      const int k = rm.lane + 32 * ka, kp = partner_col(rm.row, k);
+      const int k = lane + 32 * ka, kp = partner_col(rm.row, k);
       float2 xl, xr, hl, hr;
-      split_pair(v[ka], ps[kp], xl, xr);
-      split_pair(__ldg(H + base + k), __ldg(H + pbase + kp), hl, hr);
+      split_pair(v[ka], pA[kp], xl, xr);
+      split_pair(sH[k], pH[kp], hl, hr);
       const float2 y1 = cmul(xl, hl), y2 = cmul(xr, hr);
-      v[ka] = make_float2(y1.x - y2.y, y1.y + y2.x);
-      chunk_fence(ka);
+      v[ka] = make_float2(y1.x - y2.y, -(y1.y + y2.x));  // conj: inverse via the forward code
     }
   }
-  __syncthreads();  // partner reads done before T is reused as the transpose buffer
   if (!rm.active) return;
-  row_fft<true>(v, T, rm.lane);
-  twiddle_run<g::LOGN, 32, true>(v, rm.row * rm.lane, rm.row * 32);
 #pragma unroll
-  for (int n = 0; n < 32; ++n) Bo[base + rm.lane + 32 * n] = v[n];
+  for (int n = 0; n < 32; ++n) v[n].y = -v[n].y;
+  twiddle_run<g::LOGN, 32, true>(v, rm.row * lane, rm.row * 32);
+#pragma unroll
+  for (int n = 0; n < 32; ++n) Bo[base + lane + 32 * n] = v[n];
 }
 
 // backward rows: G = FFT rows of Ag; GX = G_l conj(H_l) + i G_r conj(H_r) -> B1,
-// GH = G_l conj(X_l) + i G_r conj(X_r) -> B2, both inverse row FFT'd and conj-twiddled
+// GH = G_l conj(X_l) + i G_r conj(X_r) -> B2, both inverse row FFT'd and conj-twiddled.
+// Ag, X and H rows are prefetched with cp.async into the warp's region; the three
+// transforms share one code copy (pass loop).
 template <int N1>
-__global__ void __launch_bounds__(2 * RP * 32, 3) k_rowG(const float2* __restrict__ Ag, const float2* __restrict__ X,
+__global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__ Ag, const float2* __restrict__ X,
                                                      const float2* __restrict__ H, float2* __restrict__ B1,
                                                      float2* __restrict__ B2) {
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int w = threadIdx.x >> 5;
-  float2* T = reinterpret_cast<float2*>(smraw) + w * TBUF;
-  float2* S = reinterpret_cast<float2*>(smraw) + 2 * RP * TBUF + w * N2;        // own G spectrum
-  float2* Sp = reinterpret_cast<float2*>(smraw) + 2 * RP * TBUF + (w ^ 1) * N2;  // partner's
+  float2* T = warp_region<3>(smraw, w);
+  float2* sA = T + TBUF;       // Ag row, then this row's G spectrum (natural order)
+  float2* sX = sA + N2;
+  float2* sH = sX + N2;
   const RowMap rm = row_map<N1>();
   const bool self = rm.row == rm.prow;
-  const long long bb = (long long)blockIdx.y * g::N;
-  const long long base = bb + (long long)rm.row * N2, pbase = bb + (long long)rm.prow * N2;
-  float2 v[32];
-  if (rm.active) {
-#pragma unroll
-    for (int m = 0; m < 32; ++m) v[m] = Ag[base + rm.lane + 32 * m];
-    row_fft<false>(v, T, rm.lane);
-#pragma unroll
-    for (int ka = 0; ka < 32; ++ka) S[rm.lane + 32 * ka] = v[ka];
-  }
-  __syncthreads();
-  if (!rm.active) return;
-  const float2* ps = self ? S : Sp;
-#pragma unroll
-  for (int ka = 0; ka < 32; ++ka) {
-    const int k = rm.lane + 32 * ka, kp = partner_col(rm.row, k);
-    float2 gl, gr, hl, hr;
-    split_pair(v[ka], ps[kp], gl, gr);
-    split_pair(__ldg(H + base + k), __ldg(H + pbase + kp), hl, hr);
-    const float2 y1 = cmulc(gl, hl), y2 = cmulc(gr, hr);
-    v[ka] = make_float2(y1.x - y2.y, y1.y + y2.x);
-    chunk_fence(ka);
-  }
-  row_fft<true>(v, T, rm.lane);
-  twiddle_run<g::LOGN, 32, true>(v, rm.row * rm.lane, rm.row * 32);
-#pragma unroll
-  for (int n = 0; n < 32; ++n) B1[base + rm.lane + 32 * n] = v[n];
-#pragma unroll
-  for (int ka = 0; ka < 32; ++ka) {
-    const int k = rm.lane + 32 * ka, kp = partner_col(rm.row, k);
-    float2 gl, gr, xl, xr;
-    split_pair(S[k], ps[kp], gl, gr);
-    split_pair(__ldg(X + base + k), __ldg(X + pbase + kp), xl, xr);
-    const float2 y1 = cmulc(gl, xl), y2 = cmulc(gr, xr);
-    v[ka] = make_float2(y1.x - y2.y, y1.y + y2.x);
-    chunk_fence(ka);
-  }
+  float2* pA = self ? sA : warp_region<3>(smraw, w ^ 1) + TBUF;
+  float2* pX = pA + N2;
+  float2* pH = pX + N2;
+  const long long base = (long long)blockIdx.y * g::N + (long long)rm.row * N2;
+  const int lane = rm.lane;
+  row_prefetch(sA, Ag + base, lane);
+  row_prefetch(sX, X + base, lane);
+  row_prefetch(sH, H + base, lane);
+  cp_async_wait_all();
   __syncwarp();
-  row_fft<true>(v, T, rm.lane);
-  twiddle_run<g::LOGN, 32, true>(v, rm.row * rm.lane, rm.row * 32);
+  float2 v[32];
 #pragma unroll
-  for (int n = 0; n < 32; ++n) B2[base + rm.lane + 32 * n] = v[n];
+  for (int m = 0; m < 32; ++m) v[m] = sA[lane + 32 * m];
+#pragma unroll 1
+  for (int pass = 0; pass < 3; ++pass) {
+    row_fft_compact(v, T, lane);
+    if (pass == 0) {
+#pragma unroll
+      for (int ka = 0; ka < 32; ++ka) sA[lane + 32 * ka] = v[ka];
+      __syncthreads();
+    } else {
+#pragma unroll
+      for (int n = 0; n < 32; ++n) v[n].y = -v[n].y;
+      twiddle_run<g::LOGN, 32, true>(v, rm.row * lane, rm.row * 32);
+      float2* dst = (pass == 1 ? B1 : B2) + base + lane;
+      if (rm.active) {
+#pragma unroll
+        for (int n = 0; n < 32; ++n) dst[32 * n] = v[n];
+      }
+      if (pass == 2) break;
+    }
+    // next transform's input: conj(G_l conj(O_l) + i G_r conj(O_r)), O = H (pass 1) or X (pass 2)
+    const float2* oS = pass == 0 ? sH : sX;
+    const float2* oP = pass == 0 ? pH : pX;
+#pragma unroll
+    for (int ka = 0; ka < 32; ++ka) {
+      const int k = lane + 32 * ka, kp = partner_col(rm.row, k);
+      float2 gl, gr, ol, orr;
+      split_pair(sA[k], pA[kp], gl, gr);
+      split_pair(oS[k], oP[kp], ol, orr);
+      const float2 y1 = cmulc(gl, ol), y2 = cmulc(gr, orr);
+      v[ka] = make_float2(y1.x - y2.y, -(y1.y + y2.x));
+    }
+  }
 }
 
 }  // namespace fs2

@@ -224,10 +224,11 @@ __device__ __forceinline__ void mags_inplace(double2* S, int tt) {
       const double2 a = make_double2(0.5 * (zk.x + zp.x), 0.5 * (zk.y - zp.y));
       const double2 d = make_double2(0.5 * (zk.x - zp.x), 0.5 * (zk.y + zp.y));
       const double2 bb = make_double2(d.y, -d.x);
-      m[i][0] = (float)sqrt(a.x * a.x + a.y * a.y);
-      m[i][1] = (float)sqrt(bb.x * bb.x + bb.y * bb.y);
-      m[i][2] = (float)sqrt((a.x + bb.x) * (a.x + bb.x) + (a.y + bb.y) * (a.y + bb.y));
-      m[i][3] = (float)sqrt((a.x - bb.x) * (a.x - bb.x) + (a.y - bb.y) * (a.y - bb.y));
+      // |X|^2 in float64, the root in float32 (the magnitude is stored as float32)
+      m[i][0] = sqrtf((float)(a.x * a.x + a.y * a.y));
+      m[i][1] = sqrtf((float)(bb.x * bb.x + bb.y * bb.y));
+      m[i][2] = sqrtf((float)((a.x + bb.x) * (a.x + bb.x) + (a.y + bb.y) * (a.y + bb.y)));
+      m[i][3] = sqrtf((float)((a.x - bb.x) * (a.x - bb.x) + (a.y - bb.y) * (a.y - bb.y)));
     }
   }
   __syncthreads();
@@ -247,7 +248,7 @@ __device__ __forceinline__ void mags_inplace(double2* S, int tt) {
 // mode 1: estimate (write mel, part[.,g,0] = sum |dlog|, part[.,g,1] = sum (mel - tmel)^2)
 // FPC frames per CTA; within a frame, T/4 threads per group g walk the mel bands.
 template <int N>
-__global__ void __launch_bounds__(FC<N>::NT) k_mr_fwd(MgbLossRes r, const float* __restrict__ xl,
+__global__ void __launch_bounds__(FC<N>::NT, 1024 / FC<N>::NT) k_mr_fwd(MgbLossRes r, const float* __restrict__ xl,
                                                       const float* __restrict__ xr, int Ls, int mode) {
   using C = FC<N>;
   constexpr int T = C::T, NB = C::NB;
@@ -343,7 +344,7 @@ __global__ void k_mr_total(MgbLoss L) {
 // dX per group -> packed Hermitian adjoint of both channels, one inverse FFT,
 // windowed frame adjoints to gframes (float32) for the overlap-add gather.
 template <int N>
-__global__ void __launch_bounds__(FC<N>::NT, (FC<N>::NT <= 256 ? 2 : 1)) k_mr_bwd(MgbLossRes r, const double* __restrict__ stats, MgbLoss L,
+__global__ void __launch_bounds__(FC<N>::NT, 1024 / FC<N>::NT) k_mr_bwd(MgbLossRes r, const double* __restrict__ stats, MgbLoss L,
                                                       const float* __restrict__ xl, const float* __restrict__ xr,
                                                       int Ls) {
   using C = FC<N>;
