@@ -348,7 +348,7 @@ __global__ void k_dw_finalize(const double* __restrict__ part, int nblk, const i
   }
 }
 
-constexpr int kDlyBwdSmem = (2 * MGB_DLY_WIN) * 8 + (3040 + MGB_DLY_WIN) * 4;
+constexpr int kDlyBwdSmem = 0;
 
 // ---------------------------------------------------------------------------
 // per-size drivers
@@ -534,8 +534,6 @@ int mgb_conv_init() {
 #define X(l, a, b) Conv<a, b>::attrs();
   MGB_CONV_SIZES_OLD(X)
 #undef X
-  if (cudaFuncSetAttribute(k_dly_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDlyBwdSmem) != cudaSuccess)
-    return 2;
   cudaFuncSetAttribute(k_eqos_hspec, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
   cudaFuncSetAttribute(k_eqos_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
   cudaFuncSetAttribute(k_eqos_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);

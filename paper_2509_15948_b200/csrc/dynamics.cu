@@ -414,9 +414,8 @@ __global__ void __launch_bounds__(256) k_dyn_bwd0(char tag, const float* const* 
    }
    store4(go, L, n4, vec, make_float4(OL[0], OL[1], OL[2], OL[3]), make_float4(OR[0], OR[1], OR[2], OR[3]), dgo,
           make_float4(OD[0], OD[1], OD[2], OD[3]));
-   sT += fT; sW += fW; sR += fR; sw += fw;
-   fT = fW = fR = fw = 0.f;
   }
+  // (float partials: at most a few float4 groups per thread before the float64 block sum)
   sT += fT; sW += fW; sR += fR; sw += fw;
   sT = block_sum(sT, red);
   __syncthreads();

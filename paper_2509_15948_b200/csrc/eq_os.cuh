@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
   const float cy = (ny > 0.0) ? (float)(sg / ((ny + MGB_GS_EPS) * ny)) : 0.f;
   const float cu = (nu > 0.0) ? (float)(-sg / ((nu + MGB_GS_EPS) * nu)) : 0.f;
   float2 v[32];
-  // 1. d window (dybar) and D
+  // pass 0 input: the d window (dybar)
 #pragma unroll
   for (int m0 = 0; m0 < 32; m0 += 4) {
     float4 g[4];
@@ -247,62 +247,68 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
       v[m0 + q] = make_float2(fmaf(cy, my, wf * g[q].x), fmaf(cy, my, wf * g[q].y));
     }
   }
-  eos_fft(v, S);
-  // D parks in this block's pspec slot (thread-private [r][t] entries, L2-resident) until step 3
   float2* ps = pspec + ((size_t)b * nblk + blk) * EOS_N + t;
+  // pass 0: D = FFT(d) (parked in this block's pspec slot), gx = IDFT(D conj H) -> gu;
+  // pass 1: Xm = FFT(x masked to the block), C = conj(D) Xm -> pspec.  One copy of the
+  // forward-transform code serves both passes (instruction-cache footprint).
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    eos_fft(v, S);
+    if (pass == 1) {
 #pragma unroll
-  for (int r = 0; r < 32; ++r) ps[r * 256] = v[r];
-  // 2. gx = IDFT(D conj H): window index i < HOP is gx[n0 + i]
-  const float2* H = Hs + (size_t)b * EOS_N + t;
-  const float sc = 1.f / (float)EOS_N;
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const float2 h = __ldg(H + r * 256);
-    v[r] = make_float2(sc * (v[r].x * h.x + v[r].y * h.y), sc * (v[r].y * h.x - v[r].x * h.y));
-  }
-  eos_ifft(v, S);
-  float* go = gu + (size_t)b * 2 * L;
-  float fw = 0.f;
-#pragma unroll
-  for (int m0 = 0; m0 < EOS_HOP / 256 + 1; m0 += 5) {  // window indices i < HOP: m <= 24
-    float4 gq[5];
-    float2 uq[5];
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      const int i = t + 256 * (m0 + q);
-      const long long n = n0 + i;
-      const bool in = i < EOS_HOP && n < L;
-      gq[q] = in ? make_float4(__ldg(gy + n), __ldg(gy + L + n), __ldg(yb + n), __ldg(yb + L + n))
-                 : make_float4(0.f, 0.f, 0.f, 0.f);
-      uq[q] = in ? make_float2(__ldg(u + n), __ldg(u + L + n)) : make_float2(0.f, 0.f);
+      for (int r = 0; r < 32; ++r) ps[r * 256] = cmulc(v[r], ps[r * 256]);
+      break;
     }
 #pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      const int i = t + 256 * (m0 + q);
-      const long long n = n0 + i;
-      if (i < EOS_HOP && n < L) {
-        const float2 gx = v[m0 + q];
-        const float mu = uq[q].x + uq[q].y;
-        const float ul = bypass ? gq[q].x : om * gq[q].x, ur = bypass ? gq[q].y : om * gq[q].y;
-        go[n] = fmaf(cu, mu, ul) + gx.x;
-        go[L + n] = fmaf(cu, mu, ur) + gx.y;
-        if (!bypass) fw = fmaf(gq[q].x, gq[q].z - uq[q].x, fmaf(gq[q].y, gq[q].w - uq[q].y, fw));
+    for (int r = 0; r < 32; ++r) ps[r * 256] = v[r];
+    const float2* H = Hs + (size_t)b * EOS_N + t;
+    const float sc = 1.f / (float)EOS_N;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const float2 h = __ldg(H + r * 256);
+      v[r] = make_float2(sc * (v[r].x * h.x + v[r].y * h.y), sc * (v[r].y * h.x - v[r].x * h.y));
+    }
+    eos_ifft(v, S);
+    float* go = gu + (size_t)b * 2 * L;
+    float fw = 0.f;
+#pragma unroll
+    for (int m0 = 0; m0 < EOS_HOP / 256 + 1; m0 += 5) {  // window indices i < HOP: m <= 24
+      float4 gq[5];
+      float2 uq[5];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const int i = t + 256 * (m0 + q);
+        const long long n = n0 + i;
+        const bool in = i < EOS_HOP && n < L;
+        gq[q] = in ? make_float4(__ldg(gy + n), __ldg(gy + L + n), __ldg(yb + n), __ldg(yb + L + n))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        uq[q] = in ? make_float2(__ldg(u + n), __ldg(u + L + n)) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const int i = t + 256 * (m0 + q);
+        const long long n = n0 + i;
+        if (i < EOS_HOP && n < L) {
+          const float2 gx = v[m0 + q];
+          const float mu = uq[q].x + uq[q].y;
+          const float ul = bypass ? gq[q].x : om * gq[q].x, ur = bypass ? gq[q].y : om * gq[q].y;
+          go[n] = fmaf(cu, mu, ul) + gx.x;
+          go[L + n] = fmaf(cu, mu, ur) + gx.y;
+          if (!bypass) fw = fmaf(gq[q].x, gq[q].z - uq[q].x, fmaf(gq[q].y, gq[q].w - uq[q].y, fw));
+        }
       }
     }
-  }
-  const double tw = block_sum((double)fw, red);
-  if (t == 0) part[((size_t)b * kMaxParts + blk) * 4 + 2] = tw;
-  // 3. x masked to the block, its spectrum, C = conj(D) Xm
+    const double tw = block_sum((double)fw, red);
+    if (t == 0) part[((size_t)b * kMaxParts + blk) * 4 + 2] = tw;
+    // pass 1 input: x masked to the block
 #pragma unroll
-  for (int m = 0; m < 32; ++m) {
-    const int i = t + 256 * m;
-    const long long n = w0 + i;
-    v[m] = (i >= EOS_OFF && i < EOS_OFF + EOS_HOP && n < L) ? make_float2(__ldg(u + n), __ldg(u + L + n))
-                                                              : make_float2(0.f, 0.f);
+    for (int m = 0; m < 32; ++m) {
+      const int i = t + 256 * m;
+      const long long n = w0 + i;
+      v[m] = (i >= EOS_OFF && i < EOS_OFF + EOS_HOP && n < L) ? make_float2(__ldg(u + n), __ldg(u + L + n))
+                                                                : make_float2(0.f, 0.f);
+    }
   }
-  eos_fft(v, S);
-#pragma unroll
-  for (int r = 0; r < 32; ++r) ps[r * 256] = cmulc(v[r], ps[r * 256]);
 }
 
 // Csum[b][slot] = sum over blocks of C (float64, fixed order), one thread per slot

@@ -313,22 +313,20 @@ __global__ void __launch_bounds__(NT) k_dly_place(const float* __restrict__ colo
 }
 
 // One CTA per (tap, channel, row): colour gradient (gather + zero-phase FIR
-// adjoint) and the damped-sinusoid surrogate z-gradient
-// graw = conj( (1/n) sum_k k z^{k-1} E_k ),  E_k = sum_t e_t e^{+2 pi i k t / n},
-// e_t = sum_j dh[m*3000 + t + j] colour[j]   (mg/processors.py:274-300).
-// E is a 3000-point DFT done as 60 x 50 (t = t1 + 50 t2, k = k2 + 60 k1).
+// adjoint) and the damped-sinusoid surrogate z-gradient (mg/processors.py:274-300)
+//   graw = conj( sum_t e_t deriv_t ),  deriv = ifft(k z^{k-1}) (length n = 3000, k = 0 term 0),
+//   e_t = sum_j dh[m*3000 + t + j] colour[j].
+// deriv has a closed form: with w = e^{2 pi i / n} and q = z w^t (so q^n = z^n),
+//   deriv_t = (1/n) w^t f(q),  f(q) = sum_{k=1}^{n-1} k q^{k-1} = (1 - n z^{n-1} w^{-t} + (n-1) z^n) / (1 - q)^2,
+// evaluated in float64 (relative error ~ 2 eps / (n |1-q|^2)); for |1-q| < 1e-6 the
+// series itself is summed.  This replaces the 3000-point DFT of e_t.
 __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank, const int* __restrict__ prow,
                                                 const float* __restrict__ colour, const int* __restrict__ offs,
                                                 const float2* __restrict__ GH, int N,
                                                 double* __restrict__ gbank) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  float2* A = reinterpret_cast<float2*>(dsm);                  // 3000
-  float2* E = A + MGB_DLY_WIN;                                 // 3000
-  float* seg = reinterpret_cast<float*>(E + MGB_DLY_WIN);      // 3040
-  float* et = seg + 3040;                                      // 3000
+  __shared__ float seg[3040];
   __shared__ float col[MGB_COLOR_LEN];
   __shared__ double dhz[MGB_COLOR_LEN];
-  __shared__ float2 w60[60], w50[50];
   __shared__ double red[32];
   const int tap = blockIdx.x, ch = blockIdx.y, b = blockIdx.z;
   const float2* g = GH + (size_t)b * N;
@@ -339,16 +337,6 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
   }
   if (threadIdx.x < MGB_COLOR_LEN)
     col[threadIdx.x] = colour[(((size_t)b * 2 + ch) * MGB_DLY_TAPS + tap) * MGB_COLOR_LEN + threadIdx.x];
-  if (threadIdx.x < 60) {
-    float s, c;
-    sincospif(2.0f * threadIdx.x / 60.0f, &s, &c);
-    w60[threadIdx.x] = make_float2(c, s);
-  }
-  if (threadIdx.x < 50) {
-    float s, c;
-    sincospif(2.0f * threadIdx.x / 50.0f, &s, &c);
-    w50[threadIdx.x] = make_float2(c, s);
-  }
   const int d = offs[((size_t)b * 2 + ch) * MGB_DLY_TAPS + tap];
   const double* p = bank + (size_t)prow[b] * 880 + ch * 440;
   double* gp = gbank + (size_t)prow[b] * 880 + ch * 440;
@@ -359,13 +347,6 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
     const double win = 0.5 - 0.5 * cospi(2.0 * tp / 38.0);
     dhz[(tp + 20) % MGB_COLOR_LEN] = (double)seg[d + tp] * win;
   }
-  // e_t
-  for (int t = threadIdx.x; t < MGB_DLY_WIN; t += NT) {
-    float acc = 0.f;
-#pragma unroll
-    for (int j = 0; j < MGB_COLOR_LEN; ++j) acc = fmaf(seg[t + j], col[j], acc);
-    et[t] = acc;
-  }
   __syncthreads();
   if (threadIdx.x < MGB_COLOR_BINS) {
     const int k = threadIdx.x;
@@ -374,69 +355,71 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
     const double sc = (k == 0 ? 1.0 : 2.0) / 39.0;
     gp[40 + tap * MGB_COLOR_BINS + k] = acc * sc * exp(p[40 + tap * MGB_COLOR_BINS + k]);
   }
-  // step A: A[t1][k2] = w_3000^{k2 t1} * sum_{t2} e[t1 + 50 t2] w_60^{k2 t2}
-  for (int o = threadIdx.x; o < MGB_DLY_WIN; o += NT) {
-    const int t1 = o / 60, k2 = o % 60;
-    float re = 0.f, im = 0.f;
-    int idx = 0;
-    for (int t2 = 0; t2 < 60; ++t2) {
-      const float e = et[t1 + 50 * t2];
-      re = fmaf(e, w60[idx].x, re);
-      im = fmaf(e, w60[idx].y, im);
-      idx += k2;
-      if (idx >= 60) idx -= 60;
-    }
-    float s, c;
-    sincospif(2.0f * (float)(k2 * t1) / 3000.0f, &s, &c);
-    A[o] = make_float2(re * c - im * s, re * s + im * c);
-  }
-  __syncthreads();
-  // step B: E[k2 + 60 k1] = sum_{t1} A[t1][k2] w_50^{k1 t1}
-  for (int o = threadIdx.x; o < MGB_DLY_WIN; o += NT) {
-    const int k1 = o / 60, k2 = o % 60;
-    float re = 0.f, im = 0.f;
-    int idx = 0;
-    for (int t1 = 0; t1 < 50; ++t1) {
-      const float2 a = A[t1 * 60 + k2];
-      const float2 w = w50[idx];
-      re += a.x * w.x - a.y * w.y;
-      im += a.x * w.y + a.y * w.x;
-      idx += k1;
-      if (idx >= 50) idx -= 50;
-    }
-    E[k2 + 60 * k1] = make_float2(re, im);
-  }
-  __syncthreads();
-  // S = (1/n) sum_{k>=1} k z^{k-1} E_k   (z projected into the unit disk)
+  // z projected into the unit disk; z^n, z^{n-1} from log space (as the reference's powers)
+  constexpr int n = MGB_DLY_WIN;
   double zr = p[tap], zi = p[20 + tap];
   const double mag = sqrt(zr * zr + zi * zi);
   if (mag > 1.0) { zr /= mag; zi /= mag; }
   const bool zero = (zr == 0.0 && zi == 0.0);
-  const double lmag = zero ? 0.0 : log(zero ? 1.0 : fmin(mag, 1.0));
+  const double lmag = zero ? 0.0 : log(fmin(mag, 1.0));
   const double th = atan2(zi, zr);
+  double zn_r = 0.0, zn_i = 0.0, zm_r = 0.0, zm_i = 0.0;  // z^n, z^{n-1}
+  if (!zero) {
+    double s, c;
+    const double an = exp((double)n * lmag), am = exp((double)(n - 1) * lmag);
+    sincos((double)n * th, &s, &c);
+    zn_r = an * c;
+    zn_i = an * s;
+    sincos((double)(n - 1) * th, &s, &c);
+    zm_r = am * c;
+    zm_i = am * s;
+  }
+  // this thread's contiguous run of t; w^t by a float64 recurrence from one sincospi
+  constexpr int PER = (n + NT - 1) / NT;
+  const int t0 = threadIdx.x * PER;
+  double wr, wi, sr, si;
+  sincospi(2.0 * (double)t0 / (double)n, &wi, &wr);
+  sincospi(2.0 / (double)n, &si, &sr);
   double sre = 0.0, sim = 0.0;
-  for (int k = 1 + threadIdx.x; k < MGB_DLY_WIN; k += NT) {
-    double pr, pi;
-    if (zero) {
-      pr = (k == 1) ? 1.0 : 0.0;
-      pi = 0.0;
-    } else {
-      const double a = exp((double)(k - 1) * lmag);
-      double s, c;
-      sincos((double)(k - 1) * th, &s, &c);
-      pr = a * c;
-      pi = a * s;
+  for (int t = t0; t < t0 + PER && t < n; ++t) {
+    float et = 0.f;
+#pragma unroll
+    for (int j = 0; j < MGB_COLOR_LEN; ++j) et = fmaf(seg[t + j], col[j], et);
+    // q = z w^t
+    const double qr = zr * wr - zi * wi, qi = zr * wi + zi * wr;
+    const double ar = 1.0 - qr, ai = -qi;  // 1 - q
+    double fr, fi;
+    if (ar * ar + ai * ai >= 1e-12) {
+      // numerator 1 - n z^{n-1} conj(w^t) + (n-1) z^n
+      const double nr = 1.0 - (double)n * (zm_r * wr + zm_i * wi) + (double)(n - 1) * zn_r;
+      const double ni = -(double)n * (zm_i * wr - zm_r * wi) + (double)(n - 1) * zn_i;
+      const double dr = ar * ar - ai * ai, di = 2.0 * ar * ai;  // (1 - q)^2
+      const double den = dr * dr + di * di;
+      fr = (nr * dr + ni * di) / den;
+      fi = (ni * dr - nr * di) / den;
+    } else {  // q ~ 1: Horner on the series
+      fr = (double)(n - 1);
+      fi = 0.0;
+      for (int k = n - 2; k >= 1; --k) {
+        const double tr = fr * qr - fi * qi + (double)k;
+        fi = fr * qi + fi * qr;
+        fr = tr;
+      }
     }
-    const double er = E[k].x, ei = E[k].y;
-    sre += (double)k * (pr * er - pi * ei);
-    sim += (double)k * (pr * ei + pi * er);
+    // deriv_t = w^t f / n
+    const double der = (wr * fr - wi * fi) / (double)n, dei = (wr * fi + wi * fr) / (double)n;
+    sre += (double)et * der;
+    sim += (double)et * dei;
+    const double nw = wr * sr - wi * si;
+    wi = wr * si + wi * sr;
+    wr = nw;
   }
   sre = block_sum(sre, red);
   __syncthreads();
   sim = block_sum(sim, red);
   if (threadIdx.x == 0) {
-    gp[tap] = sre / (double)MGB_DLY_WIN;
-    gp[20 + tap] = -sim / (double)MGB_DLY_WIN;
+    gp[tap] = sre;
+    gp[20 + tap] = -sim;
   }
 }
 
