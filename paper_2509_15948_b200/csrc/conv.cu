@@ -182,7 +182,9 @@ struct LdBwdPro {
     return c;
   }
   __device__ __forceinline__ Raw fetch(const Ctx& c, int, long long n, bool ok) const {
-    Raw r;
+    // zero defaults (not "undefined"): otherwise the compiler seeds the predicated-off
+    // destinations with earlier loaded registers, chaining each batch on the last one
+    Raw r{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, false};
     const long long m = n - off;
     r.in = ok && m >= 0 && m < L;
     if (r.in) {

@@ -522,9 +522,55 @@ int loss_attrs() {
   return rc;
 }
 
+// Per-device side streams: the resolutions of one MRSTFT call are independent
+// until the finalize, so they are forked onto their own streams (event fork /
+// join on the caller's stream; legal under stream capture) to fill the GPU
+// instead of running three ~1-wave launches back to back.
+constexpr int kMaxDev = 64;
+constexpr int kSide = 7;
+cudaStream_t g_side[kMaxDev][kSide];
+cudaEvent_t g_fork[kMaxDev], g_join[kMaxDev][kSide];
+bool g_side_ok[kMaxDev];
+
+int side_init() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= kMaxDev) return 2;
+  if (g_side_ok[dev]) return 0;
+  if (cudaEventCreateWithFlags(&g_fork[dev], cudaEventDisableTiming) != cudaSuccess) return 2;
+  for (int i = 0; i < kSide; ++i) {
+    if (cudaStreamCreateWithFlags(&g_side[dev][i], cudaStreamNonBlocking) != cudaSuccess) return 2;
+    if (cudaEventCreateWithFlags(&g_join[dev][i], cudaEventDisableTiming) != cudaSuccess) return 2;
+  }
+  g_side_ok[dev] = true;
+  return 0;
+}
+
+// run fn(i, stream) for i < n, resolution i on side stream i (i > 0) or the caller (i = 0)
+template <class F>
+int fork_res(int n, cudaStream_t st, F fn) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (n <= 1 || dev >= kMaxDev || !g_side_ok[dev]) {
+    for (int i = 0; i < n; ++i)
+      if (int rc = fn(i, st)) return rc;
+    return 0;
+  }
+  if (cudaEventRecord(g_fork[dev], st) != cudaSuccess) return 2;
+  for (int i = 1; i < n; ++i)
+    if (cudaStreamWaitEvent(g_side[dev][i - 1], g_fork[dev], 0) != cudaSuccess) return 2;
+  for (int i = 0; i < n; ++i)
+    if (int rc = fn(i, i == 0 ? st : g_side[dev][i - 1])) return rc;
+  for (int i = 1; i < n; ++i) {
+    if (cudaEventRecord(g_join[dev][i - 1], g_side[dev][i - 1]) != cudaSuccess) return 2;
+    if (cudaStreamWaitEvent(st, g_join[dev][i - 1], 0) != cudaSuccess) return 2;
+  }
+  return 0;
+}
+
 }  // namespace
 
 int mgb_loss_init() {
+  if (side_init()) return 2;
   // smem attributes set eagerly (outside any stream capture)
   int rc = loss_attrs<256>() | loss_attrs<512>() | loss_attrs<1024>() | loss_attrs<2048>() | loss_attrs<4096>() |
            loss_attrs<8192>();
@@ -534,8 +580,8 @@ int mgb_loss_init() {
 extern "C" int mgb_mrstft_target(const MgbLoss* L, const float* tl, const float* tr, void* stream) {
   if (int rc = check_loss(L)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  for (int i = 0; i < L->n_res; ++i)
-    if (int rc = dispatch_fwd(L->res[i], tl, tr, L->Ls, 0, st)) return rc;
+  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) { return dispatch_fwd(L->res[i], tl, tr, L->Ls, 0, s); }))
+    return rc;
   k_mr_finalize<<<4 * L->n_res, 256, 0, st>>>(*L, 0);
   MGB_CHECK_LAUNCH();
   return 0;
@@ -544,8 +590,8 @@ extern "C" int mgb_mrstft_target(const MgbLoss* L, const float* tl, const float*
 extern "C" int mgb_mrstft_forward(const MgbLoss* L, const float* yl, const float* yr, void* stream) {
   if (int rc = check_loss(L)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  for (int i = 0; i < L->n_res; ++i)
-    if (int rc = dispatch_fwd(L->res[i], yl, yr, L->Ls, 1, st)) return rc;
+  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) { return dispatch_fwd(L->res[i], yl, yr, L->Ls, 1, s); }))
+    return rc;
   k_mr_finalize<<<4 * L->n_res, 256, 0, st>>>(*L, 1);
   MGB_CHECK_LAUNCH();
   k_mr_total<<<1, 32, 0, st>>>(*L);
@@ -557,8 +603,10 @@ extern "C" int mgb_mrstft_backward(const MgbLoss* L, const float* yl, const floa
                                    void* stream) {
   if (int rc = check_loss(L)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  for (int i = 0; i < L->n_res; ++i)
-    if (int rc = dispatch_bwd(L->res[i], L->stats + (size_t)i * 16, *L, yl, yr, L->Ls, st)) return rc;
+  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) {
+        return dispatch_bwd(L->res[i], L->stats + (size_t)i * 16, *L, yl, yr, L->Ls, s);
+      }))
+    return rc;
   k_mr_ola<<<(L->Ls + 255) / 256, 256, 0, st>>>(*L, gl, gr);
   MGB_CHECK_LAUNCH();
   return 0;
