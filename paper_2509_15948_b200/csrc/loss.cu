@@ -2,7 +2,7 @@
 //
 // Per resolution n (hop n/4, reflect pad n/2, periodic Hann), a few frames
 // per CTA: both output channels ride one complex float64 FFT (left + i*right),
-// done as register radix-16 Stockham stages with shared-memory exchanges; the four groups [L, R, L+R, L-R] are separated from the
+// done as register radix-8 Stockham stages with shared-memory exchanges; the four groups [L, R, L+R, L-R] are separated from the
 // spectrum by linearity; |X| x (A-weight * HTK mel) is applied as a banded
 // (CSR) product; log-mel L1 and spectral-convergence partial sums are reduced
 // per frame (float64) and combined by a one-CTA finalize.
@@ -29,9 +29,9 @@ __device__ __forceinline__ long long reflect_idx(long long i, long long n) {
 }
 
 // ---------------------------------------------------------------------------
-// Frame FFTs in registers (float32): Stockham autosort, radix-16 stages (+ one
-// radix-2/4/8 stage where log2 N is not a multiple of 4); a frame is transformed
-// by T threads holding V = 16 values each; the first stage's inputs come straight
+// Frame FFTs in registers (float32): Stockham autosort, radix-8 stages (+ one
+// radix-2/4 stage where log2 N is not a multiple of 3); a frame is transformed
+// by T threads holding V = 8 values each; the first stage's inputs come straight
 // from global memory (windowed, reflect-padded), later stages read the previous
 // stage's outputs from padded shared memory.
 //
@@ -43,17 +43,27 @@ __device__ __forceinline__ long long reflect_idx(long long i, long long n) {
 
 __device__ __forceinline__ int pd16(int i) { return i + (i >> 4); }  // 8-byte slots, 1 pad per 16
 
-template <int N> struct FP;
-template <> struct FP<256> { static constexpr int T = 16, R1 = 16, R2 = 16, R3 = 1, R4 = 1; };
-template <> struct FP<512> { static constexpr int T = 32, R1 = 16, R2 = 16, R3 = 2, R4 = 1; };
-template <> struct FP<1024> { static constexpr int T = 64, R1 = 16, R2 = 16, R3 = 4, R4 = 1; };
-template <> struct FP<2048> { static constexpr int T = 128, R1 = 16, R2 = 16, R3 = 8, R4 = 1; };
-template <> struct FP<4096> { static constexpr int T = 256, R1 = 16, R2 = 16, R3 = 16, R4 = 1; };
-template <> struct FP<8192> { static constexpr int T = 512, R1 = 16, R2 = 16, R3 = 16, R4 = 2; };
+// plans: V = 16 values per thread (radix-16 stages, used by the forward) or
+// V = 8 (radix-8 stages, the backward: shorter per-bin unrolls, less register
+// pressure next to the adjoint work)
+template <int N, int V> struct FP;
+template <> struct FP<256, 16> { static constexpr int T = 16, R1 = 16, R2 = 16, R3 = 1, R4 = 1, R5 = 1; };
+template <> struct FP<512, 16> { static constexpr int T = 32, R1 = 16, R2 = 16, R3 = 2, R4 = 1, R5 = 1; };
+template <> struct FP<1024, 16> { static constexpr int T = 64, R1 = 16, R2 = 16, R3 = 4, R4 = 1, R5 = 1; };
+template <> struct FP<2048, 16> { static constexpr int T = 128, R1 = 16, R2 = 16, R3 = 8, R4 = 1, R5 = 1; };
+template <> struct FP<4096, 16> { static constexpr int T = 256, R1 = 16, R2 = 16, R3 = 16, R4 = 1, R5 = 1; };
+template <> struct FP<8192, 16> { static constexpr int T = 512, R1 = 16, R2 = 16, R3 = 16, R4 = 2, R5 = 1; };
+template <> struct FP<256, 8> { static constexpr int T = 32, R1 = 8, R2 = 8, R3 = 4, R4 = 1, R5 = 1; };
+template <> struct FP<512, 8> { static constexpr int T = 64, R1 = 8, R2 = 8, R3 = 8, R4 = 1, R5 = 1; };
+template <> struct FP<1024, 8> { static constexpr int T = 128, R1 = 8, R2 = 8, R3 = 8, R4 = 2, R5 = 1; };
+template <> struct FP<2048, 8> { static constexpr int T = 256, R1 = 8, R2 = 8, R3 = 8, R4 = 4, R5 = 1; };
+template <> struct FP<4096, 8> { static constexpr int T = 512, R1 = 8, R2 = 8, R3 = 8, R4 = 8, R5 = 1; };
+template <> struct FP<8192, 8> { static constexpr int T = 1024, R1 = 8, R2 = 8, R3 = 8, R4 = 8, R5 = 2; };
 
-template <int N>
+template <int N, int VV>
 struct FC {
-  static constexpr int T = FP<N>::T, V = N / T;
+  using P = FP<N, VV>;
+  static constexpr int T = P::T, V = N / T;
   static constexpr int FPC = T >= 256 ? 1 : 256 / T;  // frames per CTA (CTA = max(256, T) threads)
   static constexpr int NT = T * FPC;
   static constexpr int NB = N / 2 + 1;
@@ -63,9 +73,9 @@ struct FC {
 
 // One Stockham stage over this thread's butterflies j = tt + T i (i < V/R):
 // inputs v[i*R + m] = x[j + m N/R]; outputs y[(j/NS) NS R + j%NS + m NS] -> S
-template <int N, int R, int NS, bool INV>
+template <int N, int VV, int R, int NS, bool INV>
 __device__ __forceinline__ void st_stage(float2* v, float2* S, int tt) {
-  constexpr int T = FC<N>::T, V = FC<N>::V;
+  constexpr int T = FC<N, VV>::T, V = FC<N, VV>::V;
 #pragma unroll
   for (int i = 0; i < V / R; ++i) {
     const int j = tt + T * i, k = j % NS;
@@ -86,9 +96,9 @@ __device__ __forceinline__ void st_stage(float2* v, float2* S, int tt) {
 }
 
 // gather the inputs of a radix-R stage from S
-template <int N, int R>
+template <int N, int VV, int R>
 __device__ __forceinline__ void st_gather(float2* v, const float2* S, int tt) {
-  constexpr int T = FC<N>::T, V = FC<N>::V;
+  constexpr int T = FC<N, VV>::T, V = FC<N, VV>::V;
 #pragma unroll
   for (int i = 0; i < V / R; ++i)
 #pragma unroll
@@ -97,34 +107,40 @@ __device__ __forceinline__ void st_gather(float2* v, const float2* S, int tt) {
 
 // all stages after the first stage's inputs are in v; result (natural order) in S.
 // Contains __syncthreads: every thread of the CTA must call it.
-template <int N, bool INV>
+template <int N, int VV, bool INV>
 __device__ __forceinline__ void frame_fft(float2* v, float2* S, int tt) {
-  using P = FP<N>;
-  st_stage<N, P::R1, 1, INV>(v, S, tt);
+  using P = FP<N, VV>;
+  st_stage<N, VV, P::R1, 1, INV>(v, S, tt);
   __syncthreads();
-  st_gather<N, P::R2>(v, S, tt);
+  st_gather<N, VV, P::R2>(v, S, tt);
   __syncthreads();
-  st_stage<N, P::R2, P::R1, INV>(v, S, tt);
+  st_stage<N, VV, P::R2, P::R1, INV>(v, S, tt);
   __syncthreads();
   if constexpr (P::R3 > 1) {
-    st_gather<N, P::R3>(v, S, tt);
+    st_gather<N, VV, P::R3>(v, S, tt);
     __syncthreads();
-    st_stage<N, P::R3, P::R1 * P::R2, INV>(v, S, tt);
+    st_stage<N, VV, P::R3, P::R1 * P::R2, INV>(v, S, tt);
     __syncthreads();
   }
   if constexpr (P::R4 > 1) {
-    st_gather<N, P::R4>(v, S, tt);
+    st_gather<N, VV, P::R4>(v, S, tt);
     __syncthreads();
-    st_stage<N, P::R4, P::R1 * P::R2 * P::R3, INV>(v, S, tt);
+    st_stage<N, VV, P::R4, P::R1 * P::R2 * P::R3, INV>(v, S, tt);
+    __syncthreads();
+  }
+  if constexpr (P::R5 > 1) {
+    st_gather<N, VV, P::R5>(v, S, tt);
+    __syncthreads();
+    st_stage<N, VV, P::R5, P::R1 * P::R2 * P::R3 * P::R4, INV>(v, S, tt);
     __syncthreads();
   }
 }
 
 // windowed, reflect-padded frame f of (xl + i xr) into the first stage's inputs
-template <int N>
+template <int N, int VV>
 __device__ __forceinline__ void load_frame(float2* v, const float* __restrict__ xl, const float* __restrict__ xr,
                                            int Ls, int hop, int f, bool valid, int tt) {
-  constexpr int T = FC<N>::T, V = FC<N>::V, R = FP<N>::R1;
+  constexpr int T = FC<N, VV>::T, V = FC<N, VV>::V, R = FP<N, VV>::R1;
 #pragma unroll
   for (int i = 0; i < V / R; ++i)
 #pragma unroll
@@ -143,9 +159,9 @@ __device__ __forceinline__ void load_frame(float2* v, const float* __restrict__ 
 
 // spectrum in S (natural, padded) -> the 4 group magnitudes as float32,
 // md[g*NB + k] over the start of the same buffer (all reads precede the barrier)
-template <int N>
+template <int N, int VV>
 __device__ __forceinline__ void mags_inplace(float2* S, int tt) {
-  constexpr int T = FC<N>::T, NB = FC<N>::NB, PER = (NB + T - 1) / T;
+  constexpr int T = FC<N, VV>::T, NB = FC<N, VV>::NB, PER = (NB + T - 1) / T;
   float m[PER][4];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
@@ -178,9 +194,9 @@ __device__ __forceinline__ void mags_inplace(float2* S, int tt) {
 // mode 1: estimate (write mel, part[.,g,0] = sum |dlog|, part[.,g,1] = sum (mel - tmel)^2)
 // FPC frames per CTA; within a frame, T/4 threads per group g walk the mel bands.
 template <int N>
-__global__ void __launch_bounds__(FC<N>::NT, 1024 / FC<N>::NT) k_mr_fwd(MgbLossRes r, const float* __restrict__ xl,
+__global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(MgbLossRes r, const float* __restrict__ xl,
                                                       const float* __restrict__ xr, int Ls, int mode) {
-  using C = FC<N>;
+  using C = FC<N, 16>;
   constexpr int T = C::T, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double red[2][C::NT];
@@ -189,9 +205,9 @@ __global__ void __launch_bounds__(FC<N>::NT, 1024 / FC<N>::NT) k_mr_fwd(MgbLossR
   const bool valid = f < r.frames;
   float2* S = reinterpret_cast<float2*>(smraw) + q * C::PADN;
   float2 v[C::V];
-  load_frame<N>(v, xl, xr, Ls, r.hop, f, valid, tt);
-  frame_fft<N, false>(v, S, tt);
-  mags_inplace<N>(S, tt);
+  load_frame<N, 16>(v, xl, xr, Ls, r.hop, f, valid, tt);
+  frame_fft<N, 16, false>(v, S, tt);
+  mags_inplace<N, 16>(S, tt);
   const float* md = reinterpret_cast<const float*>(S);
   const int nm = r.n_mels;
   const int g = tt & 3;  // items idx = tt + T i: group idx % 4 (fixed per thread), band idx / 4
@@ -274,10 +290,10 @@ __global__ void k_mr_total(MgbLoss L) {
 // dX per group -> packed Hermitian adjoint of both channels, one inverse FFT,
 // windowed frame adjoints to gframes (float32) for the overlap-add gather.
 template <int N>
-__global__ void __launch_bounds__(FC<N>::NT, 1024 / FC<N>::NT) k_mr_bwd(MgbLossRes r, const double* __restrict__ stats,
+__global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(MgbLossRes r, const double* __restrict__ stats,
                                                                        MgbLoss L, const float* __restrict__ xl,
                                                                        const float* __restrict__ xr, int Ls) {
-  using C = FC<N>;
+  using C = FC<N, 8>;
   constexpr int T = C::T, NB = C::NB, PER = (NB + T - 1) / T;
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ float dmel[C::FPC][4][128];
@@ -309,8 +325,8 @@ __global__ void __launch_bounds__(FC<N>::NT, 1024 / FC<N>::NT) k_mr_bwd(MgbLossR
     }
   }
   float2 v[C::V];
-  load_frame<N>(v, xl, xr, Ls, r.hop, f, valid, tt);
-  frame_fft<N, false>(v, S, tt);  // (its barriers also publish dmel)
+  load_frame<N, 8>(v, xl, xr, Ls, r.hop, f, valid, tt);
+  frame_fft<N, 8, false>(v, S, tt);  // (its barriers also publish dmel)
   float2 dl[PER], dr[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
@@ -355,9 +371,9 @@ __global__ void __launch_bounds__(FC<N>::NT, 1024 / FC<N>::NT) k_mr_bwd(MgbLossR
     }
   }
   __syncthreads();
-  st_gather<N, FP<N>::R1>(v, S, tt);
+  st_gather<N, 8, FP<N, 8>::R1>(v, S, tt);
   __syncthreads();
-  frame_fft<N, true>(v, S, tt);
+  frame_fft<N, 8, true>(v, S, tt);
   if (!valid) return;
   float* gf = r.gframes + (size_t)f * 2 * N;
   for (int t = tt; t < N; t += T) {
@@ -403,7 +419,7 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
 
 template <int N>
 int launch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, int mode, cudaStream_t st) {
-  using C = FC<N>;
+  using C = FC<N, 16>;
   k_mr_fwd<N><<<(r.frames + C::FPC - 1) / C::FPC, C::NT, C::SMEM, st>>>(r, xl, xr, Ls, mode);
   MGB_CHECK_LAUNCH();
   return 0;
@@ -412,7 +428,7 @@ int launch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, in
 template <int N>
 int launch_bwd(const MgbLossRes& r, const double* stats, const MgbLoss& L, const float* xl, const float* xr,
                int Ls, cudaStream_t st) {
-  using C = FC<N>;
+  using C = FC<N, 8>;
   k_mr_bwd<N><<<(r.frames + C::FPC - 1) / C::FPC, C::NT, C::SMEM, st>>>(r, stats, L, xl, xr, Ls);
   MGB_CHECK_LAUNCH();
   return 0;
@@ -455,8 +471,8 @@ int check_loss(const MgbLoss* L) {
 template <int N>
 int loss_attrs() {
   int rc = 0;
-  rc |= cudaFuncSetAttribute(k_mr_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC<N>::SMEM);
-  rc |= cudaFuncSetAttribute(k_mr_bwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC<N>::SMEM);
+  rc |= cudaFuncSetAttribute(k_mr_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC<N, 16>::SMEM);
+  rc |= cudaFuncSetAttribute(k_mr_bwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC<N, 8>::SMEM);
   return rc;
 }
 
