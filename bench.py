@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--length", type=int, default=L_SAMPLES)
     ap.add_argument("--eager-profile", type=int, default=0,
                     help="run N eager (non-graph) steps and exit: for ncu launch lists")
+    ap.add_argument("--profile-level", default="",
+                    help="e.g. d@step6: after one eager step, run only that level's forward+backward "
+                         "(--eager-profile times) and exit: per-level ncu traffic")
     return ap.parse_args()
 
 
@@ -197,6 +200,24 @@ def main():
     opt = make_optimizer(params, cfg, device=dev)
     eng = TrainEngine(graph, L, _EngineCfg(opt, cfg), device=dev, use_graph=not args.eager_profile)
     eng.load_params(params)
+    if args.eager_profile and args.profile_level:
+        import ctypes
+
+        from paper_2509_15948_b200._lib import check, lib
+        from paper_2509_15948_b200.engine import stream_ptr
+        eng.plan.set_stems(stems)
+        eng.target.copy_(torch.from_numpy(target))
+        eng.grads_only()
+        lv = next(lv for lv in eng.plan.levels if lv.struct is not None and f"{lv.tag}@step{lv.step}" == args.profile_level)
+        Ld = lib()
+        n0 = Ld.mgb_launch_count()
+        for _ in range(args.eager_profile):
+            check(Ld.mgb_level_forward(ctypes.byref(lv.struct), stream_ptr()), "fwd")
+            check(Ld.mgb_level_backward(ctypes.byref(lv.struct), stream_ptr()), "bwd")
+        torch.cuda.synchronize()
+        per = (Ld.mgb_launch_count() - n0) // args.eager_profile
+        print(json.dumps({"profile_level": args.profile_level, "reps": args.eager_profile, "launches_per_rep": per}))
+        return
     if args.eager_profile:
         eng.plan.set_stems(stems)
         eng.target.copy_(torch.from_numpy(target))
@@ -269,9 +290,18 @@ def main():
     if dom:
         name, rec = dom
         ach = rec["bytes"] / (rec["ms"] / 1e3) / 1e9
+        traffic, traffic_src = None, None
+        try:  # DRAM bytes of this level's kernels, one ncu capture (tools/ncu_traffic.sh)
+            with open(os.path.join(ROOT, "profiles", "level_traffic_config2.json")) as fh:
+                lt = json.load(fh)
+            if lt.get("level") == name.split("(")[0]:
+                traffic, traffic_src = lt["dram_bytes_per_rep"], lt.get("source")
+        except (OSError, ValueError, KeyError):
+            pass
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": None, "kernel": name, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": rec["bytes"], "launch_ms": rec["ms"]}
+                "traffic": traffic, "traffic_source": traffic_src, "kernel": name, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": rec["bytes"], "launch_ms": rec["ms"],
+                "unit_of_launch": "one level forward+backward (SURVEY 8d: 40 L bytes per node)"}
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:

@@ -7,6 +7,9 @@ import re
 import sys
 
 path = sys.argv[1]
+level = sys.argv[sys.argv.index("--level") + 1] if "--level" in sys.argv else None
+reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 1
+per = int(sys.argv[sys.argv.index("--per") + 1]) if "--per" in sys.argv else 0
 rows = list(csv.reader(open(path)))
 hdr, data = None, []
 for r in rows:
@@ -29,8 +32,11 @@ for d in data:
         scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1e-3)
         L["us"] = v * scale
 lst = list(launches.values())
-ends = [i for i, L in enumerate(lst) if "k_project" in L["name"]]
-step = lst[ends[-2] + 1: ends[-1] + 1] if len(ends) >= 2 else lst
+if level:  # --profile-level run: the last reps x per launches are the level's fwd+bwd repetitions
+    step = lst[-reps * per:]
+else:
+    ends = [i for i, L in enumerate(lst) if "k_project" in L["name"]]
+    step = lst[ends[-2] + 1: ends[-1] + 1] if len(ends) >= 2 else lst
 tot_b = sum(L.get("dram__bytes_read.sum", 0) + L.get("dram__bytes_write.sum", 0) for L in step)
 tot_t = sum(L.get("us", 0) for L in step)
 print(f"launches {len(step)}  DRAM {tot_b / 1e9:.3f} GB  serialised {tot_t / 1e3:.3f} ms  "
@@ -43,5 +49,10 @@ for L in step:
     a[2] += L.get("dram__bytes_read.sum", 0) + L.get("dram__bytes_write.sum", 0)
 for k, (n, us, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     print(f"{us:8.1f} us x{n:2d}  {b / 1e6:8.1f} MB  {b / (us * 1e-6) / 1e12 if us else 0:5.2f} TB/s  {k}")
-json.dump({"launches": step, "dram_bytes_step": tot_b, "serialised_us": tot_t},
-          open(path.replace(".csv", ".json"), "w"), indent=1)
+out = {"launches": step, "dram_bytes_step": tot_b, "serialised_us": tot_t}
+if level:
+    out = {"level": level, "reps": reps, "dram_bytes_per_rep": tot_b / reps, "serialised_us_per_rep": tot_t / reps,
+           "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (cold, serialised)",
+           "launches": step}
+    print(f"level {level}: {tot_b / reps / 1e6:.1f} MB DRAM per fwd+bwd, {tot_t / reps:.1f} us serialised")
+json.dump(out, open(path.replace(".csv", ".json"), "w"), indent=1)
