@@ -252,6 +252,32 @@ __device__ __forceinline__ double softplus64(double x) {  // np.logaddexp(0, x)
   return fmax(x, 0.0) + log1p(exp(-fabs(x)));
 }
 
+// Every library kernel is launched with programmatic dependent launch (PDL):
+// its launch processing may overlap the previous kernel's drain, and it starts
+// with mgb_pdl_entry() = griddepcontrol.wait (returns once the previous grid's
+// results are visible; a no-op without PDL), so stream-order semantics hold.
+// (An early griddepcontrol.launch_dependents was measured slower: waiting
+// dependent CTAs took SM slots from the primary's last wave.)
+__device__ __forceinline__ void mgb_pdl_entry() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t mgb_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // after EVERY kernel launch: error check + the host launch counter (mgb_launch_count)
 extern long long g_mgb_launches;
 #define MGB_CHECK_LAUNCH() \

@@ -317,6 +317,7 @@ struct EpGh {
 // norms and gain-staging term |log(ny+eps) - log(nu+eps)|  (mg/processors.py:83-90)
 __global__ void k_gs_norms(const double* __restrict__ part, int nblk, double* __restrict__ stats,
                            double* __restrict__ reg) {
+  mgb_pdl_entry();
   __shared__ double red[32];
   const int b = blockIdx.x;
   double su = 0.0, sy = 0.0;
@@ -339,6 +340,7 @@ __global__ void k_gs_norms(const double* __restrict__ part, int nblk, double* __
 
 __global__ void k_dw_finalize(const double* __restrict__ part, int nblk, const int* __restrict__ widx,
                               const double* __restrict__ w, double* __restrict__ gw) {
+  mgb_pdl_entry();
   __shared__ double red[32];
   const int b = blockIdx.x;
   double s = 0.0;
@@ -374,7 +376,7 @@ struct Conv {
   static int prep(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
     const dim3 gc(N2 / G::TC, lv->B);
     const int fir_rows = (int)((g.M + N2 - 1) / N2);
-    fs::k_colA<N1, N2><<<gc, G::NTC, fs::col_smem<N1, N2>(), st>>>(LdFir{w.hbuf, g.M}, w.Ah,
+    mgb_launch(fs::k_colA<N1, N2, LdFir>, dim3(gc), dim3(G::NTC), fs::col_smem<N1, N2>(), st, LdFir{w.hbuf, g.M}, w.Ah,
                                                                   fir_rows < N1 ? fir_rows : N1);
     MGB_CHECK_LAUNCH();
     return 0;
@@ -385,14 +387,14 @@ struct Conv {
     const dim3 gc(N2 / G::TC, B), gr(N1 / 2 + 1, B);
     const size_t sc = fs::col_smem<N1, N2>(), sr = fs::row_smem<N1, N2>();
     const int x_rows = (int)((L + N2 - 1) / N2);
-    fs::k_colA<N1, N2><<<gc, G::NTC, sc, st>>>(LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1);
+    mgb_launch(fs::k_colA<N1, N2, LdRows>, dim3(gc), dim3(G::NTC), sc, st, LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1);
     MGB_CHECK_LAUNCH();
-    fs::k_rowB_fwd<N1, N2><<<gr, G::NTR, sr, st>>>(w.Ax, w.Ah, w.X, w.H, w.Bo);
+    mgb_launch(fs::k_rowB_fwd<N1, N2>, dim3(gr), dim3(G::NTR), sr, st, w.Ax, w.Ah, w.X, w.H, w.Bo);
     MGB_CHECK_LAUNCH();
     EpFwd ep{lv->u_rows, lv->widx, lv->w, lv->y, lv->ybar, w.part, L, g.off};
-    fs::k_colC<N1, N2><<<gc, G::NTC, sc, st>>>(w.Bo, ep, 1.f / (float)G::N, N1);
+    mgb_launch(fs::k_colC<N1, N2, EpFwd>, dim3(gc), dim3(G::NTC), sc, st, w.Bo, ep, 1.f / (float)G::N, N1);
     MGB_CHECK_LAUNCH();
-    k_gs_norms<<<B, 256, 0, st>>>(w.part, N2 / G::TC, w.stats, lv->reg);
+    mgb_launch(k_gs_norms, dim3(B), dim3(256), 0, st, w.part, N2 / G::TC, w.stats, lv->reg);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -403,16 +405,16 @@ struct Conv {
     const size_t sc = fs::col_smem<N1, N2>(), sr = fs::row_smem<N1, N2>();
     LdBwdPro ld{lv->u_rows, lv->gy_rows, lv->ybar, lv->widx, lv->w, lv->greg, w.stats, lv->gu, w.part, L, g.off};
     const int g_rows = (int)((g.off + L + N2 - 1) / N2);
-    fs::k_colA<N1, N2><<<gc, G::NTC, sc, st>>>(ld, w.Ax, g_rows < N1 ? g_rows : N1);
+    mgb_launch(fs::k_colA<N1, N2, LdBwdPro>, dim3(gc), dim3(G::NTC), sc, st, ld, w.Ax, g_rows < N1 ? g_rows : N1);
     MGB_CHECK_LAUNCH();
-    k_dw_finalize<<<B, 256, 0, st>>>(w.part, N2 / G::TC, lv->widx, lv->w, lv->gw);
+    mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, N2 / G::TC, lv->widx, lv->w, lv->gw);
     MGB_CHECK_LAUNCH();
-    fs::k_rowB_bwd<N1, N2><<<gr, G::NTR, fs::rowbwd_smem<N1, N2>(), st>>>(w.Ax, w.X, w.H, w.Bo, w.Ah);
+    mgb_launch(fs::k_rowB_bwd<N1, N2>, dim3(gr), dim3(G::NTR), fs::rowbwd_smem<N1, N2>(), st, w.Ax, w.X, w.H, w.Bo, w.Ah);
     MGB_CHECK_LAUNCH();
-    fs::k_colC<N1, N2><<<gc, G::NTC, sc, st>>>(w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1);
+    mgb_launch(fs::k_colC<N1, N2, EpGx>, dim3(gc), dim3(G::NTC), sc, st, w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1);
     MGB_CHECK_LAUNCH();
     const int h_rows = (int)((g.M + N2 - 1) / N2);
-    fs::k_colC<N1, N2><<<gc, G::NTC, sc, st>>>(w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
+    mgb_launch(fs::k_colC<N1, N2, EpGh>, dim3(gc), dim3(G::NTC), sc, st, w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
                                               h_rows < N1 ? h_rows : N1);
     MGB_CHECK_LAUNCH();
     return 0;
@@ -442,9 +444,9 @@ struct Conv2 {
   static int prep(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
     const dim3 gc(N2 / G::TC, lv->B), gr(G::ROW_CTAS, lv->B);
     const int fir_rows = (int)((g.M + N2 - 1) / N2);
-    fs2::k_colA<N1><<<gc, G::NT, G::COL_SMEM, st>>>(LdFir{w.hbuf, g.M}, w.Ah, fir_rows < N1 ? fir_rows : N1);
+    mgb_launch(fs2::k_colA<N1, LdFir>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, LdFir{w.hbuf, g.M}, w.Ah, fir_rows < N1 ? fir_rows : N1);
     MGB_CHECK_LAUNCH();
-    fs2::k_rowH<N1><<<gr, 2 * fs2::RP * 32, fs2::ROWH_SMEM, st>>>(w.Ah, w.H);
+    mgb_launch(fs2::k_rowH<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWH_SMEM, st, w.Ah, w.H);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -453,14 +455,14 @@ struct Conv2 {
     const int B = lv->B, L = lv->L;
     const dim3 gc(N2 / G::TC, B), gr(G::ROW_CTAS, B);
     const int x_rows = (int)((L + N2 - 1) / N2);
-    fs2::k_colA<N1><<<gc, G::NT, G::COL_SMEM, st>>>(LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1);
+    mgb_launch(fs2::k_colA<N1, LdRows>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1);
     MGB_CHECK_LAUNCH();
-    fs2::k_rowF<N1><<<gr, 2 * fs2::RP * 32, fs2::ROWF_SMEM, st>>>(w.Ax, w.H, w.X, w.Bo);
+    mgb_launch(fs2::k_rowF<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWF_SMEM, st, w.Ax, w.H, w.X, w.Bo);
     MGB_CHECK_LAUNCH();
     EpFwd ep{lv->u_rows, lv->widx, lv->w, lv->y, lv->ybar, w.part, L, g.off};
-    fs2::k_colC<N1><<<gc, G::NT, G::COL_SMEM, st>>>(w.Bo, ep, 1.f / (float)G::N, N1);
+    mgb_launch(fs2::k_colC<N1, EpFwd>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, ep, 1.f / (float)G::N, N1);
     MGB_CHECK_LAUNCH();
-    k_gs_norms<<<B, 256, 0, st>>>(w.part, G::NBLK, w.stats, lv->reg);
+    mgb_launch(k_gs_norms, dim3(B), dim3(256), 0, st, w.part, G::NBLK, w.stats, lv->reg);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -470,16 +472,16 @@ struct Conv2 {
     const dim3 gc(N2 / G::TC, B), gr(G::ROW_CTAS, B);
     LdBwdPro ld{lv->u_rows, lv->gy_rows, lv->ybar, lv->widx, lv->w, lv->greg, w.stats, lv->gu, w.part, L, g.off};
     const int g_rows = (int)((g.off + L + N2 - 1) / N2);
-    fs2::k_colA<N1><<<gc, G::NT, G::COL_SMEM, st>>>(ld, w.Ax, g_rows < N1 ? g_rows : N1);
+    mgb_launch(fs2::k_colA<N1, LdBwdPro>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, ld, w.Ax, g_rows < N1 ? g_rows : N1);
     MGB_CHECK_LAUNCH();
-    k_dw_finalize<<<B, 256, 0, st>>>(w.part, G::NBLK, lv->widx, lv->w, lv->gw);
+    mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, G::NBLK, lv->widx, lv->w, lv->gw);
     MGB_CHECK_LAUNCH();
-    fs2::k_rowG<N1><<<gr, 2 * fs2::RP * 32, fs2::ROWG_SMEM, st>>>(w.Ax, w.X, w.H, w.Bo, w.Ah);
+    mgb_launch(fs2::k_rowG<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWG_SMEM, st, w.Ax, w.X, w.H, w.Bo, w.Ah);
     MGB_CHECK_LAUNCH();
-    fs2::k_colC<N1><<<gc, G::NT, G::COL_SMEM, st>>>(w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1);
+    mgb_launch(fs2::k_colC<N1, EpGx>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1);
     MGB_CHECK_LAUNCH();
     const int h_rows = (int)((g.M + N2 - 1) / N2);
-    fs2::k_colC<N1><<<gc, G::NT, G::COL_SMEM, st>>>(w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
+    mgb_launch(fs2::k_colC<N1, EpGh>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
                                                    h_rows < N1 ? h_rows : N1);
     MGB_CHECK_LAUNCH();
     return 0;
@@ -558,22 +560,22 @@ int mgb_conv_prepare(const MgbLevel* lv, cudaStream_t st) {
   MgbArena a{(char*)lv->ws, 0};
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
-    k_eq_fir<<<dim3((MGB_EQ_LEN + 31) / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.hbuf);
+    mgb_launch(k_eq_fir, dim3(dim3((MGB_EQ_LEN + 31) / 32, B)), dim3(256), 0, st, lv->bank, lv->prow, w.hbuf);
     MGB_CHECK_LAUNCH();
-    k_eqos_hspec<<<B, EOS_NT, kEosSmem1, st>>>(w.hbuf, w.Hs);
+    mgb_launch(k_eqos_hspec, dim3(B), dim3(EOS_NT), kEosSmem1, st, w.hbuf, w.Hs);
     MGB_CHECK_LAUNCH();
     return 0;
   }
   if (tag == 'r') {
-    k_rev_frames_fft<<<dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B), RV_NT, kRevFftSmem, st>>>(lv->bank, lv->prow,
+    mgb_launch(k_rev_frames_fft, dim3(dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B)), dim3(RV_NT), kRevFftSmem, st, lv->bank, lv->prow,
                                                                                               w.aux);
     MGB_CHECK_LAUNCH();
-    k_rev_assemble<<<dim3((MGB_REV_LEN + NT - 1) / NT, B), NT, 0, st>>>(w.aux, w.hbuf);
+    mgb_launch(k_rev_assemble, dim3(dim3((MGB_REV_LEN + NT - 1) / NT, B)), dim3(NT), 0, st, w.aux, w.hbuf);
     MGB_CHECK_LAUNCH();
   } else {
-    k_dly_colour<<<dim3(MGB_DLY_TAPS, 2, B), 64, 0, st>>>(lv->bank, lv->prow, w.aux, w.offs);
+    mgb_launch(k_dly_colour, dim3(dim3(MGB_DLY_TAPS, 2, B)), dim3(64), 0, st, lv->bank, lv->prow, w.aux, w.offs);
     MGB_CHECK_LAUNCH();
-    k_dly_place<<<dim3((MGB_DLY_FIR + NT - 1) / NT, B), NT, 0, st>>>(w.aux, w.offs, w.hbuf);
+    mgb_launch(k_dly_place, dim3(dim3((MGB_DLY_FIR + NT - 1) / NT, B)), dim3(NT), 0, st, w.aux, w.offs, w.hbuf);
     MGB_CHECK_LAUNCH();
   }
   return conv_prep_dispatch(lv, w, g, st);
@@ -590,10 +592,10 @@ int mgb_conv_forward(const MgbLevel* lv, cudaStream_t st) {
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
     const int nb = eos_nblk(L);
-    k_eqos_fwd<<<dim3(nb, B), EOS_NT, kEosSmem1, st>>>(lv->u_rows, w.Hs, lv->widx, lv->w, lv->y, lv->ybar, w.part,
+    mgb_launch(k_eqos_fwd, dim3(dim3(nb, B)), dim3(EOS_NT), kEosSmem1, st, lv->u_rows, w.Hs, lv->widx, lv->w, lv->y, lv->ybar, w.part,
                                                        L);
     MGB_CHECK_LAUNCH();
-    k_gs_norms<<<B, 256, 0, st>>>(w.part, nb, w.stats, lv->reg);
+    mgb_launch(k_gs_norms, dim3(B), dim3(256), 0, st, w.part, nb, w.stats, lv->reg);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -610,10 +612,10 @@ int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st) {
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
     const int nb = eos_nblk(L);
-    k_eqos_bwd<<<dim3(nb, B), EOS_NT, kEosSmem1, st>>>(lv->u_rows, lv->gy_rows, lv->ybar, w.Hs, lv->widx, lv->w,
+    mgb_launch(k_eqos_bwd, dim3(dim3(nb, B)), dim3(EOS_NT), kEosSmem1, st, lv->u_rows, lv->gy_rows, lv->ybar, w.Hs, lv->widx, lv->w,
                                                        lv->greg, w.stats, lv->gu, w.part, w.pspec, L, nb);
     MGB_CHECK_LAUNCH();
-    k_dw_finalize<<<B, 256, 0, st>>>(w.part, nb, lv->widx, lv->w, lv->gw);
+    mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, nb, lv->widx, lv->w, lv->gw);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -628,18 +630,18 @@ int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st) {
   MgbArena a{(char*)lv->ws, 0};
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
-    k_eqos_csum<<<dim3(EOS_N / 256, B), 256, 0, st>>>(w.pspec, eos_nblk(L), w.csum);
+    mgb_launch(k_eqos_csum, dim3(dim3(EOS_N / 256, B)), dim3(256), 0, st, w.pspec, eos_nblk(L), w.csum);
     MGB_CHECK_LAUNCH();
-    k_eqos_gh<<<B, EOS_NT, kEosSmem1, st>>>(w.csum, w.ghbuf);
+    mgb_launch(k_eqos_gh, dim3(B), dim3(EOS_NT), kEosSmem1, st, w.csum, w.ghbuf);
     MGB_CHECK_LAUNCH();
-    k_eq_fir_bwd<<<dim3(MGB_EQ_BINS / 32, B), 256, 0, st>>>(lv->bank, lv->prow, w.ghbuf, g.M, lv->gbank);
+    mgb_launch(k_eq_fir_bwd, dim3(dim3(MGB_EQ_BINS / 32, B)), dim3(256), 0, st, lv->bank, lv->prow, w.ghbuf, g.M, lv->gbank);
   } else if (tag == 'r') {
-    k_rev_bwd_frames_fft<<<dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B), RV_NT, kRevFftSmem, st>>>(
+    mgb_launch(k_rev_bwd_frames_fft, dim3(dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B)), dim3(RV_NT), kRevFftSmem, st, 
         lv->bank, lv->prow, w.ghbuf, g.M, w.aux2);
     MGB_CHECK_LAUNCH();
-    k_rev_bwd_reduce<<<dim3((MGB_REV_PBINS + 31) / 32, 2, B), 256, 0, st>>>(w.aux2, lv->prow, lv->gbank);
+    mgb_launch(k_rev_bwd_reduce, dim3(dim3((MGB_REV_PBINS + 31) / 32, 2, B)), dim3(256), 0, st, w.aux2, lv->prow, lv->gbank);
   } else {
-    k_dly_bwd<<<dim3(MGB_DLY_TAPS, 2, B), NT, kDlyBwdSmem, st>>>(lv->bank, lv->prow, w.aux, w.offs, w.ghbuf, g.M,
+    mgb_launch(k_dly_bwd, dim3(dim3(MGB_DLY_TAPS, 2, B)), dim3(NT), kDlyBwdSmem, st, lv->bank, lv->prow, w.aux, w.offs, w.ghbuf, g.M,
                                                                  lv->gbank);
   }
   MGB_CHECK_LAUNCH();

@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_fwd(char tag, const float* const*
                                                 const double* __restrict__ bank, const int* __restrict__ prow,
                                                 const int* __restrict__ widx, const double* __restrict__ w,
                                                 float* __restrict__ env, float* __restrict__ y, int L) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   double* xd = reinterpret_cast<double*>(dsm);        // [SPAD] x' of this chunk (segment-major)
   float* xps = reinterpret_cast<float*>(xd + SPAD);   // [SPAD] mid^2 of the previous chunk
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(256) k_dyn_bwd0(char tag, const float* const* 
                                                   const int* __restrict__ widx, const double* __restrict__ w,
                                                   const float* __restrict__ env, float* __restrict__ dg,
                                                   float* __restrict__ gu, double* __restrict__ part, int L) {
+  mgb_pdl_entry();
   __shared__ double red[32];
   const int b = blockIdx.y;
   const float* u = u_rows[b];
@@ -497,6 +499,7 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd1(const float* const* __restri
                                                  const double* __restrict__ bank, const int* __restrict__ prow,
                                                  const float* __restrict__ dg, float* __restrict__ gu,
                                                  double* __restrict__ part, int L, int nch) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float* ds = reinterpret_cast<float*>(dsm);  // [2][SPAD]: cur chunk, next chunk
   __shared__ double pw[NPW];
@@ -618,6 +621,7 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd1(const float* const* __restri
 __global__ void k_dyn_final(const double* __restrict__ part0, int nblk0, int nch, const double* __restrict__ bank,
                             const int* __restrict__ prow, const int* __restrict__ widx, const double* __restrict__ w,
                             double* __restrict__ gbank, double* __restrict__ gw, const double* __restrict__ part1) {
+  mgb_pdl_entry();
   __shared__ double red[32];
   const int b = blockIdx.x;
   double s[6] = {0, 0, 0, 0, 0, 0};
@@ -685,7 +689,7 @@ int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st) {
   const int B = lv->B, L = lv->L, nch = nchunks(L);
   MgbArena a{(char*)lv->ws, 0};
   DynWs w = dcarve(a, B, L);
-  k_dyn_fwd<<<dim3(nch, B), NT, kDynSmemF, st>>>(lv->tag, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w,
+  mgb_launch(k_dyn_fwd, dim3(dim3(nch, B)), dim3(NT), kDynSmemF, st, lv->tag, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w,
                                                  lv->aux, lv->y, L);
   MGB_CHECK_LAUNCH();
   return 0;
@@ -696,12 +700,12 @@ int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st) {
   const int B = lv->B, L = lv->L, nch = nchunks(L), g0 = bwd0_grid(L);
   MgbArena a{(char*)lv->ws, 0};
   DynWs w = dcarve(a, B, L);
-  k_dyn_bwd0<<<dim3(g0, B), 256, 0, st>>>(lv->tag, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx, lv->w,
+  mgb_launch(k_dyn_bwd0, dim3(dim3(g0, B)), dim3(256), 0, st, lv->tag, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx, lv->w,
                                           lv->aux, w.dg, lv->gu, w.part0, L);
   MGB_CHECK_LAUNCH();
-  k_dyn_bwd1<<<dim3(nch, B), NT, kDynSmem, st>>>(lv->u_rows, lv->bank, lv->prow, w.dg, lv->gu, w.part1, L, nch);
+  mgb_launch(k_dyn_bwd1, dim3(dim3(nch, B)), dim3(NT), kDynSmem, st, lv->u_rows, lv->bank, lv->prow, w.dg, lv->gu, w.part1, L, nch);
   MGB_CHECK_LAUNCH();
-  k_dyn_final<<<B, 256, 0, st>>>(w.part0, g0, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank, lv->gw,
+  mgb_launch(k_dyn_final, dim3(B), dim3(256), 0, st, w.part0, g0, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank, lv->gw,
                                  w.part1);
   MGB_CHECK_LAUNCH();
   return 0;

@@ -118,6 +118,7 @@ __device__ __forceinline__ void eos_ifft(float2 (&v)[32], float2* S) {
 
 // H = FFT_8192(h) per node, (t, r) order: Hs[b][r * 256 + t]
 __global__ void __launch_bounds__(EOS_NT) k_eqos_hspec(const float2* __restrict__ hbuf, float2* __restrict__ Hs) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* S = reinterpret_cast<float2*>(dsm);
   const int b = blockIdx.x, t = threadIdx.x;
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_fwd(const float* const* __re
                                                      const float2* __restrict__ Hs, const int* __restrict__ widx,
                                                      const double* __restrict__ w, float* __restrict__ y,
                                                      float* __restrict__ ybar, double* __restrict__ part, int L) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* S = reinterpret_cast<float2*>(dsm);
   __shared__ double red[32];
@@ -215,6 +217,7 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
                                                      const double* __restrict__ stats, float* __restrict__ gu,
                                                      double* __restrict__ part, float2* __restrict__ pspec,
                                                      int L, int nblk) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* S = reinterpret_cast<float2*>(dsm);
   __shared__ double red[32];
@@ -314,6 +317,7 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
 // Csum[b][slot] = sum over blocks of C (float64, fixed order), one thread per slot
 __global__ void __launch_bounds__(256) k_eqos_csum(const float2* __restrict__ pspec, int nblk,
                                                    float2* __restrict__ csum) {
+  mgb_pdl_entry();
   const int b = blockIdx.y, slot = blockIdx.x * 256 + threadIdx.x;
   const float2* ps = pspec + (size_t)b * nblk * EOS_N + slot;
   double re = 0.0, im = 0.0;
@@ -328,6 +332,7 @@ __global__ void __launch_bounds__(256) k_eqos_csum(const float2* __restrict__ ps
 
 // dh[t] = Re IDFT(Csum)[(1023 - t) mod N] / N
 __global__ void __launch_bounds__(EOS_NT) k_eqos_gh(const float2* __restrict__ csum, float2* __restrict__ ghbuf) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* S = reinterpret_cast<float2*>(dsm);
   const int b = blockIdx.x, t = threadIdx.x;

@@ -23,6 +23,7 @@ __device__ float2 g_fs_lo[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
 __device__ float2 g_fs_hi[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
 
 __global__ void k_init_fs_twiddles() {
+  mgb_pdl_entry();
   const int l = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
   const long long N = 1LL << (l + MGB_FS_LMIN);
   if (j < 2048) {
@@ -36,6 +37,7 @@ __global__ void k_init_fs_twiddles() {
 }
 
 __global__ void k_init_twiddles() {
+  mgb_pdl_entry();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < MGB_TW_N) {
     double s, c;
@@ -46,9 +48,9 @@ __global__ void k_init_twiddles() {
 }
 
 int mgb_init_device(cudaStream_t st) {
-  k_init_twiddles<<<MGB_TW_N / 256, 256, 0, st>>>();
+  mgb_launch(k_init_twiddles, dim3(MGB_TW_N / 256), dim3(256), 0, st);
   MGB_CHECK_LAUNCH();
-  k_init_fs_twiddles<<<dim3(2048 / 256, MGB_FS_LMAX - MGB_FS_LMIN + 1), 256, 0, st>>>();
+  mgb_launch(k_init_fs_twiddles, dim3(dim3(2048 / 256, MGB_FS_LMAX - MGB_FS_LMIN + 1)), dim3(256), 0, st);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -59,6 +61,7 @@ int mgb_init_device(cudaStream_t st) {
 template <int N, int SEQ, int NT>
 __global__ void __launch_bounds__(NT) k_fft_small(const float2* __restrict__ in, float2* __restrict__ out,
                                                   int batch, bool inv, float scale) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char smraw[];
   float2* sm = reinterpret_cast<float2*>(smraw);
   const long long b0 = (long long)blockIdx.x * SEQ;
@@ -79,6 +82,7 @@ __global__ void __launch_bounds__(NT) k_fft_small(const float2* __restrict__ in,
 
 template <int N1, int N2, int TC, int NT>
 __global__ void __launch_bounds__(NT) k_fft_col(const float2* __restrict__ in, float2* __restrict__ out, bool inv) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char smraw[];
   float2* sm = reinterpret_cast<float2*>(smraw);  // [N1][TC]
   const long long N = (long long)N1 * N2;
@@ -100,6 +104,7 @@ __global__ void __launch_bounds__(NT) k_fft_col(const float2* __restrict__ in, f
 template <int N1, int N2, int TR, int NT>
 __global__ void __launch_bounds__(NT) k_fft_row(const float2* __restrict__ in, float2* __restrict__ out, bool inv,
                                                 float scale) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char smraw[];
   float2* sm = reinterpret_cast<float2*>(smraw);  // [TR][padded N2]
   constexpr int P = padded_len<N2>();
@@ -129,7 +134,7 @@ static int launch_small(const float2* in, float2* out, int batch, bool inv, floa
     cudaFuncSetAttribute(k_fft_small<N, SEQ, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_fft_small<N, SEQ, NT><<<(batch + SEQ - 1) / SEQ, NT, smem, st>>>(in, out, batch, inv, scale);
+  mgb_launch(k_fft_small<N, SEQ, NT>, dim3((batch + SEQ - 1) / SEQ), dim3(NT), smem, st, in, out, batch, inv, scale);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -148,9 +153,9 @@ static int launch_four_step(const float2* in, float2* out, float2* tmp, int batc
     cudaFuncSetAttribute(k_fft_row<N1, N2, TR, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
     attr = true;
   }
-  k_fft_col<N1, N2, TC, NT><<<dim3(N2 / TC, batch), NT, smc, st>>>(in, tmp, inv);
+  mgb_launch(k_fft_col<N1, N2, TC, NT>, dim3(dim3(N2 / TC, batch)), dim3(NT), smc, st, in, tmp, inv);
   MGB_CHECK_LAUNCH();
-  k_fft_row<N1, N2, TR, NT><<<dim3(N1 / TR, batch), NT, smr, st>>>(tmp, out, inv, scale);
+  mgb_launch(k_fft_row<N1, N2, TR, NT>, dim3(dim3(N1 / TR, batch)), dim3(NT), smr, st, tmp, out, inv, scale);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -187,6 +192,7 @@ int mgb_fft_c2c(const float2* in, float2* out, float2* tmp, int batch, int log2n
 
 // Z[b][k] = (u_l, u_r)[k] for k < L, 0 up to N
 __global__ void k_pack_rows(const float* const* __restrict__ rows, float2* __restrict__ Z, int L, long long N) {
+  mgb_pdl_entry();
   const int b = blockIdx.y;
   const float* u = rows[b];
   float2* z = Z + (long long)b * N;
@@ -196,7 +202,7 @@ __global__ void k_pack_rows(const float* const* __restrict__ rows, float2* __res
 
 int mgb_pack_rows(const float* const* rows, float2* Z, int B, int L, long long N, cudaStream_t st) {
   const int blocks = (int)min((N + 255) / 256, (long long)1184);
-  k_pack_rows<<<dim3(blocks, B), 256, 0, st>>>(rows, Z, L, N);
+  mgb_launch(k_pack_rows, dim3(dim3(blocks, B)), dim3(256), 0, st, rows, Z, L, N);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -215,6 +221,7 @@ __device__ __forceinline__ void split_pair(float2 zk, float2 zp, float2& a, floa
 
 __global__ void k_spec_pair(const float2* __restrict__ Z, const float2* __restrict__ H, float2* __restrict__ Q,
                             const float2* __restrict__ C, float2* __restrict__ Q2, long long N, int mode) {
+  mgb_pdl_entry();
   const int b = blockIdx.y;
   const long long off = (long long)b * N;
   const long long half = N / 2;
@@ -243,7 +250,7 @@ __global__ void k_spec_pair(const float2* __restrict__ Z, const float2* __restri
 int mgb_spec_pair(const float2* Z, const float2* H, float2* Q, const float2* C, float2* Q2, int B, long long N,
                   int mode, cudaStream_t st) {
   const int blocks = (int)min((N / 2 + 256) / 256, (long long)1184);
-  k_spec_pair<<<dim3(blocks, B), 256, 0, st>>>(Z, H, Q, C, Q2, N, mode);
+  mgb_launch(k_spec_pair, dim3(dim3(blocks, B)), dim3(256), 0, st, Z, H, Q, C, Q2, N, mode);
   MGB_CHECK_LAUNCH();
   return 0;
 }

@@ -6,6 +6,7 @@
 // 32 outputs per CTA (lane), 8 warps split the 1023 cosine terms; compact (B, 2047) output
 __global__ void __launch_bounds__(256) k_eq_fir(const double* __restrict__ bank, const int* __restrict__ prow,
                                                 float2* __restrict__ H) {
+  mgb_pdl_entry();
   __shared__ double X[MGB_EQ_BINS];
   __shared__ double ct[MGB_EQ_LEN];
   __shared__ double part[8][33];
@@ -42,6 +43,7 @@ __global__ void __launch_bounds__(256) k_eq_fir(const double* __restrict__ bank,
 __global__ void __launch_bounds__(256) k_eq_fir_bwd(const double* __restrict__ bank, const int* __restrict__ prow,
                                                     const float2* __restrict__ GH, int M,
                                                     double* __restrict__ gbank) {
+  mgb_pdl_entry();
   __shared__ double dh[MGB_EQ_LEN];
   __shared__ double ct[MGB_EQ_LEN];
   __shared__ double part[8][33];
@@ -81,6 +83,7 @@ __global__ void __launch_bounds__(256) k_eq_fir_bwd(const double* __restrict__ b
 __global__ void __launch_bounds__(MGB_REV_NFFT) k_rev_frames(const double* __restrict__ bank,
                                                              const int* __restrict__ prow,
                                                              float* __restrict__ frames) {
+  mgb_pdl_entry();
   __shared__ float2 X[2][MGB_REV_BINS];
   __shared__ float2 cs[MGB_REV_NFFT];
   const int m = blockIdx.x, b = blockIdx.y;
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(MGB_REV_NFFT) k_rev_frames(const double* __res
 }
 
 __global__ void __launch_bounds__(NT) k_rev_assemble(const float* __restrict__ frames, float2* __restrict__ H) {
+  mgb_pdl_entry();
   const int b = blockIdx.y;
   const long long N = MGB_REV_LEN;
   float2* h = H + (size_t)b * N;
@@ -149,6 +153,7 @@ __global__ void __launch_bounds__(MGB_REV_NFFT) k_rev_bwd_frames(const double* _
                                                                  const int* __restrict__ prow,
                                                                  const float2* __restrict__ GH, int N,
                                                                  float* __restrict__ dexpo) {
+  mgb_pdl_entry();
   __shared__ float fr[2][MGB_REV_NFFT];
   __shared__ float2 cs[MGB_REV_NFFT];
   const int m = blockIdx.x, b = blockIdx.y;
@@ -202,6 +207,7 @@ __global__ void __launch_bounds__(MGB_REV_NFFT) k_rev_bwd_frames(const double* _
 __global__ void __launch_bounds__(256) k_rev_bwd_reduce(const float* __restrict__ dexpo,
                                                         const int* __restrict__ prow,
                                                         double* __restrict__ gbank) {
+  mgb_pdl_entry();
   __shared__ double s0[8][33], s1[8][33];
   const int ch = blockIdx.y, b = blockIdx.z;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -257,6 +263,7 @@ __global__ void __launch_bounds__(256) k_rev_bwd_reduce(const float* __restrict_
 // quantised offset d = rint(((-angle z) mod 2pi) / 2pi * 3000) mod 3000 in fp64
 __global__ void k_dly_colour(const double* __restrict__ bank, const int* __restrict__ prow,
                              float* __restrict__ colour, int* __restrict__ offs) {
+  mgb_pdl_entry();
   const int tap = blockIdx.x, ch = blockIdx.y, b = blockIdx.z;
   const double* p = bank + (size_t)prow[b] * 880 + ch * 440;
   const int tp = threadIdx.x;
@@ -284,6 +291,7 @@ __global__ void k_dly_colour(const double* __restrict__ bank, const int* __restr
 
 __global__ void __launch_bounds__(NT) k_dly_place(const float* __restrict__ colour, const int* __restrict__ offs,
                                                   float2* __restrict__ H) {
+  mgb_pdl_entry();
   const long long N = MGB_DLY_FIR;
   __shared__ float col[2][MGB_DLY_TAPS][MGB_COLOR_LEN];
   __shared__ int dd[2][MGB_DLY_TAPS];
@@ -324,6 +332,7 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
                                                 const float* __restrict__ colour, const int* __restrict__ offs,
                                                 const float2* __restrict__ GH, int N,
                                                 double* __restrict__ gbank) {
+  mgb_pdl_entry();
   __shared__ float seg[3040];
   __shared__ float col[MGB_COLOR_LEN];
   __shared__ double dhz[MGB_COLOR_LEN];

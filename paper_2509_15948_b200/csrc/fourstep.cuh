@@ -48,6 +48,7 @@ __device__ __forceinline__ void split_pair(float2 zk, float2 zp, float2& a, floa
 // column pass, forward direction: A[b][k1*N2 + n2] = w_N^{k1 n2} * FFT_{N1}(x[. * N2 + n2])
 template <int N1, int N2, class Ld>
 __global__ void __launch_bounds__(Geo<N1, N2>::NTC, 4) k_colA(Ld ld, float2* __restrict__ A, int nz_rows) {
+  mgb_pdl_entry();
   constexpr int TC = Geo<N1, N2>::TC, NT = Geo<N1, N2>::NTC;
   constexpr long long N = Geo<N1, N2>::N;
   constexpr int PER = Geo<N1, N2>::PERC, BATCH = Geo<N1, N2>::BATCHC;
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTC, 4) k_colA(Ld ld, float2* __r
 template <int N1, int N2, class Ep>
 __global__ void __launch_bounds__(Geo<N1, N2>::NTC, 4) k_colC(const float2* __restrict__ Bb, Ep ep, float scale,
                                                              int out_rows) {
+  mgb_pdl_entry();
   constexpr int TC = Geo<N1, N2>::TC, NT = Geo<N1, N2>::NTC;
   constexpr long long N = Geo<N1, N2>::N;
   constexpr int PER = Geo<N1, N2>::PERC, BATCH = Geo<N1, N2>::BATCHC;
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTR, 3) k_rowB_fwd(const float2* 
                                                                  const float2* __restrict__ Ah,
                                                                  float2* __restrict__ X, float2* __restrict__ H,
                                                                  float2* __restrict__ Bo) {
+  mgb_pdl_entry();
   constexpr int NT = Geo<N1, N2>::NTR, P = Geo<N1, N2>::P;
   constexpr long long N = Geo<N1, N2>::N;
   constexpr int PER = 2 * N2 / NT;
@@ -226,6 +229,7 @@ __global__ void __launch_bounds__(Geo<N1, N2>::NTR, 3) k_rowB_bwd(const float2* 
                                                                  const float2* __restrict__ X,
                                                                  const float2* __restrict__ H,
                                                                  float2* __restrict__ B1, float2* __restrict__ B2) {
+  mgb_pdl_entry();
   constexpr int NT = Geo<N1, N2>::NTR, P = Geo<N1, N2>::P;
   constexpr long long N = Geo<N1, N2>::N;
   constexpr int PER = 2 * N2 / NT;

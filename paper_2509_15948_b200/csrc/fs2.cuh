@@ -158,6 +158,7 @@ __device__ __forceinline__ void row_fft_compact(float2 (&v)[32], float2* T, int 
 // column pass, forward: A[b][k1*N2 + n2] = w_N^{k1 n2} FFT_{N1}(x[. * N2 + n2])
 template <int N1, class Ld>
 __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colA(Ld ld, float2* __restrict__ A, int nz_rows) {
+  mgb_pdl_entry();
   using g = G<N1>;
   constexpr int Q = g::Q, P = g::P, TC = g::TC, B8 = Q < 8 ? Q : 8;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colA(Ld ld, floa
 template <int N1, class Ep>
 __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colC(const float2* __restrict__ Bb, Ep ep, float scale,
                                                    int out_rows) {
+  mgb_pdl_entry();
   using g = G<N1>;
   constexpr int Q = g::Q, P = g::P, TC = g::TC, B8 = Q < 8 ? Q : 8;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -274,6 +276,7 @@ __device__ __forceinline__ float2* warp_region(unsigned char* smraw, int w) {
 // prep: H[b][row][k] = FFT_{N2}(Ah[b][row][.])  (FIR spectrum, row layout)
 template <int N1>
 __global__ void __launch_bounds__(2 * RP * 32) k_rowH(const float2* __restrict__ Ah, float2* __restrict__ H) {
+  mgb_pdl_entry();
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
   const RowMap rm = row_map<N1>();
@@ -301,6 +304,7 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowH(const float2* __restrict__
 template <int N1>
 __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__ Ax, const float2* __restrict__ H,
                                                      float2* __restrict__ X, float2* __restrict__ Bo) {
+  mgb_pdl_entry();
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int w = threadIdx.x >> 5;
@@ -356,6 +360,7 @@ template <int N1>
 __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__ Ag, const float2* __restrict__ X,
                                                      const float2* __restrict__ H, float2* __restrict__ B1,
                                                      float2* __restrict__ B2) {
+  mgb_pdl_entry();
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int w = threadIdx.x >> 5;

@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(NT) k_gs_fwd(const float* const* __restrict__ 
                                                const double* __restrict__ bank, const int* __restrict__ prow,
                                                const int* __restrict__ widx, const double* __restrict__ w,
                                                float* __restrict__ y, int L) {
+  mgb_pdl_entry();
   const int b = blockIdx.y;
   const float* u = u_rows[b];
   float* yo = y + (size_t)b * 2 * L;
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(NT) k_gs_bwd(const float* const* __restrict__ 
                                                const double* __restrict__ bank, const int* __restrict__ prow,
                                                const int* __restrict__ widx, const double* __restrict__ w,
                                                float* __restrict__ gu, double* __restrict__ part, int L) {
+  mgb_pdl_entry();
   __shared__ double scratch[32];
   const int b = blockIdx.y;
   const float* u = u_rows[b];
@@ -189,6 +191,7 @@ __global__ void __launch_bounds__(NT) k_gs_bwd(const float* const* __restrict__ 
 __global__ void k_gs_finalize(char tag, const double* __restrict__ part, int nblk, const double* __restrict__ bank,
                               const int* __restrict__ prow, const int* __restrict__ widx,
                               const double* __restrict__ w, double* __restrict__ gbank, double* __restrict__ gw) {
+  mgb_pdl_entry();
   const int b = blockIdx.x;
   double s0 = 0.0, s1 = 0.0;
   for (int i = threadIdx.x; i < nblk; i += 32) {
@@ -213,6 +216,7 @@ __global__ void k_gs_finalize(char tag, const double* __restrict__ part, int nbl
 
 __global__ void k_weights(const double* __restrict__ raw, const double* __restrict__ mask, double* __restrict__ w,
                           int P) {
+  mgb_pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < P) {
     double v = expit64(raw[i]);
@@ -225,6 +229,7 @@ __global__ void k_weights(const double* __restrict__ raw, const double* __restri
 template <bool VEC>
 __global__ void __launch_bounds__(NT) k_bus_sum(const float* const* __restrict__ in_rows,
                                                 const int* __restrict__ seg_off, float* __restrict__ out, int L) {
+  mgb_pdl_entry();
   const int s = blockIdx.y;
   const int i0 = seg_off[s], i1 = seg_off[s + 1];
   float* o = out + (size_t)s * 2 * L;
@@ -264,7 +269,7 @@ static bool rows_vec_ok(int L) { return (L & 3) == 0; }  // row starts are then 
 int mgb_simple_forward(const MgbLevel* lv, cudaStream_t st) {
   const dim3 grid(simple_nblk(lv->L), lv->B);
   const bool vec = rows_vec_ok(lv->L);
-#define LAUNCH(T, V) k_gs_fwd<T, V><<<grid, NT, 0, st>>>(lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w, lv->y, lv->L)
+#define LAUNCH(T, V) mgb_launch(k_gs_fwd<T, V>, dim3(grid), dim3(NT), 0, st, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w, lv->y, lv->L)
   if (lv->tag == 'g') { if (vec) LAUNCH('g', true); else LAUNCH('g', false); }
   else { if (vec) LAUNCH('s', true); else LAUNCH('s', false); }
 #undef LAUNCH
@@ -277,13 +282,13 @@ int mgb_simple_backward(const MgbLevel* lv, cudaStream_t st) {
   const dim3 grid(nblk, lv->B);
   const bool vec = rows_vec_ok(lv->L);
   double* part = reinterpret_cast<double*>(lv->ws);
-#define LAUNCH(T, V) k_gs_bwd<T, V><<<grid, NT, 0, st>>>(lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx, \
+#define LAUNCH(T, V) mgb_launch(k_gs_bwd<T, V>, dim3(grid), dim3(NT), 0, st, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx, \
                                                           lv->w, lv->gu, part, lv->L)
   if (lv->tag == 'g') { if (vec) LAUNCH('g', true); else LAUNCH('g', false); }
   else { if (vec) LAUNCH('s', true); else LAUNCH('s', false); }
 #undef LAUNCH
   MGB_CHECK_LAUNCH();
-  k_gs_finalize<<<lv->B, 32, 0, st>>>(lv->tag, part, nblk, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,
+  mgb_launch(k_gs_finalize, dim3(lv->B), dim3(32), 0, st, lv->tag, part, nblk, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,
                                       lv->gw);
   MGB_CHECK_LAUNCH();
   return 0;
@@ -291,7 +296,7 @@ int mgb_simple_backward(const MgbLevel* lv, cudaStream_t st) {
 
 extern "C" int mgb_weights(const double* raw, const double* mask, double* w, int P, void* stream) {
   if (P <= 0) return 0;
-  k_weights<<<(P + 255) / 256, 256, 0, (cudaStream_t)stream>>>(raw, mask, w, P);
+  mgb_launch(k_weights, dim3((P + 255) / 256), dim3(256), 0, (cudaStream_t)stream, raw, mask, w, P);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -300,8 +305,8 @@ extern "C" int mgb_bus_sum(const float* const* in_rows, const int* seg_off, floa
                            void* stream) {
   if (S <= 0) return 0;
   const dim3 grid(simple_nblk(2 * L), S);
-  if (rows_vec_ok(L)) k_bus_sum<true><<<grid, NT, 0, (cudaStream_t)stream>>>(in_rows, seg_off, out, L);
-  else k_bus_sum<false><<<grid, NT, 0, (cudaStream_t)stream>>>(in_rows, seg_off, out, L);
+  if (rows_vec_ok(L)) mgb_launch(k_bus_sum<true>, dim3(grid), dim3(NT), 0, (cudaStream_t)stream, in_rows, seg_off, out, L);
+  else mgb_launch(k_bus_sum<false>, dim3(grid), dim3(NT), 0, (cudaStream_t)stream, in_rows, seg_off, out, L);
   MGB_CHECK_LAUNCH();
   return 0;
 }

@@ -196,6 +196,7 @@ __device__ __forceinline__ void mags_inplace(float2* S, int tt) {
 template <int N>
 __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(MgbLossRes r, const float* __restrict__ xl,
                                                       const float* __restrict__ xr, int Ls, int mode) {
+  mgb_pdl_entry();
   using C = FC<N, 16>;
   constexpr int T = C::T, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(
 // stats layout per (res, group): [tnorm, slog, sdiff2, dn]
 // one CTA per (resolution, group)
 __global__ void k_mr_finalize(MgbLoss L, int mode) {
+  mgb_pdl_entry();
   __shared__ double red[32];
   const int ri = blockIdx.x >> 2, g = blockIdx.x & 3;
   const MgbLossRes& r = L.res[ri];
@@ -276,6 +278,7 @@ __global__ void k_mr_finalize(MgbLoss L, int mode) {
 
 // L_a = sum over (res, group) of w_g (slog / frames + dn / tnorm), in a fixed order
 __global__ void k_mr_total(MgbLoss L) {
+  mgb_pdl_entry();
   if (threadIdx.x) return;
   double tot = 0.0;
   for (int ri = 0; ri < L.n_res; ++ri)
@@ -293,6 +296,7 @@ template <int N>
 __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(MgbLossRes r, const double* __restrict__ stats,
                                                                        MgbLoss L, const float* __restrict__ xl,
                                                                        const float* __restrict__ xr, int Ls) {
+  mgb_pdl_entry();
   using C = FC<N, 8>;
   constexpr int T = C::T, NB = C::NB, PER = (NB + T - 1) / T;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -387,6 +391,7 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
 // dL/dy[t] = sum over resolutions of the frame adjoints covering the padded
 // position t + n/2, plus the reflect-pad adjoint near both ends (gather, no atomics)
 __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ gl, float* __restrict__ gr) {
+  mgb_pdl_entry();
   const int Ls = L.Ls;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= Ls) return;
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
 template <int N>
 int launch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, int mode, cudaStream_t st) {
   using C = FC<N, 16>;
-  k_mr_fwd<N><<<(r.frames + C::FPC - 1) / C::FPC, C::NT, C::SMEM, st>>>(r, xl, xr, Ls, mode);
+  mgb_launch(k_mr_fwd<N>, dim3((r.frames + C::FPC - 1) / C::FPC), dim3(C::NT), C::SMEM, st, r, xl, xr, Ls, mode);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -429,7 +434,7 @@ template <int N>
 int launch_bwd(const MgbLossRes& r, const double* stats, const MgbLoss& L, const float* xl, const float* xr,
                int Ls, cudaStream_t st) {
   using C = FC<N, 8>;
-  k_mr_bwd<N><<<(r.frames + C::FPC - 1) / C::FPC, C::NT, C::SMEM, st>>>(r, stats, L, xl, xr, Ls);
+  mgb_launch(k_mr_bwd<N>, dim3((r.frames + C::FPC - 1) / C::FPC), dim3(C::NT), C::SMEM, st, r, stats, L, xl, xr, Ls);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -536,7 +541,7 @@ extern "C" int mgb_mrstft_target(const MgbLoss* L, const float* tl, const float*
   cudaStream_t st = (cudaStream_t)stream;
   if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) { return dispatch_fwd(L->res[i], tl, tr, L->Ls, 0, s); }))
     return rc;
-  k_mr_finalize<<<4 * L->n_res, 256, 0, st>>>(*L, 0);
+  mgb_launch(k_mr_finalize, dim3(4 * L->n_res), dim3(256), 0, st, *L, 0);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -546,9 +551,9 @@ extern "C" int mgb_mrstft_forward(const MgbLoss* L, const float* yl, const float
   cudaStream_t st = (cudaStream_t)stream;
   if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) { return dispatch_fwd(L->res[i], yl, yr, L->Ls, 1, s); }))
     return rc;
-  k_mr_finalize<<<4 * L->n_res, 256, 0, st>>>(*L, 1);
+  mgb_launch(k_mr_finalize, dim3(4 * L->n_res), dim3(256), 0, st, *L, 1);
   MGB_CHECK_LAUNCH();
-  k_mr_total<<<1, 32, 0, st>>>(*L);
+  mgb_launch(k_mr_total, dim3(1), dim3(32), 0, st, *L);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -561,7 +566,7 @@ extern "C" int mgb_mrstft_backward(const MgbLoss* L, const float* yl, const floa
         return dispatch_bwd(L->res[i], L->stats + (size_t)i * 16, *L, yl, yr, L->Ls, s);
       }))
     return rc;
-  k_mr_ola<<<(L->Ls + 255) / 256, 256, 0, st>>>(*L, gl, gr);
+  mgb_launch(k_mr_ola, dim3((L->Ls + 255) / 256), dim3(256), 0, st, *L, gl, gr);
   MGB_CHECK_LAUNCH();
   return 0;
 }

@@ -15,6 +15,7 @@ namespace {
 __global__ void k_raw_grad(const double* __restrict__ p, double* __restrict__ g, long long w_off, int P,
                            const double* __restrict__ gw, const double* __restrict__ mask,
                            const double* __restrict__ sc) {
+  mgb_pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const double s = expit64(p[w_off + i]);
@@ -26,6 +27,7 @@ __global__ void k_raw_grad(const double* __restrict__ p, double* __restrict__ g,
 }
 
 __global__ void k_delay_rule(const double* __restrict__ p, double* __restrict__ g, long long d_off, int rows) {
+  mgb_pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (row, channel, tap)
   if (i >= rows * 40) return;
   const int row = i / 40, c = (i / 20) % 2, m = i % 20;
@@ -46,6 +48,7 @@ __global__ void k_delay_rule(const double* __restrict__ p, double* __restrict__ 
 __global__ void k_adamw(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
                         double* __restrict__ v, long long n, const double* __restrict__ sc,
                         const double* __restrict__ guard) {
+  mgb_pdl_entry();
   if (guard && !isfinite(*guard)) return;  // NonFiniteLoss: the reference raises before updating
   const double lr = sc[0], b1 = sc[1], b2 = sc[2], eps = sc[3], wd = sc[4], c1 = sc[5], c2 = sc[6];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -64,6 +67,7 @@ __global__ void k_adamw(double* __restrict__ p, const double* __restrict__ g, do
 }
 
 __global__ void k_project(double* __restrict__ p, long long d_off, int rows, const double* __restrict__ guard) {
+  mgb_pdl_entry();
   if (guard && !isfinite(*guard)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * 40) return;
@@ -77,6 +81,7 @@ __global__ void k_project(double* __restrict__ p, long long d_off, int rows, con
 }
 
 __global__ void k_sparsity(const double* __restrict__ raw, int P, double* __restrict__ out) {
+  mgb_pdl_entry();
   __shared__ double red[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < P; i += blockDim.x) s += expit64(raw[i]);
@@ -92,25 +97,25 @@ extern "C" int mgb_adamw_step(double* p, double* g, double* m, double* v, long l
   cudaStream_t st = (cudaStream_t)stream;
   if (n <= 0) return 0;
   if (P > 0) {
-    k_raw_grad<<<(P + 255) / 256, 256, 0, st>>>(p, g, w_off, P, gw, mask, step_scalars);
+    mgb_launch(k_raw_grad, dim3((P + 255) / 256), dim3(256), 0, st, p, g, w_off, P, gw, mask, step_scalars);
     MGB_CHECK_LAUNCH();
   }
   if (d_rows > 0) {
-    k_delay_rule<<<(d_rows * 40 + 255) / 256, 256, 0, st>>>(p, g, d_off, d_rows);
+    mgb_launch(k_delay_rule, dim3((d_rows * 40 + 255) / 256), dim3(256), 0, st, p, g, d_off, d_rows);
     MGB_CHECK_LAUNCH();
   }
   const int blocks = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
-  k_adamw<<<blocks, 256, 0, st>>>(p, g, m, v, n, step_scalars, loss_guard);
+  mgb_launch(k_adamw, dim3(blocks), dim3(256), 0, st, p, g, m, v, n, step_scalars, loss_guard);
   MGB_CHECK_LAUNCH();
   if (d_rows > 0) {
-    k_project<<<(d_rows * 40 + 255) / 256, 256, 0, st>>>(p, d_off, d_rows, loss_guard);
+    mgb_launch(k_project, dim3((d_rows * 40 + 255) / 256), dim3(256), 0, st, p, d_off, d_rows, loss_guard);
     MGB_CHECK_LAUNCH();
   }
   return 0;
 }
 
 extern "C" int mgb_sparsity(const double* raw, int P, double* out, void* stream) {
-  k_sparsity<<<1, 256, 0, (cudaStream_t)stream>>>(raw, P, out);
+  mgb_launch(k_sparsity, dim3(1), dim3(256), 0, (cudaStream_t)stream, raw, P, out);
   MGB_CHECK_LAUNCH();
   return 0;
 }

@@ -48,6 +48,7 @@ __device__ __forceinline__ void dft384(float2* s, bool inv) {
 __global__ void __launch_bounds__(RV_NT) k_rev_frames_fft(const double* __restrict__ bank,
                                                            const int* __restrict__ prow,
                                                            float* __restrict__ frames) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* s = reinterpret_cast<float2*>(dsm);
   const int m0 = blockIdx.x * RV_F, b = blockIdx.y;
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(RV_NT) k_rev_bwd_frames_fft(const double* __re
                                                                const int* __restrict__ prow,
                                                                const float2* __restrict__ GH, int M,
                                                                float* __restrict__ dexpo) {
+  mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* s = reinterpret_cast<float2*>(dsm);
   const int m0 = blockIdx.x * RV_F, b = blockIdx.y;
