@@ -637,9 +637,10 @@ int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st) {
     mgb_launch(k_eq_fir_bwd, dim3(dim3(MGB_EQ_BINS / 32, B)), dim3(256), 0, st, lv->bank, lv->prow, w.ghbuf, g.M, lv->gbank);
   } else if (tag == 'r') {
     mgb_launch(k_rev_bwd_frames_fft, dim3(dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B)), dim3(RV_NT), kRevFftSmem, st, 
-        lv->bank, lv->prow, w.ghbuf, g.M, w.aux2);
+        lv->bank, lv->prow, w.ghbuf, g.M, reinterpret_cast<double*>(w.aux2));
     MGB_CHECK_LAUNCH();
-    mgb_launch(k_rev_bwd_reduce, dim3(dim3((MGB_REV_PBINS + 31) / 32, 2, B)), dim3(256), 0, st, w.aux2, lv->prow, lv->gbank);
+    mgb_launch(k_rev_bwd_reduce, dim3(dim3((2 * MGB_REV_PBINS + 255) / 256, B)), dim3(256), 0, st,
+               reinterpret_cast<const double*>(w.aux2), lv->prow, lv->gbank);
   } else {
     mgb_launch(k_dly_bwd, dim3(dim3(MGB_DLY_TAPS, 2, B)), dim3(NT), kDlyBwdSmem, st, lv->bank, lv->prow, w.aux, w.offs, w.ghbuf, g.M,
                                                                  lv->gbank);

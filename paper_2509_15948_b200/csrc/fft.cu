@@ -15,12 +15,29 @@
 // (z = left + i*right), and the per-channel spectra are separated with the
 // Hermitian pairing X_l[k] = (Z[k] + conj Z[-k])/2, X_r[k] = (Z[k] - conj Z[-k])/2i.
 #include "common.cuh"
+#include "tables.cuh"
 #include "mgb_internal.h"
 
 __device__ float2 g_tw32[MGB_TW_N];
 __device__ double2 g_tw64[MGB_TW_N];
 __device__ float2 g_fs_lo[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
 __device__ float2 g_fs_hi[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
+// FIR-synthesis tables (float64): cos(2 pi j / n) and the symmetric Hann of n = 2047 (EQ) / 39 (colour)
+__device__ double g_cos2047[MGB_EQ_LEN], g_hann2047[MGB_EQ_LEN];
+__device__ double g_cos39[MGB_COLOR_LEN], g_hann39[MGB_COLOR_LEN];
+
+__global__ void k_init_fir_tables() {
+  mgb_pdl_entry();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < MGB_EQ_LEN) {
+    g_cos2047[j] = cospi(2.0 * j / (double)MGB_EQ_LEN);
+    g_hann2047[j] = 0.5 - 0.5 * cospi(2.0 * j / (double)(MGB_EQ_LEN - 1));
+  }
+  if (j < MGB_COLOR_LEN) {
+    g_cos39[j] = cospi(2.0 * j / (double)MGB_COLOR_LEN);
+    g_hann39[j] = 0.5 - 0.5 * cospi(2.0 * j / (double)(MGB_COLOR_LEN - 1));
+  }
+}
 
 __global__ void k_init_fs_twiddles() {
   mgb_pdl_entry();
@@ -49,6 +66,8 @@ __global__ void k_init_twiddles() {
 
 int mgb_init_device(cudaStream_t st) {
   mgb_launch(k_init_twiddles, dim3(MGB_TW_N / 256), dim3(256), 0, st);
+  MGB_CHECK_LAUNCH();
+  mgb_launch(k_init_fir_tables, dim3((MGB_EQ_LEN + 255) / 256), dim3(256), 0, st);
   MGB_CHECK_LAUNCH();
   mgb_launch(k_init_fs_twiddles, dim3(dim3(2048 / 256, MGB_FS_LMAX - MGB_FS_LMIN + 1)), dim3(256), 0, st);
   MGB_CHECK_LAUNCH();

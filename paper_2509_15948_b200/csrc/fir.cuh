@@ -13,7 +13,7 @@ __global__ void __launch_bounds__(256) k_eq_fir(const double* __restrict__ bank,
   const int b = blockIdx.y;
   const double* p = bank + (size_t)prow[b] * MGB_EQ_BINS;
   for (int k = threadIdx.x; k < MGB_EQ_BINS; k += 256) X[k] = exp(p[k]);
-  for (int j = threadIdx.x; j < MGB_EQ_LEN; j += 256) ct[j] = cospi(2.0 * j / (double)MGB_EQ_LEN);
+  for (int j = threadIdx.x; j < MGB_EQ_LEN; j += 256) ct[j] = g_cos2047[j];
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tp = blockIdx.x * 32 + lane;
@@ -32,8 +32,7 @@ __global__ void __launch_bounds__(256) k_eq_fir(const double* __restrict__ bank,
     double s = 0.0;
     for (int i = 0; i < 8; ++i) s += part[i][lane];
     const double hv = (X[0] + 2.0 * s) / (double)MGB_EQ_LEN;
-    const double win = 0.5 - 0.5 * cospi(2.0 * tp / (double)(MGB_EQ_LEN - 1));
-    const float c = (float)(hv * win);
+    const float c = (float)(hv * g_hann2047[tp]);
     H[(size_t)b * MGB_EQ_LEN + tp] = make_float2(c, c);
   }
 }
@@ -50,10 +49,9 @@ __global__ void __launch_bounds__(256) k_eq_fir_bwd(const double* __restrict__ b
   const int b = blockIdx.y;
   const float2* g = GH + (size_t)b * M;
   for (int tp = threadIdx.x; tp < MGB_EQ_LEN; tp += 256) {
-    const double win = 0.5 - 0.5 * cospi(2.0 * tp / (double)(MGB_EQ_LEN - 1));
     const float2 v = g[tp];
-    dh[(tp + 1024) % MGB_EQ_LEN] = ((double)v.x + (double)v.y) * win;
-    ct[tp] = cospi(2.0 * tp / (double)MGB_EQ_LEN);
+    dh[(tp + 1024) % MGB_EQ_LEN] = ((double)v.x + (double)v.y) * g_hann2047[tp];
+    ct[tp] = g_cos2047[tp];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -79,47 +77,6 @@ __global__ void __launch_bounds__(256) k_eq_fir_bwd(const double* __restrict__ b
 
 // ---------------------------------------------------------------------------
 // Reverb FIR synthesis
-
-__global__ void __launch_bounds__(MGB_REV_NFFT) k_rev_frames(const double* __restrict__ bank,
-                                                             const int* __restrict__ prow,
-                                                             float* __restrict__ frames) {
-  mgb_pdl_entry();
-  __shared__ float2 X[2][MGB_REV_BINS];
-  __shared__ float2 cs[MGB_REV_NFFT];
-  const int m = blockIdx.x, b = blockIdx.y;
-  const double* p = bank + (size_t)prow[b] * 768;
-  const int i = threadIdx.x;
-  {
-    double s, c;
-    sincospi(2.0 * i / (double)MGB_REV_NFFT, &s, &c);
-    cs[i] = make_float2((float)c, (float)s);
-  }
-  for (int q = threadIdx.x; q < 2 * MGB_REV_BINS; q += blockDim.x) {
-    const int ch = q / MGB_REV_BINS, k = q % MGB_REV_BINS;
-    const int kk = k < MGB_REV_PBINS ? k : MGB_REV_PBINS - 1;  // Nyquist repeats the last bin
-    const double h0 = p[ch * 384 + kk], hd = p[ch * 384 + 192 + kk];
-    const float mag = (float)exp(h0 + hd * (double)m);
-    const float2 s = g_rev_spec[ch][m][k];
-    X[ch][k] = make_float2(mag * s.x, mag * s.y);
-  }
-  __syncthreads();
-  float a0 = 0.f, a1 = 0.f;
-  int idx = i;
-  for (int k = 1; k < MGB_REV_PBINS; ++k) {
-    const float2 w = cs[idx];
-    a0 = fmaf(X[0][k].x, w.x, fmaf(-X[0][k].y, w.y, a0));
-    a1 = fmaf(X[1][k].x, w.x, fmaf(-X[1][k].y, w.y, a1));
-    idx += i;
-    if (idx >= MGB_REV_NFFT) idx -= MGB_REV_NFFT;
-  }
-  const float sgn = (i & 1) ? -1.f : 1.f;
-  const float win = 0.5f - 0.5f * cs[i].x;
-  const float inv = 1.0f / (float)MGB_REV_NFFT;
-  const float f0 = (X[0][0].x + sgn * X[0][MGB_REV_PBINS].x + 2.f * a0) * inv * win;
-  const float f1 = (X[1][0].x + sgn * X[1][MGB_REV_PBINS].x + 2.f * a1) * inv * win;
-  frames[(((size_t)b * 2 + 0) * MGB_REV_FRAMES + m) * MGB_REV_NFFT + i] = f0;
-  frames[(((size_t)b * 2 + 1) * MGB_REV_FRAMES + m) * MGB_REV_NFFT + i] = f1;
-}
 
 __global__ void __launch_bounds__(NT) k_rev_assemble(const float* __restrict__ frames, float2* __restrict__ H) {
   mgb_pdl_entry();
@@ -148,112 +105,33 @@ __global__ void __launch_bounds__(NT) k_rev_assemble(const float* __restrict__ f
   }
 }
 
-// dexpo[c][m][k] = Re(dX_k conj(S_mk)) * M_mk, dX = irfft adjoint of the windowed frame grad
-__global__ void __launch_bounds__(MGB_REV_NFFT) k_rev_bwd_frames(const double* __restrict__ bank,
-                                                                 const int* __restrict__ prow,
-                                                                 const float2* __restrict__ GH, int N,
-                                                                 float* __restrict__ dexpo) {
-  mgb_pdl_entry();
-  __shared__ float fr[2][MGB_REV_NFFT];
-  __shared__ float2 cs[MGB_REV_NFFT];
-  const int m = blockIdx.x, b = blockIdx.y;
-  const float2* g = GH + (size_t)b * N;
-  const int i = threadIdx.x;
-  {
-    double s, c;
-    sincospi(2.0 * i / (double)MGB_REV_NFFT, &s, &c);
-    cs[i] = make_float2((float)c, (float)s);
-  }
-  {
-    const int t = m * MGB_REV_HOP + i - MGB_REV_HOP;  // position in the sliced FIR
-    float dm = 0.f, ds = 0.f;
-    if (t >= 0 && t < MGB_REV_LEN) {
-      const float2 v = g[t];
-      const float iw = g_rev_inv_wss[t];
-      dm = 0.5f * (v.x + v.y) * iw;
-      ds = 0.5f * (v.x - v.y) * iw;
-    }
-    const float win = 0.5f - 0.5f * (float)cospi(2.0 * i / (double)MGB_REV_NFFT);
-    fr[0][i] = dm * win;
-    fr[1][i] = ds * win;
-  }
-  __syncthreads();
-  const double* p = bank + (size_t)prow[b] * 768;
-  for (int q = threadIdx.x; q < 2 * MGB_REV_BINS; q += blockDim.x) {
-    const int ch = q / MGB_REV_BINS, k = q % MGB_REV_BINS;
-    float re = 0.f, im = 0.f;
-    int idx = 0;
-    for (int t = 0; t < MGB_REV_NFFT; ++t) {
-      const float2 w = cs[idx];
-      re = fmaf(fr[ch][t], w.x, re);
-      im = fmaf(-fr[ch][t], w.y, im);
-      idx += k;
-      if (idx >= MGB_REV_NFFT) idx -= MGB_REV_NFFT;
-    }
-    float sc = 2.f / (float)MGB_REV_NFFT;
-    if (k == 0 || k == MGB_REV_PBINS) sc *= 0.5f;
-    re *= sc;
-    im *= sc;
-    const float2 s = g_rev_spec[ch][m][k];
-    const int kk = k < MGB_REV_PBINS ? k : MGB_REV_PBINS - 1;
-    const float mag = (float)exp(p[ch * 384 + kk] + p[ch * 384 + 192 + kk] * (double)m);
-    dexpo[(((size_t)b * 2 + ch) * MGB_REV_FRAMES + m) * MGB_REV_BINS + k] = (re * s.x + im * s.y) * mag;
-  }
-}
-
-// d H0[c][k] = sum_m dexpo[c][m][k],  d HD[c][k] = sum_m m dexpo[c][m][k]; the Nyquist bin
-// folds into the last parameter bin.  Grid (bin groups of 32, 2 channels, B); 8 warps
-// split the frames, lanes walk consecutive bins; fixed-order float64 sums.
-__global__ void __launch_bounds__(256) k_rev_bwd_reduce(const float* __restrict__ dexpo,
+// d H0[c][k] = sum_m dexpo[c][m][k],  d HD[c][k] = sum_m m dexpo[c][m][k]: k_rev_bwd_frames_fft
+// leaves per-CTA (8-frame) float64 partials part[b][cta][c][k][2]; this sums the
+// RV_CTAS partials in a fixed order and folds the Nyquist bin into the last
+// parameter bin.  One thread per (c, k).
+constexpr int RV_CTAS = (MGB_REV_FRAMES + 7) / 8;
+__global__ void __launch_bounds__(256) k_rev_bwd_reduce(const double* __restrict__ part,
                                                         const int* __restrict__ prow,
                                                         double* __restrict__ gbank) {
   mgb_pdl_entry();
-  __shared__ double s0[8][33], s1[8][33];
-  const int ch = blockIdx.y, b = blockIdx.z;
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int k = blockIdx.x * 32 + lane;
-  const float* e = dexpo + ((size_t)b * 2 + ch) * MGB_REV_FRAMES * MGB_REV_BINS;
-  double a0 = 0.0, a1 = 0.0, n0 = 0.0, n1 = 0.0;
-  const bool last = (k == MGB_REV_PBINS - 1);
-  for (int m = wp; m < MGB_REV_FRAMES; m += 8) {
-    if (k < MGB_REV_PBINS) {
-      const double v = e[(size_t)m * MGB_REV_BINS + k];
-      a0 += v;
-      a1 += v * m;
-    }
-    if (last) {
-      const double v = e[(size_t)m * MGB_REV_BINS + MGB_REV_PBINS];
-      n0 += v;
-      n1 += v * m;
+  const int b = blockIdx.y;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= 2 * MGB_REV_PBINS) return;
+  const int ch = q / MGB_REV_PBINS, k = q % MGB_REV_PBINS;
+  const double* pp = part + (size_t)b * RV_CTAS * 2 * MGB_REV_BINS * 2;
+  double a0 = 0.0, a1 = 0.0;
+  for (int c = 0; c < RV_CTAS; ++c) {
+    const double* e = pp + ((size_t)c * 2 + ch) * MGB_REV_BINS * 2;
+    a0 += e[2 * k];
+    a1 += e[2 * k + 1];
+    if (k == MGB_REV_PBINS - 1) {
+      a0 += e[2 * MGB_REV_PBINS];
+      a1 += e[2 * MGB_REV_PBINS + 1];
     }
   }
-  s0[wp][lane] = a0;
-  s1[wp][lane] = a1;
-  __syncthreads();
-  if (last) {  // the thread owning bin 191 of each warp slice pushes its Nyquist sums
-    s0[wp][32] = n0;
-    s1[wp][32] = n1;
-  }
-  __syncthreads();
-  if (wp == 0 && k < MGB_REV_PBINS) {
-    double t0 = 0.0, t1 = 0.0;
-    for (int i = 0; i < 8; ++i) {
-      t0 += s0[i][lane];
-      t1 += s1[i][lane];
-    }
-    if (last) {
-      double u0 = 0.0, u1 = 0.0;
-      for (int i = 0; i < 8; ++i) {
-        u0 += s0[i][32];
-        u1 += s1[i][32];
-      }
-      t0 += u0;
-      t1 += u1;
-    }
-    double* g = gbank + (size_t)prow[b] * 768 + ch * 384;
-    g[k] = t0;
-    g[192 + k] = t1;
-  }
+  double* g = gbank + (size_t)prow[b] * 768 + ch * 384;
+  g[k] = a0;
+  g[192 + k] = a1;
 }
 
 // ---------------------------------------------------------------------------
@@ -271,10 +149,9 @@ __global__ void k_dly_colour(const double* __restrict__ bank, const int* __restr
     const double* bins = p + 40 + tap * MGB_COLOR_BINS;
     const int t = (tp + 20) % MGB_COLOR_LEN;
     double acc = 0.0;
-    for (int k = 1; k < MGB_COLOR_BINS; ++k) acc += exp(bins[k]) * cospi(2.0 * ((k * t) % MGB_COLOR_LEN) / 39.0);
+    for (int k = 1; k < MGB_COLOR_BINS; ++k) acc += exp(bins[k]) * g_cos39[(k * t) % MGB_COLOR_LEN];
     const double hv = (exp(bins[0]) + 2.0 * acc) / 39.0;
-    const double win = 0.5 - 0.5 * cospi(2.0 * tp / 38.0);
-    colour[(((size_t)b * 2 + ch) * MGB_DLY_TAPS + tap) * MGB_COLOR_LEN + tp] = (float)(hv * win);
+    colour[(((size_t)b * 2 + ch) * MGB_DLY_TAPS + tap) * MGB_COLOR_LEN + tp] = (float)(hv * g_hann39[tp]);
   }
   if (tp == 0) {
     const double re = p[tap], im = p[20 + tap];
@@ -353,14 +230,13 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
   // colour gradient -> bins
   if (threadIdx.x < MGB_COLOR_LEN) {
     const int tp = threadIdx.x;
-    const double win = 0.5 - 0.5 * cospi(2.0 * tp / 38.0);
-    dhz[(tp + 20) % MGB_COLOR_LEN] = (double)seg[d + tp] * win;
+    dhz[(tp + 20) % MGB_COLOR_LEN] = (double)seg[d + tp] * g_hann39[tp];
   }
   __syncthreads();
   if (threadIdx.x < MGB_COLOR_BINS) {
     const int k = threadIdx.x;
     double acc = 0.0;
-    for (int t = 0; t < MGB_COLOR_LEN; ++t) acc += dhz[t] * cospi(2.0 * ((k * t) % MGB_COLOR_LEN) / 39.0);
+    for (int t = 0; t < MGB_COLOR_LEN; ++t) acc += dhz[t] * g_cos39[(k * t) % MGB_COLOR_LEN];
     const double sc = (k == 0 ? 1.0 : 2.0) / 39.0;
     gp[40 + tap * MGB_COLOR_BINS + k] = acc * sc * exp(p[40 + tap * MGB_COLOR_BINS + k]);
   }

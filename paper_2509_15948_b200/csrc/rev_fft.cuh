@@ -90,11 +90,11 @@ __global__ void __launch_bounds__(RV_NT) k_rev_frames_fft(const double* __restri
 __global__ void __launch_bounds__(RV_NT) k_rev_bwd_frames_fft(const double* __restrict__ bank,
                                                                const int* __restrict__ prow,
                                                                const float2* __restrict__ GH, int M,
-                                                               float* __restrict__ dexpo) {
+                                                               double* __restrict__ dpart) {
   mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* s = reinterpret_cast<float2*>(dsm);
-  const int m0 = blockIdx.x * RV_F, b = blockIdx.y;
+  const int m0 = blockIdx.x * RV_F, m0f = m0, b = blockIdx.y;
   const float2* g = GH + (size_t)b * M;
   for (int q = threadIdx.x; q < RV_F * MGB_REV_NFFT; q += RV_NT) {
     const int f = q / MGB_REV_NFFT, i = q % MGB_REV_NFFT;
@@ -111,27 +111,37 @@ __global__ void __launch_bounds__(RV_NT) k_rev_bwd_frames_fft(const double* __re
   dft384(s, false);
   const double* p = bank + (size_t)prow[b] * 768;
   const float sc = 2.f / (float)MGB_REV_NFFT;
-  for (int q = threadIdx.x; q < RV_F * (MGB_REV_PBINS + 1); q += RV_NT) {
-    const int f = q / (MGB_REV_PBINS + 1), k = q % (MGB_REV_PBINS + 1);
-    const int m = m0 + f;
-    if (m >= MGB_REV_FRAMES) continue;
+  // per (bin k, channel): this CTA's sums over its RV_F frames of dexpo and m * dexpo
+  double* out = dpart + ((size_t)b * gridDim.x + blockIdx.x) * 2 * MGB_REV_BINS * 2;
+  for (int k = threadIdx.x; k < MGB_REV_BINS; k += RV_NT) {
     const int kn = (MGB_REV_NFFT - k) % MGB_REV_NFFT;
-    // output index k = k1 + 3 k2 lives at row k1, column k2
-    const float2 zk = s[f * RV_FRAME + (k % 3) * RV_P + pidx<true>(k / 3)];
-    const float2 zp = s[f * RV_FRAME + (kn % 3) * RV_P + pidx<true>(kn / 3)];
-    // split the packed spectrum: Dm = (Zk + conj Zp)/2, Ds = (Zk - conj Zp)/(2i)
-    float2 dmx = make_float2(0.5f * (zk.x + zp.x), 0.5f * (zk.y - zp.y));
-    const float2 dd = make_float2(0.5f * (zk.x - zp.x), 0.5f * (zk.y + zp.y));
-    float2 dsx = make_float2(dd.y, -dd.x);
-    float scale = sc;
-    if (k == 0 || k == MGB_REV_PBINS) scale *= 0.5f;
     const int kk = k < MGB_REV_PBINS ? k : MGB_REV_PBINS - 1;
-    const float mm = expf((float)(p[kk] + p[192 + kk] * (double)m));
-    const float ms = expf((float)(p[384 + kk] + p[576 + kk] * (double)m));
-    const float2 sm = g_rev_spec[0][m][k], ss = g_rev_spec[1][m][k];
-    dexpo[(((size_t)b * 2 + 0) * MGB_REV_FRAMES + m) * MGB_REV_BINS + k] =
-        scale * (dmx.x * sm.x + dmx.y * sm.y) * mm;
-    dexpo[(((size_t)b * 2 + 1) * MGB_REV_FRAMES + m) * MGB_REV_BINS + k] =
-        scale * (dsx.x * ss.x + dsx.y * ss.y) * ms;
+    const double h0m = p[kk], hdm = p[192 + kk], h0s = p[384 + kk], hds = p[576 + kk];
+    const float scale = (k == 0 || k == MGB_REV_PBINS) ? 0.5f * sc : sc;
+    double m0 = 0.0, m1 = 0.0, s0 = 0.0, s1 = 0.0;
+    for (int f = 0; f < RV_F; ++f) {
+      const int m = m0f + f;
+      if (m >= MGB_REV_FRAMES) break;
+      // output index k = k1 + 3 k2 lives at row k1, column k2
+      const float2 zk = s[f * RV_FRAME + (k % 3) * RV_P + pidx<true>(k / 3)];
+      const float2 zp = s[f * RV_FRAME + (kn % 3) * RV_P + pidx<true>(kn / 3)];
+      // split the packed spectrum: Dm = (Zk + conj Zp)/2, Ds = (Zk - conj Zp)/(2i)
+      const float2 dmx = make_float2(0.5f * (zk.x + zp.x), 0.5f * (zk.y - zp.y));
+      const float2 dd = make_float2(0.5f * (zk.x - zp.x), 0.5f * (zk.y + zp.y));
+      const float2 dsx = make_float2(dd.y, -dd.x);
+      const float mm = expf((float)(h0m + hdm * (double)m));
+      const float ms = expf((float)(h0s + hds * (double)m));
+      const float2 sm = g_rev_spec[0][m][k], ss = g_rev_spec[1][m][k];
+      const double vm = (double)(scale * (dmx.x * sm.x + dmx.y * sm.y) * mm);
+      const double vs = (double)(scale * (dsx.x * ss.x + dsx.y * ss.y) * ms);
+      m0 += vm;
+      m1 += vm * (double)m;
+      s0 += vs;
+      s1 += vs * (double)m;
+    }
+    out[(0 * MGB_REV_BINS + k) * 2] = m0;
+    out[(0 * MGB_REV_BINS + k) * 2 + 1] = m1;
+    out[(1 * MGB_REV_BINS + k) * 2] = s0;
+    out[(1 * MGB_REV_BINS + k) * 2 + 1] = s1;
   }
 }
