@@ -22,7 +22,7 @@
 // the previous one (same local offset).  The gain computer runs in float32
 // with MUFU exp/log (abs. error ~1e-6 in the log domain, far inside 1e-4).
 //
-// Backward: the adjoint of the truncated causal filter is the truncated
+// Backward (one kernel per level + a per-node finalize): the adjoint of the truncated causal filter is the truncated
 // anti-causal filter — the same construction on reversed time with the
 // 2-state recursion  v[m] = a v[m+1] + dg[m],  w[m] = a (w[m+1] + v[m+1]):
 //     dx[m] = (1-a)(v[m] - a^C v[m+C])
@@ -331,108 +331,64 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_fwd(char tag, const float* const*
   }
 }
 
-// backward part 1: elementwise chain down to dg (grad wrt the unclamped envelope)
-__global__ void __launch_bounds__(256) k_dyn_bwd0(char tag, const float* const* __restrict__ u_rows,
-                                                  const float* const* __restrict__ gy_rows,
-                                                  const double* __restrict__ bank, const int* __restrict__ prow,
-                                                  const int* __restrict__ widx, const double* __restrict__ w,
-                                                  const float* __restrict__ env, float* __restrict__ dg,
-                                                  float* __restrict__ gu, double* __restrict__ part, int L) {
-  mgb_pdl_entry();
-  __shared__ double red[32];
-  const int b = blockIdx.y;
-  const float* u = u_rows[b];
-  const float* gy = gy_rows[b];
-  const DynP q = load_params(bank, prow[b]);
-  const bool gate = tag == 'n';
-  const double wv = w ? w[widx[b]] : 1.0;
-  const float wf = (float)wv, om = (float)(1.0 - wv);
-  const bool bypass = wv == 0.0;
-  const float* eo = env + (size_t)b * L;
-  float* dgo = dg + (size_t)b * L;
-  float* go = gu + (size_t)b * 2 * L;
-  double sT = 0.0, sW = 0.0, sR = 0.0, sw = 0.0;
-  float fT = 0.f, fW = 0.f, fR = 0.f, fw = 0.f;
-  const bool vec = vec_ok(u, L) && vec_ok(gy, L) && vec_ok(eo, L) && vec_ok(go, L) && vec_ok(dgo, L);
-  for (long long n4 = 4 * ((long long)blockIdx.x * 256 + threadIdx.x); n4 < L; n4 += 4LL * gridDim.x * 256) {
-   float4 ul4, ur4, gl4, gr4;
-   load4(u, L, n4, vec, ul4, ur4);
-   load4(gy, L, n4, vec, gl4, gr4);
-   const float4 ev4 = load4m(eo, L, n4, vec);
-   const float U[4] = {ul4.x, ul4.y, ul4.z, ul4.w}, V[4] = {ur4.x, ur4.y, ur4.z, ur4.w};
-   const float GL[4] = {gl4.x, gl4.y, gl4.z, gl4.w}, GR[4] = {gr4.x, gr4.y, gr4.z, gr4.w};
-   const float EV[4] = {ev4.x, ev4.y, ev4.z, ev4.w};
-   float OL[4], OR[4], OD[4];
-#pragma unroll
-   for (int e = 0; e < 4; ++e) {
-    const float l = U[e], r = V[e], gl = GL[e], gr = GR[e];
-    const float gc = EV[e];
-    const float gcl = fmaxf(gc, 0.f);
-    const float G = __logf(gcl + 1e-8f);
-    const bool above = G >= q.T + q.W, below = G < q.T - q.W;
-    float Gy, dGu, dT = 0.f, dW = 0.f, dR = 0.f;
-    if (gate) {
-      if (above) { Gy = G; dGu = 1.f; }
-      else if (below) { Gy = q.T + q.R * (G - q.T); dGu = q.R; dT = 1.f - q.R; dR = G - q.T; }
-      else {
-        const float z = G - q.T - q.W, k = 1.f - q.R, zh = z * q.i2W, zq = z * z * q.i4W;
-        Gy = G + k * zq;
-        dGu = 1.f + k * zh;
-        dT = -k * zh;
-        dW = k * (-zh - zq * (4.f * q.i4W));
-        dR = -zq;
-      }
-    } else {
-      if (above) {
-        Gy = q.T + (G - q.T) * q.iR;
-        dGu = q.iR;
-        dT = 1.f - q.iR;
-        dR = -(G - q.T) * q.iR * q.iR;
-      } else if (below) { Gy = G; dGu = 1.f; }
-      else {
-        const float z = G - q.T + q.W, k = q.iR - 1.f, zh = z * q.i2W, zq = z * z * q.i4W;
-        Gy = G + k * zq;
-        dGu = 1.f + k * zh;
-        dT = -k * zh;
-        dW = k * (zh - zq * (4.f * q.i4W));
-        dR = -zq * q.iR * q.iR;
-      }
-    }
-    const float gain = __expf(Gy - G);
-    float dl, dr, ul, ur;
-    if (bypass) { dl = dr = 0.f; ul = gl; ur = gr; }
+// Per-sample adjoint of the gain computer and dry/wet (mg/processors.py:195-243):
+// given u (l, r), dL/dy (gl, gr) and the stored envelope gc, returns dL/du's
+// elementwise part (ol, orr), dL/d(envelope) og, and accumulates the T/W/R/w
+// partials.  The knee masks are constants of the backward (mg/engine.py:328-341).
+struct DynAcc {
+  float T, W, R, w;
+};
+__device__ __forceinline__ void dyn_adjoint(float l, float r, float gl, float gr, float gc, const DynP& q, bool gate,
+                                            float wf, float om, bool bypass, bool acc_on, float& ol, float& orr,
+                                            float& og, DynAcc& A) {
+  const float gcl = fmaxf(gc, 0.f);
+  const float G = __logf(gcl + 1e-8f);
+  const bool above = G >= q.T + q.W, below = G < q.T - q.W;
+  float Gy, dGu, dT = 0.f, dW = 0.f, dR = 0.f;
+  if (gate) {
+    if (above) { Gy = G; dGu = 1.f; }
+    else if (below) { Gy = q.T + q.R * (G - q.T); dGu = q.R; dT = 1.f - q.R; dR = G - q.T; }
     else {
-      dl = wf * gl; dr = wf * gr; ul = om * gl; ur = om * gr;
-      fw = fmaf(gl, l * gain - l, fmaf(gr, r * gain - r, fw));
+      const float z = G - q.T - q.W, k = 1.f - q.R, zh = z * q.i2W, zq = z * z * q.i4W;
+      Gy = G + k * zq;
+      dGu = 1.f + k * zh;
+      dT = -k * zh;
+      dW = k * (-zh - zq * (4.f * q.i4W));
+      dR = -zq;
     }
-    OL[e] = fmaf(dl, gain, ul);
-    OR[e] = fmaf(dr, gain, ur);
-    const float D = (dl * l + dr * r) * gain;
-    fT = fmaf(D, dT, fT);
-    fW = fmaf(D, dW, fW);
-    fR = fmaf(D, dR, fR);
-    const float dG = D * dGu - D;
-    OD[e] = (gc > 0.f) ? __fdividef(dG, gcl + 1e-8f) : 0.f;
-   }
-   store4(go, L, n4, vec, make_float4(OL[0], OL[1], OL[2], OL[3]), make_float4(OR[0], OR[1], OR[2], OR[3]), dgo,
-          make_float4(OD[0], OD[1], OD[2], OD[3]));
+  } else {
+    if (above) {
+      Gy = q.T + (G - q.T) * q.iR;
+      dGu = q.iR;
+      dT = 1.f - q.iR;
+      dR = -(G - q.T) * q.iR * q.iR;
+    } else if (below) { Gy = G; dGu = 1.f; }
+    else {
+      const float z = G - q.T + q.W, k = q.iR - 1.f, zh = z * q.i2W, zq = z * z * q.i4W;
+      Gy = G + k * zq;
+      dGu = 1.f + k * zh;
+      dT = -k * zh;
+      dW = k * (zh - zq * (4.f * q.i4W));
+      dR = -zq * q.iR * q.iR;
+    }
   }
-  // (float partials: at most a few float4 groups per thread before the float64 block sum)
-  sT += fT; sW += fW; sR += fR; sw += fw;
-  sT = block_sum(sT, red);
-  __syncthreads();
-  sW = block_sum(sW, red);
-  __syncthreads();
-  sR = block_sum(sR, red);
-  __syncthreads();
-  sw = block_sum(sw, red);
-  if (threadIdx.x == 0) {
-    double* pp = part + ((size_t)b * gridDim.x + blockIdx.x) * 8;
-    pp[0] = sT;
-    pp[1] = sW;
-    pp[2] = sR;
-    pp[3] = sw;
+  const float gain = __expf(Gy - G);
+  float dl, dr, ul, ur;
+  if (bypass) { dl = dr = 0.f; ul = gl; ur = gr; }
+  else {
+    dl = wf * gl; dr = wf * gr; ul = om * gl; ur = om * gr;
+    if (acc_on) A.w = fmaf(gl, l * gain - l, fmaf(gr, r * gain - r, A.w));
   }
+  ol = fmaf(dl, gain, ul);
+  orr = fmaf(dr, gain, ur);
+  const float D = (dl * l + dr * r) * gain;
+  if (acc_on) {
+    A.T = fmaf(D, dT, A.T);
+    A.W = fmaf(D, dW, A.W);
+    A.R = fmaf(D, dR, A.R);
+  }
+  const float dG = D * dGu - D;
+  og = (gc > 0.f) ? __fdividef(dG, gcl + 1e-8f) : 0.f;
 }
 
 struct VW {
@@ -495,10 +451,17 @@ __device__ __forceinline__ void rscan2_excl(VW& a, VW& c, const double* pw, doub
   c = VW{ncv + wc.v, ncw + wc.w};
 }
 
-__global__ void __launch_bounds__(NT, 2) k_dyn_bwd1(const float* const* __restrict__ u_rows,
-                                                 const double* __restrict__ bank, const int* __restrict__ prow,
-                                                 const float* __restrict__ dg, float* __restrict__ gu,
-                                                 double* __restrict__ part, int L, int nch) {
+// Backward of one chunk: (A) the elementwise chain for this chunk and the next
+// (dL/d envelope staged segment-major in shared memory; this chunk's elementwise
+// dL/du written to gu, T/W/R/w partials), then (B) the truncated reverse scans,
+// dx and r, dL/du += 2 mid dx and the x.dx / x.r partials.  The next chunk's
+// envelope adjoint is recomputed instead of round-tripping dg through HBM.
+__global__ void __launch_bounds__(NT, 2) k_dyn_bwd(char tag, const float* const* __restrict__ u_rows,
+                                                const float* const* __restrict__ gy_rows,
+                                                const double* __restrict__ bank, const int* __restrict__ prow,
+                                                const int* __restrict__ widx, const double* __restrict__ w,
+                                                const float* __restrict__ env, float* __restrict__ gu,
+                                                double* __restrict__ part, int L, int nch) {
   mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float* ds = reinterpret_cast<float*>(dsm);  // [2][SPAD]: cur chunk, next chunk
@@ -508,26 +471,59 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd1(const float* const* __restri
   __shared__ double red[32];
   const int j = blockIdx.x, b = blockIdx.y;
   const float* u = u_rows[b];
+  const float* gy = gy_rows[b];
   const DynP q = load_params(bank, prow[b]);
-  const float* d = dg + (size_t)b * L;
+  const bool gate = tag == 'n';
+  const double wv = w ? w[widx[b]] : 1.0;
+  const float wf = (float)wv, om = (float)(1.0 - wv);
+  const bool bypass = wv == 0.0;
+  const float* eo = env + (size_t)b * L;
+  float* go = gu + (size_t)b * 2 * L;
   init_pw(pw, q.la);
   const long long c0 = (long long)j * CH;
-  const bool vec = vec_ok(u, L) && vec_ok(d, L);
-  {
-    float4 vc[Q4], vn[Q4];
-#pragma unroll
+  const bool vec = vec_ok(u, L) && vec_ok(gy, L) && vec_ok(eo, L) && vec_ok(go, L);
+  DynAcc A{0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {  // (A) c = 0: this chunk (full), c = 1: next chunk (dg only)
+#pragma unroll 2
     for (int k = 0; k < Q4; ++k) {
       const int o = 4 * (threadIdx.x + NT * k);
-      vc[k] = load4m(d, L, c0 + o, vec);
-      vn[k] = load4m(d, L, c0 + CH + o, vec);
+      const long long n = c0 + (long long)c * CH + o;
+      float4 ul4, ur4, gl4, gr4;
+      load4(u, L, n, vec, ul4, ur4);
+      load4(gy, L, n, vec, gl4, gr4);
+      const float4 ev4 = load4m(eo, L, n, vec);
+      const float U[4] = {ul4.x, ul4.y, ul4.z, ul4.w}, V[4] = {ur4.x, ur4.y, ur4.z, ur4.w};
+      const float GL[4] = {gl4.x, gl4.y, gl4.z, gl4.w}, GR[4] = {gr4.x, gr4.y, gr4.z, gr4.w};
+      const float EV[4] = {ev4.x, ev4.y, ev4.z, ev4.w};
+      float OL[4], OR[4];
+      float* dst = ds + c * SPAD + sidx_n(o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float og;
+        dyn_adjoint(U[e], V[e], GL[e], GR[e], EV[e], q, gate, wf, om, bypass, c == 0 && n + e < L, OL[e], OR[e],
+                    og, A);
+        dst[e] = og;
+      }
+      if (c == 0)
+        store4(go, L, n, vec, make_float4(OL[0], OL[1], OL[2], OL[3]), make_float4(OR[0], OR[1], OR[2], OR[3]),
+               nullptr, make_float4(0.f, 0.f, 0.f, 0.f));
     }
-#pragma unroll
-    for (int k = 0; k < Q4; ++k) {
-      const int o = 4 * (threadIdx.x + NT * k);
-      float* a = ds + sidx_n(o);
-      float* c = ds + SPAD + sidx_n(o);
-      a[0] = vc[k].x; a[1] = vc[k].y; a[2] = vc[k].z; a[3] = vc[k].w;
-      c[0] = vn[k].x; c[1] = vn[k].y; c[2] = vn[k].z; c[3] = vn[k].w;
+  }
+  {
+    double t0 = block_sum((double)A.T, red);
+    __syncthreads();
+    double t1 = block_sum((double)A.W, red);
+    __syncthreads();
+    double t2 = block_sum((double)A.R, red);
+    __syncthreads();
+    double t3 = block_sum((double)A.w, red);
+    if (threadIdx.x == 0) {
+      double* pp = part + ((size_t)b * nch + j) * 8;
+      pp[0] = t0;
+      pp[1] = t1;
+      pp[2] = t2;
+      pp[3] = t3;
     }
   }
   __syncthreads();
@@ -570,8 +566,7 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd1(const float* const* __restri
   }
   __syncthreads();
   double sxd = 0.0, sxr = 0.0;
-  float* go = gu + (size_t)b * 2 * L;
-  const bool vg = vec && vec_ok(go, L);
+  const bool vg = vec;
 #pragma unroll
   for (int k0 = 0; k0 < Q4; k0 += 2) {  // coalesced: dmid = 2 mid dx; sums for d a_raw (2 groups at a time)
   float4 ul[2], ur[2], gl[2], gr[2];
@@ -650,23 +645,14 @@ __global__ void k_dyn_final(const double* __restrict__ part0, int nblk0, int nch
 }
 
 int nchunks(int L) { return (L + CH - 1) / CH; }
-int bwd0_grid(int L) {
-  int n = (L + 8 * 256 - 1) / (8 * 256);
-  return n < 1 ? 1 : (n > 512 ? 512 : n);
-}
-
 struct DynWs {
-  double *part0, *part1;
-  float* dg;
+  double* part;  // [B][nch][8]: T, W, R, w partials (phase A) and x.dx, x.r (phase B) per chunk
 };
 
 template <class A>
 DynWs dcarve(A& a, int B, int L) {
   DynWs w;
-  const int nch = nchunks(L);
-  w.part0 = a.template take<double>((size_t)B * bwd0_grid(L) * 8);
-  w.part1 = a.template take<double>((size_t)B * nch * 8);
-  w.dg = a.template take<float>((size_t)B * L);
+  w.part = a.template take<double>((size_t)B * nchunks(L) * 8);
   return w;
 }
 
@@ -674,7 +660,7 @@ DynWs dcarve(A& a, int B, int L) {
 
 int mgb_dyn_init() {
   cudaFuncSetAttribute(k_dyn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemF);
-  cudaFuncSetAttribute(k_dyn_bwd1, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+  cudaFuncSetAttribute(k_dyn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -697,16 +683,14 @@ int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st) {
 
 int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st) {
   if (!lv->aux) return 1;
-  const int B = lv->B, L = lv->L, nch = nchunks(L), g0 = bwd0_grid(L);
+  const int B = lv->B, L = lv->L, nch = nchunks(L);
   MgbArena a{(char*)lv->ws, 0};
   DynWs w = dcarve(a, B, L);
-  mgb_launch(k_dyn_bwd0, dim3(dim3(g0, B)), dim3(256), 0, st, lv->tag, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx, lv->w,
-                                          lv->aux, w.dg, lv->gu, w.part0, L);
+  mgb_launch(k_dyn_bwd, dim3(nch, B), dim3(NT), kDynSmem, st, lv->tag, lv->u_rows, lv->gy_rows, lv->bank, lv->prow,
+             lv->widx, lv->w, lv->aux, lv->gu, w.part, L, nch);
   MGB_CHECK_LAUNCH();
-  mgb_launch(k_dyn_bwd1, dim3(dim3(nch, B)), dim3(NT), kDynSmem, st, lv->u_rows, lv->bank, lv->prow, w.dg, lv->gu, w.part1, L, nch);
-  MGB_CHECK_LAUNCH();
-  mgb_launch(k_dyn_final, dim3(B), dim3(256), 0, st, w.part0, g0, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank, lv->gw,
-                                 w.part1);
+  mgb_launch(k_dyn_final, dim3(B), dim3(256), 0, st, w.part, nch, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,
+             lv->gw, w.part);
   MGB_CHECK_LAUNCH();
   return 0;
 }
