@@ -210,16 +210,26 @@ __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colC(const float
   float2 v[Q];
 #pragma unroll
   for (int m = 0; m < Q; ++m) v[m] = src[(long long)(j + P * m) * N2];
-  col_fft<N1, true>(v, sm, c, j);
   const typename Ep::Ctx ctx = ep.prepare(b);
+  typename Ep::Raw raw[2][B8];
+  // first epilogue batch issued before the transform so its latency hides behind it
+#pragma unroll
+  for (int i = 0; i < B8; ++i) {
+    const int n1 = j + P * i;
+    raw[0][i] = ep.fetch(ctx, b, (long long)n1 * N2 + col, n1 < out_rows);
+  }
+  col_fft<N1, true>(v, sm, c, j);
   float a0 = 0.f, a1 = 0.f;
+  // software-pipelined epilogue: batch m0 + B8 is fetched before batch m0 is consumed
 #pragma unroll
   for (int m0 = 0; m0 < Q; m0 += B8) {
-    typename Ep::Raw raw[B8];
+    const int cur = (m0 / B8) & 1;
+    if (m0 + B8 < Q) {
 #pragma unroll
-    for (int i = 0; i < B8; ++i) {
-      const int n1 = j + P * (m0 + i);
-      raw[i] = ep.fetch(ctx, b, (long long)n1 * N2 + col, n1 < out_rows);
+      for (int i = 0; i < B8; ++i) {
+        const int n1 = j + P * (m0 + B8 + i);
+        raw[cur ^ 1][i] = ep.fetch(ctx, b, (long long)n1 * N2 + col, n1 < out_rows);
+      }
     }
 #pragma unroll
     for (int i = 0; i < B8; ++i) {
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colC(const float
         float2 y = v[m0 + i];
         y.x *= scale;
         y.y *= scale;
-        ep.finish(ctx, b, (long long)n1 * N2 + col, y, raw[i], a0, a1);
+        ep.finish(ctx, b, (long long)n1 * N2 + col, y, raw[cur][i], a0, a1);
       }
     }
   }
