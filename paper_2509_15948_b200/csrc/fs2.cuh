@@ -49,13 +49,15 @@ struct G {
 
 constexpr int TP = 33;                 // transpose pitch
 constexpr int TBUF = 32 * TP;          // per-warp transpose buffer (float2)
-// per-warp shared memory of the row kernels: the transpose buffer plus NROW
-// staged rows of N2 float2 (cp.async prefetch of every operand row)
-template <int NROW>
-constexpr size_t row_smem() { return (size_t)2 * RP * (TBUF + NROW * N2) * sizeof(float2); }
-constexpr size_t ROWH_SMEM = row_smem<1>();
-constexpr size_t ROWF_SMEM = row_smem<2>();
-constexpr size_t ROWG_SMEM = row_smem<3>();
+// per-warp shared memory of the row kernels: the staged operand rows (cp.async
+// prefetch), padded to TBUF where a row buffer doubles as the transpose scratch
+// once its contents are in registers (no separate transpose buffer)
+constexpr int ROWH_WARP = TBUF;                 // [Ah row | scratch]
+constexpr int ROWF_WARP = TBUF + N2;            // [Ax row -> spectrum | scratch], [H row]
+constexpr int ROWG_WARP = TBUF + N2 + TBUF;     // [Ag row -> G spectrum | scratch], [X row], [H row | scratch]
+constexpr size_t ROWH_SMEM = (size_t)2 * RP * ROWH_WARP * sizeof(float2);
+constexpr size_t ROWF_SMEM = (size_t)2 * RP * ROWF_WARP * sizeof(float2);
+constexpr size_t ROWG_SMEM = (size_t)2 * RP * ROWG_WARP * sizeof(float2);
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -277,10 +279,10 @@ __device__ __forceinline__ RowMap row_map() {
 // Hermitian partner column of spectral column k in row `row` (partner row prow)
 __device__ __forceinline__ int partner_col(int row, int k) { return row == 0 ? ((N2 - k) & (N2 - 1)) : (N2 - 1 - k); }
 
-// warp-private regions of the row kernels: [T (TBUF) | row 0 | row 1 | ...]
-template <int NROW>
+// warp-private region of a row kernel with WARP float2 per warp
+template <int WARP>
 __device__ __forceinline__ float2* warp_region(unsigned char* smraw, int w) {
-  return reinterpret_cast<float2*>(smraw) + (size_t)w * (TBUF + NROW * N2);
+  return reinterpret_cast<float2*>(smraw) + (size_t)w * WARP;
 }
 
 // prep: H[b][row][k] = FFT_{N2}(Ah[b][row][.])  (FIR spectrum, row layout)
@@ -291,8 +293,7 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowH(const float2* __restrict__
   extern __shared__ __align__(16) unsigned char smraw[];
   const RowMap rm = row_map<N1>();
   if (!rm.active) return;
-  float2* T = warp_region<1>(smraw, threadIdx.x >> 5);
-  float2* sA = T + TBUF;
+  float2* sA = warp_region<ROWH_WARP>(smraw, threadIdx.x >> 5);  // Ah row, then the transpose scratch
   const long long base = (long long)blockIdx.y * g::N + (long long)rm.row * N2;
   row_prefetch(sA, Ah + base, rm.lane);
   cp_async_wait_all();
@@ -300,7 +301,8 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowH(const float2* __restrict__
   float2 v[32];
 #pragma unroll
   for (int m = 0; m < 32; ++m) v[m] = sA[rm.lane + 32 * m];
-  row_fft<false>(v, T, rm.lane);
+  __syncwarp();
+  row_fft<false>(v, sA, rm.lane);
 #pragma unroll
   for (int ka = 0; ka < 32; ++ka) H[base + rm.lane + 32 * ka] = v[ka];
 }
@@ -318,13 +320,12 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int w = threadIdx.x >> 5;
-  float2* T = warp_region<2>(smraw, w);
-  float2* sA = T + TBUF;       // Ax row, then this row's spectrum (natural order)
-  float2* sH = sA + N2;        // H row
+  float2* sA = warp_region<ROWF_WARP>(smraw, w);  // Ax row, scratch, this row's spectrum, scratch
+  float2* sH = sA + TBUF;                          // H row
   const RowMap rm = row_map<N1>();
   const bool self = rm.row == rm.prow;
-  float2* pA = self ? sA : warp_region<2>(smraw, w ^ 1) + TBUF;
-  float2* pH = pA + N2;
+  float2* pA = self ? sA : warp_region<ROWF_WARP>(smraw, w ^ 1);
+  float2* pH = pA + TBUF;
   const long long base = (long long)blockIdx.y * g::N + (long long)rm.row * N2;
   const int lane = rm.lane;
   row_prefetch(sA, Ax + base, lane);
@@ -334,9 +335,10 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__
   float2 v[32];
 #pragma unroll
   for (int m = 0; m < 32; ++m) v[m] = sA[lane + 32 * m];
+  __syncwarp();  // sA becomes the transpose scratch
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    row_fft_compact(v, T, lane);
+    row_fft_compact(v, sA, lane);
     if (pass == 1) break;
 #pragma unroll
     for (int ka = 0; ka < 32; ++ka) {
@@ -353,6 +355,7 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__
       const float2 y1 = cmul(xl, hl), y2 = cmul(xr, hr);
       v[ka] = make_float2(y1.x - y2.y, -(y1.y + y2.x));  // conj: inverse via the forward code
     }
+    __syncthreads();  // both warps done reading the spectra before sA is scratch again
   }
   if (!rm.active) return;
 #pragma unroll
@@ -374,14 +377,13 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int w = threadIdx.x >> 5;
-  float2* T = warp_region<3>(smraw, w);
-  float2* sA = T + TBUF;       // Ag row, then this row's G spectrum (natural order)
-  float2* sX = sA + N2;
-  float2* sH = sX + N2;
+  float2* sA = warp_region<ROWG_WARP>(smraw, w);  // Ag row, scratch, then this row's G spectrum
+  float2* sX = sA + TBUF;
+  float2* sH = sX + N2;                            // H row, then the scratch of passes 1-2
   const RowMap rm = row_map<N1>();
   const bool self = rm.row == rm.prow;
-  float2* pA = self ? sA : warp_region<3>(smraw, w ^ 1) + TBUF;
-  float2* pX = pA + N2;
+  float2* pA = self ? sA : warp_region<ROWG_WARP>(smraw, w ^ 1);
+  float2* pX = pA + TBUF;
   float2* pH = pX + N2;
   const long long base = (long long)blockIdx.y * g::N + (long long)rm.row * N2;
   const int lane = rm.lane;
@@ -393,9 +395,10 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__
   float2 v[32];
 #pragma unroll
   for (int m = 0; m < 32; ++m) v[m] = sA[lane + 32 * m];
+  __syncwarp();  // sA becomes the transpose scratch of pass 0
 #pragma unroll 1
   for (int pass = 0; pass < 3; ++pass) {
-    row_fft_compact(v, T, lane);
+    row_fft_compact(v, pass == 0 ? sA : sH, lane);
     if (pass == 0) {
 #pragma unroll
       for (int ka = 0; ka < 32; ++ka) sA[lane + 32 * ka] = v[ka];
@@ -423,6 +426,7 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__
       const float2 y1 = cmulc(gl, ol), y2 = cmulc(gr, orr);
       v[ka] = make_float2(y1.x - y2.y, -(y1.y + y2.x));
     }
+    if (pass == 0) __syncthreads();  // partner done reading our H row: it is scratch from here on
   }
 }
 
