@@ -112,6 +112,7 @@ struct NoCtx {};
 
 struct LdRows {
   static constexpr bool kAccum = false;
+  static constexpr int kBatch = 8;  // loads per pipelined batch (register budget)
   typedef NoCtx Ctx;
   typedef float2 Raw;
   const float* const* rows;
@@ -128,6 +129,7 @@ struct LdRows {
 
 struct LdFir {
   static constexpr bool kAccum = false;
+  static constexpr int kBatch = 8;
   typedef NoCtx Ctx;
   typedef float2 Raw;
   const float2* h;
@@ -143,6 +145,7 @@ struct LdFir {
 // Backward prologue (dry/wet + gain-staging adjoints) as the G loader.
 struct LdBwdPro {
   static constexpr bool kAccum = true;
+  static constexpr int kBatch = 4;
   struct Ctx {
     const float* u;
     const float* gy;

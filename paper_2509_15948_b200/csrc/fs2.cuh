@@ -171,18 +171,28 @@ __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colA(Ld ld, floa
   const typename Ld::Ctx ctx = ld.prepare(b);
   float acc = 0.f;
   float2 v[Q];
+  // software-pipelined loader: batch m0 + BL is fetched before batch m0 is finished
+  constexpr int BL = Ld::kBatch < B8 ? Ld::kBatch : B8;
+  typename Ld::Raw raw[2][BL];
 #pragma unroll
-  for (int m0 = 0; m0 < Q; m0 += B8) {
-    typename Ld::Raw raw[B8];
+  for (int i = 0; i < BL; ++i) {
+    const int n1 = j + P * i;
+    raw[0][i] = ld.fetch(ctx, b, (long long)n1 * N2 + col, n1 < nz_rows);
+  }
 #pragma unroll
-    for (int i = 0; i < B8; ++i) {
-      const int n1 = j + P * (m0 + i);
-      raw[i] = ld.fetch(ctx, b, (long long)n1 * N2 + col, n1 < nz_rows);
+  for (int m0 = 0; m0 < Q; m0 += BL) {
+    const int cur = (m0 / BL) & 1;
+    if (m0 + BL < Q) {
+#pragma unroll
+      for (int i = 0; i < BL; ++i) {
+        const int n1 = j + P * (m0 + BL + i);
+        raw[cur ^ 1][i] = ld.fetch(ctx, b, (long long)n1 * N2 + col, n1 < nz_rows);
+      }
     }
 #pragma unroll
-    for (int i = 0; i < B8; ++i) {
+    for (int i = 0; i < BL; ++i) {
       const int n1 = j + P * (m0 + i);
-      v[m0 + i] = ld.finish(ctx, b, (long long)n1 * N2 + col, raw[i], acc);
+      v[m0 + i] = ld.finish(ctx, b, (long long)n1 * N2 + col, raw[cur][i], acc);
     }
   }
   if (Ld::kAccum) {
