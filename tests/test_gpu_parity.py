@@ -254,3 +254,45 @@ def test_conv_level_matches_oracle_at_length(dev, tag, L):
     np.testing.assert_allclose(float(reg.detach()), float(rego.detach()), rtol=1e-5, atol=2e-6)
     assert normrel(ut.grad.cpu().numpy(), uo.grad.numpy()) < 1e-4
     assert normrel(pt.grad.cpu().numpy(), po.grad.numpy(), floor=1e-6) < 1e-4
+
+
+@pytest.mark.parametrize("tag", list("erdcgs"))
+def test_phase_split_equals_whole_level_calls(dev, tag):
+    """mgb_level_{forward,backward}_phase 1 then 2 == mgb_level_{forward,backward} bit-exactly,
+    and the library's launch counter advances."""
+    import ctypes
+    from golden_inputs import kernel_inputs
+    from paper_2509_15948_b200._lib import check, lib
+    from paper_2509_15948_b200.engine import dev_ptr_array, ptr, stream_ptr
+    from paper_2509_15948_b200.processors import _Level
+    Ld = lib()
+    u, p, w = kernel_inputs(tag)
+    ut = torch.tensor(u, dtype=torch.float32, device=dev)
+    pt = torch.tensor(p, dtype=torch.float64, device=dev)
+    B, _, L = ut.shape
+    outs = []
+    for split in (False, True):
+        lv = _Level(tag, ut, pt)
+        st = lv.struct()
+        gy = torch.tensor(w, dtype=torch.float32, device=dev)
+        gyr = dev_ptr_array([ptr(gy, b * 2 * L) for b in range(B)], dev)
+        greg = torch.ones((), dtype=torch.float64, device=dev)
+        gu = torch.empty((B, 2, L), dtype=torch.float32, device=dev)
+        gp = torch.zeros_like(pt)
+        gw = torch.zeros(B, dtype=torch.float64, device=dev)
+        st.gy_rows, st.greg, st.gu, st.gbank, st.gw = ptr(gyr), ptr(greg), ptr(gu), ptr(gp), ptr(gw)
+        n0 = Ld.mgb_launch_count()
+        if split:
+            for ph in (1, 2):
+                check(Ld.mgb_level_forward_phase(ctypes.byref(st), ph, stream_ptr()), "fwd phase")
+            for ph in (1, 2):
+                check(Ld.mgb_level_backward_phase(ctypes.byref(st), ph, stream_ptr()), "bwd phase")
+        else:
+            check(Ld.mgb_level_forward(ctypes.byref(st), stream_ptr()), "fwd")
+            check(Ld.mgb_level_backward(ctypes.byref(st), stream_ptr()), "bwd")
+        torch.cuda.synchronize()
+        assert Ld.mgb_launch_count() > n0
+        outs.append([t.cpu().numpy().copy() for t in (lv.y, gu, gp)])
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+    assert Ld.mgb_level_forward_phase(None, 1, stream_ptr()) != 0  # bad argument -> status 1

@@ -16,14 +16,15 @@ from conftest import ROOT, golden, normrel
 
 def _declared_symbols():
     text = open(os.path.join(ROOT, "include", "mixgraph_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t)\s+(mgb_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|long long)\s+(mgb_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_the_boundary():
     syms = _declared_symbols()
     for s in ("mgb_init", "mgb_level_forward", "mgb_level_backward", "mgb_level_workspace", "mgb_weights",
               "mgb_bus_sum", "mgb_mrstft_target", "mgb_mrstft_forward", "mgb_mrstft_backward",
-              "mgb_adamw_step", "mgb_sparsity", "mgb_fft"):
+              "mgb_adamw_step", "mgb_sparsity", "mgb_fft", "mgb_level_forward_phase",
+              "mgb_level_backward_phase", "mgb_launch_count"):
         assert s in syms, s
 
 
@@ -39,6 +40,7 @@ def test_library_exports_every_declared_symbol():
     # workspace queries are host-only arithmetic
     assert lib.mgb_level_workspace(b"g", 4, 1000) > 0
     assert lib.mgb_level_workspace(b"r", 16, 441000) > 16 * (1 << 19) * 8 * 5
+    assert lib.mgb_launch_count() >= 0  # host counter, no device work
 
 
 def test_workspace_scales_with_level():
