@@ -296,3 +296,49 @@ def test_phase_split_equals_whole_level_calls(dev, tag):
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
     assert Ld.mgb_level_forward_phase(None, 1, stream_ptr()) != 0  # bad argument -> status 1
+
+
+def test_pruning_passes_make_the_oracles_decisions(dev, monkeypatch):
+    """Teacher-forced pruning parity: from the same state, τ and RNG
+    stream, a dry/wet pass and a brute-force pass with device trials produce the same
+    ledger (candidates, accept bits) and survivors as with the float64 oracle's eval_loss;
+    the smallest decision margin |L_a - (L_min + τ)| / τ is reported."""
+    from oracle import mixgraph_oracle as O
+    from paper_2509_15948_b200 import pruning as P
+    from paper_2509_15948_b200.common import rng_for
+    from paper_2509_15948_b200.losses import LossConfig
+    gs = golden("step.npz")
+    graph, params, stems, L = _step_setup()
+    ws = 30000
+    tgt = gs["target"].astype(np.float32)
+    eval_set = P.EvalSet([(stems, tgt[:, ws:])], ws, LossConfig(), device=dev)
+    prep = O.prepare_target(tgt[:, ws:].astype(np.float64), O.LossConfig())
+    oseg = [(stems.astype(np.float64), prep)]
+
+    def oracle_eval(graph, params, mask, eval_set, schedule=None):
+        return O.eval_loss(graph, params.params, params.raw_weights, mask, oseg, ws, O.LossConfig())
+
+    n = len(graph.processor_nodes())
+    la0 = oracle_eval(graph, params, np.ones(n), None)
+    tau = 0.02 * la0
+
+    def run(pass_fn, fn):
+        monkeypatch.setattr(P, "eval_loss", fn)
+        state = P.PruneState(alive=np.ones(n, dtype=bool), la_min=la0, tolerance=tau, iteration=1)
+        mask = pass_fn(state, graph, params, eval_set, np.ones(n), list(range(n)), rng_for(0, "prune-order"))
+        return mask, state.ledger
+
+    margins = []
+    for pass_fn in (P.prune_drywet_pass, P.prune_bruteforce_pass):
+        m_dev, led_dev = run(pass_fn, _device_eval)
+        m_ora, led_ora = run(pass_fn, oracle_eval)
+        assert [(r.candidates, r.accepted) for r in led_dev] == [(r.candidates, r.accepted) for r in led_ora]
+        np.testing.assert_array_equal(m_dev, m_ora)
+        margins += [abs(r.loss - (r.la_min_before + tau)) / tau for r in led_ora]
+        for a, b in zip(led_dev, led_ora):
+            np.testing.assert_allclose(a.loss, b.loss, rtol=1e-5)
+    print(f"pruning parity: {len(margins)} trials, min decision margin {min(margins):.3e} tau")
+
+
+def _device_eval(graph, params, mask, eval_set, schedule=None):
+    return eval_set.engine(graph, params).loss(mask)
