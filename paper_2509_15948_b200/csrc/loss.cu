@@ -150,7 +150,7 @@ __device__ __forceinline__ void load_frame(float2* v, const float* __restrict__ 
       if (valid) {
         long long idx = (long long)f * hop + t - N / 2;
         if (idx < 0 || idx >= Ls) idx = reflect_idx(idx, Ls);
-        const float win = 0.5f - 0.5f * g_tw32[t * (MGB_TW_N / N)].x;  // cos(2 pi t / N)
+        const float win = 0.5f - 0.5f * cospif(2.f * (float)t / (float)N);  // periodic Hann
         z = make_float2(__ldg(xl + idx) * win, __ldg(xr + idx) * win);
       }
       v[i * R + m] = z;
@@ -205,31 +205,48 @@ __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(
   const int f = blockIdx.x * C::FPC + q;
   const bool valid = f < r.frames;
   float2* S = reinterpret_cast<float2*>(smraw) + q * C::PADN;
+  __shared__ int bst[128], blen[128], boff[128];  // band tables (n_mels <= 128)
+  const int nm = r.n_mels;
+  for (int i = threadIdx.x; i < nm; i += C::NT) {
+    bst[i] = r.band_start[i];
+    blen[i] = r.band_len[i];
+    boff[i] = r.band_off[i];
+  }
   float2 v[C::V];
   load_frame<N, 16>(v, xl, xr, Ls, r.hop, f, valid, tt);
-  frame_fft<N, 16, false>(v, S, tt);
+  frame_fft<N, 16, false>(v, S, tt);  // (its barriers publish the band tables)
   mags_inplace<N, 16>(S, tt);
   const float* md = reinterpret_cast<const float*>(S);
-  const int nm = r.n_mels;
   const int g = tt & 3;  // items idx = tt + T i: group idx % 4 (fixed per thread), band idx / 4
   double a0 = 0.0, a1 = 0.0;
   if (valid) {
     for (int idx = tt; idx < 4 * nm; idx += T) {
       const int j = idx >> 2;
-      const int k0 = r.band_start[j], len = r.band_len[j], off = r.band_off[j];
-      const float* mg = md + g * NB + k0;
-      const double* bw = r.band_w + off;
-      double mel = 0.0;
-      for (int i = 0; i < len; ++i) mel = fma((double)mg[i], __ldg(bw + i), mel);
       const size_t o = ((size_t)g * r.frames + f) * nm + j;
+      double tl = 0.0, tm = 0.0;
+      if (mode != 0) {  // issued ahead of the band sum
+        tl = r.tlog[o];
+        tm = r.tmel[o];
+      }
+      const int k0 = bst[j], len = blen[j];
+      const float* mg = md + g * NB + k0;
+      const double* bw = r.band_w + boff[j];
+      double m0 = 0.0, m1 = 0.0;  // two chains for ILP
+      int i = 0;
+      for (; i + 1 < len; i += 2) {
+        m0 = fma((double)mg[i], __ldg(bw + i), m0);
+        m1 = fma((double)mg[i + 1], __ldg(bw + i + 1), m1);
+      }
+      if (i < len) m0 = fma((double)mg[i], __ldg(bw + i), m0);
+      const double mel = m0 + m1;
       if (mode == 0) {
         r.tmel[o] = mel;
         r.tlog[o] = log(mel + LOG_EPS);
         a0 += mel * mel;
       } else {
         r.mel[o] = mel;
-        const double dlog = log(mel + LOG_EPS) - r.tlog[o];
-        const double dm = mel - r.tmel[o];
+        const double dlog = log(mel + LOG_EPS) - tl;
+        const double dm = mel - tm;
         a0 += fabs(dlog);
         a1 += dm * dm;
       }
@@ -381,7 +398,7 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
   if (!valid) return;
   float* gf = r.gframes + (size_t)f * 2 * N;
   for (int t = tt; t < N; t += T) {
-    const float win = 0.5f - 0.5f * g_tw32[t * (MGB_TW_N / N)].x;
+    const float win = 0.5f - 0.5f * cospif(2.f * (float)t / (float)N);
     const float2 z = S[pd16(t)];
     gf[t] = z.x * win;
     gf[N + t] = z.y * win;
