@@ -338,57 +338,90 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_fwd(char tag, const float* const*
 struct DynAcc {
   float T, W, R, w;
 };
-__device__ __forceinline__ void dyn_adjoint(float l, float r, float gl, float gr, float gc, const DynP& q, bool gate,
-                                            float wf, float om, bool bypass, bool acc_on, float& ol, float& orr,
-                                            float& og, DynAcc& A) {
+// Branch-free: the three knee regions are evaluated arithmetically and selected.
+template <bool GATE, bool ACC>
+__device__ __forceinline__ void dyn_adjoint(float l, float r, float gl, float gr, float gc, const DynP& q,
+                                            float wf, float om, bool bypass, float& ol, float& orr, float& og,
+                                            DynAcc& A) {
   const float gcl = fmaxf(gc, 0.f);
   const float G = __logf(gcl + 1e-8f);
   const bool above = G >= q.T + q.W, below = G < q.T - q.W;
-  float Gy, dGu, dT = 0.f, dW = 0.f, dR = 0.f;
-  if (gate) {
-    if (above) { Gy = G; dGu = 1.f; }
-    else if (below) { Gy = q.T + q.R * (G - q.T); dGu = q.R; dT = 1.f - q.R; dR = G - q.T; }
-    else {
-      const float z = G - q.T - q.W, k = 1.f - q.R, zh = z * q.i2W, zq = z * z * q.i4W;
-      Gy = G + k * zq;
-      dGu = 1.f + k * zh;
-      dT = -k * zh;
-      dW = k * (-zh - zq * (4.f * q.i4W));
-      dR = -zq;
-    }
+  const float d = G - q.T;
+  float Gy, dGu, dT, dW, dR;
+  if (GATE) {
+    const float z = d - q.W, k = 1.f - q.R, zh = z * q.i2W, zq = z * z * q.i4W;
+    Gy = G + k * zq;  // knee
+    dGu = fmaf(k, zh, 1.f);
+    dT = -k * zh;
+    dW = k * (-zh - zq * (4.f * q.i4W));
+    dR = -zq;
+    Gy = above ? G : (below ? fmaf(q.R, d, q.T) : Gy);
+    dGu = above ? 1.f : (below ? q.R : dGu);
+    dT = above ? 0.f : (below ? 1.f - q.R : dT);
+    dW = (above || below) ? 0.f : dW;
+    dR = above ? 0.f : (below ? d : dR);
   } else {
-    if (above) {
-      Gy = q.T + (G - q.T) * q.iR;
-      dGu = q.iR;
-      dT = 1.f - q.iR;
-      dR = -(G - q.T) * q.iR * q.iR;
-    } else if (below) { Gy = G; dGu = 1.f; }
-    else {
-      const float z = G - q.T + q.W, k = q.iR - 1.f, zh = z * q.i2W, zq = z * z * q.i4W;
-      Gy = G + k * zq;
-      dGu = 1.f + k * zh;
-      dT = -k * zh;
-      dW = k * (zh - zq * (4.f * q.i4W));
-      dR = -zq * q.iR * q.iR;
-    }
+    const float z = d + q.W, k = q.iR - 1.f, zh = z * q.i2W, zq = z * z * q.i4W;
+    Gy = G + k * zq;  // knee
+    dGu = fmaf(k, zh, 1.f);
+    dT = -k * zh;
+    dW = k * (zh - zq * (4.f * q.i4W));
+    dR = -zq * q.iR * q.iR;
+    Gy = below ? G : (above ? fmaf(d, q.iR, q.T) : Gy);
+    dGu = below ? 1.f : (above ? q.iR : dGu);
+    dT = below ? 0.f : (above ? 1.f - q.iR : dT);
+    dW = (above || below) ? 0.f : dW;
+    dR = below ? 0.f : (above ? -d * q.iR * q.iR : dR);
   }
   const float gain = __expf(Gy - G);
   float dl, dr, ul, ur;
   if (bypass) { dl = dr = 0.f; ul = gl; ur = gr; }
   else {
     dl = wf * gl; dr = wf * gr; ul = om * gl; ur = om * gr;
-    if (acc_on) A.w = fmaf(gl, l * gain - l, fmaf(gr, r * gain - r, A.w));
+    if (ACC) A.w = fmaf(gl, l * gain - l, fmaf(gr, r * gain - r, A.w));
   }
   ol = fmaf(dl, gain, ul);
   orr = fmaf(dr, gain, ur);
   const float D = (dl * l + dr * r) * gain;
-  if (acc_on) {
+  if (ACC) {
     A.T = fmaf(D, dT, A.T);
     A.W = fmaf(D, dW, A.W);
     A.R = fmaf(D, dR, A.R);
   }
   const float dG = D * dGu - D;
   og = (gc > 0.f) ? __fdividef(dG, gcl + 1e-8f) : 0.f;
+}
+
+// phase A of the backward for one chunk (C = 0: this chunk, accumulate and write the
+// elementwise dL/du; C = 1: the next chunk, envelope adjoint only)
+template <bool GATE, int C>
+__device__ __forceinline__ void dyn_phase_a(const float* u, const float* gy, const float* eo, float* go, int L,
+                                            long long c0, bool vec, const DynP& q, float wf, float om, bool bypass,
+                                            float* ds, DynAcc& A) {
+#pragma unroll 2
+  for (int k = 0; k < Q4; ++k) {
+    const int o = 4 * (threadIdx.x + NT * k);
+    const long long n = c0 + (long long)C * CH + o;
+    float4 ul4, ur4, gl4, gr4;
+    load4(u, L, n, vec, ul4, ur4);
+    load4(gy, L, n, vec, gl4, gr4);
+    const float4 ev4 = load4m(eo, L, n, vec);
+    const float U[4] = {ul4.x, ul4.y, ul4.z, ul4.w}, V[4] = {ur4.x, ur4.y, ur4.z, ur4.w};
+    const float GL[4] = {gl4.x, gl4.y, gl4.z, gl4.w}, GR[4] = {gr4.x, gr4.y, gr4.z, gr4.w};
+    const float EV[4] = {ev4.x, ev4.y, ev4.z, ev4.w};
+    float OL[4], OR[4];
+    float* dst = ds + C * SPAD + sidx_n(o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float og;
+      // samples beyond L load as zeros and contribute nothing to the partial sums
+      dyn_adjoint<GATE, C == 0>(U[e], V[e], GL[e], GR[e], EV[e], q, wf, om, bypass, OL[e], OR[e], og, A);
+      dst[e] = og;
+    }
+    if (C == 0)
+      store4(go, L, n, vec, make_float4(OL[0], OL[1], OL[2], OL[3]), make_float4(OR[0], OR[1], OR[2], OR[3]),
+             nullptr, make_float4(0.f, 0.f, 0.f, 0.f));
+  }
 }
 
 struct VW {
@@ -456,7 +489,8 @@ __device__ __forceinline__ void rscan2_excl(VW& a, VW& c, const double* pw, doub
 // dL/du written to gu, T/W/R/w partials), then (B) the truncated reverse scans,
 // dx and r, dL/du += 2 mid dx and the x.dx / x.r partials.  The next chunk's
 // envelope adjoint is recomputed instead of round-tripping dg through HBM.
-__global__ void __launch_bounds__(NT, 2) k_dyn_bwd(char tag, const float* const* __restrict__ u_rows,
+template <bool GATE>
+__global__ void __launch_bounds__(NT, 2) k_dyn_bwd(const float* const* __restrict__ u_rows,
                                                 const float* const* __restrict__ gy_rows,
                                                 const double* __restrict__ bank, const int* __restrict__ prow,
                                                 const int* __restrict__ widx, const double* __restrict__ w,
@@ -473,7 +507,6 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd(char tag, const float* const*
   const float* u = u_rows[b];
   const float* gy = gy_rows[b];
   const DynP q = load_params(bank, prow[b]);
-  const bool gate = tag == 'n';
   const double wv = w ? w[widx[b]] : 1.0;
   const float wf = (float)wv, om = (float)(1.0 - wv);
   const bool bypass = wv == 0.0;
@@ -483,33 +516,8 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd(char tag, const float* const*
   const long long c0 = (long long)j * CH;
   const bool vec = vec_ok(u, L) && vec_ok(gy, L) && vec_ok(eo, L) && vec_ok(go, L);
   DynAcc A{0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-  for (int c = 0; c < 2; ++c) {  // (A) c = 0: this chunk (full), c = 1: next chunk (dg only)
-#pragma unroll 2
-    for (int k = 0; k < Q4; ++k) {
-      const int o = 4 * (threadIdx.x + NT * k);
-      const long long n = c0 + (long long)c * CH + o;
-      float4 ul4, ur4, gl4, gr4;
-      load4(u, L, n, vec, ul4, ur4);
-      load4(gy, L, n, vec, gl4, gr4);
-      const float4 ev4 = load4m(eo, L, n, vec);
-      const float U[4] = {ul4.x, ul4.y, ul4.z, ul4.w}, V[4] = {ur4.x, ur4.y, ur4.z, ur4.w};
-      const float GL[4] = {gl4.x, gl4.y, gl4.z, gl4.w}, GR[4] = {gr4.x, gr4.y, gr4.z, gr4.w};
-      const float EV[4] = {ev4.x, ev4.y, ev4.z, ev4.w};
-      float OL[4], OR[4];
-      float* dst = ds + c * SPAD + sidx_n(o);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float og;
-        dyn_adjoint(U[e], V[e], GL[e], GR[e], EV[e], q, gate, wf, om, bypass, c == 0 && n + e < L, OL[e], OR[e],
-                    og, A);
-        dst[e] = og;
-      }
-      if (c == 0)
-        store4(go, L, n, vec, make_float4(OL[0], OL[1], OL[2], OL[3]), make_float4(OR[0], OR[1], OR[2], OR[3]),
-               nullptr, make_float4(0.f, 0.f, 0.f, 0.f));
-    }
-  }
+  dyn_phase_a<GATE, 0>(u, gy, eo, go, L, c0, vec, q, wf, om, bypass, ds, A);
+  dyn_phase_a<GATE, 1>(u, gy, eo, go, L, c0, vec, q, wf, om, bypass, ds, A);
   {
     double t0 = block_sum((double)A.T, red);
     __syncthreads();
@@ -660,7 +668,8 @@ DynWs dcarve(A& a, int B, int L) {
 
 int mgb_dyn_init() {
   cudaFuncSetAttribute(k_dyn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemF);
-  cudaFuncSetAttribute(k_dyn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+  cudaFuncSetAttribute(k_dyn_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+  cudaFuncSetAttribute(k_dyn_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -686,8 +695,9 @@ int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st) {
   const int B = lv->B, L = lv->L, nch = nchunks(L);
   MgbArena a{(char*)lv->ws, 0};
   DynWs w = dcarve(a, B, L);
-  mgb_launch(k_dyn_bwd, dim3(nch, B), dim3(NT), kDynSmem, st, lv->tag, lv->u_rows, lv->gy_rows, lv->bank, lv->prow,
-             lv->widx, lv->w, lv->aux, lv->gu, w.part, L, nch);
+  auto kern = lv->tag == 'n' ? k_dyn_bwd<true> : k_dyn_bwd<false>;
+  mgb_launch(kern, dim3(nch, B), dim3(NT), kDynSmem, st, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx,
+             lv->w, lv->aux, lv->gu, w.part, L, nch);
   MGB_CHECK_LAUNCH();
   mgb_launch(k_dyn_final, dim3(B), dim3(256), 0, st, w.part, nch, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,
              lv->gw, w.part);
