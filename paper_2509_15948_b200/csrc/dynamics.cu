@@ -82,18 +82,18 @@ __device__ __forceinline__ double powseg(const double* pw, int k) {
 }
 
 // gain-computer G_y (mg/processors.py:217-232), float32
-__device__ __forceinline__ float knee_gy(float G, const DynP& q, bool gate) {
+template <bool GATE>
+__device__ __forceinline__ float knee_gy(float G, const DynP& q) {
   const bool above = G >= q.T + q.W, below = G < q.T - q.W;
-  if (gate) {
-    if (above) return G;
-    if (below) return q.T + q.R * (G - q.T);
-    const float z = G - q.T - q.W;
-    return G + (1.f - q.R) * (z * z * q.i4W);
+  const float d = G - q.T;
+  if (GATE) {
+    const float z = d - q.W;
+    const float knee = G + (1.f - q.R) * (z * z * q.i4W);
+    return above ? G : (below ? fmaf(q.R, d, q.T) : knee);
   }
-  if (above) return q.T + (G - q.T) * q.iR;
-  if (below) return G;
-  const float z = G - q.T + q.W;
-  return G + (q.iR - 1.f) * (z * z * q.i4W);
+  const float z = d + q.W;
+  const float knee = G + (q.iR - 1.f) * (z * z * q.i4W);
+  return below ? G : (above ? fmaf(d, q.iR, q.T) : knee);
 }
 
 __device__ __forceinline__ float env_log(float gc) { return __logf(fmaxf(gc, 0.f) + 1e-8f); }
@@ -237,7 +237,8 @@ __device__ __forceinline__ float4 load4m(const float* d, int L, long long n, boo
   return make_float4(a[0], a[1], a[2], a[3]);
 }
 
-__global__ void __launch_bounds__(NT, 2) k_dyn_fwd(char tag, const float* const* __restrict__ u_rows,
+template <bool GATE>
+__global__ void __launch_bounds__(NT, 2) k_dyn_fwd(const float* const* __restrict__ u_rows,
                                                 const double* __restrict__ bank, const int* __restrict__ prow,
                                                 const int* __restrict__ widx, const double* __restrict__ w,
                                                 float* __restrict__ env, float* __restrict__ y, int L) {
@@ -252,7 +253,6 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_fwd(char tag, const float* const*
   const int j = blockIdx.x, b = blockIdx.y;
   const float* u = u_rows[b];
   const DynP q = load_params(bank, prow[b]);
-  const bool gate = tag == 'n';
   init_pw(pw, q.la);
   const long long c0 = (long long)j * CH;
   const bool vec = vec_ok(u, L);
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_fwd(char tag, const float* const*
     yc = fma(q.a, yc, xd[sidx(threadIdx.x, i)]);
     const float gc = (float)(q.b * yc);
     const float G = env_log(gc);
-    eg[sidx(threadIdx.x, i)] = make_float2(gc, __expf(knee_gy(G, q, gate) - G));
+    eg[sidx(threadIdx.x, i)] = make_float2(gc, __expf(knee_gy<GATE>(G, q) - G));
   }
   __syncthreads();
   const double wv = w ? w[widx[b]] : 1.0;
@@ -667,7 +667,8 @@ DynWs dcarve(A& a, int B, int L) {
 }  // namespace
 
 int mgb_dyn_init() {
-  cudaFuncSetAttribute(k_dyn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemF);
+  cudaFuncSetAttribute(k_dyn_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemF);
+  cudaFuncSetAttribute(k_dyn_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemF);
   cudaFuncSetAttribute(k_dyn_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
   cudaFuncSetAttribute(k_dyn_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
@@ -684,7 +685,8 @@ int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st) {
   const int B = lv->B, L = lv->L, nch = nchunks(L);
   MgbArena a{(char*)lv->ws, 0};
   DynWs w = dcarve(a, B, L);
-  mgb_launch(k_dyn_fwd, dim3(dim3(nch, B)), dim3(NT), kDynSmemF, st, lv->tag, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w,
+  auto kern = lv->tag == 'n' ? k_dyn_fwd<true> : k_dyn_fwd<false>;
+  mgb_launch(kern, dim3(dim3(nch, B)), dim3(NT), kDynSmemF, st, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w,
                                                  lv->aux, lv->y, L);
   MGB_CHECK_LAUNCH();
   return 0;
