@@ -447,9 +447,9 @@ struct Conv2 {
   static int prep(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
     const dim3 gc(N2 / G::TC, lv->B), gr(G::ROW_CTAS, lv->B);
     const int fir_rows = (int)((g.M + N2 - 1) / N2);
-    mgb_launch(fs2::k_colA<N1, LdFir>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, LdFir{w.hbuf, g.M}, w.Ah, fir_rows < N1 ? fir_rows : N1);
+    mgb_launch(fs2::k_colA<N1, LdFir>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, LdFir{w.hbuf, g.M}, w.Ah, fir_rows < N1 ? fir_rows : N1, 0);
     MGB_CHECK_LAUNCH();
-    mgb_launch(fs2::k_rowH<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWH_SMEM, st, w.Ah, w.H);
+    mgb_launch(fs2::k_rowH<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWH_SMEM, st, w.Ah, w.H, 1);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -458,12 +458,12 @@ struct Conv2 {
     const int B = lv->B, L = lv->L;
     const dim3 gc(N2 / G::TC, B), gr(G::ROW_CTAS, B);
     const int x_rows = (int)((L + N2 - 1) / N2);
-    mgb_launch(fs2::k_colA<N1, LdRows>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1);
+    mgb_launch(fs2::k_colA<N1, LdRows>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1, 0);
     MGB_CHECK_LAUNCH();
-    mgb_launch(fs2::k_rowF<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWF_SMEM, st, w.Ax, w.H, w.X, w.Bo);
+    mgb_launch(fs2::k_rowF<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWF_SMEM, st, w.Ax, w.H, w.X, w.Bo, 1);
     MGB_CHECK_LAUNCH();
     EpFwd ep{lv->u_rows, lv->widx, lv->w, lv->y, lv->ybar, w.part, L, g.off};
-    mgb_launch(fs2::k_colC<N1, EpFwd>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, ep, 1.f / (float)G::N, N1);
+    mgb_launch(fs2::k_colC<N1, EpFwd>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, ep, 1.f / (float)G::N, N1, 0);
     MGB_CHECK_LAUNCH();
     mgb_launch(k_gs_norms, dim3(B), dim3(256), 0, st, w.part, G::NBLK, w.stats, lv->reg);
     MGB_CHECK_LAUNCH();
@@ -475,17 +475,17 @@ struct Conv2 {
     const dim3 gc(N2 / G::TC, B), gr(G::ROW_CTAS, B);
     LdBwdPro ld{lv->u_rows, lv->gy_rows, lv->ybar, lv->widx, lv->w, lv->greg, w.stats, lv->gu, w.part, L, g.off};
     const int g_rows = (int)((g.off + L + N2 - 1) / N2);
-    mgb_launch(fs2::k_colA<N1, LdBwdPro>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, ld, w.Ax, g_rows < N1 ? g_rows : N1);
+    mgb_launch(fs2::k_colA<N1, LdBwdPro>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, ld, w.Ax, g_rows < N1 ? g_rows : N1, 1);
     MGB_CHECK_LAUNCH();
     mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, G::NBLK, lv->widx, lv->w, lv->gw);
     MGB_CHECK_LAUNCH();
-    mgb_launch(fs2::k_rowG<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWG_SMEM, st, w.Ax, w.X, w.H, w.Bo, w.Ah);
+    mgb_launch(fs2::k_rowG<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWG_SMEM, st, w.Ax, w.X, w.H, w.Bo, w.Ah, 0);
     MGB_CHECK_LAUNCH();
-    mgb_launch(fs2::k_colC<N1, EpGx>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1);
+    mgb_launch(fs2::k_colC<N1, EpGx>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1, 1);
     MGB_CHECK_LAUNCH();
     const int h_rows = (int)((g.M + N2 - 1) / N2);
     mgb_launch(fs2::k_colC<N1, EpGh>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
-                                                   h_rows < N1 ? h_rows : N1);
+                                                   h_rows < N1 ? h_rows : N1, 1);
     MGB_CHECK_LAUNCH();
     return 0;
   }

@@ -159,7 +159,7 @@ __device__ __forceinline__ void row_fft_compact(float2 (&v)[32], float2* T, int 
 // ---------------------------------------------------------------------------
 // column pass, forward: A[b][k1*N2 + n2] = w_N^{k1 n2} FFT_{N1}(x[. * N2 + n2])
 template <int N1, class Ld>
-__global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colA(Ld ld, float2* __restrict__ A, int nz_rows) {
+__global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colA(Ld ld, float2* __restrict__ A, int nz_rows, int rev) {
   mgb_pdl_entry();
   using g = G<N1>;
   constexpr int Q = g::Q, P = g::P, TC = g::TC, B8 = Q < 8 ? Q : 8;
@@ -167,7 +167,9 @@ __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colA(Ld ld, floa
   float2* sm = reinterpret_cast<float2*>(smraw);
   __shared__ double red[32];
   const int c = threadIdx.x % TC, j = threadIdx.x / TC;
-  const int b = blockIdx.y, col = blockIdx.x * TC + c;
+  // rev: walk the nodes backwards, so the kernel starts on the nodes the previous
+  // kernel touched last (still in L2)
+  const int b = rev ? gridDim.y - 1 - blockIdx.y : blockIdx.y, col = blockIdx.x * TC + c;
   const typename Ld::Ctx ctx = ld.prepare(b);
   float acc = 0.f;
   float2 v[Q];
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colA(Ld ld, floa
 // column pass, inverse: y[b][n1*N2 + n2] = scale * IFFT_{N1}(B[. * N2 + n2]); epilogue consumes y
 template <int N1, class Ep>
 __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colC(const float2* __restrict__ Bb, Ep ep, float scale,
-                                                   int out_rows) {
+                                                   int out_rows, int rev) {
   mgb_pdl_entry();
   using g = G<N1>;
   constexpr int Q = g::Q, P = g::P, TC = g::TC, B8 = Q < 8 ? Q : 8;
@@ -217,7 +219,9 @@ __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colC(const float
   float2* sm = reinterpret_cast<float2*>(smraw);
   __shared__ double red[32];
   const int c = threadIdx.x % TC, j = threadIdx.x / TC;
-  const int b = blockIdx.y, col = blockIdx.x * TC + c;
+  // rev: walk the nodes backwards, so the kernel starts on the nodes the previous
+  // kernel touched last (still in L2)
+  const int b = rev ? gridDim.y - 1 - blockIdx.y : blockIdx.y, col = blockIdx.x * TC + c;
   const float2* src = Bb + (long long)b * g::N + col;
   float2 v[Q];
 #pragma unroll
@@ -297,14 +301,15 @@ __device__ __forceinline__ float2* warp_region(unsigned char* smraw, int w) {
 
 // prep: H[b][row][k] = FFT_{N2}(Ah[b][row][.])  (FIR spectrum, row layout)
 template <int N1>
-__global__ void __launch_bounds__(2 * RP * 32) k_rowH(const float2* __restrict__ Ah, float2* __restrict__ H) {
+__global__ void __launch_bounds__(2 * RP * 32) k_rowH(const float2* __restrict__ Ah, float2* __restrict__ H, int rev) {
   mgb_pdl_entry();
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
   const RowMap rm = row_map<N1>();
   if (!rm.active) return;
   float2* sA = warp_region<ROWH_WARP>(smraw, threadIdx.x >> 5);  // Ah row, then the transpose scratch
-  const long long base = (long long)blockIdx.y * g::N + (long long)rm.row * N2;
+  const int bnode = rev ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
+  const long long base = (long long)bnode * g::N + (long long)rm.row * N2;
   row_prefetch(sA, Ah + base, rm.lane);
   cp_async_wait_all();
   __syncwarp();
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowH(const float2* __restrict__
 // self-paired row computes along but stores nothing.
 template <int N1>
 __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__ Ax, const float2* __restrict__ H,
-                                                     float2* __restrict__ X, float2* __restrict__ Bo) {
+                                                     float2* __restrict__ X, float2* __restrict__ Bo, int rev) {
   mgb_pdl_entry();
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -336,7 +341,8 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__
   const bool self = rm.row == rm.prow;
   float2* pA = self ? sA : warp_region<ROWF_WARP>(smraw, w ^ 1);
   float2* pH = pA + TBUF;
-  const long long base = (long long)blockIdx.y * g::N + (long long)rm.row * N2;
+  const int bnode = rev ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
+  const long long base = (long long)bnode * g::N + (long long)rm.row * N2;
   const int lane = rm.lane;
   row_prefetch(sA, Ax + base, lane);
   row_prefetch(sH, H + base, lane);
@@ -382,7 +388,7 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__
 template <int N1>
 __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__ Ag, const float2* __restrict__ X,
                                                      const float2* __restrict__ H, float2* __restrict__ B1,
-                                                     float2* __restrict__ B2) {
+                                                     float2* __restrict__ B2, int rev) {
   mgb_pdl_entry();
   using g = G<N1>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -395,7 +401,8 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__
   float2* pA = self ? sA : warp_region<ROWG_WARP>(smraw, w ^ 1);
   float2* pX = pA + TBUF;
   float2* pH = pX + N2;
-  const long long base = (long long)blockIdx.y * g::N + (long long)rm.row * N2;
+  const int bnode = rev ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
+  const long long base = (long long)bnode * g::N + (long long)rm.row * N2;
   const int lane = rm.lane;
   row_prefetch(sA, Ag + base, lane);
   row_prefetch(sX, X + base, lane);
