@@ -49,7 +49,8 @@ typedef struct MgbLevel {
   float* ybar;                  /* (B,2,L) wet output (required for e,r,d) */
   float* aux;                   /* c,n: (B,L) envelope store; otherwise unused */
   double* reg;                  /* [B] gain-staging term per row (e,r,d); may be NULL */
-  float* gu;                    /* (B,2,L) dLoss/du (backward) */
+  float* gu;                    /* (B,2,L) dLoss/du (backward); NULL = not requested (a level
+                                   reading only the stems): the input-gradient work is skipped */
   double* gbank;                /* (N_t,P_t) gradient bank; rows prow[] are written */
   double* gw;                   /* [P] dLoss/dw; entries widx[] are written */
   void* ws;                     /* per-level workspace, persistent between fwd and bwd */
@@ -70,8 +71,8 @@ size_t mgb_level_workspace(char tag, int B, int L);
  * also writes ybar / aux / reg as the tag requires. */
 int mgb_level_forward(const MgbLevel* level, void* stream);
 
-/* Backward of one level: consumes gy_rows (and greg), writes gu, gbank rows, gw
- * entries.  Must follow mgb_level_forward on the same workspace. */
+/* Backward of one level: consumes gy_rows (and greg), writes gu (unless NULL),
+ * gbank rows, gw entries.  Must follow mgb_level_forward on the same workspace. */
 int mgb_level_backward(const MgbLevel* level, void* stream);
 
 /* The same two calls split in phases so a caller can overlap the

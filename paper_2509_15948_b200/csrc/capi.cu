@@ -71,7 +71,7 @@ extern "C" int mgb_level_forward_phase(const MgbLevel* lv, int phase, void* stre
 
 extern "C" int mgb_level_backward_phase(const MgbLevel* lv, int phase, void* stream) {
   if (int rc = check_level(lv)) return rc;
-  if (!lv->gy_rows || !lv->gu || !lv->gbank) return 1;
+  if (!lv->gy_rows || !lv->gbank) return 1;  // gu == NULL: the input gradient is not requested
   if (phase != 1 && phase != 2) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   switch (lv->tag) {

@@ -181,7 +181,7 @@ struct LdBwdPro {
     c.u = u_rows[b];
     c.gy = gy_rows[b];
     c.yb = ybar + (size_t)b * 2 * L;
-    c.go = gu + (size_t)b * 2 * L;
+    c.go = gu ? gu + (size_t)b * 2 * L : nullptr;  // null: input gradient not requested
     return c;
   }
   __device__ __forceinline__ Raw fetch(const Ctx& c, int, long long n, bool ok) const {
@@ -216,8 +216,10 @@ struct LdBwdPro {
       ur = c.om * r.gr;
       acc = fmaf(r.gl, r.yl - r.l, fmaf(r.gr, r.yr - r.r, acc));
     }
-    c.go[m] = fmaf(c.cu, mu, ul);
-    c.go[L + m] = fmaf(c.cu, mu, ur);
+    if (c.go) {
+      c.go[m] = fmaf(c.cu, mu, ul);
+      c.go[L + m] = fmaf(c.cu, mu, ur);
+    }
     return make_float2(fmaf(c.cy, my, dl), fmaf(c.cy, my, dr));
   }
   __device__ __forceinline__ void commit(int b, int blk, double t) const { part[((size_t)b * kMaxParts + blk) * 4 + 2] = t; }
@@ -414,8 +416,11 @@ struct Conv {
     MGB_CHECK_LAUNCH();
     mgb_launch(fs::k_rowB_bwd<N1, N2>, dim3(gr), dim3(G::NTR), fs::rowbwd_smem<N1, N2>(), st, w.Ax, w.X, w.H, w.Bo, w.Ah);
     MGB_CHECK_LAUNCH();
-    mgb_launch(fs::k_colC<N1, N2, EpGx>, dim3(gc), dim3(G::NTC), sc, st, w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1);
-    MGB_CHECK_LAUNCH();
+    if (lv->gu) {
+      mgb_launch(fs::k_colC<N1, N2, EpGx>, dim3(gc), dim3(G::NTC), sc, st, w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N,
+                 N1);
+      MGB_CHECK_LAUNCH();
+    }
     const int h_rows = (int)((g.M + N2 - 1) / N2);
     mgb_launch(fs::k_colC<N1, N2, EpGh>, dim3(gc), dim3(G::NTC), sc, st, w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
                                               h_rows < N1 ? h_rows : N1);
@@ -481,8 +486,11 @@ struct Conv2 {
     MGB_CHECK_LAUNCH();
     mgb_launch(fs2::k_rowG<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWG_SMEM, st, w.Ax, w.X, w.H, w.Bo, w.Ah, 0);
     MGB_CHECK_LAUNCH();
-    mgb_launch(fs2::k_colC<N1, EpGx>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, EpGx{lv->gu, L}, 1.f / (float)G::N, N1, 1);
-    MGB_CHECK_LAUNCH();
+    if (lv->gu) {
+      mgb_launch(fs2::k_colC<N1, EpGx>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, EpGx{lv->gu, L},
+                 1.f / (float)G::N, N1, 1);
+      MGB_CHECK_LAUNCH();
+    }
     const int h_rows = (int)((g.M + N2 - 1) / N2);
     mgb_launch(fs2::k_colC<N1, EpGh>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
                                                    h_rows < N1 ? h_rows : N1, 1);

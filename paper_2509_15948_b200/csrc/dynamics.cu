@@ -418,7 +418,7 @@ __device__ __forceinline__ void dyn_phase_a(const float* u, const float* gy, con
       dyn_adjoint<GATE, C == 0>(U[e], V[e], GL[e], GR[e], EV[e], q, wf, om, bypass, OL[e], OR[e], og, A);
       dst[e] = og;
     }
-    if (C == 0)
+    if (C == 0 && go)
       store4(go, L, n, vec, make_float4(OL[0], OL[1], OL[2], OL[3]), make_float4(OR[0], OR[1], OR[2], OR[3]),
              nullptr, make_float4(0.f, 0.f, 0.f, 0.f));
   }
@@ -511,10 +511,10 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd(const float* const* __restric
   const float wf = (float)wv, om = (float)(1.0 - wv);
   const bool bypass = wv == 0.0;
   const float* eo = env + (size_t)b * L;
-  float* go = gu + (size_t)b * 2 * L;
+  float* go = gu ? gu + (size_t)b * 2 * L : nullptr;  // null: input gradient not requested
   init_pw(pw, q.la);
   const long long c0 = (long long)j * CH;
-  const bool vec = vec_ok(u, L) && vec_ok(gy, L) && vec_ok(eo, L) && vec_ok(go, L);
+  const bool vec = vec_ok(u, L) && vec_ok(gy, L) && vec_ok(eo, L) && (!go || vec_ok(go, L));
   DynAcc A{0.f, 0.f, 0.f, 0.f};
   dyn_phase_a<GATE, 0>(u, gy, eo, go, L, c0, vec, q, wf, om, bypass, ds, A);
   dyn_phase_a<GATE, 1>(u, gy, eo, go, L, c0, vec, q, wf, om, bypass, ds, A);
@@ -582,7 +582,8 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd(const float* const* __restric
   for (int kk = 0; kk < 2; ++kk) {
     const long long m = c0 + 4 * (threadIdx.x + NT * (k0 + kk));
     load4(u, L, m, vg, ul[kk], ur[kk]);
-    load4(go, L, m, vg, gl[kk], gr[kk]);
+    if (go) load4(go, L, m, vg, gl[kk], gr[kk]);
+    else gl[kk] = gr[kk] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 #pragma unroll
   for (int kk = 0; kk < 2; ++kk) {
@@ -607,8 +608,9 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd(const float* const* __restric
     }
     sxd += (double)fxd;
     sxr += (double)fxr;
-    store4(go, L, m, vg, make_float4(ol[0], ol[1], ol[2], ol[3]), make_float4(orr[0], orr[1], orr[2], orr[3]),
-           nullptr, make_float4(0.f, 0.f, 0.f, 0.f));
+    if (go)
+      store4(go, L, m, vg, make_float4(ol[0], ol[1], ol[2], ol[3]), make_float4(orr[0], orr[1], orr[2], orr[3]),
+             nullptr, make_float4(0.f, 0.f, 0.f, 0.f));
   }
   }
   sxd = block_sum(sxd, red);

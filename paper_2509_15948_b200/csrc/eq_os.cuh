@@ -264,15 +264,17 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
     }
 #pragma unroll
     for (int r = 0; r < 32; ++r) ps[r * 256] = v[r];
-    const float2* H = Hs + (size_t)b * EOS_N + t;
-    const float sc = 1.f / (float)EOS_N;
+    float* go = gu ? gu + (size_t)b * 2 * L : nullptr;  // null: input gradient not requested (no gx transform)
+    if (go) {
+      const float2* H = Hs + (size_t)b * EOS_N + t;
+      const float sc = 1.f / (float)EOS_N;
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const float2 h = __ldg(H + r * 256);
-      v[r] = make_float2(sc * (v[r].x * h.x + v[r].y * h.y), sc * (v[r].y * h.x - v[r].x * h.y));
+      for (int r = 0; r < 32; ++r) {
+        const float2 h = __ldg(H + r * 256);
+        v[r] = make_float2(sc * (v[r].x * h.x + v[r].y * h.y), sc * (v[r].y * h.x - v[r].x * h.y));
+      }
+      eos_ifft(v, S);
     }
-    eos_ifft(v, S);
-    float* go = gu + (size_t)b * 2 * L;
     float fw = 0.f;
 #pragma unroll
     for (int m0 = 0; m0 < EOS_HOP / 256 + 1; m0 += 5) {  // window indices i < HOP: m <= 24
@@ -292,11 +294,13 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
         const int i = t + 256 * (m0 + q);
         const long long n = n0 + i;
         if (i < EOS_HOP && n < L) {
-          const float2 gx = v[m0 + q];
-          const float mu = uq[q].x + uq[q].y;
-          const float ul = bypass ? gq[q].x : om * gq[q].x, ur = bypass ? gq[q].y : om * gq[q].y;
-          go[n] = fmaf(cu, mu, ul) + gx.x;
-          go[L + n] = fmaf(cu, mu, ur) + gx.y;
+          if (go) {
+            const float2 gx = v[m0 + q];
+            const float mu = uq[q].x + uq[q].y;
+            const float ul = bypass ? gq[q].x : om * gq[q].x, ur = bypass ? gq[q].y : om * gq[q].y;
+            go[n] = fmaf(cu, mu, ul) + gx.x;
+            go[L + n] = fmaf(cu, mu, ur) + gx.y;
+          }
           if (!bypass) fw = fmaf(gq[q].x, gq[q].z - uq[q].x, fmaf(gq[q].y, gq[q].w - uq[q].y, fw));
         }
       }

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(NT) k_gs_bwd(const float* const* __restrict__ 
   const int b = blockIdx.y;
   const float* u = u_rows[b];
   const float* gy = gy_rows[b];
-  float* go = gu + (size_t)b * 2 * L;
+  float* go = gu ? gu + (size_t)b * 2 * L : nullptr;  // null: input gradient not requested
   const double wv = w ? w[widx[b]] : 1.0;
   const bool bypass = (wv == 0.0);
   float c0 = 1.f, c1 = 1.f, k = 0.f, wf = 0.f, om = 0.f;
@@ -175,8 +175,10 @@ __global__ void __launch_bounds__(NT) k_gs_bwd(const float* const* __restrict__ 
         }
       }
     }
-    st4<VEC>(go, n, L, ol);
-    st4<VEC>(go + L, n, L, orr);
+    if (go) {
+      st4<VEC>(go, n, L, ol);
+      st4<VEC>(go + L, n, L, orr);
+    }
   }
   const double t0 = block_sum((double)s0, scratch);
   const double t1 = block_sum((double)s1, scratch);

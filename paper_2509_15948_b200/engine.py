@@ -176,7 +176,8 @@ class RenderPlan:
                 ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
                 ybar = torch.empty((B, 2, L), dtype=F32, device=dev) if tag in "erd" else None
                 aux = torch.empty((B, L), dtype=F32, device=dev) if tag in "cn" else None
-                gu = torch.empty((B, 2, L), dtype=F32, device=dev) if backward else None
+                # dL/du of a level reading only the stems (step 1) has no consumer: not computed
+                gu = torch.empty((B, 2, L), dtype=F32, device=dev) if backward and s > 1 else None
                 self.gus[s] = gu
                 st = MgbLevel()
                 st.tag = tag.encode()
