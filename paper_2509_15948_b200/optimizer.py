@@ -139,6 +139,101 @@ def train_step(graph, params: ParamStore, segment, cfg: TrainConfig, opt: AdamW,
     return values
 
 
+def _pinned_f32(a):
+    t = a if torch.is_tensor(a) else torch.from_numpy(np.ascontiguousarray(a))
+    if t.dtype != F32:
+        t = t.to(dtype=F32)
+    if t.device.type == "cpu" and not t.is_pinned():
+        t = t.pin_memory()
+    return t
+
+
+def train_segments(graph, params: ParamStore, segments, cfg: TrainConfig, opt: AdamW = None,
+                   schedule=None, alpha_p_fn=None, history=None):
+    """One optimiser step per host ``(stems, target)`` segment of an iterable, pipelined.
+
+    The streaming form of ``train_step`` for segments that live on the host
+    (a data loader): segment k+1's host→device copy runs on a copy stream
+    into a staging slot while step k computes, each step's metrics are read
+    back into a pinned ring without stalling the stream, and ``params`` is
+    updated once at the end.  Same arithmetic and per-step semantics as
+    calling ``train_step`` in a loop (mg/optimizer.py:140-186); a non-finite
+    loss leaves that step's update undone on the device and raises
+    ``NonFiniteLoss`` after the run, like ``train``.  Pass pinned torch
+    tensors to avoid a pinning copy per segment."""
+    history = history if history is not None else []
+    it = iter(segments)
+    seg = next(it, None)
+    if seg is None:
+        return history
+    opt = opt or make_optimizer(params, cfg)
+    L = seg[0].shape[-1]
+    eng = opt.engine(graph, L, cfg, schedule)
+    eng.load_params(params)
+    dev = eng.device
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(device=dev)
+    stage = [(torch.empty_like(eng.plan.stems), torch.empty_like(eng.target)) for _ in range(2)]
+    freed = [None, None]  # event: the compute stream is done reading the slot
+
+    def upload(seg, slot):
+        st, tg = _pinned_f32(seg[0]), _pinned_f32(seg[1])
+        if st.shape != eng.plan.stems.shape or tg.shape != eng.target.shape:
+            raise ValueError(f"segment shapes {tuple(st.shape)}, {tuple(tg.shape)} differ from the first")
+        with torch.cuda.stream(copy):
+            if freed[slot] is not None:
+                copy.wait_event(freed[slot])
+            stage[slot][0].copy_(st, non_blocking=True)
+            stage[slot][1].copy_(tg, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        return ev, (st, tg)  # keep the host tensors alive until the copy ran
+
+    ring = torch.zeros((64, 4), dtype=torch.float64).pin_memory()
+    ring_ev = [None] * 64
+    out = []
+    t0 = time.perf_counter()
+    ready, keep = upload(seg, 0)
+    k = 0
+    while seg is not None:
+        slot = k % 2
+        comp.wait_event(ready)
+        eng.plan.stems.copy_(stage[slot][0], non_blocking=True)
+        eng.target.copy_(stage[slot][1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        freed[slot] = ev
+        seg = next(it, None)
+        if seg is not None:
+            nxt = upload(seg, 1 - slot)
+        eng.step_async(alpha_p_fn(k) if alpha_p_fn else 0.0)
+        r = k % 64
+        if ring_ev[r] is not None:
+            ring_ev[r].synchronize()
+            out.append(ring[r].tolist())
+        ring[r].copy_(eng.vals, non_blocking=True)
+        ring_ev[r] = torch.cuda.Event()
+        ring_ev[r].record(comp)
+        if seg is not None:
+            ready, keep = nxt
+        k += 1
+    for j in range(k - min(k, 64), k):
+        r = j % 64
+        ring_ev[r].synchronize()
+        out.append(ring[r].tolist())
+    del keep
+    wall = (time.perf_counter() - t0) / k
+    opt.t = eng.t
+    eng.store_params(params)
+    base = len(history)
+    for i, v in enumerate(out):
+        if not np.isfinite(v[0]):
+            raise NonFiniteLoss(f"non-finite loss at step {i}: {v}")
+        history.append({"loss": v[0], "L_a": v[1], "L_g": v[2], "L_p": v[3], "step": base + i,
+                        "wall_s": wall})
+    return history
+
+
 def train(graph, params: ParamStore, session: Session, cfg: TrainConfig, schedule=None,
           alpha_p_fn=None, rng=None, history=None, device="cuda"):
     """Optimise params in place for cfg.steps (mg/optimizer.py:196-216)."""

@@ -124,6 +124,30 @@ def test_public_train_step_two_steps(dev):
         np.testing.assert_allclose(params.params[t], gs[f"after2_{t}"], atol=5e-3)
 
 
+def test_train_segments_equals_train_step_loop(dev):
+    """The pipelined segment trainer makes exactly the updates of a train_step loop."""
+    from paper_2509_15948_b200.optimizer import TrainConfig, make_optimizer, train_segments, train_step
+    gs = golden("step.npz")
+    graph, params, stems, L = _step_setup()
+    rng = np.random.default_rng(3)
+    segs = [(stems * (1.0 + 0.1 * i), gs["target"] + 0.01 * rng.standard_normal(gs["target"].shape))
+            for i in range(5)]
+    segs = [(torch.from_numpy(s.astype(np.float32)).pin_memory(), torch.from_numpy(t.astype(np.float32)))
+            for s, t in segs]
+    cfg = TrainConfig(segment_seconds=L / 30000, steps=1)
+    p_loop, p_pipe = params.copy(), params.copy()
+    opt = make_optimizer(p_loop, cfg)
+    loop = [train_step(graph, p_loop, s, cfg, opt) for s in segs]
+    pipe = train_segments(graph, p_pipe, segs, cfg, make_optimizer(p_pipe, cfg))
+    assert len(pipe) == len(loop)
+    for a, b in zip(loop, pipe):
+        for key in ("loss", "L_a", "L_g", "L_p"):
+            assert a[key] == b[key], key
+    for t in "gsecnrd":
+        np.testing.assert_array_equal(p_loop.params[t], p_pipe.params[t])
+    np.testing.assert_array_equal(p_loop.raw_weights, p_pipe.raw_weights)
+
+
 def _random_console(rng, kmax=4, prune=0.0):
     from paper_2509_15948_b200.console import SessionManifest, TrackEntry, build_console
     from paper_2509_15948_b200.graph import PARAM_COUNTS, ParamStore, bypass_remove
