@@ -77,8 +77,9 @@ int mgb_level_backward(const MgbLevel* level, void* stream);
 
 /* The same two calls split in phases so a caller can overlap the
  * parameter-only work with other levels on a second stream:
- *   forward  phase 1: FIR synthesis and FIR spectra (e, r, d; depends on
- *                     bank/prow only; no-op for g, s, c, n);
+ *   forward  phase 1: FIR synthesis and FIR spectra (e, r, d), ballistics
+ *                     parameter blocks (c, n); depends on bank/prow only;
+ *                     no-op for g, s;
  *            phase 2: the signal pass (everything else).
  *   backward phase 1: the signal adjoint: gu, gw, and the FIR gradient kept in
  *                     the workspace (all of the backward for g, s, c, n);

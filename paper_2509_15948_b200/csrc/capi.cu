@@ -64,7 +64,7 @@ extern "C" int mgb_level_forward_phase(const MgbLevel* lv, int phase, void* stre
     case 'r':
     case 'd': return phase == 1 ? mgb_conv_prepare(lv, st) : mgb_conv_forward(lv, st);
     case 'c':
-    case 'n': return phase == 2 ? mgb_dyn_forward(lv, st) : 0;
+    case 'n': return phase == 1 ? mgb_dyn_prepare(lv, st) : mgb_dyn_forward(lv, st);
     default: return 1;
   }
 }

@@ -66,6 +66,22 @@ __device__ __forceinline__ DynP load_params(const double* bank, int row) {
   return q;
 }
 
+// per-node parameter block, computed once per forward by k_dyn_pre (forward
+// phase 1, params only) so the signal kernels' CTAs do not each redo the
+// float64 softplus/exp chains before issuing their loads
+struct DynPre {
+  DynP q;
+  double pw[NPW];  // a^(SEG * 2^i)
+};
+
+__global__ void k_dyn_pre(const double* __restrict__ bank, const int* __restrict__ prow, DynPre* __restrict__ pre) {
+  mgb_pdl_entry();
+  const int b = blockIdx.x;
+  const DynP q = load_params(bank, prow[b]);
+  if (threadIdx.x == 0) pre[b].q = q;
+  if (threadIdx.x < NPW) pre[b].pw[threadIdx.x] = exp((double)SEG * (double)(1 << threadIdx.x) * q.la);
+}
+
 __device__ __forceinline__ float mid_sq(const float* u, int L, long long n) {
   if (n < 0 || n >= L) return 0.f;
   const float m = __ldg(u + n) + __ldg(u + L + n);
@@ -156,8 +172,8 @@ __device__ __forceinline__ void scan1_excl(double& v0, const double* pw, double*
   v0 = fma(sh[wid], powseg(pw, lane), p0);
 }
 
-__device__ __forceinline__ void init_pw(double* pw, double la) {
-  if (threadIdx.x < NPW) pw[threadIdx.x] = exp((double)SEG * (double)(1 << threadIdx.x) * la);
+__device__ __forceinline__ void init_pw(double* pw, const DynPre& p) {
+  if (threadIdx.x < NPW) pw[threadIdx.x] = p.pw[threadIdx.x];
 }
 
 // padded segment-major staging index: thread t's sample i of a chunk
@@ -239,7 +255,7 @@ __device__ __forceinline__ float4 load4m(const float* d, int L, long long n, boo
 
 template <bool GATE>
 __global__ void __launch_bounds__(NT, 2) k_dyn_fwd(const float* const* __restrict__ u_rows,
-                                                const double* __restrict__ bank, const int* __restrict__ prow,
+                                                const DynPre* __restrict__ pre,
                                                 const int* __restrict__ widx, const double* __restrict__ w,
                                                 float* __restrict__ env, float* __restrict__ y, int L) {
   mgb_pdl_entry();
@@ -252,8 +268,8 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_fwd(const float* const* __restric
   __shared__ double red[32];
   const int j = blockIdx.x, b = blockIdx.y;
   const float* u = u_rows[b];
-  const DynP q = load_params(bank, prow[b]);
-  init_pw(pw, q.la);
+  const DynP q = pre[b].q;
+  init_pw(pw, pre[b]);
   const long long c0 = (long long)j * CH;
   const bool vec = vec_ok(u, L);
   {  // coalesced staging of x' = mid^2 - a^C mid_prev^2 (float64), two float4 groups at a time
@@ -492,7 +508,7 @@ __device__ __forceinline__ void rscan2_excl(VW& a, VW& c, const double* pw, doub
 template <bool GATE>
 __global__ void __launch_bounds__(NT, 2) k_dyn_bwd(const float* const* __restrict__ u_rows,
                                                 const float* const* __restrict__ gy_rows,
-                                                const double* __restrict__ bank, const int* __restrict__ prow,
+                                                const DynPre* __restrict__ pre,
                                                 const int* __restrict__ widx, const double* __restrict__ w,
                                                 const float* __restrict__ env, float* __restrict__ gu,
                                                 double* __restrict__ part, int L, int nch) {
@@ -506,13 +522,13 @@ __global__ void __launch_bounds__(NT, 2) k_dyn_bwd(const float* const* __restric
   const int j = blockIdx.x, b = blockIdx.y;
   const float* u = u_rows[b];
   const float* gy = gy_rows[b];
-  const DynP q = load_params(bank, prow[b]);
+  const DynP q = pre[b].q;
   const double wv = w ? w[widx[b]] : 1.0;
   const float wf = (float)wv, om = (float)(1.0 - wv);
   const bool bypass = wv == 0.0;
   const float* eo = env + (size_t)b * L;
   float* go = gu ? gu + (size_t)b * 2 * L : nullptr;  // null: input gradient not requested
-  init_pw(pw, q.la);
+  init_pw(pw, pre[b]);
   const long long c0 = (long long)j * CH;
   const bool vec = vec_ok(u, L) && vec_ok(gy, L) && vec_ok(eo, L) && (!go || vec_ok(go, L));
   DynAcc A{0.f, 0.f, 0.f, 0.f};
@@ -657,12 +673,14 @@ __global__ void k_dyn_final(const double* __restrict__ part0, int nblk0, int nch
 int nchunks(int L) { return (L + CH - 1) / CH; }
 struct DynWs {
   double* part;  // [B][nch][8]: T, W, R, w partials (phase A) and x.dx, x.r (phase B) per chunk
+  DynPre* pre;   // [B]
 };
 
 template <class A>
 DynWs dcarve(A& a, int B, int L) {
   DynWs w;
   w.part = a.template take<double>((size_t)B * nchunks(L) * 8);
+  w.pre = a.template take<DynPre>((size_t)B);
   return w;
 }
 
@@ -682,14 +700,24 @@ size_t mgb_dyn_workspace(char, int B, int L) {
   return a.off;
 }
 
+// forward phase 1 (params only): the per-node parameter blocks
+int mgb_dyn_prepare(const MgbLevel* lv, cudaStream_t st) {
+  const int B = lv->B, L = lv->L;
+  MgbArena a{(char*)lv->ws, 0};
+  DynWs w = dcarve(a, B, L);
+  mgb_launch(k_dyn_pre, dim3(B), dim3(32), 0, st, lv->bank, lv->prow, w.pre);
+  MGB_CHECK_LAUNCH();
+  return 0;
+}
+
 int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st) {
   if (!lv->aux) return 1;
   const int B = lv->B, L = lv->L, nch = nchunks(L);
   MgbArena a{(char*)lv->ws, 0};
   DynWs w = dcarve(a, B, L);
   auto kern = lv->tag == 'n' ? k_dyn_fwd<true> : k_dyn_fwd<false>;
-  mgb_launch(kern, dim3(dim3(nch, B)), dim3(NT), kDynSmemF, st, lv->u_rows, lv->bank, lv->prow, lv->widx, lv->w,
-                                                 lv->aux, lv->y, L);
+  mgb_launch(kern, dim3(dim3(nch, B)), dim3(NT), kDynSmemF, st, lv->u_rows, (const DynPre*)w.pre, lv->widx, lv->w,
+             lv->aux, lv->y, L);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -700,7 +728,7 @@ int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st) {
   MgbArena a{(char*)lv->ws, 0};
   DynWs w = dcarve(a, B, L);
   auto kern = lv->tag == 'n' ? k_dyn_bwd<true> : k_dyn_bwd<false>;
-  mgb_launch(kern, dim3(nch, B), dim3(NT), kDynSmem, st, lv->u_rows, lv->gy_rows, lv->bank, lv->prow, lv->widx,
+  mgb_launch(kern, dim3(nch, B), dim3(NT), kDynSmem, st, lv->u_rows, lv->gy_rows, (const DynPre*)w.pre, lv->widx,
              lv->w, lv->aux, lv->gu, w.part, L, nch);
   MGB_CHECK_LAUNCH();
   mgb_launch(k_dyn_final, dim3(B), dim3(256), 0, st, w.part, nch, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,

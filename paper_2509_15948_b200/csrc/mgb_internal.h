@@ -25,6 +25,7 @@ size_t mgb_conv_workspace(char tag, int B, int L);
 int mgb_conv_init();
 int mgb_loss_init();
 int mgb_dyn_init();
+int mgb_dyn_prepare(const MgbLevel* lv, cudaStream_t st);
 int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st);
 int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_dyn_workspace(char tag, int B, int L);

@@ -259,7 +259,8 @@ class RenderPlan:
         self.stems.copy_(t.to(dtype=F32), non_blocking=True)
 
     def prepare(self, side=None):
-        """Forward phase 1 of every e/r/d level (FIR synthesis; params only).
+        """Forward phase 1 of every e/r/d/c/n level (FIR synthesis, ballistics
+        parameter blocks; params only).
 
         With ``side`` (a torch stream) the work is enqueued there and one event
         per level is returned for ``forward`` to wait on; else it runs inline."""
@@ -268,14 +269,14 @@ class RenderPlan:
         if side is None:
             sp = stream_ptr()
             for lv in self.levels:
-                if lv.struct is not None and lv.tag in "erd":
+                if lv.struct is not None and lv.tag in "erdcn":
                     check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 1, sp), f"level {lv.tag} prepare")
             return events
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             sp = stream_ptr()
             for lv in self.levels:
-                if lv.struct is not None and lv.tag in "erd":
+                if lv.struct is not None and lv.tag in "erdcn":
                     check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 1, sp), f"level {lv.tag} prepare")
                     ev = torch.cuda.Event()
                     ev.record(side)
