@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=24)
+    ap.add_argument("--e2e-steps", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tracks", type=int, default=K_TRACKS)
     ap.add_argument("--subgroups", type=int, default=S_GROUPS)
@@ -335,6 +335,8 @@ def main():
             "e2e": {"value": e2e_val, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "paper_2509_15948_b200.train_segments (pinned host stems/target per step, "
                            "H2D overlapped with the previous step)",
+                    "steps": args.e2e_steps, "includes": "engine param load, first (unoverlapped) upload, "
+                    "final param read-back",
                     "train_step_sync": sync_val},
             "gpu_launches": eng.launches_per_step() * args.steps,
             "clocks": clk.summary(),
