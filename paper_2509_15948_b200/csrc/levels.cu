@@ -14,7 +14,10 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int KP = 4;      // partial slots per CTA
-constexpr int VPT = 4;     // float4 (or scalar groups of 4) per thread per channel
+#ifndef MGB_GS_VPT
+#define MGB_GS_VPT 2
+#endif
+constexpr int VPT = MGB_GS_VPT;  // float4 (or scalar groups of 4) per thread per channel
 constexpr int CHUNK = NT * VPT * 4;  // samples per channel per CTA
 
 __host__ __device__ inline int simple_nblk(int L) {

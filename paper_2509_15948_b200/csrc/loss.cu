@@ -323,6 +323,9 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
   const bool valid = f < r.frames;
   float2* S = reinterpret_cast<float2*>(smraw) + q * C::PADN;
   const int nm = r.n_mels;
+  float2 v[C::V];
+  // the frame's global loads go out first; the dmel prologue's loads overlap them
+  load_frame<N, 8>(v, xl, xr, Ls, r.hop, f, valid, tt);
   if (valid) {
     for (int idx = tt; idx < 4 * nm; idx += T) {
       const int g = idx / nm, j = idx % nm;
@@ -345,8 +348,6 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
       dmel[q][g][j] = (float)(L.group_w[g] * v);
     }
   }
-  float2 v[C::V];
-  load_frame<N, 8>(v, xl, xr, Ls, r.hop, f, valid, tt);
   frame_fft<N, 8, false>(v, S, tt);  // (its barriers also publish dmel)
   float2 dl[PER], dr[PER];
 #pragma unroll
