@@ -281,6 +281,21 @@ def main():
     sync_val = world / float(e2e_t[1].item())
     e2e_t = e2e_t[:1]
     e2e_val = world * args.e2e_steps / float(e2e_t.item())
+    # one pruning trial (masked forward-only render + MRSTFT, mg/pruning.py:115-123) on the
+    # same clip: the forward-only r/d levels take the cluster overlap-save path
+    from paper_2509_15948_b200.engine import EvalEngine
+    ev = EvalEngine(graph, [(stems, target)], WARMUP, cfg.loss, device=dev, params=params)
+    mask = np.ones(eng.layout.P)
+    for _ in range(3):
+        ev.run_async(mask)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        ev.run_async(mask)
+    e1.record()
+    torch.cuda.synchronize()
+    trial_ms = e0.elapsed_time(e1) / 20
     lay = eng.layout
     # per step: its segment and the 8 step scalars in, the 4 metrics out (params move once per run)
     h2d = stems.nbytes + target.nbytes + 8 * 8
@@ -338,6 +353,7 @@ def main():
                     "steps": args.e2e_steps, "includes": "engine param load, first (unoverlapped) upload, "
                     "final param read-back",
                     "train_step_sync": sync_val},
+            "eval_trial_ms": trial_ms,
             "gpu_launches": eng.launches_per_step() * args.steps,
             "clocks": clk.summary(),
             "roofline": roof,

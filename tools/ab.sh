@@ -14,7 +14,7 @@ for v in base paper_2509_15948_b200/variants/*.so; do
     python - gpurun_out/ab_bench_${name}_$rep.log $name <<'PY'
 import json,sys
 d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); lv=d["levels_ms"]
-print("  %-8s value=%.1f  " % (sys.argv[2], d["value"]) + " ".join("%s=%.4f" % (k.split("@")[0]+k.split("B=")[1][:-1], v) for k, v in lv.items()))
+print("  %-8s value=%.1f trial=%.3f " % (sys.argv[2], d["value"], d.get("eval_trial_ms", 0)) + " ".join("%s=%.4f" % (k.split("@")[0]+k.split("B=")[1][:-1], v) for k, v in lv.items()))
 PY
   done
 done

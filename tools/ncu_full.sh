@@ -9,7 +9,7 @@ for spec in "$@"; do
   [[ "$spec" == *:* ]] && skip=${spec##*:}
   rep=/tmp/ncu_${k}_${skip}
   timeout 600 ncu --set full --import-source on --clock-control none -k "regex:$k" --launch-skip "$skip" -c 1 \
-    -o "$rep" -f python bench.py --eager-profile 1 > "gpurun_out/ncu_${k}.log" 2>&1
+    -o "$rep" -f ${NCU_CMD:-python bench.py --eager-profile 1} > "gpurun_out/ncu_${k}.log" 2>&1
   echo "$k rc=$?"
   ncu -i "$rep.ncu-rep" --page details > "gpurun_out/ncu_${k}_${skip}.txt" 2>&1
   ncu -i "$rep.ncu-rep" --page raw --csv > "gpurun_out/ncu_${k}_${skip}_raw.csv" 2>&1
