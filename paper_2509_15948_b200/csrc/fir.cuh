@@ -173,8 +173,18 @@ __global__ void __launch_bounds__(NT) k_dly_place(const float* __restrict__ colo
   __shared__ float col[2][MGB_DLY_TAPS][MGB_COLOR_LEN];
   __shared__ int dd[2][MGB_DLY_TAPS];
   const int b = blockIdx.y;
-  for (int i = threadIdx.x; i < 2 * MGB_DLY_TAPS * MGB_COLOR_LEN; i += NT)
-    (&col[0][0][0])[i] = colour[(size_t)b * 2 * MGB_DLY_TAPS * MGB_COLOR_LEN + i];
+  {
+    constexpr int CN = 2 * MGB_DLY_TAPS * MGB_COLOR_LEN, IT = (CN + NT - 1) / NT;
+    float cv[IT];
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int i = threadIdx.x + k * NT;
+      cv[k] = i < CN ? __ldg(colour + (size_t)b * CN + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < IT; ++k)
+      if (threadIdx.x + k * NT < CN) (&col[0][0][0])[threadIdx.x + k * NT] = cv[k];
+  }
   for (int i = threadIdx.x; i < 2 * MGB_DLY_TAPS; i += NT) (&dd[0][0])[i] = offs[(size_t)b * 2 * MGB_DLY_TAPS + i];
   __syncthreads();
   float2* h = H + (size_t)b * N;
@@ -217,9 +227,21 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
   const int tap = blockIdx.x, ch = blockIdx.y, b = blockIdx.z;
   const float2* g = GH + (size_t)b * N;
   const int base = tap * MGB_DLY_WIN;
-  for (int i = threadIdx.x; i < MGB_DLY_WIN + MGB_COLOR_LEN - 1; i += NT) {
-    const float2 v = g[base + i];
-    seg[i] = ch == 0 ? v.x : v.y;
+  {  // all loads in flight at once (a rolled loop waits on each in turn)
+    constexpr int SEGN = MGB_DLY_WIN + MGB_COLOR_LEN - 1, IT = (SEGN + NT - 1) / NT;
+    float sv[IT];
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int i = threadIdx.x + k * NT;
+      sv[k] = 0.f;
+      if (i < SEGN) {
+        const float2 v = __ldg(g + base + i);
+        sv[k] = ch == 0 ? v.x : v.y;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < IT; ++k)
+      if (threadIdx.x + k * NT < SEGN) seg[threadIdx.x + k * NT] = sv[k];
   }
   if (threadIdx.x < MGB_COLOR_LEN)
     col[threadIdx.x] = colour[(((size_t)b * 2 + ch) * MGB_DLY_TAPS + tap) * MGB_COLOR_LEN + threadIdx.x];
@@ -279,9 +301,9 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
       const double nr = 1.0 - (double)n * (zm_r * wr + zm_i * wi) + (double)(n - 1) * zn_r;
       const double ni = -(double)n * (zm_i * wr - zm_r * wi) + (double)(n - 1) * zn_i;
       const double dr = ar * ar - ai * ai, di = 2.0 * ar * ai;  // (1 - q)^2
-      const double den = dr * dr + di * di;
-      fr = (nr * dr + ni * di) / den;
-      fi = (ni * dr - nr * di) / den;
+      const double iden = 1.0 / (dr * dr + di * di);
+      fr = (nr * dr + ni * di) * iden;
+      fi = (ni * dr - nr * di) * iden;
     } else {  // q ~ 1: Horner on the series
       fr = (double)(n - 1);
       fi = 0.0;
@@ -292,7 +314,8 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
       }
     }
     // deriv_t = w^t f / n
-    const double der = (wr * fr - wi * fi) / (double)n, dei = (wr * fi + wi * fr) / (double)n;
+    constexpr double inv_n = 1.0 / (double)n;
+    const double der = (wr * fr - wi * fi) * inv_n, dei = (wr * fi + wi * fr) * inv_n;
     sre += (double)et * der;
     sim += (double)et * dei;
     const double nw = wr * sr - wi * si;

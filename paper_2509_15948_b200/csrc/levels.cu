@@ -192,19 +192,21 @@ __global__ void __launch_bounds__(NT) k_gs_bwd(const float* const* __restrict__ 
   }
 }
 
-// one warp per row: deterministic fixed-order float64 sum of the CTA partials
+// one CTA per row: deterministic fixed-order float64 sum of the CTA partials
 __global__ void k_gs_finalize(char tag, const double* __restrict__ part, int nblk, const double* __restrict__ bank,
                               const int* __restrict__ prow, const int* __restrict__ widx,
                               const double* __restrict__ w, double* __restrict__ gbank, double* __restrict__ gw) {
   mgb_pdl_entry();
+  __shared__ double red[32];
   const int b = blockIdx.x;
   double s0 = 0.0, s1 = 0.0;
-  for (int i = threadIdx.x; i < nblk; i += 32) {
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
     s0 += part[((size_t)b * nblk + i) * KP];
     s1 += part[((size_t)b * nblk + i) * KP + 1];
   }
-  s0 = warp_sum(s0);
-  s1 = warp_sum(s1);
+  s0 = block_sum(s0, red);
+  __syncthreads();
+  s1 = block_sum(s1, red);
   if (threadIdx.x != 0) return;
   const double wv = w ? w[widx[b]] : 1.0;
   if (tag == 'g') {
@@ -293,7 +295,7 @@ int mgb_simple_backward(const MgbLevel* lv, cudaStream_t st) {
   else { if (vec) LAUNCH('s', true); else LAUNCH('s', false); }
 #undef LAUNCH
   MGB_CHECK_LAUNCH();
-  mgb_launch(k_gs_finalize, dim3(lv->B), dim3(32), 0, st, lv->tag, part, nblk, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,
+  mgb_launch(k_gs_finalize, dim3(lv->B), dim3(256), 0, st, lv->tag, part, nblk, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,
                                       lv->gw);
   MGB_CHECK_LAUNCH();
   return 0;
