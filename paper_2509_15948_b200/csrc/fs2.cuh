@@ -66,6 +66,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 // one warp copies a row of N2 float2 (8 KB) into shared memory, 16 B per request
 __device__ __forceinline__ void row_prefetch(float2* dst, const float2* __restrict__ src, int lane) {
 #pragma unroll
@@ -345,8 +348,10 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__
   const long long base = (long long)bnode * g::N + (long long)rm.row * N2;
   const int lane = rm.lane;
   row_prefetch(sA, Ax + base, lane);
-  row_prefetch(sH, H + base, lane);
-  cp_async_wait_all();
+  cp_async_commit();
+  row_prefetch(sH, H + base, lane);  // not needed before the product: its latency hides behind the FFT
+  cp_async_commit();
+  cp_async_wait<1>();
   __syncwarp();
   float2 v[32];
 #pragma unroll
@@ -361,6 +366,7 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__
       if (rm.active) X[base + lane + 32 * ka] = v[ka];
       sA[lane + 32 * ka] = v[ka];  // natural order for the partner warp
     }
+    cp_async_wait<0>();  // own H row landed (the barrier publishes it to the partner)
     __syncthreads();
 #pragma unroll
     for (int ka = 0; ka < 32; ++ka) {
@@ -405,9 +411,11 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__
   const long long base = (long long)bnode * g::N + (long long)rm.row * N2;
   const int lane = rm.lane;
   row_prefetch(sA, Ag + base, lane);
-  row_prefetch(sX, X + base, lane);
+  cp_async_commit();
+  row_prefetch(sX, X + base, lane);  // X and H are first read after the G transform
   row_prefetch(sH, H + base, lane);
-  cp_async_wait_all();
+  cp_async_commit();
+  cp_async_wait<1>();
   __syncwarp();
   float2 v[32];
 #pragma unroll
@@ -419,6 +427,7 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__
     if (pass == 0) {
 #pragma unroll
       for (int ka = 0; ka < 32; ++ka) sA[lane + 32 * ka] = v[ka];
+      cp_async_wait<0>();  // own X and H rows landed (the barrier publishes them to the partner)
       __syncthreads();
     } else {
 #pragma unroll
