@@ -78,6 +78,32 @@ def gather_results(results, rank, world, dist=None):
     return sorted(merged, key=lambda r: r["song"])
 
 
+DESK_SEGMENT = 57_000  # samples (1.9 "s" at the reference's 30 kHz constants)
+
+
+def desk_prune_config(seed, iterations=12):
+    """The reference README's desk search (pkg/README.md:54-58): console 600 steps, 12 hybrid
+    rounds, 50 fine-tune steps, 1.9 s segments, 4 eval segments of 1.9 s, tolerance 0.02 relative."""
+    from .optimizer import TrainConfig
+    from .pruning import PruneConfig
+    seg = DESK_SEGMENT / 30_000
+    return PruneConfig(tolerance_relative=0.02, mode="hybrid", iterations=iterations, seed=seed,
+                       console_steps=600, finetune_steps=50, eval_segments=4, eval_segment_seconds=seg,
+                       train=TrainConfig(segment_seconds=seg, warmup_seconds=1.0, seed=seed))
+
+
+def search_song(spec, graph, params, stems, target, iterations=12, device="cuda"):
+    """One song's full pruning search (``prune_song``) with the desk recipe; a JSON-able summary."""
+    from .optimizer import Session
+    from .pruning import prune_song
+    t0 = time.perf_counter()
+    _, _, _, rep, _ = prune_song(graph, params, Session(stems, target), desk_prune_config(spec.index, iterations),
+                                 device=device)
+    return {"song": spec.index, "tracks": spec.tracks, "subgroups": spec.subgroups,
+            "search_s": time.perf_counter() - t0, "trials": rep.trial_count,
+            "pruning_ratio": rep.pruning_ratio, "console_loss": rep.console_loss, "final_loss": rep.final_loss}
+
+
 def songs_per_hour(results, wall_s):
     return len(results) / max(wall_s, 1e-9) * 3600.0
 
@@ -87,4 +113,4 @@ def spec_dict(spec):
 
 
 __all__ = ["SongSpec", "song_costs", "assign_lpt", "desk_specs", "run_rank", "gather_results",
-           "songs_per_hour", "spec_dict", "np"]
+           "songs_per_hour", "spec_dict", "desk_prune_config", "search_song", "DESK_SEGMENT", "np"]
