@@ -57,6 +57,25 @@ def ensure_device(device) -> torch.device:
     return dev
 
 
+def capture_graph(body, device):
+    """Capture ``body`` into a CUDA graph on a side stream.
+
+    torch.cuda.graph's context manager empties the device and pinned-host caches
+    before every capture (~60 ms each); a pruning search re-captures its engines
+    every round, so capture here without that."""
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream(device=device)
+    s.wait_stream(torch.cuda.current_stream(device))
+    with torch.cuda.stream(s):
+        g.capture_begin()
+        try:
+            body()
+        finally:
+            g.capture_end()
+    torch.cuda.current_stream(device).wait_stream(s)
+    return g
+
+
 def stream_ptr():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -557,11 +576,7 @@ class TrainEngine:
                 self.v.copy_(snap[2])
             torch.cuda.current_stream().wait_stream(s)
             torch.cuda.synchronize(self.device)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._body()
-            self._graph = g
-            torch.cuda.synchronize(self.device)
+            self._graph = capture_graph(self._body, self.device)
         self._graph.replay()
 
     def read_values(self):
@@ -626,10 +641,7 @@ class EvalEngine:
                 self._body()
             torch.cuda.current_stream().wait_stream(s)
             torch.cuda.synchronize(self.device)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._body()
-            self._graph = g
+            self._graph = capture_graph(self._body, self.device)
         self._graph.replay()
 
     def loss(self, mask) -> float:
