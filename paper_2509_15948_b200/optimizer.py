@@ -25,6 +25,9 @@ from .losses import LossConfig
 from .schedule import plan_indices, schedule_for
 
 
+GRAPH_MIN_STEPS = 200  # train() captures its step only for runs at least this long
+
+
 class SongTooShort(Exception):
     pass
 
@@ -82,12 +85,12 @@ class AdamW:
         self.device = device
         self._engines = {}
 
-    def engine(self, graph: MixGraph, L: int, cfg: TrainConfig, schedule=None) -> TrainEngine:
-        key = (id(graph), graph.node_types, graph.edges, int(L), int(cfg.warmup_len), cfg.loss)
+    def engine(self, graph: MixGraph, L: int, cfg: TrainConfig, schedule=None, use_graph=True) -> TrainEngine:
+        key = (id(graph), graph.node_types, graph.edges, int(L), int(cfg.warmup_len), cfg.loss, bool(use_graph))
         eng = self._engines.get(key)
         if eng is None:
             ecfg = _EngineCfg(self, cfg)
-            eng = TrainEngine(graph, L, ecfg, device=self.device, schedule=schedule)
+            eng = TrainEngine(graph, L, ecfg, device=self.device, schedule=schedule, use_graph=use_graph)
             self._engines = {key: eng}  # one live engine per optimiser
         eng.cfg = _EngineCfg(self, cfg)
         return eng
@@ -250,7 +253,8 @@ def train(graph, params: ParamStore, session: Session, cfg: TrainConfig, schedul
     if cfg.steps <= 0:
         return history
     dev = ensure_device(device)
-    eng = opt.engine(graph, seg, cfg, schedule)
+    # a short run (a fine-tune round) is as fast eager as replayed: skip the capture
+    eng = opt.engine(graph, seg, cfg, schedule, use_graph=cfg.steps >= GRAPH_MIN_STEPS)
     eng.load_params(params)
     full = session.length == seg
     st_dev = torch.as_tensor(np.asarray(session.stems), dtype=F32).to(dev)
