@@ -288,10 +288,27 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
   sincospi(2.0 * (double)t0 / (double)n, &wi, &wr);
   sincospi(2.0 / (double)n, &si, &sr);
   double sre = 0.0, sim = 0.0;
-  for (int t = t0; t < t0 + PER && t < n; ++t) {
-    float et = 0.f;
+  // e_t for this thread's run from a register window of seg (one shared-memory read
+  // per sample and per colour tap instead of two per multiply-add; same summation order)
+  float et[PER];
+  {
+    constexpr int WIN = PER + MGB_COLOR_LEN - 1, SEGN = MGB_DLY_WIN + MGB_COLOR_LEN - 1;
+    float win[WIN];
 #pragma unroll
-    for (int j = 0; j < MGB_COLOR_LEN; ++j) et = fmaf(seg[t + j], col[j], et);
+    for (int i = 0; i < WIN; ++i) win[i] = (t0 + i < SEGN) ? seg[t0 + i] : 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) et[i] = 0.f;
+#pragma unroll
+    for (int j = 0; j < MGB_COLOR_LEN; ++j) {
+      const float c = col[j];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) et[i] = fmaf(win[i + j], c, et[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int t = t0 + i;
+    if (t >= n) break;
     // q = z w^t
     const double qr = zr * wr - zi * wi, qi = zr * wi + zi * wr;
     const double ar = 1.0 - qr, ai = -qi;  // 1 - q
@@ -316,8 +333,8 @@ __global__ void __launch_bounds__(NT) k_dly_bwd(const double* __restrict__ bank,
     // deriv_t = w^t f / n
     constexpr double inv_n = 1.0 / (double)n;
     const double der = (wr * fr - wi * fi) * inv_n, dei = (wr * fi + wi * fr) * inv_n;
-    sre += (double)et * der;
-    sim += (double)et * dei;
+    sre += (double)et[i] * der;
+    sim += (double)et[i] * dei;
     const double nw = wr * sr - wi * si;
     wi = wr * si + wi * sr;
     wr = nw;
