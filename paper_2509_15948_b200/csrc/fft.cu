@@ -22,15 +22,14 @@ __device__ float2 g_tw32[MGB_TW_N];
 __device__ double2 g_tw64[MGB_TW_N];
 __device__ float2 g_fs_lo[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
 __device__ float2 g_fs_hi[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
-// FIR-synthesis tables (float64): cos(2 pi j / n) and the symmetric Hann of n = 2047 (EQ) / 39 (colour)
-__device__ double g_cos2047[MGB_EQ_LEN], g_hann2047[MGB_EQ_LEN];
+// FIR-synthesis tables (float64): the symmetric Hann of n = 2047 (EQ); cos(2 pi j / n) and Hann of n = 39 (colour)
+__device__ double g_hann2047[MGB_EQ_LEN];
 __device__ double g_cos39[MGB_COLOR_LEN], g_hann39[MGB_COLOR_LEN];
 
 __global__ void k_init_fir_tables() {
   mgb_pdl_entry();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < MGB_EQ_LEN) {
-    g_cos2047[j] = cospi(2.0 * j / (double)MGB_EQ_LEN);
     g_hann2047[j] = 0.5 - 0.5 * cospi(2.0 * j / (double)(MGB_EQ_LEN - 1));
   }
   if (j < MGB_COLOR_LEN) {

@@ -8,23 +8,25 @@ __global__ void __launch_bounds__(256) k_eq_fir(const double* __restrict__ bank,
                                                 float2* __restrict__ H) {
   mgb_pdl_entry();
   __shared__ double X[MGB_EQ_BINS];
-  __shared__ double ct[MGB_EQ_LEN];
   __shared__ double part[8][33];
   const int b = blockIdx.y;
   const double* p = bank + (size_t)prow[b] * MGB_EQ_BINS;
   for (int k = threadIdx.x; k < MGB_EQ_BINS; k += 256) X[k] = exp(p[k]);
-  for (int j = threadIdx.x; j < MGB_EQ_LEN; j += 256) ct[j] = g_cos2047[j];
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tp = blockIdx.x * 32 + lane;
   const int t = (tp + 1024) % MGB_EQ_LEN;
   const int k0 = 1 + w * 128, k1 = min(MGB_EQ_BINS, k0 + 128);
-  double acc = 0.0;
-  int idx = (int)(((long long)k0 * t) % MGB_EQ_LEN);
+  // cos(2 pi k t / n) by a float64 rotation recurrence from an exactly reduced start
+  // (per-lane table lookups at scattered indices were shared-memory bound)
+  double acc = 0.0, cr, ci, sr, si;
+  sincospi(2.0 * (double)(((long long)k0 * t) % MGB_EQ_LEN) / (double)MGB_EQ_LEN, &ci, &cr);
+  sincospi(2.0 * (double)t / (double)MGB_EQ_LEN, &si, &sr);
   for (int k = k0; k < k1; ++k) {
-    acc = fma(X[k], ct[idx], acc);
-    idx += t;
-    if (idx >= MGB_EQ_LEN) idx -= MGB_EQ_LEN;
+    acc = fma(X[k], cr, acc);
+    const double nr = cr * sr - ci * si;
+    ci = fma(cr, si, ci * sr);
+    cr = nr;
   }
   part[w][lane] = acc;
   __syncthreads();
@@ -44,25 +46,25 @@ __global__ void __launch_bounds__(256) k_eq_fir_bwd(const double* __restrict__ b
                                                     double* __restrict__ gbank) {
   mgb_pdl_entry();
   __shared__ double dh[MGB_EQ_LEN];
-  __shared__ double ct[MGB_EQ_LEN];
   __shared__ double part[8][33];
   const int b = blockIdx.y;
   const float2* g = GH + (size_t)b * M;
   for (int tp = threadIdx.x; tp < MGB_EQ_LEN; tp += 256) {
     const float2 v = g[tp];
     dh[(tp + 1024) % MGB_EQ_LEN] = ((double)v.x + (double)v.y) * g_hann2047[tp];
-    ct[tp] = g_cos2047[tp];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int k = blockIdx.x * 32 + lane;
   const int t0 = w * 256, t1 = min(MGB_EQ_LEN, t0 + 256);
-  double acc = 0.0;
-  int idx = (int)(((long long)k * t0) % MGB_EQ_LEN);
+  double acc = 0.0, cr, ci, sr, si;  // rotation recurrence, as in k_eq_fir
+  sincospi(2.0 * (double)(((long long)k * t0) % MGB_EQ_LEN) / (double)MGB_EQ_LEN, &ci, &cr);
+  sincospi(2.0 * (double)k / (double)MGB_EQ_LEN, &si, &sr);
   for (int t = t0; t < t1; ++t) {
-    acc = fma(dh[t], ct[idx], acc);
-    idx += k;
-    if (idx >= MGB_EQ_LEN) idx -= MGB_EQ_LEN;
+    acc = fma(dh[t], cr, acc);
+    const double nr = cr * sr - ci * si;
+    ci = fma(cr, si, ci * sr);
+    cr = nr;
   }
   part[w][lane] = acc;
   __syncthreads();
