@@ -473,9 +473,11 @@ class TrainEngine:
         plan, lp = self.plan, self.lossp
         Ld = lib()
         main, side = torch.cuda.current_stream(), self.side
-        # side stream: FIR syntheses (params only), then the target spectra
+        # side stream: FIR syntheses (params only), the warm-up part of dL/dy (read by the
+        # level backward; the loss backward writes the rest), then the target spectra
         prepared = plan.prepare(side)
         with torch.cuda.stream(side):
+            plan.dY[:, :ws].zero_()
             lp.target(ptr(self.target, ws), ptr(self.target, L + ws))
             tev = torch.cuda.Event()
             tev.record(side)
@@ -483,15 +485,18 @@ class TrainEngine:
         y = plan.y
         main.wait_event(tev)
         lp.forward(ptr(y, ws), ptr(y, L + ws))
-        reg = plan.reg_total()
-        if P:
-            check(Ld.mgb_sparsity(ptr(self.params, self.layout.w_off), P, ptr(self.sparsity), stream_ptr()),
-                  "mgb_sparsity")
-        ap = self.scalars[7]
-        total = lp.loss + reg * float(self.cfg.loss.gain_staging_weight) + \
-            torch.where(ap > 0, ap * self.sparsity, torch.zeros_like(ap))
-        torch.stack([total, lp.loss, reg, self.sparsity], out=self.vals)
-        plan.dY[:, :ws].zero_()
+        # loss assembly (read by the optimiser step only) on the side stream, off the path
+        # from the loss forward into the backward sweep
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            reg = plan.reg_total()
+            if P:
+                check(Ld.mgb_sparsity(ptr(self.params, self.layout.w_off), P, ptr(self.sparsity), stream_ptr()),
+                      "mgb_sparsity")
+            ap = self.scalars[7]
+            total = lp.loss + reg * float(self.cfg.loss.gain_staging_weight) + \
+                torch.where(ap > 0, ap * self.sparsity, torch.zeros_like(ap))
+            torch.stack([total, lp.loss, reg, self.sparsity], out=self.vals)
         lp.backward(ptr(y, ws), ptr(y, L + ws), ptr(plan.dY, ws), ptr(plan.dY, L + ws))
         plan.backward(side)
         main.wait_stream(side)
