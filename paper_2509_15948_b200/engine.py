@@ -601,8 +601,10 @@ class EvalEngine:
         self.graph = graph
         self.layout = lay = ParamLayout(graph)
         self.params = torch.zeros(lay.n, dtype=F64, device=dev)
+        self._packed = None      # host copy of the loaded parameter vector
+        self._prep_dirty = True  # FIR syntheses / ballistics blocks stale (eager mode)
         if params is not None:
-            self.params.copy_(torch.from_numpy(lay.pack(params)))
+            self.load_params(params)
         L = segments[0][0].shape[-1]
         self.L, self.ws = L, int(warmup_len)
         self.plan = RenderPlan(graph, None, L, dev, self.params, None, lay, backward=False)
@@ -621,11 +623,20 @@ class EvalEngine:
         self._graph = None
 
     def load_params(self, params):
-        self.params.copy_(torch.from_numpy(self.layout.pack(params)))
+        packed = self.layout.pack(params)
+        if self._packed is not None and np.array_equal(packed, self._packed):
+            return  # a pruning pass evaluates many masks on the same parameters
+        self._packed = packed.copy()
+        self.params.copy_(torch.from_numpy(packed))
+        self._prep_dirty = True
 
     def _body(self):
         L, ws = self.L, self.ws
-        self.plan.prepare()  # FIR syntheses once per trial, shared by all segments
+        # FIR syntheses (parameters only) shared by all segments; an eager engine redoes
+        # them only when the parameters changed (a captured graph always includes them)
+        if self.use_graph or self._prep_dirty:
+            self.plan.prepare()
+            self._prep_dirty = False
         for i, stems in enumerate(self.seg_stems):
             self.plan.stems.copy_(stems)
             self.plan.forward(use_mask=True, prepared=True)
