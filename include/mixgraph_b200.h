@@ -81,9 +81,12 @@ int mgb_level_backward(const MgbLevel* level, void* stream);
  *                     parameter blocks (c, n); depends on bank/prow only;
  *                     no-op for g, s;
  *            phase 2: the signal pass (everything else).
- *   backward phase 1: the signal adjoint: gu, gw, and the FIR gradient kept in
- *                     the workspace (all of the backward for g, s, c, n);
- *            phase 2: the FIR adjoint into gbank (e, r, d; no-op otherwise).
+ *   backward phase 1: the signal adjoint gu, plus the per-CTA parameter
+ *                     partials and (e, r, d) the FIR gradient, kept in the
+ *                     workspace;
+ *            phase 2: everything written to gbank and gw: the per-node
+ *                     reductions of those partials and the FIR adjoint (e, r, d).
+ *                     Nothing downstream of the level's gu needs it.
  * mgb_level_forward == phase 1 then 2 on one stream; likewise backward.
  * Within one level the phases must be ordered (1 before 2, forward before
  * backward); phase 2 of the backward may run concurrently with other levels. */

@@ -76,12 +76,12 @@ extern "C" int mgb_level_backward_phase(const MgbLevel* lv, int phase, void* str
   cudaStream_t st = (cudaStream_t)stream;
   switch (lv->tag) {
     case 'g':
-    case 's': return phase == 1 ? mgb_simple_backward(lv, st) : 0;
+    case 's': return phase == 1 ? mgb_simple_backward(lv, st) : mgb_simple_param_grad(lv, st);
     case 'e':
     case 'r':
     case 'd': return phase == 1 ? mgb_conv_backward(lv, st) : mgb_conv_param_grad(lv, st);
     case 'c':
-    case 'n': return phase == 1 ? mgb_dyn_backward(lv, st) : 0;
+    case 'n': return phase == 1 ? mgb_dyn_backward(lv, st) : mgb_dyn_param_grad(lv, st);
     default: return 1;
   }
 }

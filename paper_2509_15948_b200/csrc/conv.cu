@@ -365,6 +365,7 @@ constexpr int kDlyBwdSmem = 0;
 template <int N1, int N2>
 struct Conv {
   using G = fs::Geo<N1, N2>;
+  static constexpr int DW_NBLK = N2 / G::TC;  // column CTAs per node = dw partial slots
   static void attrs() {
     const int sc = (int)fs::col_smem<N1, N2>(), sr = (int)fs::row_smem<N1, N2>();
     cudaFuncSetAttribute(fs::k_colA<N1, N2, LdRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
@@ -412,8 +413,6 @@ struct Conv {
     const int g_rows = (int)((g.off + L + N2 - 1) / N2);
     mgb_launch(fs::k_colA<N1, N2, LdBwdPro>, dim3(gc), dim3(G::NTC), sc, st, ld, w.Ax, g_rows < N1 ? g_rows : N1);
     MGB_CHECK_LAUNCH();
-    mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, N2 / G::TC, lv->widx, lv->w, lv->gw);
-    MGB_CHECK_LAUNCH();
     mgb_launch(fs::k_rowB_bwd<N1, N2>, dim3(gr), dim3(G::NTR), fs::rowbwd_smem<N1, N2>(), st, w.Ax, w.X, w.H, w.Bo, w.Ah);
     MGB_CHECK_LAUNCH();
     if (lv->gu) {
@@ -434,6 +433,7 @@ template <int N1>
 struct Conv2 {
   using G = fs2::G<N1>;
   static constexpr int N2 = fs2::N2;
+  static constexpr int DW_NBLK = G::NBLK;  // column CTAs per node = dw partial slots
   static void attrs() {
     const int sc = (int)G::COL_SMEM;
     if (sc > 0) {
@@ -482,8 +482,6 @@ struct Conv2 {
     const int g_rows = (int)((g.off + L + N2 - 1) / N2);
     mgb_launch(fs2::k_colA<N1, LdBwdPro>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, ld, w.Ax, g_rows < N1 ? g_rows : N1, 1);
     MGB_CHECK_LAUNCH();
-    mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, G::NBLK, lv->widx, lv->w, lv->gw);
-    MGB_CHECK_LAUNCH();
     mgb_launch(fs2::k_rowG<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWG_SMEM, st, w.Ax, w.X, w.H, w.Bo, w.Ah, 0);
     MGB_CHECK_LAUNCH();
     if (lv->gu) {
@@ -513,6 +511,18 @@ int conv_fwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cu
     MGB_CONV_SIZES_OLD(X)
 #undef X
     default: return 1;
+  }
+}
+
+int conv_dw_nblk(const ConvGeom& g) {
+  switch (g.logN) {
+#define X(l, a) case l: return Conv2<a>::DW_NBLK;
+    MGB_CONV_SIZES(X)
+#undef X
+#define X(l, a, b) case l: return Conv<a, b>::DW_NBLK;
+    MGB_CONV_SIZES_OLD(X)
+#undef X
+    default: return 0;
   }
 }
 
@@ -626,8 +636,6 @@ int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st) {
     mgb_launch(k_eqos_bwd, dim3(dim3(nb, B)), dim3(EOS_NT), kEosSmem1, st, lv->u_rows, lv->gy_rows, lv->ybar, w.Hs, lv->widx, lv->w,
                                                        lv->greg, w.stats, lv->gu, w.part, w.pspec, L, nb);
     MGB_CHECK_LAUNCH();
-    mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, nb, lv->widx, lv->w, lv->gw);
-    MGB_CHECK_LAUNCH();
     return 0;
   }
   return conv_bwd_dispatch(lv, w, g, st);
@@ -640,6 +648,10 @@ int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st) {
   const ConvGeom g = geom(tag, L);
   MgbArena a{(char*)lv->ws, 0};
   const ConvWs w = carve_into(a, tag, B, L);
+  // dL/dw from the backward prologue's per-CTA partials (phase 1)
+  mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, tag == 'e' ? eos_nblk(L) : conv_dw_nblk(g), lv->widx,
+             lv->w, lv->gw);
+  MGB_CHECK_LAUNCH();
   if (tag == 'e') {
     mgb_launch(k_eqos_csum, dim3(dim3(EOS_N / 256, B)), dim3(256), 0, st, w.pspec, eos_nblk(L), w.csum);
     MGB_CHECK_LAUNCH();

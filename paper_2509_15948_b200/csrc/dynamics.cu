@@ -731,6 +731,14 @@ int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st) {
   mgb_launch(kern, dim3(nch, B), dim3(NT), kDynSmem, st, lv->u_rows, lv->gy_rows, (const DynPre*)w.pre, lv->widx,
              lv->w, lv->aux, lv->gu, w.part, L, nch);
   MGB_CHECK_LAUNCH();
+  return 0;
+}
+
+// backward phase 2: per-node reductions into gbank / gw
+int mgb_dyn_param_grad(const MgbLevel* lv, cudaStream_t st) {
+  const int B = lv->B, L = lv->L, nch = nchunks(L);
+  MgbArena a{(char*)lv->ws, 0};
+  DynWs w = dcarve(a, B, L);
   mgb_launch(k_dyn_final, dim3(B), dim3(256), 0, st, w.part, nch, nch, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,
              lv->gw, w.part);
   MGB_CHECK_LAUNCH();

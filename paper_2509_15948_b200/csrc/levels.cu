@@ -295,8 +295,15 @@ int mgb_simple_backward(const MgbLevel* lv, cudaStream_t st) {
   else { if (vec) LAUNCH('s', true); else LAUNCH('s', false); }
 #undef LAUNCH
   MGB_CHECK_LAUNCH();
+  return 0;
+}
+
+// backward phase 2: per-row reductions into gbank / gw
+int mgb_simple_param_grad(const MgbLevel* lv, cudaStream_t st) {
+  const int nblk = simple_nblk(lv->L);
+  const double* part = reinterpret_cast<const double*>(lv->ws);
   mgb_launch(k_gs_finalize, dim3(lv->B), dim3(256), 0, st, lv->tag, part, nblk, lv->bank, lv->prow, lv->widx, lv->w, lv->gbank,
-                                      lv->gw);
+             lv->gw);
   MGB_CHECK_LAUNCH();
   return 0;
 }

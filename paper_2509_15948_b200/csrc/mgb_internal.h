@@ -16,6 +16,7 @@ int mgb_spec_pair(const float2* Z, const float2* H, float2* Q, const float2* C, 
 // level implementations (levels.cu / conv.cu / dynamics.cu)
 int mgb_simple_forward(const MgbLevel* lv, cudaStream_t st);
 int mgb_simple_backward(const MgbLevel* lv, cudaStream_t st);
+int mgb_simple_param_grad(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_simple_workspace(char tag, int B, int L);
 int mgb_conv_prepare(const MgbLevel* lv, cudaStream_t st);
 int mgb_conv_forward(const MgbLevel* lv, cudaStream_t st);
@@ -28,6 +29,7 @@ int mgb_dyn_init();
 int mgb_dyn_prepare(const MgbLevel* lv, cudaStream_t st);
 int mgb_dyn_forward(const MgbLevel* lv, cudaStream_t st);
 int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st);
+int mgb_dyn_param_grad(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_dyn_workspace(char tag, int B, int L);
 
 // host-side launch counter (mgb_launch_count); every launch site bumps it

@@ -328,9 +328,10 @@ class RenderPlan:
         return self.reg.sum()
 
     def backward(self, side=None):
-        """Reverse level sweep.  With ``side`` the FIR adjoints (backward phase 2)
-        run there, overlapping the following levels; the caller must join
-        (``current_stream().wait_stream(side)``) before reading the e/r/d grads."""
+        """Reverse level sweep.  With ``side`` each level's parameter-gradient phase
+        (backward phase 2: gbank / gw reductions, FIR adjoints) runs there,
+        overlapping the following levels; the caller must join
+        (``current_stream().wait_stream(side)``) before reading the gradients."""
         L = lib()
         sp = stream_ptr()
         main = torch.cuda.current_stream()
@@ -339,7 +340,7 @@ class RenderPlan:
                 check(L.mgb_bus_sum(ptr(src), ptr(off), ptr(buf), 1, self.L, sp), "fan-out sum")
             if lv.struct is None:
                 continue
-            if side is None or lv.tag not in "erd":
+            if side is None:
                 check(L.mgb_level_backward(ctypes.byref(lv.struct), sp), f"level {lv.tag} backward")
                 continue
             check(L.mgb_level_backward_phase(ctypes.byref(lv.struct), 1, sp), f"level {lv.tag} backward")
