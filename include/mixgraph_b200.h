@@ -80,14 +80,17 @@ int mgb_level_backward(const MgbLevel* level, void* stream);
  *   forward  phase 1: FIR synthesis and FIR spectra (e, r, d), ballistics
  *                     parameter blocks (c, n); depends on bank/prow only;
  *                     no-op for g, s;
- *            phase 2: the signal pass (everything else).
+ *            phase 2: the signal pass: y and ybar;
+ *            phase 3: the gain-staging norms and term (reg) of e, r, d, read by
+ *                     the backward and by the caller's reg (no-op otherwise;
+ *                     a forward-only caller that ignores reg may skip it).
  *   backward phase 1: the signal adjoint gu, plus the per-CTA parameter
  *                     partials and (e, r, d) the FIR gradient, kept in the
  *                     workspace;
  *            phase 2: everything written to gbank and gw: the per-node
  *                     reductions of those partials and the FIR adjoint (e, r, d).
  *                     Nothing downstream of the level's gu needs it.
- * mgb_level_forward == phase 1 then 2 on one stream; likewise backward.
+ * mgb_level_forward == phases 1, 2, 3 on one stream; mgb_level_backward == 1, 2.
  * Within one level the phases must be ordered (1 before 2, forward before
  * backward); phase 2 of the backward may run concurrently with other levels. */
 int mgb_level_forward_phase(const MgbLevel* level, int phase, void* stream);

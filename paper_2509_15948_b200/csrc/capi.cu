@@ -55,16 +55,16 @@ static int check_level(const MgbLevel* lv) {
 
 extern "C" int mgb_level_forward_phase(const MgbLevel* lv, int phase, void* stream) {
   if (int rc = check_level(lv)) return rc;
-  if (phase != 1 && phase != 2) return 1;
+  if (phase < 1 || phase > 3) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   switch (lv->tag) {
     case 'g':
     case 's': return phase == 2 ? mgb_simple_forward(lv, st) : 0;
     case 'e':
     case 'r':
-    case 'd': return phase == 1 ? mgb_conv_prepare(lv, st) : mgb_conv_forward(lv, st);
+    case 'd': return phase == 1 ? mgb_conv_prepare(lv, st) : (phase == 2 ? mgb_conv_forward(lv, st) : mgb_conv_norms(lv, st));
     case 'c':
-    case 'n': return phase == 1 ? mgb_dyn_prepare(lv, st) : mgb_dyn_forward(lv, st);
+    case 'n': return phase == 1 ? mgb_dyn_prepare(lv, st) : (phase == 2 ? mgb_dyn_forward(lv, st) : 0);
     default: return 1;
   }
 }
@@ -87,8 +87,9 @@ extern "C" int mgb_level_backward_phase(const MgbLevel* lv, int phase, void* str
 }
 
 extern "C" int mgb_level_forward(const MgbLevel* lv, void* stream) {
-  if (int rc = mgb_level_forward_phase(lv, 1, stream)) return rc;
-  return mgb_level_forward_phase(lv, 2, stream);
+  for (int ph = 1; ph <= 3; ++ph)
+    if (int rc = mgb_level_forward_phase(lv, ph, stream)) return rc;
+  return 0;
 }
 
 extern "C" int mgb_level_backward(const MgbLevel* lv, void* stream) {

@@ -400,8 +400,6 @@ struct Conv {
     EpFwd ep{lv->u_rows, lv->widx, lv->w, lv->y, lv->ybar, w.part, L, g.off};
     mgb_launch(fs::k_colC<N1, N2, EpFwd>, dim3(gc), dim3(G::NTC), sc, st, w.Bo, ep, 1.f / (float)G::N, N1);
     MGB_CHECK_LAUNCH();
-    mgb_launch(k_gs_norms, dim3(B), dim3(256), 0, st, w.part, N2 / G::TC, w.stats, lv->reg);
-    MGB_CHECK_LAUNCH();
     return 0;
   }
 
@@ -469,8 +467,6 @@ struct Conv2 {
     MGB_CHECK_LAUNCH();
     EpFwd ep{lv->u_rows, lv->widx, lv->w, lv->y, lv->ybar, w.part, L, g.off};
     mgb_launch(fs2::k_colC<N1, EpFwd>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, ep, 1.f / (float)G::N, N1, 0);
-    MGB_CHECK_LAUNCH();
-    mgb_launch(k_gs_norms, dim3(B), dim3(256), 0, st, w.part, G::NBLK, w.stats, lv->reg);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -616,11 +612,22 @@ int mgb_conv_forward(const MgbLevel* lv, cudaStream_t st) {
     mgb_launch(k_eqos_fwd, dim3(dim3(nb, B)), dim3(EOS_NT), kEosSmem1, st, lv->u_rows, w.Hs, lv->widx, lv->w, lv->y, lv->ybar, w.part,
                                                        L);
     MGB_CHECK_LAUNCH();
-    mgb_launch(k_gs_norms, dim3(B), dim3(256), 0, st, w.part, nb, w.stats, lv->reg);
-    MGB_CHECK_LAUNCH();
     return 0;
   }
   return conv_fwd_dispatch(lv, w, g, st);
+}
+
+// forward phase 3: gain-staging norms and term per node (read by reg and by the backward)
+int mgb_conv_norms(const MgbLevel* lv, cudaStream_t st) {
+  const char tag = lv->tag;
+  const int B = lv->B, L = lv->L;
+  const ConvGeom g = geom(tag, L);
+  MgbArena a{(char*)lv->ws, 0};
+  const ConvWs w = carve_into(a, tag, B, L);
+  mgb_launch(k_gs_norms, dim3(B), dim3(256), 0, st, w.part, tag == 'e' ? eos_nblk(L) : conv_dw_nblk(g), w.stats,
+             lv->reg);
+  MGB_CHECK_LAUNCH();
+  return 0;
 }
 
 // backward phase 1: signal adjoint (gu, gw) and the FIR gradient in the workspace

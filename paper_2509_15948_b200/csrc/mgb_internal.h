@@ -19,6 +19,7 @@ int mgb_simple_backward(const MgbLevel* lv, cudaStream_t st);
 int mgb_simple_param_grad(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_simple_workspace(char tag, int B, int L);
 int mgb_conv_prepare(const MgbLevel* lv, cudaStream_t st);
+int mgb_conv_norms(const MgbLevel* lv, cudaStream_t st);
 int mgb_conv_forward(const MgbLevel* lv, cudaStream_t st);
 int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st);
 int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st);

@@ -302,9 +302,12 @@ class RenderPlan:
                     events[lv.step] = ev
         return events
 
-    def forward(self, use_mask: bool, prepared=None):
+    def forward(self, use_mask: bool, prepared=None, norms="inline"):
         """The render.  ``prepared``: None => run the FIR syntheses inline; a dict of
-        events from ``prepare(side)`` => wait on them; True => already done."""
+        events from ``prepare(side)`` => wait on them; True => already done.
+        ``norms`` (forward phase 3, the gain-staging norms and reg of e/r/d levels):
+        "inline", a torch stream to run them on (off the render chain; the caller
+        joins it before the backward or reg), or None to skip (reg not needed)."""
         L = lib()
         sp = stream_ptr()
         if prepared is None:
@@ -319,6 +322,14 @@ class RenderPlan:
                 if isinstance(prepared, dict) and lv.step in prepared:
                     main.wait_event(prepared[lv.step])
                 check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 2, sp), f"level {lv.tag} forward")
+                if lv.tag in "erd" and norms is not None:
+                    if norms == "inline":
+                        check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 3, sp), f"level {lv.tag} norms")
+                    else:
+                        norms.wait_stream(main)
+                        with torch.cuda.stream(norms):
+                            check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 3, stream_ptr()),
+                                  f"level {lv.tag} norms")
             else:
                 in_rows, seg, B = lv.bus
                 check(L.mgb_bus_sum(ptr(in_rows), ptr(seg), ptr(self.outs[lv.step]), B, self.L, sp),
@@ -482,10 +493,11 @@ class TrainEngine:
             lp.target(ptr(self.target, ws), ptr(self.target, L + ws))
             tev = torch.cuda.Event()
             tev.record(side)
-        plan.forward(use_mask=False, prepared=prepared)
+        plan.forward(use_mask=False, prepared=prepared, norms=side)
         y = plan.y
         main.wait_event(tev)
         lp.forward(ptr(y, ws), ptr(y, L + ws))
+        main.wait_stream(side)  # the levels' norms (read by the backward prologues)
         # loss assembly (read by the optimiser step only) on the side stream, off the path
         # from the loss forward into the backward sweep
         side.wait_stream(main)
@@ -640,7 +652,7 @@ class EvalEngine:
             self._prep_dirty = False
         for i, stems in enumerate(self.seg_stems):
             self.plan.stems.copy_(stems)
-            self.plan.forward(use_mask=True, prepared=True)
+            self.plan.forward(use_mask=True, prepared=True, norms=None)  # eval_loss is the audio loss only
             lp, _ = self.losses[i]
             lp.forward(ptr(self.plan.y, ws), ptr(self.plan.y, L + ws))
             self.acc[i].copy_(lp.loss)

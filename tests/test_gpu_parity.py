@@ -307,7 +307,7 @@ def test_phase_split_equals_whole_level_calls(dev, tag):
         st.gy_rows, st.greg, st.gu, st.gbank, st.gw = ptr(gyr), ptr(greg), ptr(gu), ptr(gp), ptr(gw)
         n0 = Ld.mgb_launch_count()
         if split:
-            for ph in (1, 2):
+            for ph in (1, 2, 3):
                 check(Ld.mgb_level_forward_phase(ctypes.byref(st), ph, stream_ptr()), "fwd phase")
             for ph in (1, 2):
                 check(Ld.mgb_level_backward_phase(ctypes.byref(st), ph, stream_ptr()), "bwd phase")
