@@ -230,6 +230,11 @@ class RenderPlan:
                 lv.keep = [in_rows, seg_t]
             self.levels.append(lv)
         self.y = self.outs[nsteps - 1][0]  # (2, L) output node
+        # processor index -> position of its level in self.levels (incremental re-render)
+        self.proc_level = np.zeros(max(self.P, 1), dtype=np.int64)
+        for i, s in enumerate(range(1, nsteps)):
+            if schedule.type_sequence[s] in KERNEL_TYPES:
+                self.proc_level[np.asarray(schedule.plans[s].weight_idx, dtype=np.int64)] = i
 
         # ---- backward gradient routing
         self.dY = torch.zeros((2, L), dtype=F32, device=dev) if backward else None
@@ -302,12 +307,14 @@ class RenderPlan:
                     events[lv.step] = ev
         return events
 
-    def forward(self, use_mask: bool, prepared=None, norms="inline"):
+    def forward(self, use_mask: bool, prepared=None, norms="inline", start=0):
         """The render.  ``prepared``: None => run the FIR syntheses inline; a dict of
         events from ``prepare(side)`` => wait on them; True => already done.
         ``norms`` (forward phase 3, the gain-staging norms and reg of e/r/d levels):
         "inline", a torch stream to run them on (off the render chain; the caller
-        joins it before the backward or reg), or None to skip (reg not needed)."""
+        joins it before the backward or reg), or None to skip (reg not needed).
+        ``start``: first level to render; the outputs of earlier levels are reused
+        as they are in the buffers (the caller guarantees they are current)."""
         L = lib()
         sp = stream_ptr()
         if prepared is None:
@@ -317,7 +324,7 @@ class RenderPlan:
         if self.P:
             check(L.mgb_weights(ptr(self.params, self.layout.w_off), ptr(self.mask) if use_mask else None,
                                 ptr(self.w), self.P, sp), "mgb_weights")
-        for lv in self.levels:
+        for lv in self.levels[start:]:
             if lv.struct is not None:
                 if isinstance(prepared, dict) and lv.step in prepared:
                     main.wait_event(prepared[lv.step])
@@ -605,7 +612,16 @@ class TrainEngine:
 
 
 class EvalEngine:
-    """Forward-only masked render + MRSTFT over a fixed eval set (mg/pruning.py:99-123)."""
+    """Forward-only masked render + MRSTFT over a fixed eval set (mg/pruning.py:99-123).
+
+    Long segments (or a single one) get a render plan each, stems loaded once,
+    and eager engines (the pruning passes') re-render them incrementally: a
+    trial whose mask differs from the segment's previous render only in
+    processors of level k and later starts the render at level k, the earlier
+    levels' outputs being the same values (trial engine).  Several
+    short segments share one plan (built once per round, ~10 ms per plan)."""
+
+    INCREMENTAL_MIN_L = 200_000  # segments at least this long get a plan each
 
     def __init__(self, graph: MixGraph, segments, warmup_len, loss_cfg, device="cuda", params=None,
                  use_graph=True):
@@ -620,20 +636,31 @@ class EvalEngine:
             self.load_params(params)
         L = segments[0][0].shape[-1]
         self.L, self.ws = L, int(warmup_len)
-        self.plan = RenderPlan(graph, None, L, dev, self.params, None, lay, backward=False)
-        self.seg_stems = []
-        self.losses = []
+        schedule = schedule_for(graph)
+        # Several short segments share one plan (a plan costs ~10 ms to build and an
+        # engine lives for one pruning round); otherwise each segment keeps its own
+        # plan, so its level outputs persist between trials for incremental renders.
+        self.shared = len(segments) > 1 and L < self.INCREMENTAL_MIN_L
+        self.plans, self.losses, self._last_mask, self.seg_stems = [], [], [], []
         for stems, target in segments:
-            self.seg_stems.append(torch.as_tensor(np.asarray(stems), dtype=F32).to(dev))
+            st = torch.as_tensor(np.asarray(stems), dtype=F32).to(dev)
+            if not self.shared or not self.plans:
+                plan = RenderPlan(graph, schedule, L, dev, self.params, None, lay, backward=False)
+                plan.set_stems(st)
+                self.plans.append(plan)
+            self.seg_stems.append(st)
             lp = LossPlan(loss_cfg, L - self.ws, dev)
             t = torch.as_tensor(np.asarray(target), dtype=F32).to(dev).contiguous()
             lp.target(ptr(t, 0), ptr(t, t.shape[-1]))
             self.losses.append((lp, t))
+            self._last_mask.append(None)
+        self.plan = self.plans[0]
         self.acc = torch.zeros(len(segments), dtype=F64, device=dev)
         self.mask_host = torch.ones(max(lay.P, 1), dtype=F64).pin_memory()
         self.acc_host = torch.zeros(len(segments), dtype=F64).pin_memory()
         self.use_graph = use_graph
         self._graph = None
+        self._mask_np = None
 
     def load_params(self, params):
         packed = self.layout.pack(params)
@@ -645,21 +672,35 @@ class EvalEngine:
 
     def _body(self):
         L, ws = self.L, self.ws
-        # FIR syntheses (parameters only) shared by all segments; an eager engine redoes
-        # them only when the parameters changed (a captured graph always includes them)
-        if self.use_graph or self._prep_dirty:
-            self.plan.prepare()
-            self._prep_dirty = False
-        for i, stems in enumerate(self.seg_stems):
-            self.plan.stems.copy_(stems)
-            self.plan.forward(use_mask=True, prepared=True, norms=None)  # eval_loss is the audio loss only
+        # FIR syntheses (parameters only); an eager engine redoes them only when the
+        # parameters changed (a captured graph always includes them)
+        full = self.use_graph or self._prep_dirty
+        if full:
+            for plan in self.plans:
+                plan.prepare()
+        for i in range(len(self.losses)):
+            plan = self.plans[0 if self.shared else i]
+            start = 0
+            if self.shared:
+                plan.stems.copy_(self.seg_stems[i])
+            elif not full and self._mask_np is not None and self._last_mask[i] is not None:
+                changed = np.nonzero(self._mask_np != self._last_mask[i])[0]
+                start = int(plan.proc_level[changed].min()) if changed.size else len(plan.levels)
+            plan.forward(use_mask=True, prepared=True, norms=None, start=start)  # eval_loss is the audio loss only
+            if not self.use_graph and not self.shared:
+                self._last_mask[i] = None if self._mask_np is None else self._mask_np.copy()
             lp, _ = self.losses[i]
-            lp.forward(ptr(self.plan.y, ws), ptr(self.plan.y, L + ws))
+            lp.forward(ptr(plan.y, ws), ptr(plan.y, L + ws))
             self.acc[i].copy_(lp.loss)
+        self._prep_dirty = False
 
     def run_async(self, mask):
-        self.mask_host[: len(mask)].copy_(torch.as_tensor(np.asarray(mask, dtype=np.float64)))
-        self.plan.mask.copy_(self.mask_host, non_blocking=True)
+        m = np.asarray(mask, dtype=np.float64)
+        self.mask_host[: len(m)].copy_(torch.from_numpy(m))
+        self._mask_np = np.ones(self.mask_host.numel())
+        self._mask_np[: len(m)] = m
+        for plan in self.plans:
+            plan.mask.copy_(self.mask_host, non_blocking=True)
         if not self.use_graph:
             self._body()
             return

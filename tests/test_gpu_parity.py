@@ -254,6 +254,30 @@ def test_eval_loss_matches_oracle(dev):
     np.testing.assert_allclose(got, want, rtol=1e-5)
 
 
+@pytest.mark.parametrize("min_l", [0, 10 ** 9])  # per-segment plans (incremental) / one shared plan
+def test_incremental_trial_render_equals_full_render(dev, monkeypatch, min_l):
+    """The eager eval engine re-renders a trial from the first level whose mask changed;
+    every loss must equal (bit for bit) a full render of the same mask."""
+    from paper_2509_15948_b200.engine import EvalEngine
+    monkeypatch.setattr(EvalEngine, "INCREMENTAL_MIN_L", min_l)
+    from paper_2509_15948_b200.losses import LossConfig
+    gs = golden("step.npz")
+    graph, params, stems, L = _step_setup()
+    segs = [(stems, gs["target"][:, 30000:]), (stems[..., ::-1].copy(), gs["target"][:, 30000:][..., ::-1].copy())]
+    inc = EvalEngine(graph, segs, 30000, LossConfig(), device=dev, params=params, use_graph=False)
+    full = EvalEngine(graph, segs, 30000, LossConfig(), device=dev, params=params, use_graph=True)
+    P = len(graph.processor_nodes())
+    rng = np.random.default_rng(5)
+    base = np.ones(P)
+    for trial in range(12):
+        mask = base.copy()
+        mask[rng.choice(P, size=int(rng.integers(1, 4)), replace=False)] = 0.0
+        if trial == 6:
+            base = mask.copy()  # an accepted trial: the next ones differ from a new base
+        assert inc.loss(mask) == full.loss(mask), trial
+    assert inc.loss(base) == full.loss(base)
+
+
 # FFT-size coverage of the convolution levels (N = next_pow2(L + M - 1)): the
 # register four-step at N1 = 128..1024 (2^17..2^20), the Stockham four-step at
 # 2^21, and the overlap-save EQ at the production length, against the oracle.
