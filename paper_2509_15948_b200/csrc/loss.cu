@@ -274,9 +274,10 @@ __global__ void k_mr_finalize(MgbLoss L, int mode) {
   const int ri = blockIdx.x >> 2, g = blockIdx.x & 3;
   const MgbLossRes& r = L.res[ri];
   double s0 = 0.0, s1 = 0.0;
-  for (int f = threadIdx.x; f < r.frames; f += blockDim.x) {
-    s0 += r.part[((size_t)f * 4 + g) * 3 + 0];
-    s1 += r.part[((size_t)f * 4 + g) * 3 + 1];
+#pragma unroll 4
+  for (int f = threadIdx.x; f < r.frames; f += blockDim.x) {  // (loads of several frames in flight)
+    s0 += __ldg(r.part + ((size_t)f * 4 + g) * 3 + 0);
+    s1 += __ldg(r.part + ((size_t)f * 4 + g) * 3 + 1);
   }
   s0 = block_sum(s0, red);
   __syncthreads();
@@ -559,7 +560,7 @@ extern "C" int mgb_mrstft_target(const MgbLoss* L, const float* tl, const float*
   cudaStream_t st = (cudaStream_t)stream;
   if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) { return dispatch_fwd(L->res[i], tl, tr, L->Ls, 0, s); }))
     return rc;
-  mgb_launch(k_mr_finalize, dim3(4 * L->n_res), dim3(256), 0, st, *L, 0);
+  mgb_launch(k_mr_finalize, dim3(4 * L->n_res), dim3(1024), 0, st, *L, 0);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -569,7 +570,7 @@ extern "C" int mgb_mrstft_forward(const MgbLoss* L, const float* yl, const float
   cudaStream_t st = (cudaStream_t)stream;
   if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) { return dispatch_fwd(L->res[i], yl, yr, L->Ls, 1, s); }))
     return rc;
-  mgb_launch(k_mr_finalize, dim3(4 * L->n_res), dim3(256), 0, st, *L, 1);
+  mgb_launch(k_mr_finalize, dim3(4 * L->n_res), dim3(1024), 0, st, *L, 1);
   MGB_CHECK_LAUNCH();
   mgb_launch(k_mr_total, dim3(1), dim3(32), 0, st, *L);
   MGB_CHECK_LAUNCH();
