@@ -85,7 +85,7 @@ int mgb_level_backward(const MgbLevel* level, void* stream);
  *                     the backward and by the caller's reg (no-op otherwise;
  *                     a forward-only caller that ignores reg may skip it).
  *   backward phase 1: the signal adjoint gu, plus the per-CTA parameter
- *                     partials and (e, r, d) the FIR gradient, kept in the
+ *                     partials and (e, r, d) the FIR-gradient spectra, kept in the
  *                     workspace;
  *            phase 2: everything written to gbank and gw: the per-node
  *                     reductions of those partials and the FIR adjoint (e, r, d).

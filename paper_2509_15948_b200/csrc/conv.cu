@@ -418,9 +418,15 @@ struct Conv {
                  N1);
       MGB_CHECK_LAUNCH();
     }
+    return 0;
+  }
+
+  // FIR gradient dh = IFFT(G conj(X))[0:M] (backward phase 2)
+  static int fir_grad(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
+    const dim3 gc(N2 / G::TC, lv->B);
     const int h_rows = (int)((g.M + N2 - 1) / N2);
-    mgb_launch(fs::k_colC<N1, N2, EpGh>, dim3(gc), dim3(G::NTC), sc, st, w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
-                                              h_rows < N1 ? h_rows : N1);
+    mgb_launch(fs::k_colC<N1, N2, EpGh>, dim3(gc), dim3(G::NTC), fs::col_smem<N1, N2>(), st, w.Ah, EpGh{w.ghbuf, g.M},
+               1.f / (float)G::N, h_rows < N1 ? h_rows : N1);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -485,9 +491,15 @@ struct Conv2 {
                  1.f / (float)G::N, N1, 1);
       MGB_CHECK_LAUNCH();
     }
+    return 0;
+  }
+
+  // FIR gradient dh = IFFT(G conj(X))[0:M] (backward phase 2: only the FIR adjoint reads it)
+  static int fir_grad(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
+    const dim3 gc(N2 / G::TC, lv->B);
     const int h_rows = (int)((g.M + N2 - 1) / N2);
     mgb_launch(fs2::k_colC<N1, EpGh>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
-                                                   h_rows < N1 ? h_rows : N1, 1);
+               h_rows < N1 ? h_rows : N1, 1);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -528,6 +540,18 @@ int conv_prep_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, c
     MGB_CONV_SIZES(X)
 #undef X
 #define X(l, a, b) case l: return Conv<a, b>::prep(lv, w, g, st);
+    MGB_CONV_SIZES_OLD(X)
+#undef X
+    default: return 1;
+  }
+}
+
+int conv_firgrad_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
+  switch (g.logN) {
+#define X(l, a) case l: return Conv2<a>::fir_grad(lv, w, g, st);
+    MGB_CONV_SIZES(X)
+#undef X
+#define X(l, a, b) case l: return Conv<a, b>::fir_grad(lv, w, g, st);
     MGB_CONV_SIZES_OLD(X)
 #undef X
     default: return 1;
@@ -666,12 +690,14 @@ int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st) {
     MGB_CHECK_LAUNCH();
     mgb_launch(k_eq_fir_bwd, dim3(dim3(MGB_EQ_BINS / 32, B)), dim3(256), 0, st, lv->bank, lv->prow, w.ghbuf, g.M, lv->gbank);
   } else if (tag == 'r') {
+    if (int rc = conv_firgrad_dispatch(lv, w, g, st)) return rc;
     mgb_launch(k_rev_bwd_frames_fft, dim3(dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B)), dim3(RV_NT), kRevFftSmem, st, 
         lv->bank, lv->prow, w.ghbuf, g.M, reinterpret_cast<double*>(w.aux2));
     MGB_CHECK_LAUNCH();
     mgb_launch(k_rev_bwd_reduce, dim3(dim3((2 * MGB_REV_PBINS + 255) / 256, B)), dim3(256), 0, st,
                reinterpret_cast<const double*>(w.aux2), lv->prow, lv->gbank);
   } else {
+    if (int rc = conv_firgrad_dispatch(lv, w, g, st)) return rc;
     mgb_launch(k_dly_bwd, dim3(dim3(MGB_DLY_TAPS, 2, B)), dim3(NT), kDlyBwdSmem, st, lv->bank, lv->prow, w.aux, w.offs, w.ghbuf, g.M,
                                                                  lv->gbank);
   }
