@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "fourstep.cuh"
 #include "fs2.cuh"
+#include "fs2_col64.cuh"
 #include "mgb_internal.h"
 #include "tables.cuh"
 
@@ -437,10 +438,38 @@ template <int N1>
 struct Conv2 {
   using G = fs2::G<N1>;
   static constexpr int N2 = fs2::N2;
-  static constexpr int DW_NBLK = G::NBLK;  // column CTAs per node = dw partial slots
+  static constexpr bool C64 = (N1 == 2048);  // 2048-point columns: fs2_col64.cuh
+  static constexpr int DW_NBLK = C64 ? fs2::C64::NBLK : G::NBLK;  // column CTAs per node = dw partial slots
+  template <class Ld>
+  static void colA(const Ld& ld, float2* A, int nz, int rev, int B, cudaStream_t st) {
+    if constexpr (C64) {
+      mgb_launch(fs2::k_colA64<Ld>, dim3(dim3(N2 / fs2::C64::TC, B)), dim3(fs2::C64::NT), fs2::C64::SMEM, st, ld, A, nz, rev);
+    } else {
+      mgb_launch(fs2::k_colA<N1, Ld>, dim3(dim3(N2 / G::TC, B)), dim3(G::NT), G::COL_SMEM, st, ld, A, nz, rev);
+    }
+  }
+  template <class Ep>
+  static void colC(const float2* Bb, const Ep& ep, int out_rows, int rev, int B, cudaStream_t st) {
+    if constexpr (C64) {
+      mgb_launch(fs2::k_colC64<Ep>, dim3(dim3(N2 / fs2::C64::TC, B)), dim3(fs2::C64::NT), fs2::C64::SMEM, st, Bb, ep,
+                 1.f / (float)G::N, out_rows, rev);
+    } else {
+      mgb_launch(fs2::k_colC<N1, Ep>, dim3(dim3(N2 / G::TC, B)), dim3(G::NT), G::COL_SMEM, st, Bb, ep, 1.f / (float)G::N,
+                 out_rows, rev);
+    }
+  }
   static void attrs() {
-    const int sc = (int)G::COL_SMEM;
-    if (sc > 0) {
+    if constexpr (C64) {
+      const int s64 = (int)fs2::C64::SMEM;
+      cudaFuncSetAttribute(fs2::k_colA64<LdRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64);
+      cudaFuncSetAttribute(fs2::k_colA64<LdFir>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64);
+      cudaFuncSetAttribute(fs2::k_colA64<LdBwdPro>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64);
+      cudaFuncSetAttribute(fs2::k_colC64<EpFwd>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64);
+      cudaFuncSetAttribute(fs2::k_colC64<EpGx>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64);
+      cudaFuncSetAttribute(fs2::k_colC64<EpGh>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64);
+    }
+    const int sc = C64 ? 0 : (int)G::COL_SMEM;
+    if constexpr (!C64) if (sc > 0) {
       cudaFuncSetAttribute(fs2::k_colA<N1, LdRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
       cudaFuncSetAttribute(fs2::k_colA<N1, LdFir>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
       cudaFuncSetAttribute(fs2::k_colA<N1, LdBwdPro>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
@@ -456,7 +485,7 @@ struct Conv2 {
   static int prep(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
     const dim3 gc(N2 / G::TC, lv->B), gr(G::ROW_CTAS, lv->B);
     const int fir_rows = (int)((g.M + N2 - 1) / N2);
-    mgb_launch(fs2::k_colA<N1, LdFir>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, LdFir{w.hbuf, g.M}, w.Ah, fir_rows < N1 ? fir_rows : N1, 0);
+    colA(LdFir{w.hbuf, g.M}, w.Ah, fir_rows < N1 ? fir_rows : N1, 0, lv->B, st);
     MGB_CHECK_LAUNCH();
     mgb_launch(fs2::k_rowH<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWH_SMEM, st, w.Ah, w.H, 1);
     MGB_CHECK_LAUNCH();
@@ -467,12 +496,12 @@ struct Conv2 {
     const int B = lv->B, L = lv->L;
     const dim3 gc(N2 / G::TC, B), gr(G::ROW_CTAS, B);
     const int x_rows = (int)((L + N2 - 1) / N2);
-    mgb_launch(fs2::k_colA<N1, LdRows>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1, 0);
+    colA(LdRows{lv->u_rows, L}, w.Ax, x_rows < N1 ? x_rows : N1, 0, B, st);
     MGB_CHECK_LAUNCH();
     mgb_launch(fs2::k_rowF<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWF_SMEM, st, w.Ax, w.H, w.X, w.Bo, 1);
     MGB_CHECK_LAUNCH();
     EpFwd ep{lv->u_rows, lv->widx, lv->w, lv->y, lv->ybar, w.part, L, g.off};
-    mgb_launch(fs2::k_colC<N1, EpFwd>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, ep, 1.f / (float)G::N, N1, 0);
+    colC(w.Bo, ep, N1, 0, B, st);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -482,13 +511,12 @@ struct Conv2 {
     const dim3 gc(N2 / G::TC, B), gr(G::ROW_CTAS, B);
     LdBwdPro ld{lv->u_rows, lv->gy_rows, lv->ybar, lv->widx, lv->w, lv->greg, w.stats, lv->gu, w.part, L, g.off};
     const int g_rows = (int)((g.off + L + N2 - 1) / N2);
-    mgb_launch(fs2::k_colA<N1, LdBwdPro>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, ld, w.Ax, g_rows < N1 ? g_rows : N1, 1);
+    colA(ld, w.Ax, g_rows < N1 ? g_rows : N1, 1, B, st);
     MGB_CHECK_LAUNCH();
     mgb_launch(fs2::k_rowG<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWG_SMEM, st, w.Ax, w.X, w.H, w.Bo, w.Ah, 0);
     MGB_CHECK_LAUNCH();
     if (lv->gu) {
-      mgb_launch(fs2::k_colC<N1, EpGx>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Bo, EpGx{lv->gu, L},
-                 1.f / (float)G::N, N1, 1);
+      colC(w.Bo, EpGx{lv->gu, L}, N1, 1, B, st);
       MGB_CHECK_LAUNCH();
     }
     return 0;
@@ -498,17 +526,17 @@ struct Conv2 {
   static int fir_grad(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
     const dim3 gc(N2 / G::TC, lv->B);
     const int h_rows = (int)((g.M + N2 - 1) / N2);
-    mgb_launch(fs2::k_colC<N1, EpGh>, dim3(gc), dim3(G::NT), G::COL_SMEM, st, w.Ah, EpGh{w.ghbuf, g.M}, 1.f / (float)G::N,
-               h_rows < N1 ? h_rows : N1, 1);
+    colC(w.Ah, EpGh{w.ghbuf, g.M}, h_rows < N1 ? h_rows : N1, 1, lv->B, st);
     MGB_CHECK_LAUNCH();
     return 0;
   }
 };
 
-// register path for N <= 2^20 (N1 <= 1024), Stockham four-step above
+// register path for N <= 2^21 (N1 <= 2048; 2048 with the split column pass of fs2_col64.cuh),
+// the shared-memory Stockham four-step above
 #define MGB_CONV_SIZES(X) \
-  X(12, 4) X(13, 8) X(14, 16) X(15, 32) X(16, 64) X(17, 128) X(18, 256) X(19, 512) X(20, 1024)
-#define MGB_CONV_SIZES_OLD(X) X(21, 1024, 2048) X(22, 1024, 4096)
+  X(12, 4) X(13, 8) X(14, 16) X(15, 32) X(16, 64) X(17, 128) X(18, 256) X(19, 512) X(20, 1024) X(21, 2048)
+#define MGB_CONV_SIZES_OLD(X) X(22, 1024, 4096)
 
 int conv_fwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
   switch (g.logN) {

@@ -34,7 +34,7 @@ template <int N1>
 struct G {
   static constexpr int Q = N1 < 32 ? N1 : 32;
   static constexpr int P = N1 / Q;
-  static_assert(P <= Q && Q % P == 0, "N1 <= 1024");
+  // (the column transform below needs P <= Q, i.e. N1 <= 1024; N1 = 2048 uses fs2_col64.cuh)
   static constexpr int TC = P >= 16 ? 16 : 256 / P;  // columns per column-pass CTA
   static constexpr int NT = TC * P;                   // 256 (512 for N1 = 1024)
   static constexpr int PITCH = N1 + 1;                // odd: conflict-free 8-byte column accesses
@@ -106,6 +106,7 @@ __device__ __forceinline__ void twiddle_run(float2* v, int e0, int de) {
 template <int N1, bool INV>
 __device__ __forceinline__ void col_fft(float2 (&v)[G<N1>::Q], float2* sm, int c, int j) {
   using g = G<N1>;
+  static_assert(g::P <= g::Q && g::Q % g::P == 0, "register column transform: N1 <= 1024");
   constexpr int Q = g::Q, P = g::P;
   rf::rdft<Q, INV>(v);
   if constexpr (P > 1) {
