@@ -81,11 +81,23 @@ __device__ __forceinline__ void st_stage(float2* v, float2* S, int tt) {
     const int j = tt + T * i, k = j % NS;
     float2* a = v + i * R;
     if (NS > 1) {
+      // w^m for m = 1..R-1: table values at m = 1 and every 4th m, products in between
+      // (<= 3 roundings from a table value; a quarter of the table loads)
+      const int e1 = k * (MGB_TW_N / (NS * R));
+      float2 w1 = g_tw32[e1 & (MGB_TW_N - 1)], wm = w1;
+      if (INV) w1.y = -w1.y;
+      wm = w1;
 #pragma unroll
       for (int m = 1; m < R; ++m) {
-        float2 w = g_tw32[(k * m * (MGB_TW_N / (NS * R))) & (MGB_TW_N - 1)];
-        if (INV) w.y = -w.y;
-        a[m] = cmul(a[m], w);
+        if (m > 1) {
+          if (m % 4 == 0) {
+            wm = g_tw32[(e1 * m) & (MGB_TW_N - 1)];
+            if (INV) wm.y = -wm.y;
+          } else {
+            wm = cmul(wm, w1);
+          }
+        }
+        a[m] = cmul(a[m], wm);
       }
     }
     rf::rdft<R, INV>(a);
