@@ -390,3 +390,21 @@ def test_pruning_passes_make_the_oracles_decisions(dev, monkeypatch):
 
 def _device_eval(graph, params, mask, eval_set, schedule=None):
     return eval_set.engine(graph, params).loss(mask)
+
+
+def test_desk_song_search_runs(dev):
+    """Config-5 unit of work end to end on the device: one desk-recipe pruning search
+    (console fit, a hybrid round with trials and a fine-tune) on a small synthetic song."""
+    import bench
+    from paper_2509_15948_b200.scheduler import execute_batched
+    from paper_2509_15948_b200.songs import SongSpec, search_song
+
+    def render(graph, tparams, stems):
+        y, _ = execute_batched(graph, tparams, stems, device=dev)
+        return y.cpu().numpy()
+
+    spec = SongSpec(index=0, tracks=4, subgroups=1, length=132_300)
+    graph, params, stems, target = bench.make_inputs(7, spec.tracks, spec.subgroups, spec.length, render)
+    res = search_song(spec, graph, params, stems, target, iterations=1, device=dev)
+    assert res["trials"] > 0 and 0.0 <= res["pruning_ratio"] <= 1.0
+    assert np.isfinite(res["console_loss"]) and np.isfinite(res["final_loss"])
