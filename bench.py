@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--songs", type=int, default=4,
+    ap.add_argument("--song-concurrency", type=int, default=4,
+                    help="songs searched concurrently per GPU (host threads + CUDA streams)")
+    ap.add_argument("--songs", type=int, default=8,
                     help="config-5 desk-recipe pruning searches per GPU for songs/hour (0: skip)")
     ap.add_argument("--tracks", type=int, default=K_TRACKS)
     ap.add_argument("--subgroups", type=int, default=S_GROUPS)
@@ -301,7 +303,7 @@ def main():
     # config 5: full pruning searches (desk recipe), this rank's LPT share of songs*world songs
     songs = None
     if args.songs > 0:
-        from paper_2509_15948_b200.songs import assign_lpt, desk_specs, gather_results, search_song, song_costs
+        from paper_2509_15948_b200.songs import assign_lpt, desk_specs, gather_results, search_songs, song_costs
         specs = desk_specs(args.songs * world, seed=0)
         mine = assign_lpt(song_costs(specs), world)[rank]
         inputs = {i: make_inputs(1000 + specs[i].index, specs[i].tracks, specs[i].subgroups, specs[i].length,
@@ -310,7 +312,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = [search_song(specs[i], *inputs[i], device=dev) for i in mine]
+        res = search_songs(specs, mine, inputs, concurrent=args.song_concurrency, device=dev)
         torch.cuda.synchronize()
         sw = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
@@ -320,7 +322,7 @@ def main():
             songs = {"value": len(res) / float(sw.item()) * 3600.0, "unit": "songs/hour", "songs": len(res),
                      "wall_s": float(sw.item()), "recipe": "desk (pkg/README.md:54-58): console 600, 12 hybrid "
                      "rounds x 50 fine-tune, 57,000-sample segments, 4 eval segments, tau_rel 0.02",
-                     "tracks": [r["tracks"] for r in res], "trials": [r["trials"] for r in res]}
+                     "concurrent_per_gpu": args.song_concurrency, "tracks": [r["tracks"] for r in res], "trials": [r["trials"] for r in res]}
     lay = eng.layout
     # per step: its segment and the 8 step scalars in, the 4 metrics out (params move once per run)
     h2d = stems.nbytes + target.nbytes + 8 * 8

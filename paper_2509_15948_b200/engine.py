@@ -21,6 +21,7 @@ on one stream and captured once into a CUDA graph per graph version.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 import torch
@@ -62,18 +63,39 @@ def capture_graph(body, device):
 
     torch.cuda.graph's context manager empties the device and pinned-host caches
     before every capture (~60 ms each); a pruning search re-captures its engines
-    every round, so capture here without that."""
+    every round, so capture here without that.  Thread-local capture mode, so
+    other host threads (concurrent song searches) may allocate meanwhile."""
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream(device=device)
     s.wait_stream(torch.cuda.current_stream(device))
     with torch.cuda.stream(s):
-        g.capture_begin()
+        g.capture_begin(capture_error_mode="thread_local")
         try:
             body()
         finally:
             g.capture_end()
     torch.cuda.current_stream(device).wait_stream(s)
     return g
+
+
+# Concurrent song searches (songs.search_songs): host threads take turns issuing
+# GPU work under one lock and hand it over only while blocked on their own
+# stream, so no other thread's API call can land inside a graph capture.
+_host = threading.local()
+
+
+def host_wait(obj) -> None:
+    """``obj.synchronize()`` (a stream or event), handing the host turn to another
+    song's thread meanwhile when searches run concurrently."""
+    lk = getattr(_host, "lock", None)
+    if lk is None:
+        obj.synchronize()
+        return
+    lk.release()
+    try:
+        obj.synchronize()
+    finally:
+        lk.acquire()
 
 
 def stream_ptr():
@@ -555,7 +577,7 @@ class TrainEngine:
             n0 = Ld.mgb_launch_count()
             self._body()
             self._launches = int(Ld.mgb_launch_count() - n0)
-            torch.cuda.synchronize(self.device)
+            torch.cuda.current_stream().synchronize()
             self.params.copy_(snap[0])
             self.m.copy_(snap[1])
             self.v.copy_(snap[2])
@@ -575,7 +597,7 @@ class TrainEngine:
             self._ring_ev = [None] * self._RING
         i = self.t % self._RING
         if self._ring_ev[i] is not None:
-            self._ring_ev[i].synchronize()
+            host_wait(self._ring_ev[i])
         self._ring[i].copy_(torch.tensor([c.lr, b1, b2, c.eps, c.weight_decay, 1.0 - b1 ** self.t,
                                           1.0 - b2 ** self.t, float(alpha_p)], dtype=F64))
         self.scalars.copy_(self._ring[i], non_blocking=True)
@@ -600,13 +622,13 @@ class TrainEngine:
                 self.m.copy_(snap[1])
                 self.v.copy_(snap[2])
             torch.cuda.current_stream().wait_stream(s)
-            torch.cuda.synchronize(self.device)
+            torch.cuda.current_stream().synchronize()  # not device-wide: other songs may be capturing
             self._graph = capture_graph(self._body, self.device)
         self._graph.replay()
 
     def read_values(self):
         self.vals_host.copy_(self.vals, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        host_wait(torch.cuda.current_stream())
         v = self.vals_host.tolist()
         return {"loss": v[0], "L_a": v[1], "L_g": v[2], "L_p": v[3]}
 
@@ -710,14 +732,14 @@ class EvalEngine:
             with torch.cuda.stream(s):
                 self._body()
             torch.cuda.current_stream().wait_stream(s)
-            torch.cuda.synchronize(self.device)
+            torch.cuda.current_stream().synchronize()  # not device-wide: other songs may be capturing
             self._graph = capture_graph(self._body, self.device)
         self._graph.replay()
 
     def loss(self, mask) -> float:
         self.run_async(mask)
         self.acc_host.copy_(self.acc, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        host_wait(torch.cuda.current_stream())
         # per-segment float() then mean, as mg/pruning.py:120-123
         total = 0.0
         for v in self.acc_host.tolist():

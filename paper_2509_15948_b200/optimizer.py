@@ -12,6 +12,7 @@ at the end.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -19,13 +20,14 @@ import numpy as np
 import torch
 
 from .common import rng_for, seconds_to_samples
-from .engine import F32, TrainEngine, ensure_device
+from .engine import F32, TrainEngine, ensure_device, host_wait
 from .graph import MixGraph, ParamStore
 from .losses import LossConfig
 from .schedule import plan_indices, schedule_for
 
 
-GRAPH_MIN_STEPS = 200  # train() captures its step only for runs at least this long
+# train() captures its step only for runs at least this long
+GRAPH_MIN_STEPS = int(os.environ.get("MG_GRAPH_MIN_STEPS", "200"))
 
 
 class SongTooShort(Exception):
@@ -142,6 +144,11 @@ def train_step(graph, params: ParamStore, segment, cfg: TrainConfig, opt: AdamW,
     return values
 
 
+def _graph_min_steps():
+    from .engine import _host
+    return getattr(_host, "graph_min_steps", None) or GRAPH_MIN_STEPS
+
+
 def _pinned_f32(a):
     t = a if torch.is_tensor(a) else torch.from_numpy(np.ascontiguousarray(a))
     if t.dtype != F32:
@@ -212,7 +219,7 @@ def train_segments(graph, params: ParamStore, segments, cfg: TrainConfig, opt: A
         eng.step_async(alpha_p_fn(k) if alpha_p_fn else 0.0)
         r = k % 64
         if ring_ev[r] is not None:
-            ring_ev[r].synchronize()
+            host_wait(ring_ev[r])
             out.append(ring[r].tolist())
         ring[r].copy_(eng.vals, non_blocking=True)
         ring_ev[r] = torch.cuda.Event()
@@ -222,7 +229,7 @@ def train_segments(graph, params: ParamStore, segments, cfg: TrainConfig, opt: A
         k += 1
     for j in range(k - min(k, 64), k):
         r = j % 64
-        ring_ev[r].synchronize()
+        host_wait(ring_ev[r])
         out.append(ring[r].tolist())
     del keep
     wall = (time.perf_counter() - t0) / k
@@ -254,7 +261,7 @@ def train(graph, params: ParamStore, session: Session, cfg: TrainConfig, schedul
         return history
     dev = ensure_device(device)
     # a short run (a fine-tune round) is as fast eager as replayed: skip the capture
-    eng = opt.engine(graph, seg, cfg, schedule, use_graph=cfg.steps >= GRAPH_MIN_STEPS)
+    eng = opt.engine(graph, seg, cfg, schedule, use_graph=cfg.steps >= _graph_min_steps())
     eng.load_params(params)
     full = session.length == seg
     st_dev = torch.as_tensor(np.asarray(session.stems), dtype=F32).to(dev)
@@ -271,6 +278,7 @@ def train(graph, params: ParamStore, session: Session, cfg: TrainConfig, schedul
             eng.target.copy_(tg_dev[..., offset:offset + seg])
         eng.step_async(alpha_p_fn(step) if alpha_p_fn else 0.0)
         vals[step].copy_(eng.vals)
+    host_wait(torch.cuda.current_stream())
     host = vals.cpu().numpy()
     wall = (time.perf_counter() - t0) / cfg.steps
     opt.t = eng.t

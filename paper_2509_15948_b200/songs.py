@@ -104,6 +104,66 @@ def search_song(spec, graph, params, stems, target, iterations=12, device="cuda"
             "pruning_ratio": rep.pruning_ratio, "console_loss": rep.console_loss, "final_loss": rep.final_loss}
 
 
+def search_songs(specs, mine, inputs, concurrent=1, iterations=12, device="cuda"):
+    """Run this rank's songs, ``concurrent`` at a time on one GPU.
+
+    A desk-recipe song trains on 57,000-sample segments, where one level
+    launch fills only part of the 148 SMs; several songs in flight (one host
+    thread and one CUDA stream each, songs taken costliest-first from a shared
+    queue) let their kernels overlap.  Searches stay independent: each has its
+    own engines, streams and graphs, and the results are the same as running
+    the songs one after another.  The threads take turns on the host (one lock,
+    released only while a thread waits on its own stream, ``engine.host_wait``),
+    so no other thread's CUDA call can land inside a graph capture.  Returns the per-song summaries in ``mine``
+    order."""
+    if concurrent <= 1:
+        return [search_song(specs[i], *inputs[i], iterations=iterations, device=device) for i in mine]
+    import threading
+
+    import torch
+
+    from . import engine
+    dev = engine.ensure_device(device)  # library + tables once, before the threads start
+    order = sorted(mine, key=lambda i: (-song_costs([specs[i]])[0], i))
+    lock = threading.Lock()
+    turn = threading.Lock()  # the host turn: held while issuing GPU work, handed over while waiting
+    out, errors = {}, []
+
+    def worker():
+        torch.cuda.set_device(dev)
+        stream = torch.cuda.Stream(device=dev)
+        engine._host.lock = turn
+        # fine-tunes replay a captured step too: a replay frees the host turn for
+        # the other songs, where an eager step would hold it for every launch
+        engine._host.graph_min_steps = 1
+        turn.acquire()
+        try:
+            with torch.cuda.stream(stream):
+                while True:
+                    with lock:
+                        if not order or errors:
+                            break
+                        i = order.pop(0)
+                    try:
+                        out[i] = search_song(specs[i], *inputs[i], iterations=iterations, device=dev)
+                    except BaseException as e:  # surfaced on the calling thread
+                        errors.append(e)
+                        break
+            engine.host_wait(stream)
+        finally:
+            engine._host.lock = engine._host.graph_min_steps = None
+            turn.release()
+
+    threads = [threading.Thread(target=worker, daemon=True) for _ in range(min(concurrent, len(mine)))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return [out[i] for i in mine]
+
+
 def songs_per_hour(results, wall_s):
     return len(results) / max(wall_s, 1e-9) * 3600.0
 
@@ -113,4 +173,4 @@ def spec_dict(spec):
 
 
 __all__ = ["SongSpec", "song_costs", "assign_lpt", "desk_specs", "run_rank", "gather_results",
-           "songs_per_hour", "spec_dict", "desk_prune_config", "search_song", "DESK_SEGMENT", "np"]
+           "songs_per_hour", "spec_dict", "desk_prune_config", "search_song", "search_songs", "DESK_SEGMENT", "np"]

@@ -408,3 +408,23 @@ def test_desk_song_search_runs(dev):
     res = search_song(spec, graph, params, stems, target, iterations=1, device=dev)
     assert res["trials"] > 0 and 0.0 <= res["pruning_ratio"] <= 1.0
     assert np.isfinite(res["console_loss"]) and np.isfinite(res["final_loss"])
+
+
+def test_concurrent_song_searches_equal_sequential(dev):
+    """Songs searched concurrently on one GPU (one host thread + stream each) make the same
+    decisions and losses as the same songs searched one after another."""
+    import bench
+    from paper_2509_15948_b200.scheduler import execute_batched
+    from paper_2509_15948_b200.songs import SongSpec, search_songs
+
+    def render(graph, tparams, stems):
+        y, _ = execute_batched(graph, tparams, stems, device=dev)
+        return y.cpu().numpy()
+
+    specs = [SongSpec(index=i, tracks=k, subgroups=1, length=132_300) for i, k in enumerate((4, 5, 3))]
+    inputs = {i: bench.make_inputs(20 + i, s.tracks, s.subgroups, s.length, render) for i, s in enumerate(specs)}
+    mine = [0, 1, 2]
+    seq = search_songs(specs, mine, inputs, concurrent=1, iterations=2, device=dev)
+    par = search_songs(specs, mine, inputs, concurrent=3, iterations=2, device=dev)
+    keys = ("song", "tracks", "trials", "pruning_ratio", "console_loss", "final_loss")
+    assert [{k: r[k] for k in keys} for r in par] == [{k: r[k] for k in keys} for r in seq]

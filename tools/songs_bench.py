@@ -26,7 +26,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2509_15948_b200.scheduler import execute_batched  # noqa: E402
-from paper_2509_15948_b200.songs import assign_lpt, desk_specs, gather_results, search_song, song_costs  # noqa: E402
+from paper_2509_15948_b200.songs import assign_lpt, desk_specs, gather_results, search_songs, song_costs  # noqa: E402
 
 
 def main():
@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--songs", type=int, default=4)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--iterations", type=int, default=12)
+    ap.add_argument("--concurrent", type=int, default=1, help="songs in flight per GPU (threads + streams)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -56,11 +57,9 @@ def main():
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    results = []
     t0 = time.perf_counter()
-    for i in mine:
-        results.append(search_song(specs[i], *inputs[i], iterations=args.iterations, device=dev))
-        torch.cuda.synchronize()
+    results = search_songs(specs, mine, inputs, concurrent=args.concurrent, iterations=args.iterations, device=dev)
+    torch.cuda.synchronize()
     wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(wall, op=dist.ReduceOp.MAX)
@@ -69,7 +68,7 @@ def main():
         w = float(wall.item())
         print(json.dumps({"metric": "songs searched/hour (config 5 desk recipe)",
                           "value": len(merged) / w * 3600.0, "unit": "songs/hour", "n_gpus": world,
-                          "songs": len(merged), "wall_s": w, "iterations": args.iterations,
+                          "songs": len(merged), "wall_s": w, "iterations": args.iterations, "concurrent": args.concurrent,
                           "per_song": merged}))
     if dist is not None:
         dist.destroy_process_group()
