@@ -99,7 +99,39 @@ def host_wait(obj) -> None:
 
 
 def stream_ptr():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
+
+
+# torch.cuda.current_stream() / torch.cuda.stream() resolve the device index
+# through several Python layers on every call (env lookups, availability
+# checks): ~20 % of a song search's host time under cProfile.  These do the same for the
+# current device straight through the torch._C stream registry.
+def current_stream() -> torch.cuda.Stream:
+    sid, di, dt = torch._C._cuda_getCurrentStream(torch._C._cuda_getDevice())
+    return torch.cuda.Stream(stream_id=sid, device_index=di, device_type=dt)
+
+
+class on_stream:
+    """``with torch.cuda.stream(s)`` for a stream on the current device."""
+    __slots__ = ("s", "prev", "ctx")
+
+    def __init__(self, s):
+        self.s = s
+
+    def __enter__(self):
+        s = self.s
+        if s.device_index != torch._C._cuda_getDevice():
+            self.ctx = torch.cuda.stream(s)
+            return self.ctx.__enter__()
+        self.ctx = None
+        self.prev = torch._C._cuda_getCurrentStream(s.device_index)
+        torch._C._cuda_setStream(stream_id=s.stream_id, device_index=s.device_index, device_type=s.device_type)
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            return self.ctx.__exit__(*exc)
+        sid, di, dt = self.prev
+        torch._C._cuda_setStream(stream_id=sid, device_index=di, device_type=dt)
 
 
 def ptr(t: torch.Tensor, elem_offset: int = 0) -> int:
@@ -318,8 +350,8 @@ class RenderPlan:
                 if lv.struct is not None and lv.tag in "erdcn":
                     check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 1, sp), f"level {lv.tag} prepare")
             return events
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
+        side.wait_stream(current_stream())
+        with on_stream(side):
             sp = stream_ptr()
             for lv in self.levels:
                 if lv.struct is not None and lv.tag in "erdcn":
@@ -342,7 +374,7 @@ class RenderPlan:
         if prepared is None:
             self.prepare()
             prepared = True
-        main = torch.cuda.current_stream()
+        main = current_stream()
         if self.P:
             check(L.mgb_weights(ptr(self.params, self.layout.w_off), ptr(self.mask) if use_mask else None,
                                 ptr(self.w), self.P, sp), "mgb_weights")
@@ -356,7 +388,7 @@ class RenderPlan:
                         check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 3, sp), f"level {lv.tag} norms")
                     else:
                         norms.wait_stream(main)
-                        with torch.cuda.stream(norms):
+                        with on_stream(norms):
                             check(L.mgb_level_forward_phase(ctypes.byref(lv.struct), 3, stream_ptr()),
                                   f"level {lv.tag} norms")
             else:
@@ -374,7 +406,7 @@ class RenderPlan:
         (``current_stream().wait_stream(side)``) before reading the gradients."""
         L = lib()
         sp = stream_ptr()
-        main = torch.cuda.current_stream()
+        main = current_stream()
         for lv in reversed(self.levels):
             for src, off, buf in lv.fanouts:
                 check(L.mgb_bus_sum(ptr(src), ptr(off), ptr(buf), 1, self.L, sp), "fan-out sum")
@@ -385,7 +417,7 @@ class RenderPlan:
                 continue
             check(L.mgb_level_backward_phase(ctypes.byref(lv.struct), 1, sp), f"level {lv.tag} backward")
             side.wait_stream(main)
-            with torch.cuda.stream(side):
+            with on_stream(side):
                 check(L.mgb_level_backward_phase(ctypes.byref(lv.struct), 2, stream_ptr()),
                       f"level {lv.tag} FIR adjoint")
 
@@ -513,11 +545,11 @@ class TrainEngine:
         L, ws, P = self.L, self.ws, self.layout.P
         plan, lp = self.plan, self.lossp
         Ld = lib()
-        main, side = torch.cuda.current_stream(), self.side
+        main, side = current_stream(), self.side
         # side stream: FIR syntheses (params only), the warm-up part of dL/dy (read by the
         # level backward; the loss backward writes the rest), then the target spectra
         prepared = plan.prepare(side)
-        with torch.cuda.stream(side):
+        with on_stream(side):
             plan.dY[:, :ws].zero_()
             lp.target(ptr(self.target, ws), ptr(self.target, L + ws))
             tev = torch.cuda.Event()
@@ -530,7 +562,7 @@ class TrainEngine:
         # loss assembly (read by the optimiser step only) on the side stream, off the path
         # from the loss forward into the backward sweep
         side.wait_stream(main)
-        with torch.cuda.stream(side):
+        with on_stream(side):
             reg = plan.reg_total()
             if P:
                 check(Ld.mgb_sparsity(ptr(self.params, self.layout.w_off), P, ptr(self.sparsity), stream_ptr()),
@@ -577,7 +609,7 @@ class TrainEngine:
             n0 = Ld.mgb_launch_count()
             self._body()
             self._launches = int(Ld.mgb_launch_count() - n0)
-            torch.cuda.current_stream().synchronize()
+            current_stream().synchronize()
             self.params.copy_(snap[0])
             self.m.copy_(snap[1])
             self.v.copy_(snap[2])
@@ -614,21 +646,21 @@ class TrainEngine:
         if self._graph is None:
             # warm-up run outside capture (sets function attributes, JIT, allocations)
             s = torch.cuda.Stream(device=self.device)
-            s.wait_stream(torch.cuda.current_stream())
+            s.wait_stream(current_stream())
             with torch.cuda.stream(s):
                 snap = [self.params.clone(), self.m.clone(), self.v.clone()]
                 self._body()
                 self.params.copy_(snap[0])
                 self.m.copy_(snap[1])
                 self.v.copy_(snap[2])
-            torch.cuda.current_stream().wait_stream(s)
-            torch.cuda.current_stream().synchronize()  # not device-wide: other songs may be capturing
+            current_stream().wait_stream(s)
+            current_stream().synchronize()  # not device-wide: other songs may be capturing
             self._graph = capture_graph(self._body, self.device)
         self._graph.replay()
 
     def read_values(self):
         self.vals_host.copy_(self.vals, non_blocking=True)
-        host_wait(torch.cuda.current_stream())
+        host_wait(current_stream())
         v = self.vals_host.tolist()
         return {"loss": v[0], "L_a": v[1], "L_g": v[2], "L_p": v[3]}
 
@@ -728,18 +760,18 @@ class EvalEngine:
             return
         if self._graph is None:
             s = torch.cuda.Stream(device=self.device)
-            s.wait_stream(torch.cuda.current_stream())
+            s.wait_stream(current_stream())
             with torch.cuda.stream(s):
                 self._body()
-            torch.cuda.current_stream().wait_stream(s)
-            torch.cuda.current_stream().synchronize()  # not device-wide: other songs may be capturing
+            current_stream().wait_stream(s)
+            current_stream().synchronize()  # not device-wide: other songs may be capturing
             self._graph = capture_graph(self._body, self.device)
         self._graph.replay()
 
     def loss(self, mask) -> float:
         self.run_async(mask)
         self.acc_host.copy_(self.acc, non_blocking=True)
-        host_wait(torch.cuda.current_stream())
+        host_wait(current_stream())
         # per-segment float() then mean, as mg/pruning.py:120-123
         total = 0.0
         for v in self.acc_host.tolist():
