@@ -48,6 +48,18 @@ class Session:
     def length(self):
         return self.stems.shape[-1]
 
+    def on_device(self, dev):
+        """(stems, target) as float32 device tensors, uploaded once per device and
+        reused by every ``train`` call of a search (13 per desk-recipe song).
+        Assign new arrays to change the session; in-place edits are not seen."""
+        key = (str(dev), id(self.stems), id(self.target))
+        hit = self.__dict__.get("_dev")
+        if hit is None or hit[0] != key:
+            st = torch.as_tensor(np.asarray(self.stems), dtype=F32).to(dev)
+            tg = torch.as_tensor(np.asarray(self.target), dtype=F32).to(dev)
+            hit = self.__dict__["_dev"] = (key, st, tg)
+        return hit[1], hit[2]
+
 
 @dataclass
 class TrainConfig:
@@ -264,8 +276,7 @@ def train(graph, params: ParamStore, session: Session, cfg: TrainConfig, schedul
     eng = opt.engine(graph, seg, cfg, schedule, use_graph=cfg.steps >= _graph_min_steps())
     eng.load_params(params)
     full = session.length == seg
-    st_dev = torch.as_tensor(np.asarray(session.stems), dtype=F32).to(dev)
-    tg_dev = torch.as_tensor(np.asarray(session.target), dtype=F32).to(dev)
+    st_dev, tg_dev = session.on_device(dev)
     if full:
         eng.plan.stems.copy_(st_dev)
         eng.target.copy_(tg_dev)

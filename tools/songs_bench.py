@@ -69,6 +69,8 @@ def main():
         print(json.dumps({"metric": "songs searched/hour (config 5 desk recipe)",
                           "value": len(merged) / w * 3600.0, "unit": "songs/hour", "n_gpus": world,
                           "songs": len(merged), "wall_s": w, "iterations": args.iterations, "concurrent": args.concurrent,
+                          "max_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+                          "reserved_gb": torch.cuda.memory_reserved(dev) / 1e9,
                           "per_song": merged}))
     if dist is not None:
         dist.destroy_process_group()
