@@ -63,30 +63,76 @@ def capture_graph(body, device):
 
     torch.cuda.graph's context manager empties the device and pinned-host caches
     before every capture (~60 ms each); a pruning search re-captures its engines
-    every round, so capture here without that.  Thread-local capture mode, so
-    other host threads (concurrent song searches) may allocate meanwhile."""
-    g = torch.cuda.CUDAGraph()
-    s = torch.cuda.Stream(device=device)
-    s.wait_stream(torch.cuda.current_stream(device))
-    with torch.cuda.stream(s):
-        g.capture_begin(capture_error_mode="thread_local")
-        try:
-            body()
-        finally:
-            g.capture_end()
-    torch.cuda.current_stream(device).wait_stream(s)
+    every round, so capture here without that.  With concurrent song searches
+    the capture runs alone (``HostTurns``): no other thread's CUDA call may land
+    inside it."""
+    turns = getattr(_host, "lock", None)
+    if turns is not None:
+        turns.begin_capture()
+    try:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=device)
+        s.wait_stream(torch.cuda.current_stream(device))
+        with torch.cuda.stream(s):
+            g.capture_begin(capture_error_mode="thread_local")
+            try:
+                body()
+            finally:
+                g.capture_end()
+        torch.cuda.current_stream(device).wait_stream(s)
+    finally:
+        if turns is not None:
+            turns.end_capture()
     return g
 
 
-# Concurrent song searches (songs.search_songs): host threads take turns issuing
-# GPU work under one lock and hand it over only while blocked on their own
-# stream, so no other thread's API call can land inside a graph capture.
+class HostTurns:
+    """Host turns of concurrent song searches (songs.search_songs): any number of
+    threads issue GPU work at once, a graph capture runs alone.  A thread holds a
+    turn while it runs and gives it up only while blocked on its own stream
+    (``host_wait``), so a capture waits for every other thread to reach such a
+    wait (unguarded, other threads' pinned allocations invalidated captures)."""
+
+    def __init__(self):
+        self.cv = threading.Condition()
+        self.active = 0        # threads holding a turn
+        self.capturing = False
+        self.waiting = 0       # captures waiting to start (they go first)
+
+    def acquire(self):
+        with self.cv:
+            while self.capturing or self.waiting:
+                self.cv.wait()
+            self.active += 1
+
+    def release(self):
+        with self.cv:
+            self.active -= 1
+            self.cv.notify_all()
+
+    def begin_capture(self):  # the caller holds a turn
+        with self.cv:
+            self.active -= 1
+            self.waiting += 1
+            self.cv.notify_all()
+            while self.capturing or self.active:
+                self.cv.wait()
+            self.waiting -= 1
+            self.capturing = True
+
+    def end_capture(self):
+        with self.cv:
+            self.capturing = False
+            self.active += 1
+            self.cv.notify_all()
+
+
 _host = threading.local()
 
 
 def host_wait(obj) -> None:
-    """``obj.synchronize()`` (a stream or event), handing the host turn to another
-    song's thread meanwhile when searches run concurrently."""
+    """``obj.synchronize()`` (a stream or event), giving up the host turn meanwhile
+    when searches run concurrently (a pending capture can start)."""
     lk = getattr(_host, "lock", None)
     if lk is None:
         obj.synchronize()

@@ -112,9 +112,8 @@ def search_songs(specs, mine, inputs, concurrent=1, iterations=12, device="cuda"
     thread and one CUDA stream each, songs taken costliest-first from a shared
     queue) let their kernels overlap.  Searches stay independent: each has its
     own engines, streams and graphs, and the results are the same as running
-    the songs one after another.  The threads take turns on the host (one lock,
-    released only while a thread waits on its own stream, ``engine.host_wait``),
-    so no other thread's CUDA call can land inside a graph capture.  Returns the per-song summaries in ``mine``
+    the songs one after another.  The threads issue concurrently except around
+    graph captures, which run alone (``engine.HostTurns``).  Returns the per-song summaries in ``mine``
     order."""
     if concurrent <= 1:
         return [search_song(specs[i], *inputs[i], iterations=iterations, device=device) for i in mine]
@@ -126,15 +125,15 @@ def search_songs(specs, mine, inputs, concurrent=1, iterations=12, device="cuda"
     dev = engine.ensure_device(device)  # library + tables once, before the threads start
     order = sorted(mine, key=lambda i: (-song_costs([specs[i]])[0], i))
     lock = threading.Lock()
-    turn = threading.Lock()  # the host turn: held while issuing GPU work, handed over while waiting
+    turn = engine.HostTurns()
     out, errors = {}, []
 
     def worker():
         torch.cuda.set_device(dev)
         stream = torch.cuda.Stream(device=dev)
         engine._host.lock = turn
-        # fine-tunes replay a captured step too: a replay frees the host turn for
-        # the other songs, where an eager step would hold it for every launch
+        # fine-tunes replay a captured step too: fewer host launches per step
+        # competing for the interpreter with the other songs' threads
         engine._host.graph_min_steps = 1
         turn.acquire()
         try:
