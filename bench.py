@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--song-concurrency", type=int, default=1,
+    ap.add_argument("--song-concurrency", type=int, default=4,
                     help="songs searched concurrently per GPU (host threads + CUDA streams)")
     ap.add_argument("--songs", type=int, default=8,
                     help="config-5 desk-recipe pruning searches per GPU for songs/hour (0: skip)")
