@@ -200,3 +200,43 @@ def test_lpt_assignment_balances_and_is_deterministic():
     assert max(loads) / min(loads) < 1.15
     assert a == assign_lpt(costs, 8)
     assert all(8 <= s.tracks <= 24 and s.subgroups == max(1, round(s.tracks / 4)) for s in specs)
+
+
+def test_host_turns_run_captures_alone():
+    """Concurrent song searches (songs.search_songs): threads hold turns at once, a
+    graph capture starts only when every other thread has given its turn up
+    (engine.host_wait) and no turn is taken while it runs."""
+    import threading
+    import time
+
+    from paper_2509_15948_b200.engine import HostTurns
+
+    turns, seen, overlap = HostTurns(), [], []
+
+    def worker(k):
+        turns.acquire()
+        for i in range(40):
+            time.sleep(0.0005)       # issuing work while holding the turn
+            with turns.cv:
+                overlap.append(turns.active)
+            if i % 8 == k % 8:
+                turns.begin_capture()
+                with turns.cv:
+                    assert turns.capturing and turns.active == 0
+                seen.append(k)
+                time.sleep(0.0005)
+                turns.end_capture()
+            turns.release()          # host_wait: blocked on its own stream
+            time.sleep(0.0002)
+            turns.acquire()
+        turns.release()
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=30)
+    assert not any(t.is_alive() for t in threads)
+    assert sorted(seen) == sorted(k for k in range(4) for _ in range(5))
+    assert max(overlap) > 1  # turns were held concurrently outside captures
+    assert turns.active == 0 and not turns.capturing and turns.waiting == 0
