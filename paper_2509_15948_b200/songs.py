@@ -12,6 +12,7 @@ manifests (mg/cli.py:185-189).
 from __future__ import annotations
 
 import heapq
+import os
 import time
 from dataclasses import asdict, dataclass
 
@@ -134,7 +135,7 @@ def search_songs(specs, mine, inputs, concurrent=1, iterations=12, device="cuda"
         engine._host.lock = turn
         # fine-tunes replay a captured step too: fewer host launches per step
         # competing for the interpreter with the other songs' threads
-        engine._host.graph_min_steps = 1
+        engine._host.graph_min_steps = int(os.environ.get("MG_CONCURRENT_GRAPH_MIN_STEPS", "1"))
         turn.acquire()
         try:
             with torch.cuda.stream(stream):
