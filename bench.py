@@ -64,7 +64,7 @@ def parse():
 
 def make_inputs(seed, K, S, L, render_target):
     from paper_2509_15948_b200.console import build_console, init_params
-    from paper_2509_15948_b200.synth import SynthSpec, make_stems_f32, manifest_for
+    from workloads import SynthSpec, make_stems_f32, manifest_for
     spec = SynthSpec(tracks=K, subgroups=S, duration_seconds=L / 30000)
     stems = make_stems_f32(spec, seed, L)
     graph, zeros = build_console(manifest_for(spec))

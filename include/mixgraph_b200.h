@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define MGB_ABI_VERSION 2
+#define MGB_ABI_VERSION 3
 
 /* One homogeneous schedule level (Algorithm 1 step) of B same-type nodes.
  * Replaces processors.KERNELS[tag](u, p) + drywet_wrap(ybar, u, w)
@@ -96,9 +96,17 @@ int mgb_level_backward(const MgbLevel* level, void* stream);
 int mgb_level_forward_phase(const MgbLevel* level, int phase, void* stream);
 int mgb_level_backward_phase(const MgbLevel* level, int phase, void* stream);
 
-/* Number of kernel launches this library has enqueued so far (host counter;
- * a launch captured into a CUDA graph counts once, at capture). */
+/* Number of kernel launches this library has enqueued so far (host counter,
+ * atomic across host threads; a launch captured into a CUDA graph counts once,
+ * at capture). */
 long long mgb_launch_count(void);
+
+/* A new non-blocking CUDA stream on the current device, owned by the caller
+ * (NULL on failure); mgb_stream_destroy releases it.  Concurrent song searches
+ * give every host thread its own streams (torch hands out pooled streams, which
+ * two threads could share while one of them is capturing a CUDA graph). */
+void* mgb_stream_create(void);
+int mgb_stream_destroy(void* stream);
 
 /* Effective dry/wet weights w = sigmoid(raw) * mask (mg/scheduler.py:218-222).
  * mask may be NULL. */
@@ -162,11 +170,16 @@ int mgb_mrstft_backward(const MgbLoss* loss, const float* y_l, const float* y_r,
  * d-bank z gradients (rows of 880 at [d_off, d_off + 880*d_rows)); after it,
  * the unit-disk projection (mg/optimizer.py:127-137).  The raw-weight
  * gradient is assembled from dL/dw: g_raw = gw * mask * s(1-s) + alpha_p s(1-s)
- * over [w_off, w_off + P).  If loss_guard (device scalar) is non-finite the
- * parameters and moments are left untouched (NonFiniteLoss, mg/optimizer.py:164-171). */
+ * over [w_off, w_off + P).  If loss_guard (device scalar, this step's total
+ * loss) is non-finite the parameters and moments are left untouched
+ * (NonFiniteLoss, mg/optimizer.py:164-171).  halt (device scalar, may be NULL)
+ * makes that sticky for a run of steps: a non-finite loss_guard sets *halt = 1,
+ * and while *halt != 0 no step updates anything (the reference stops the run at
+ * the first non-finite loss, mg/optimizer.py:170-171, 208-215).  The caller
+ * zeroes *halt when a run starts. */
 int mgb_adamw_step(double* p, double* g, double* m, double* v, long long n, long long d_off, int d_rows,
                    long long w_off, int P, const double* gw, const double* mask, const double* step_scalars,
-                   const double* loss_guard, void* stream);
+                   const double* loss_guard, double* halt, void* stream);
 
 /* sum over the P effective weights' sigmoid (sparsity term, mg/losses.py:181-183) */
 int mgb_sparsity(const double* raw, int P, double* out, void* stream);

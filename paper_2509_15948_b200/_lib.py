@@ -56,6 +56,7 @@ class DeviceError(RuntimeError):
 
 
 _lib = None
+ABI_VERSION = 3  # MGB_ABI_VERSION in include/mixgraph_b200.h
 
 
 def lib():
@@ -69,6 +70,9 @@ def lib():
             "(nvcc, sm_100a). There is no CPU fallback.")
     L = ctypes.CDLL(LIB_PATH)
     L.mgb_abi_version.restype = c_int
+    if L.mgb_abi_version() != ABI_VERSION:
+        raise LibraryMissing(f"{LIB_PATH} has ABI {L.mgb_abi_version()}, this binding needs {ABI_VERSION}; "
+                             "rebuild it (__graft_entry__.build())")
     L.mgb_init.argtypes = [c_void_p, c_void_p, c_void_p]
     L.mgb_level_workspace.argtypes = [c_char, c_int, c_int]
     L.mgb_level_workspace.restype = c_size_t
@@ -86,12 +90,16 @@ def lib():
     L.mgb_mrstft_backward.argtypes = [ctypes.POINTER(MgbLoss), c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p]
     L.mgb_adamw_step.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_longlong, c_int,
-                                 c_longlong, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+                                 c_longlong, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p]
     L.mgb_sparsity.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
+    L.mgb_stream_create.argtypes = []
+    L.mgb_stream_create.restype = c_void_p
+    L.mgb_stream_destroy.argtypes = [c_void_p]
     for name in ("mgb_init", "mgb_level_forward", "mgb_level_backward", "mgb_level_forward_phase",
                  "mgb_level_backward_phase", "mgb_weights", "mgb_bus_sum",
                  "mgb_fft", "mgb_mrstft_target", "mgb_mrstft_forward", "mgb_mrstft_backward",
-                 "mgb_adamw_step", "mgb_sparsity"):
+                 "mgb_adamw_step", "mgb_sparsity", "mgb_stream_destroy"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -99,7 +107,8 @@ def lib():
 
 EXPORTED = ("mgb_abi_version", "mgb_init", "mgb_level_workspace", "mgb_level_forward",
             "mgb_level_backward", "mgb_level_forward_phase", "mgb_level_backward_phase", "mgb_launch_count", "mgb_weights", "mgb_bus_sum", "mgb_fft", "mgb_mrstft_target",
-            "mgb_mrstft_forward", "mgb_mrstft_backward", "mgb_adamw_step", "mgb_sparsity")
+            "mgb_mrstft_forward", "mgb_mrstft_backward", "mgb_adamw_step", "mgb_sparsity",
+            "mgb_stream_create", "mgb_stream_destroy")
 
 
 def check(rc, what):

@@ -1,6 +1,8 @@
 // extern "C" entry points of libmixgraph_b200 (see include/mixgraph_b200.h).
 #include <stdio.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "mgb_internal.h"
 #include "tables.cuh"
@@ -97,8 +99,19 @@ extern "C" int mgb_level_backward(const MgbLevel* lv, void* stream) {
   return mgb_level_backward_phase(lv, 2, stream);
 }
 
-long long g_mgb_launches = 0;
-extern "C" long long mgb_launch_count(void) { return g_mgb_launches; }
+static std::atomic<long long> g_mgb_launches{0};
+void mgb_count_launch() { g_mgb_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" long long mgb_launch_count(void) { return g_mgb_launches.load(std::memory_order_relaxed); }
+
+extern "C" void* mgb_stream_create(void) {
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  return (void*)s;
+}
+
+extern "C" int mgb_stream_destroy(void* stream) {
+  return cudaStreamDestroy((cudaStream_t)stream) == cudaSuccess ? 0 : 2;
+}
 
 extern "C" int mgb_fft(const void* in, void* out, void* tmp, int batch, int log2n, int inverse, float scale,
                        void* stream) {

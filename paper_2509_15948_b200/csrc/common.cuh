@@ -278,7 +278,8 @@ static inline cudaError_t mgb_launch(void (*kernel)(KArgs...), dim3 grid, dim3 b
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+void mgb_count_launch();  // capi.cu (atomic)
+
 // after EVERY kernel launch: error check + the host launch counter (mgb_launch_count)
-extern long long g_mgb_launches;
 #define MGB_CHECK_LAUNCH() \
-  do { ++g_mgb_launches; cudaError_t e__ = cudaGetLastError(); if (e__ != cudaSuccess) return 2; } while (0)
+  do { mgb_count_launch(); cudaError_t e__ = cudaGetLastError(); if (e__ != cudaSuccess) return 2; } while (0)

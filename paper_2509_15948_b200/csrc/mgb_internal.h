@@ -33,8 +33,9 @@ int mgb_dyn_backward(const MgbLevel* lv, cudaStream_t st);
 int mgb_dyn_param_grad(const MgbLevel* lv, cudaStream_t st);
 size_t mgb_dyn_workspace(char tag, int B, int L);
 
-// host-side launch counter (mgb_launch_count); every launch site bumps it
-extern long long g_mgb_launches;
+// host-side launch counter (mgb_launch_count); every launch site bumps it.  Song
+// searches issue from several host threads at once, so the counter is atomic.
+void mgb_count_launch();
 
 static inline int mgb_log2_ceil(long long n) {
   int l = 0;

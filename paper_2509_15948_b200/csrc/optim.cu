@@ -45,11 +45,26 @@ __global__ void k_delay_rule(const double* __restrict__ p, double* __restrict__ 
   g[base + 20 + m] = si + k * ci;
 }
 
+// NonFiniteLoss (mg/optimizer.py:164-171): the reference raises at the first step whose
+// loss is non-finite, before any update, and the run ends there.  On the device the
+// flag is sticky: once a step's loss is non-finite, that step and every later step of
+// the same run leave parameters and moments untouched (the host raises after reading
+// the per-step losses back, with the parameters as of the last finite step).
+__global__ void k_guard(const double* __restrict__ loss, double* __restrict__ halt) {
+  mgb_pdl_entry();
+  if (!isfinite(*loss)) *halt = 1.0;
+}
+
+__device__ __forceinline__ bool halted(const double* guard, const double* halt) {
+  if (halt) return *halt != 0.0;
+  return guard && !isfinite(*guard);
+}
+
 __global__ void k_adamw(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
                         double* __restrict__ v, long long n, const double* __restrict__ sc,
-                        const double* __restrict__ guard) {
+                        const double* __restrict__ guard, const double* __restrict__ halt) {
   mgb_pdl_entry();
-  if (guard && !isfinite(*guard)) return;  // NonFiniteLoss: the reference raises before updating
+  if (halted(guard, halt)) return;
   const double lr = sc[0], b1 = sc[1], b2 = sc[2], eps = sc[3], wd = sc[4], c1 = sc[5], c2 = sc[6];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double gi = g[i];
@@ -66,9 +81,10 @@ __global__ void k_adamw(double* __restrict__ p, const double* __restrict__ g, do
   }
 }
 
-__global__ void k_project(double* __restrict__ p, long long d_off, int rows, const double* __restrict__ guard) {
+__global__ void k_project(double* __restrict__ p, long long d_off, int rows, const double* __restrict__ guard,
+                          const double* __restrict__ halt) {
   mgb_pdl_entry();
-  if (guard && !isfinite(*guard)) return;
+  if (halted(guard, halt)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * 40) return;
   const int row = i / 40, c = (i / 20) % 2, mm = i % 20;
@@ -93,9 +109,15 @@ __global__ void k_sparsity(const double* __restrict__ raw, int P, double* __rest
 
 extern "C" int mgb_adamw_step(double* p, double* g, double* m, double* v, long long n, long long d_off, int d_rows,
                               long long w_off, int P, const double* gw, const double* mask,
-                              const double* step_scalars, const double* loss_guard, void* stream) {
+                              const double* step_scalars, const double* loss_guard, double* halt,
+                              void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n <= 0) return 0;
+  if (halt && !loss_guard) return 1;
+  if (halt) {
+    mgb_launch(k_guard, dim3(1), dim3(1), 0, st, loss_guard, halt);
+    MGB_CHECK_LAUNCH();
+  }
   if (P > 0) {
     mgb_launch(k_raw_grad, dim3((P + 255) / 256), dim3(256), 0, st, p, g, w_off, P, gw, mask, step_scalars);
     MGB_CHECK_LAUNCH();
@@ -105,10 +127,10 @@ extern "C" int mgb_adamw_step(double* p, double* g, double* m, double* v, long l
     MGB_CHECK_LAUNCH();
   }
   const int blocks = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
-  mgb_launch(k_adamw, dim3(blocks), dim3(256), 0, st, p, g, m, v, n, step_scalars, loss_guard);
+  mgb_launch(k_adamw, dim3(blocks), dim3(256), 0, st, p, g, m, v, n, step_scalars, loss_guard, (const double*)halt);
   MGB_CHECK_LAUNCH();
   if (d_rows > 0) {
-    mgb_launch(k_project, dim3((d_rows * 40 + 255) / 256), dim3(256), 0, st, p, d_off, d_rows, loss_guard);
+    mgb_launch(k_project, dim3((d_rows * 40 + 255) / 256), dim3(256), 0, st, p, d_off, d_rows, loss_guard, (const double*)halt);
     MGB_CHECK_LAUNCH();
   }
   return 0;

@@ -71,7 +71,7 @@ def capture_graph(body, device):
         turns.begin_capture()
     try:
         g = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream(device=device)
+        s = own_stream(device, "capture")
         s.wait_stream(torch.cuda.current_stream(device))
         with torch.cuda.stream(s):
             g.capture_begin(capture_error_mode="thread_local")
@@ -132,16 +132,45 @@ _host = threading.local()
 
 def host_wait(obj) -> None:
     """``obj.synchronize()`` (a stream or event), giving up the host turn meanwhile
-    when searches run concurrently (a pending capture can start)."""
+    when searches run concurrently (a pending capture can start).
+
+    A stream is waited on through an event recorded while this thread still
+    holds its turn: synchronising an event is legal while another thread
+    captures a graph, synchronising a stream that capture reaches is not."""
     lk = getattr(_host, "lock", None)
     if lk is None:
         obj.synchronize()
         return
+    if isinstance(obj, torch.cuda.Stream):
+        ev = torch.cuda.Event()
+        ev.record(obj)
+        obj = ev
     lk.release()
     try:
         obj.synchronize()
     finally:
         lk.acquire()
+
+
+_own_streams = {}
+
+
+def own_stream(device, role: str) -> torch.cuda.Stream:
+    """A stream owned by the calling host thread for ``role`` (created once by
+    ``mgb_stream_create`` and reused).  torch.cuda.Stream() hands out streams
+    round-robin from a pool shared by all threads, so two concurrent song
+    searches could otherwise end up on one stream while one of them captures."""
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    key = (threading.get_ident(), idx, role)
+    s = _own_streams.get(key)
+    if s is None:
+        with torch.cuda.device(idx):
+            raw = lib().mgb_stream_create()
+        if not raw:
+            raise _lib.DeviceError("mgb_stream_create failed")
+        s = _own_streams[key] = torch.cuda.ExternalStream(raw, device=torch.device("cuda", idx))
+    return s
 
 
 def stream_ptr():
@@ -572,7 +601,9 @@ class TrainEngine:
         self.use_graph = use_graph
         self._graph = None
         self.d_rows = lay.rows["d"]
-        self.side = torch.cuda.Stream(device=dev)
+        self.side = own_stream(dev, "side")
+        # sticky NonFiniteLoss flag of the current run (mgb_adamw_step); zeroed per run
+        self.halt = torch.zeros((), dtype=F64, device=dev)
 
     # -- state ------------------------------------------------------------
     def load_params(self, params):
@@ -623,7 +654,7 @@ class TrainEngine:
         lay = self.layout
         check(Ld.mgb_adamw_step(ptr(self.params), ptr(self.grads), ptr(self.m), ptr(self.v), lay.n,
                                 lay.off["d"], self.d_rows, lay.w_off, P, ptr(plan.gw), None,
-                                ptr(self.scalars), ptr(self.vals), stream_ptr()), "mgb_adamw_step")
+                                ptr(self.scalars), ptr(self.vals), ptr(self.halt), stream_ptr()), "mgb_adamw_step")
 
     def grads_only(self, alpha_p=0.0):
         """Eager forward + backward without the optimiser (test hook).
@@ -650,7 +681,7 @@ class TrainEngine:
         """Library kernels one step enqueues (counted by the C ABI over one eager step)."""
         if getattr(self, "_launches", None) is None:
             Ld = lib()
-            snap = [self.params.clone(), self.m.clone(), self.v.clone(), self.t]
+            snap = [self.params.clone(), self.m.clone(), self.v.clone(), self.halt.clone(), self.t]
             self._set_scalars(0.0)
             n0 = Ld.mgb_launch_count()
             self._body()
@@ -659,7 +690,8 @@ class TrainEngine:
             self.params.copy_(snap[0])
             self.m.copy_(snap[1])
             self.v.copy_(snap[2])
-            self.t = snap[3]
+            self.halt.copy_(snap[3])
+            self.t = snap[4]
         return self._launches
 
     _RING = 64
@@ -691,14 +723,15 @@ class TrainEngine:
             return
         if self._graph is None:
             # warm-up run outside capture (sets function attributes, JIT, allocations)
-            s = torch.cuda.Stream(device=self.device)
+            s = own_stream(self.device, "warm")
             s.wait_stream(current_stream())
             with torch.cuda.stream(s):
-                snap = [self.params.clone(), self.m.clone(), self.v.clone()]
+                snap = [self.params.clone(), self.m.clone(), self.v.clone(), self.halt.clone()]
                 self._body()
                 self.params.copy_(snap[0])
                 self.m.copy_(snap[1])
                 self.v.copy_(snap[2])
+                self.halt.copy_(snap[3])
             current_stream().wait_stream(s)
             current_stream().synchronize()  # not device-wide: other songs may be capturing
             self._graph = capture_graph(self._body, self.device)
@@ -805,7 +838,7 @@ class EvalEngine:
             self._body()
             return
         if self._graph is None:
-            s = torch.cuda.Stream(device=self.device)
+            s = own_stream(self.device, "warm")
             s.wait_stream(current_stream())
             with torch.cuda.stream(s):
                 self._body()

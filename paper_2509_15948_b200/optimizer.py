@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from .common import rng_for, seconds_to_samples
-from .engine import F32, TrainEngine, ensure_device, host_wait
+from .engine import F32, TrainEngine, ensure_device, host_wait, own_stream
 from .graph import MixGraph, ParamStore
 from .losses import LossConfig
 from .schedule import plan_indices, schedule_for
@@ -146,10 +146,11 @@ def train_step(graph, params: ParamStore, segment, cfg: TrainConfig, opt: AdamW,
     eng.target.copy_(torch.as_tensor(np.asarray(target) if not torch.is_tensor(target) else target,
                                      dtype=F32), non_blocking=True)
     eng.t = opt.t
+    eng.halt.zero_()
     eng.step_async(alpha_p)
     values = eng.read_values()
     if not np.isfinite(values["loss"]):
-        eng.t -= 1
+        eng.t -= 1  # the device left params and moments untouched
         raise NonFiniteLoss(f"non-finite loss: {values}")
     opt.t = eng.t
     eng.store_params(params)
@@ -181,8 +182,10 @@ def train_segments(graph, params: ParamStore, segments, cfg: TrainConfig, opt: A
     updated once at the end.  Same arithmetic and per-step semantics as
     calling ``train_step`` in a loop (mg/optimizer.py:140-186); a non-finite
     loss leaves that step's update undone on the device and raises
-    ``NonFiniteLoss`` after the run, like ``train``.  Pass pinned torch
-    tensors to avoid a pinning copy per segment."""
+    ``NonFiniteLoss`` after the run, like ``train``: no update happens from
+    the first non-finite step on, ``params`` and ``opt.t`` are those after the
+    last finite step and ``history`` holds the finite steps only.  Pass pinned
+    torch tensors to avoid a pinning copy per segment."""
     history = history if history is not None else []
     it = iter(segments)
     seg = next(it, None)
@@ -192,9 +195,11 @@ def train_segments(graph, params: ParamStore, segments, cfg: TrainConfig, opt: A
     L = seg[0].shape[-1]
     eng = opt.engine(graph, L, cfg, schedule)
     eng.load_params(params)
+    eng.halt.zero_()
+    t_start = eng.t = opt.t
     dev = eng.device
     comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(device=dev)
+    copy = own_stream(dev, "copy")
     stage = [(torch.empty_like(eng.plan.stems), torch.empty_like(eng.target)) for _ in range(2)]
     freed = [None, None]  # event: the compute stream is done reading the slot
 
@@ -245,15 +250,23 @@ def train_segments(graph, params: ParamStore, segments, cfg: TrainConfig, opt: A
         out.append(ring[r].tolist())
     del keep
     wall = (time.perf_counter() - t0) / k
-    opt.t = eng.t
+    bad = _first_nonfinite([v[0] for v in out])
+    opt.t = eng.t = t_start + (k if bad is None else bad)
     eng.store_params(params)
     base = len(history)
-    for i, v in enumerate(out):
-        if not np.isfinite(v[0]):
-            raise NonFiniteLoss(f"non-finite loss at step {i}: {v}")
+    for i, v in enumerate(out[:bad]):
         history.append({"loss": v[0], "L_a": v[1], "L_g": v[2], "L_p": v[3], "step": base + i,
                         "wall_s": wall})
+    if bad is not None:
+        raise NonFiniteLoss(f"non-finite loss at step {bad}: {out[bad]}")
     return history
+
+
+def _first_nonfinite(losses):
+    for i, v in enumerate(losses):
+        if not np.isfinite(v):
+            return i
+    return None
 
 
 def train(graph, params: ParamStore, session: Session, cfg: TrainConfig, schedule=None,
@@ -281,6 +294,8 @@ def train(graph, params: ParamStore, session: Session, cfg: TrainConfig, schedul
         eng.plan.stems.copy_(st_dev)
         eng.target.copy_(tg_dev)
     vals = torch.zeros((cfg.steps, 4), dtype=torch.float64, device=dev)
+    eng.halt.zero_()
+    rng_state = rng.bit_generator.state
     t0 = time.perf_counter()
     for step in range(cfg.steps):
         offset = int(rng.integers(0, session.length - seg + 1))
@@ -292,11 +307,19 @@ def train(graph, params: ParamStore, session: Session, cfg: TrainConfig, schedul
     host_wait(torch.cuda.current_stream())
     host = vals.cpu().numpy()
     wall = (time.perf_counter() - t0) / cfg.steps
-    opt.t = eng.t
+    # NonFiniteLoss (mg/optimizer.py:170-171): the reference stops at the first
+    # non-finite step.  The device's sticky flag skipped that step's update and
+    # every later one, so the parameters are those after the last finite step;
+    # the step count, history and segment RNG are put where the reference leaves them.
+    bad = _first_nonfinite(host[:, 0])
+    opt.t = eng.t = cfg.steps if bad is None else bad
     eng.store_params(params)
-    for i, v in enumerate(host):
-        if not np.all(np.isfinite(v[:1])):
-            raise NonFiniteLoss(f"non-finite loss at step {i}: {v.tolist()}")
+    for i, v in enumerate(host[:bad]):
         history.append({"loss": float(v[0]), "L_a": float(v[1]), "L_g": float(v[2]), "L_p": float(v[3]),
                         "step": len(history), "wall_s": wall})
+    if bad is not None:
+        rng.bit_generator.state = rng_state
+        for _ in range(bad + 1):
+            rng.integers(0, session.length - seg + 1)
+        raise NonFiniteLoss(f"non-finite loss at step {bad}: {host[bad].tolist()}")
     return history

@@ -11,6 +11,7 @@ import numpy as np
 import torch
 
 from .engine import F32, F64, ParamLayout, RenderPlan, ensure_device
+from .graph import topological_order, validate
 from .schedule import (CONSOLE_SEQUENCE, GREEDY_TIE_ORDER, LengthMismatch, NotAConsole, Schedule,  # noqa: F401
                        SchedulerError, StepPlan, console_chains, plan_indices, schedule_console,
                        schedule_for, schedule_greedy)
@@ -51,9 +52,23 @@ def execute_batched(graph, params, sources, schedule=None, mask=None, device="cu
     return plan.y.clone(), plan.reg_total()
 
 
+def node_schedule(graph) -> Schedule:
+    """One node per step in topological order (inputs first, the output last):
+    the visiting order of the reference's one-node-at-a-time executor."""
+    validate(graph)
+    inputs = set(graph.nodes_of_type("i"))
+    output = graph.nodes_of_type("o")[0]
+    order = [v for v in topological_order(graph) if v not in inputs and v != output]
+    subsets = [sorted(inputs)] + [[v] for v in order] + [[output]]
+    seq = "i" + "".join(graph.node_types[v] for v in order) + "o"
+    return plan_indices(graph, Schedule(seq, subsets))
+
+
 def execute_reference(graph, params, sources, device="cuda"):
-    """Same contract; in this implementation the batched device path IS the executor."""
-    return execute_batched(graph, params, sources, schedule_greedy(graph), device=device)
+    """One-node-at-a-time executor (mg/scheduler.py:266-298), same contract as
+    ``execute_batched``: every processor node is its own level launch of batch 1,
+    visited in topological order.  The unbatched check of the batched path."""
+    return execute_batched(graph, params, sources, node_schedule(graph), device=device)
 
 
 def effective_weights(params, mask=None):
@@ -61,6 +76,6 @@ def effective_weights(params, mask=None):
     return w * np.asarray(mask, dtype=np.float64) if mask is not None else w
 
 
-__all__ = ["execute_batched", "execute_reference", "effective_weights", "Schedule", "StepPlan",
+__all__ = ["execute_batched", "execute_reference", "node_schedule", "effective_weights", "Schedule", "StepPlan",
            "schedule_greedy", "schedule_console", "plan_indices", "console_chains", "NotAConsole",
            "LengthMismatch", "SchedulerError", "F32", "F64"]

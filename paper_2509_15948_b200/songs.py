@@ -131,7 +131,7 @@ def search_songs(specs, mine, inputs, concurrent=1, iterations=12, device="cuda"
 
     def worker():
         torch.cuda.set_device(dev)
-        stream = torch.cuda.Stream(device=dev)
+        stream = engine.own_stream(dev, "main")
         engine._host.lock = turn
         # fine-tunes replay a captured step too: fewer host launches per step
         # competing for the interpreter with the other songs' threads

@@ -81,7 +81,7 @@ def test_mrstft_matches_reference_golden(dev, name, sizes):
 
 def _step_setup():
     from paper_2509_15948_b200.console import build_console, init_params
-    from paper_2509_15948_b200.synth import SynthSpec, make_stems_f32, manifest_for
+    from workloads import SynthSpec, make_stems_f32, manifest_for
     K, S, L, s_stems, s_p, s_t = step_spec()
     spec = SynthSpec(tracks=K, subgroups=S, duration_seconds=L / 30000)
     stems = make_stems_f32(spec, s_stems, L)

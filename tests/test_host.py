@@ -16,7 +16,7 @@ from conftest import ROOT, golden, normrel
 
 def _declared_symbols():
     text = open(os.path.join(ROOT, "include", "mixgraph_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|long long)\s+(mgb_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|long long|void\s*\*)\s*(mgb_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_the_boundary():
@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     L = ctypes.CDLL(_lib.LIB_PATH)
     for s in _declared_symbols():
         assert hasattr(L, s), s
-    assert L.mgb_abi_version() == 2
+    assert L.mgb_abi_version() == 3
     lib = _lib.lib()
     # workspace queries are host-only arithmetic
     assert lib.mgb_level_workspace(b"g", 4, 1000) > 0
@@ -91,7 +91,7 @@ def test_tables_match_reference():
 
 def test_stems_match_reference():
     from golden_inputs import step_spec
-    from paper_2509_15948_b200.synth import SynthSpec, make_stems_f32
+    from workloads import SynthSpec, make_stems_f32
     gs = golden("step.npz")
     K, S, L, seed, _, _ = step_spec()
     stems = make_stems_f32(SynthSpec(tracks=K, subgroups=S, duration_seconds=L / 30000), seed, L)

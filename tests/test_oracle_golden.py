@@ -57,7 +57,7 @@ def test_oracle_mrstft_matches_reference(name, sizes):
 
 def test_oracle_train_step_matches_reference():
     from paper_2509_15948_b200.console import build_console, init_params
-    from paper_2509_15948_b200.synth import SynthSpec, make_stems_f32, manifest_for
+    from workloads import SynthSpec, make_stems_f32, manifest_for
 
     gs = golden("step.npz")
     K, S, L, s_stems, s_p, s_t = step_spec()

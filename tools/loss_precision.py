@@ -6,7 +6,7 @@ sys.path.insert(0, '.')
 import torch
 from oracle import mixgraph_oracle as O
 from paper_2509_15948_b200.console import build_console, init_params
-from paper_2509_15948_b200.synth import SynthSpec, make_stems_f32, manifest_for
+from workloads import SynthSpec, make_stems_f32, manifest_for
 K,S,L = 4,1,132300
 spec = SynthSpec(tracks=K, subgroups=S, duration_seconds=L/30000)
 stems = make_stems_f32(spec, 0, L)

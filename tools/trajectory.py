@@ -18,7 +18,7 @@ from paper_2509_15948_b200.console import build_console, init_params  # noqa: E4
 from paper_2509_15948_b200.engine import TrainEngine  # noqa: E402
 from paper_2509_15948_b200.optimizer import TrainConfig, _EngineCfg, make_optimizer  # noqa: E402
 from paper_2509_15948_b200.scheduler import execute_batched  # noqa: E402
-from paper_2509_15948_b200.synth import SynthSpec, make_stems_f32, manifest_for  # noqa: E402
+from workloads import SynthSpec, make_stems_f32, manifest_for  # noqa: E402
 
 
 def main():

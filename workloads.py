@@ -1,9 +1,12 @@
-"""Synthetic dry stems (input data generator, not on the hot path).
+"""Synthetic workloads for the bench and the tests (input data, not product code).
 
-Byte-identical restatement of ``mg/synth.py:34-115`` (``SynthSpec``,
-``make_stems``) so that the bench and the parity tests feed the device path
-exactly the stems the reference would generate for a seed.  Stems are
-round-tripped through float32 as ``mg/synth.py:217`` does.
+The reference's stem generator (``mg/synth.py:34-115``: ``SynthSpec``,
+``make_stems``) restated byte-identically so that the bench and the parity
+tests feed the device path exactly the stems the reference would generate for
+a seed (``tests/test_reference_api.py`` pins it against the reference).  Stems
+are round-tripped through float32 as ``mg/synth.py:217`` does.  It lives
+outside the ``paper_2509_15948_b200`` package: input generation is out of the
+hot path's scope.
 """
 
 from __future__ import annotations
@@ -12,8 +15,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .common import SAMPLE_RATE, rng_for
-from .console import SessionManifest, TrackEntry
+from paper_2509_15948_b200.common import SAMPLE_RATE, rng_for
+from paper_2509_15948_b200.console import SessionManifest, TrackEntry
 
 STEM_KINDS = ("tonal", "noise", "percussive")
 
