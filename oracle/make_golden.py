@@ -32,7 +32,7 @@ OUT = os.path.join(os.path.dirname(__file__), "..", "tests", "golden")
 
 def main():
     sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "tests"))
-    from golden_inputs import kernel_inputs, mrstft_inputs, step_spec
+    from golden_inputs import SCAN_ALPHAS, config1_spec, kernel_inputs, mrstft_inputs, scan_inputs, step_spec
 
     os.makedirs(OUT, exist_ok=True)
 
@@ -140,6 +140,58 @@ def main():
         out[f"after2_{t_}"] = v
     out["after2_w"] = params.raw_weights
     np.savez_compressed(os.path.join(OUT, "step.npz"), **out)
+
+    # 5. compressor / gate in the envelope scan's hard regime (alpha_raw 8..12, L = 40,000:
+    #    five 8192-sample chunks; the truncation term alpha^8192 is 0.05..0.95)
+    scan = {}
+    for tag in "cn":
+        for a in SCAN_ALPHAS:
+            u, p, w = scan_inputs(tag, a)
+            t = E.Tape()
+            ub, pb = t.leaf(u), t.leaf(p)
+            ybar, _ = P.KERNELS[tag](ub, pb)
+            t.backward(E.array_sum(E.mul(ybar, w)))
+            key = f"{tag}{int(a)}"
+            # signals stored as float32 (the device gates are 1e-4; float32 storage is 3e-8)
+            scan[f"{key}_ybar"] = E.value_of(ybar).astype(np.float32)
+            scan[f"{key}_gu"] = ub.grad.astype(np.float32)
+            scan[f"{key}_gp"] = pb.grad
+    np.savez_compressed(os.path.join(OUT, "scan.npz"), **scan)
+
+    # 6. BASELINE config 1: one full train_step, K=4 tracks + 1 subgroup, L = 132,300.
+    #    The target is rounded to float32 first so the device (float32 signals) and the
+    #    reference see the same target values.
+    K, S, L, seed_stems, seed_p, seed_t = config1_spec()
+    man = SessionManifest([TrackEntry(f"t{k}.wav", f"t{k}", f"bus{k % S}") for k in range(K)], "m.wav")
+    graph, zeros = build_console(man)
+    stems, _ = make_stems(SynthSpec(tracks=K, subgroups=S, duration_seconds=L / 30000), seed_stems)
+    stems = stems.astype(np.float32).astype(np.float64)[..., :L]
+    target = np.asarray(E.value_of(execute_reference(graph, init_params(zeros, seed_t), stems)[0]))
+    target = target.astype(np.float32).astype(np.float64)
+    params = init_params(zeros, seed_p)
+    cfg = TrainConfig(segment_seconds=L / 30000, warmup_seconds=1.0, steps=1)
+    sched = plan_indices(graph, schedule_console(graph))
+    y0 = np.asarray(E.value_of(
+        __import__("mixgraph.scheduler", fromlist=["execute_batched"]).execute_batched(
+            graph, params, stems, sched)[0]))
+    captured = {}
+    O._delay_gradient_rule, O.AdamW.step = spy, spy_step
+    try:
+        opt = make_optimizer(params, cfg)
+        values = train_step(graph, params, (stems, target), cfg, opt, sched)
+    finally:
+        O._delay_gradient_rule = orig_rule
+        O.AdamW.step = orig_step
+    out = {"target": target.astype(np.float32), "y": y0.astype(np.float32),
+           "stems_head": stems[..., :64], "stems_sum": stems.sum(axis=-1)}
+    for k in ("loss", "L_a", "L_g", "L_p"):
+        out[f"v_{k}"] = np.asarray(values[k])
+    for k, v in captured.items():
+        out[k] = v
+    for t_, v in params.params.items():
+        out[f"after_{t_}"] = v
+    out["after_w"] = params.raw_weights
+    np.savez_compressed(os.path.join(OUT, "config1_step.npz"), **out)
     print("golden fixtures written to", os.path.abspath(OUT))
 
 

@@ -52,3 +52,33 @@ def mrstft_inputs(length=40_000):
 def step_spec():
     """K, S, L, stems seed, param seed, target-param seed for the train_step golden."""
     return 2, 1, 33_000, 3, 0, 1
+
+
+SCAN_LEN, SCAN_ALPHAS = 40_000, (8.0, 10.0, 12.0)
+
+
+def scan_inputs(tag, a_raw, length=SCAN_LEN, B=2, seed=None):
+    """Compressor / gate inputs in the envelope scan's hard regime: alpha_raw 8..12
+    (time constants 3e3..1.6e5 samples, alpha^8192 = 0.05..0.95), so the exact
+    8192-tap truncation and the cross-chunk carries decide the envelope.  The
+    signal is amplitude-modulated noise so the knee branches are all visited."""
+    rng = np.random.default_rng(seed if seed is not None else 7000 + int(a_raw) + 100 * "cn".index(tag))
+    t = np.arange(length) / 30000.0
+    env = 0.15 + np.abs(np.sin(2 * np.pi * 2.3 * t)) + 0.5 * (np.sin(2 * np.pi * 0.7 * t) > 0.3)
+    u = 0.3 * rng.standard_normal((B, 2, length)) * env
+    p = np.zeros((B, 4))
+    p[:, 0] = a_raw + np.array([0.0, 0.37])[:B]
+    # thresholds at the envelope's median level (which falls as the ballistics slow
+    # down: the truncated filter's DC gain is 1 - alpha^8192), knee half-widths
+    # W = softplus(W_raw) of 0.47 / 0.31 around it: each row visits all three branches
+    t_mid = float(np.interp(a_raw, [5.0, 8.0, 10.0, 12.0], [-1.6, -1.75, -2.8, -4.7]))
+    p[:, 1] = (t_mid + np.array([-0.1, 0.2]))[:B]
+    p[:, 2] = [-0.5, -1.0][:B]
+    p[:, 3] = [0.9, 1.6][:B]
+    w = rng.standard_normal((B, 2, length))
+    return u, p, w
+
+
+def config1_spec():
+    """BASELINE config 1: K, S, L, stems seed, param seed, target-param seed."""
+    return 4, 1, 132_300, 3, 0, 1

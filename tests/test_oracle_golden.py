@@ -87,3 +87,52 @@ def test_oracle_train_step_matches_reference():
     np.testing.assert_allclose(v2["L_a"], float(gs["v2_L_a"]), rtol=1e-9)
     for t in "gsecnr":
         np.testing.assert_allclose(arrays_p[t], gs[f"after2_{t}"], rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("tag", ["c", "n"])
+@pytest.mark.parametrize("a_raw", [8.0, 10.0, 12.0])
+def test_oracle_envelope_scan_regime_matches_reference(tag, a_raw):
+    """Compressor / gate at alpha_raw 8..12 over five 8192-sample chunks (the
+    truncated-ballistics regime the device scan's correction term exists for)."""
+    from golden_inputs import scan_inputs
+    gsn = golden("scan.npz")
+    key = f"{tag}{int(a_raw)}"
+    u, p, w = scan_inputs(tag, a_raw)
+    ut = torch.tensor(u, requires_grad=True)
+    pt = torch.tensor(p, requires_grad=True)
+    ybar, _ = O.KERNELS[tag](ut, pt)
+    torch.sum(ybar * torch.tensor(w)).backward()
+    # the golden signals are stored as float32 (relative rounding ~3e-8)
+    assert normrel(ybar.detach().numpy(), gsn[f"{key}_ybar"]) < 1e-7
+    assert normrel(ut.grad.numpy(), gsn[f"{key}_gu"]) < 1e-7
+    assert normrel(pt.grad.numpy(), gsn[f"{key}_gp"]) < 1e-9
+
+
+def test_oracle_config1_step_matches_reference():
+    """BASELINE config 1 (4 tracks + 1 subgroup, L = 132,300): one train_step."""
+    from golden_inputs import config1_spec
+    from paper_2509_15948_b200.console import build_console, init_params
+    from workloads import SynthSpec, make_stems_f32, manifest_for
+
+    gs = golden("config1_step.npz")
+    K, S, L, s_stems, s_p, s_t = config1_spec()
+    spec = SynthSpec(tracks=K, subgroups=S, duration_seconds=L / 30000)
+    stems = make_stems_f32(spec, s_stems, L).astype(np.float64)
+    np.testing.assert_array_equal(stems[..., :64], gs["stems_head"])
+    graph, zeros = build_console(manifest_for(spec))
+    params = init_params(zeros, s_p)
+    p = {t: v.copy() for t, v in params.params.items()}
+    raw = params.raw_weights.copy()
+    target = gs["target"].astype(np.float64)
+    values, grads, y = O.render_loss_and_grads(graph, p, raw, stems, target, 30000, O.LossConfig())
+    assert normrel(y, gs["y"]) < 1e-7  # golden y stored as float32
+    np.testing.assert_allclose(values["L_a"], float(gs["v_L_a"]), rtol=1e-10)
+    np.testing.assert_allclose(values["L_g"], float(gs["v_L_g"]), rtol=1e-10)
+    for t in "gsecnr":
+        assert normrel(grads[t], gs[f"grad_{t}"], floor=1e-9) < 1e-7, t
+    assert normrel(grads["w"], gs["grad_w"], floor=1e-9) < 1e-7
+    assert normrel(grads["d"], gs["d_raw"], floor=1e-6) < 1e-6
+    opt = O.AdamW({**p, "w": raw})
+    O.train_step(graph, p, raw, stems, target, 30000, O.LossConfig(), opt)
+    for t in "gsecnr":
+        np.testing.assert_allclose(p[t], gs[f"after_{t}"], rtol=0, atol=1e-9)
