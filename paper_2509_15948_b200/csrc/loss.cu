@@ -515,12 +515,15 @@ int loss_attrs() {
 // Per-device side streams: the resolutions of one MRSTFT call are independent
 // until the finalize, so they are forked onto their own streams (event fork /
 // join on the caller's stream; legal under stream capture) to fill the GPU
-// instead of running three ~1-wave launches back to back.
+// instead of running three ~1-wave launches back to back.  The streams are
+// per host thread (created on the thread's first MRSTFT call, which is an eager
+// one before any capture): concurrent song searches must never share a stream,
+// or one thread's graph capture could pull in another thread's work.
 constexpr int kMaxDev = 64;
 constexpr int kSide = 7;
-cudaStream_t g_side[kMaxDev][kSide];
-cudaEvent_t g_fork[kMaxDev], g_join[kMaxDev][kSide];
-bool g_side_ok[kMaxDev];
+thread_local cudaStream_t g_side[kMaxDev][kSide];
+thread_local cudaEvent_t g_fork[kMaxDev], g_join[kMaxDev][kSide];
+thread_local bool g_side_ok[kMaxDev];
 
 int side_init() {
   int dev = 0;
@@ -540,6 +543,10 @@ template <class F>
 int fork_res(int n, cudaStream_t st, F fn) {
   int dev = 0;
   cudaGetDevice(&dev);
+  if (n > 1 && dev < kMaxDev && !g_side_ok[dev]) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) side_init();
+  }
   if (n <= 1 || dev >= kMaxDev || !g_side_ok[dev]) {
     for (int i = 0; i < n; ++i)
       if (int rc = fn(i, st)) return rc;

@@ -442,18 +442,18 @@ def test_nonfinite_loss_stops_the_run_where_the_reference_does(dev):
     tgt = gs["target"].astype(np.float64).copy()
     tgt[:, seg + 500] = np.nan  # inside every segment whose offset exceeds 500
     session = Session(stems, tgt)
-    cfg = TrainConfig(segment_seconds=seg / 30000, steps=12, seed=9)
-    probe = rng_for(9, "segments")
+    cfg = TrainConfig(segment_seconds=seg / 30000, steps=12, seed=7)
+    probe = rng_for(7, "segments")
     offs = [int(probe.integers(0, L - seg + 1)) for _ in range(cfg.steps)]
     bad = next(i for i, o in enumerate(offs) if o > 500)
     assert 0 < bad < cfg.steps - 1
-    p_fail, hist, rng = params.copy(), [], rng_for(9, "segments")
+    p_fail, hist, rng = params.copy(), [], rng_for(7, "segments")
     with pytest.raises(NonFiniteLoss):
         train(graph, p_fail, session, cfg, rng=rng, history=hist)
     assert len(hist) == bad
     after = rng.integers(0, 1 << 30)
-    p_ok, rng2 = params.copy(), rng_for(9, "segments")
-    ok_cfg = TrainConfig(segment_seconds=seg / 30000, steps=bad, seed=9)
+    p_ok, rng2 = params.copy(), rng_for(7, "segments")
+    ok_cfg = TrainConfig(segment_seconds=seg / 30000, steps=bad, seed=7)
     hist2 = train(graph, p_ok, session, ok_cfg, rng=rng2)
     rng2.integers(0, L - seg + 1)  # the reference drew the failing step's offset too
     assert after == rng2.integers(0, 1 << 30)
