@@ -118,26 +118,43 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_step_time(seed, K, S, L):
-    """Time one float64 oracle train_step on the host (the CPU baseline)."""
-    import torch
-    from oracle import mixgraph_oracle as O
+def cpu_reference_baseline(K, S, L, stems, target, songs=None):
+    """The reference's own train_step (numpy/scipy float64, one core) on the same
+    console and inputs, and a derived CPU songs/hour for the config-5 desk recipe."""
+    from oracle import ref_bench
+    g, p, st, tg, sc = ref_console_timed = ref_bench.ref_console(K, S, L, stems=stems, target=target)
+    dt = ref_bench.time_train_steps(g, p, st, tg, sc, 1)[0]
+    out = {"value": 1.0 / dt, "unit": "steps/s", "cores": 1, "kind": "reference",
+           "sample": f"1 reference train_step (mixgraph.optimizer.train_step, {K} trk + {S} sub, L={L}) "
+                     "on one host core", "cpu": ref_bench.cpu_info()}
+    del ref_console_timed
+    if songs:
+        out["songs_per_hour_derived"] = cpu_songs_per_hour(songs)
+    return out
 
-    def render(graph, tparams, stems):
-        with torch.no_grad():
-            y, _ = O.execute(graph, {t: torch.tensor(v) for t, v in tparams.params.items()},
-                             torch.tensor(tparams.raw_weights), stems.astype(np.float64))
-        return y.numpy()
 
-    graph, params, stems, target = make_inputs(seed, K, S, L, render)
-    p = {t: v.copy() for t, v in params.params.items()}
-    raw = params.raw_weights.copy()
-    opt = O.AdamW({**p, "w": raw})
-    cfg = O.LossConfig()
-    t0 = time.perf_counter()
-    O.train_step(graph, p, raw, stems.astype(np.float64), target.astype(np.float64), WARMUP, cfg, opt)
-    dt = time.perf_counter() - t0
-    return dt, torch.get_num_threads()
+def cpu_songs_per_hour(songs):
+    """Derived CPU songs/hour for the desk recipe: one measured reference
+    train_step and one eval-trial segment of a 16 + 4 console at the desk segment length,
+    scaled per song by (K+S)/20, times each song's measured trial count (from the GPU
+    searches of the same songs), on N concurrent worker processes (mixgraph prune
+    --threads N, mg/cli.py:185-189)."""
+    from oracle import ref_bench
+    from paper_2509_15948_b200.songs import DESK_SEGMENT
+    g, p, st, tg, sc = ref_bench.ref_console(16, 4, DESK_SEGMENT)
+    t_step = ref_bench.time_train_steps(g, p, st, tg, sc, 1)[0]
+    t_trial = ref_bench.time_eval_trial(g, p, st, tg, sc)
+    per_song = []
+    for k, trials in zip(songs["tracks"], songs["trials"]):
+        scale = (k + max(1, round(k / 4))) / 20.0
+        per_song.append(scale * ((600 + 12 * 50) * t_step + (trials + 2) * 4 * t_trial))
+    workers = min(os.cpu_count() or 1, max(1, int(0.6 * ref_bench.mem_available() // 2.5e9)))
+    return {"value": workers * 3600.0 / float(np.mean(per_song)), "unit": "songs/hour", "kind": "derived",
+            "workers": workers, "step_s": t_step, "trial_segment_s": t_trial,
+            "how": "per song: (600 console + 12 x 50 fine-tune steps) x reference step + (trials + 2) x 4 "
+                   "eval segments x reference trial, both measured here at 16 trk + 4 sub, 57,000 samples, "
+                   "scaled by (K+S)/20; trials = the GPU searches' counts for the same songs; "
+                   "N worker processes as mixgraph prune --threads N"}
 
 
 def dist_setup(args):
@@ -156,25 +173,33 @@ def dist_setup(args):
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the REFERENCE's own train_step (oracle/_ref archive of the
+    unmodified mixgraph package) on this host's cores: args.steps steps of the same
+    console spread over N forked worker processes, as its CLI spreads songs
+    (mg/cli.py:185-189)."""
     if rank != 0:
         return
-    dt, cores = cpu_oracle_step_time(0, args.tracks, args.subgroups, args.length)
-    # each timed "step" of the reference arm is one oracle train_step (bounded sample)
-    times = [dt]
-    for _ in range(max(0, min(args.steps, 2) - 1)):
-        t, _ = cpu_oracle_step_time(0, args.tracks, args.subgroups, args.length)
-        times.append(t)
-    v = 1.0 / statistics.mean(times)
-    line = {"metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": args.gpus, "steps": len(times),
-            "warmup": 0, "ms_per_step": 1000 * statistics.mean(times), "higher_is_better": True,
+    from oracle import ref_bench
+    try:
+        inputs = ref_bench.ref_console(args.tracks, args.subgroups, args.length)
+    except RuntimeError as exc:
+        print(json.dumps({"impl": "reference", "unavailable": str(exc)}), flush=True)
+        return
+    workers = ref_bench.default_workers(args.length)
+    res = ref_bench.parallel_throughput(inputs, args.steps, workers)
+    v = res["value"]
+    line = {"metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": args.gpus, "steps": res["steps"],
+            "warmup": 0, "ms_per_step": 1000.0 / v, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": "config2: full console 16 trk + 4 sub, L=441000 (10 s @44.1k as samples)",
                        "tracks": args.tracks, "subgroups": args.subgroups, "length": args.length},
-            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "port",
-                             "sample": f"{len(times)} oracle train_step(s) of the config-2 console "
-                                       "(float64 torch CPU restatement; the reference itself is "
-                                       "numpy and cannot run on the GPU box)"},
+            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": res["workers"], "kind": "reference",
+                             "sample": f"{res['steps']} reference train_step calls (unmodified mixgraph "
+                                       f"package, numpy/scipy float64) over {res['workers']} concurrent worker "
+                                       f"processes, one core each; wall {res['wall_s']:.1f} s; mean step "
+                                       f"{res['step_s_mean']:.2f} s (no warm-up: no JIT on this path)",
+                             "cpu": ref_bench.cpu_info()},
             "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -323,6 +348,8 @@ def main():
                      "wall_s": float(sw.item()), "recipe": "desk (pkg/README.md:54-58): console 600, 12 hybrid "
                      "rounds x 50 fine-tune, 57,000-sample segments, 4 eval segments, tau_rel 0.02",
                      "concurrent_per_gpu": args.song_concurrency, "tracks": [r["tracks"] for r in res], "trials": [r["trials"] for r in res]}
+    # BASELINE config 1 (4 tracks + 1 subgroup, L = 132,300): launch-bound, CUDA-graph replays
+    cfg1 = time_config(dev, 4, 1, 132_300, rank, render, steps=200, warmup=max(3, args.warmup))
     lay = eng.layout
     # per step: its segment and the 8 step scalars in, the 4 metrics out (params move once per run)
     h2d = stems.nbytes + target.nbytes + 8 * 8
@@ -330,25 +357,19 @@ def main():
 
     P = lay.P
     bytes_step = b_step(L, K, S, P)
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            peaks = json.load(fh)
-    except OSError:
-        pass
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    hbm, peak_src = _peak_hbm()
     dom = max(level_ms.items(), key=lambda kv: kv[1]["ms"]) if level_ms else None
     roof = None
     if dom:
         name, rec = dom
         ach = rec["bytes"] / (rec["ms"] / 1e3) / 1e9
         traffic, traffic_src = None, None
-        try:  # DRAM bytes of this level's kernels, one ncu capture (tools/ncu_traffic.sh)
+        try:  # DRAM bytes of every conv level's kernels, one ncu capture each (tools/ncu_traffic.sh)
             with open(os.path.join(ROOT, "profiles", "level_traffic_config2.json")) as fh:
                 lt = json.load(fh)
-            if lt.get("level") == name.split("(")[0]:
-                traffic, traffic_src = lt["dram_bytes_per_rep"], lt.get("source")
+            rec_t = lt["levels"].get(name.split("(")[0])
+            if rec_t is not None:
+                traffic, traffic_src = rec_t["dram_bytes_per_rep"], lt.get("source")
         except (OSError, ValueError, KeyError):
             pass
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
@@ -359,11 +380,9 @@ def main():
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                dt, cores = cpu_oracle_step_time(0, K, S, L)
-                cpu = {"value": 1.0 / dt, "unit": "steps/s", "cores": cores, "kind": "port",
-                       "sample": "1 float64 oracle train_step of the same config-2 console on the host"}
+                cpu = cpu_reference_baseline(K, S, L, stems, target, songs)
             except Exception as exc:  # pragma: no cover
-                cpu = {"value": None, "unit": "steps/s", "cores": 0, "kind": "port",
+                cpu = {"value": None, "unit": "steps/s", "cores": 0, "kind": "reference",
                        "sample": f"failed: {exc}"}
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
@@ -380,6 +399,7 @@ def main():
                     "steps": args.e2e_steps, "includes": "engine param load, first (unoverlapped) upload, "
                     "final param read-back",
                     "train_step_sync": sync_val},
+            "config1": cfg1,
             "eval_trial_ms": trial_ms,
             "songs_per_hour": songs,
             "gpu_launches": eng.launches_per_step() * args.steps,
@@ -395,6 +415,46 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def time_config(dev, K, S, L, seed, render, steps, warmup):
+    """steps/s of another BASELINE config on this GPU (graph replays, CUDA events) + its step roofline."""
+    import torch
+
+    from paper_2509_15948_b200.engine import TrainEngine
+    from paper_2509_15948_b200.optimizer import TrainConfig, _EngineCfg, make_optimizer
+    graph, params, stems, target = make_inputs(seed, K, S, L, render)
+    cfg = TrainConfig(segment_seconds=L / 30000, steps=1)
+    eng = TrainEngine(graph, L, _EngineCfg(make_optimizer(params, cfg), cfg), device=dev)
+    eng.load_params(params)
+    eng.plan.set_stems(stems)
+    eng.target.copy_(torch.from_numpy(target))
+    for _ in range(warmup):
+        eng.step_async()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        eng.step_async()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    hbm = _peak_hbm()[0]
+    by = b_step(L, K, S, eng.layout.P)
+    return {"workload": f"config1: full console {K} trk + {S} sub, L={L} (3 s @44.1k as samples)",
+            "value": 1000.0 / ms, "unit": "steps/s", "ms_per_step": ms, "steps": steps,
+            "launches_per_step": eng.launches_per_step(),
+            "step_roofline": {"algorithmic_bytes": by, "achieved": by / (ms / 1e3) / 1e9, "peak": hbm,
+                              "frac": by / (ms / 1e3) / 1e9 / hbm}}
+
+
+def _peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+        return float(peaks["hbm_gbs"]), "measured"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback"
 
 
 def time_levels(eng, reps=3):

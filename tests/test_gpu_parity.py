@@ -437,9 +437,11 @@ def test_nonfinite_loss_stops_the_run_where_the_reference_does(dev):
     from paper_2509_15948_b200.common import rng_for
     from paper_2509_15948_b200.optimizer import NonFiniteLoss, Session, TrainConfig, train
     gs = golden("step.npz")
-    graph, params, stems, L = _step_setup()
+    graph, params, stems, L0 = _step_setup()
+    stems = np.concatenate([stems, stems[..., :37_000]], axis=-1)  # a 70,000-sample session
+    tgt = np.concatenate([gs["target"], gs["target"][:, :37_000]], axis=-1).astype(np.float64)
+    L = stems.shape[-1]
     seg = L - 1000
-    tgt = gs["target"].astype(np.float64).copy()
     tgt[:, seg + 500] = np.nan  # inside every segment whose offset exceeds 500
     session = Session(stems, tgt)
     cfg = TrainConfig(segment_seconds=seg / 30000, steps=12, seed=7)
