@@ -23,6 +23,8 @@
 //        r  STFT-domain filtered noise, 313 frames x 384, OLA, / wss, offset 0
 //        d  20 taps x 39-tap colour FIRs at m*3000 + quantised offset, offset 19;
 //           custom surrogate backward (mg/processors.py:250-318)
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "fourstep.cuh"
 #include "fs2.cuh"
@@ -39,6 +41,11 @@ constexpr double PI = 3.141592653589793238462643383279502884;
 #include "fir.cuh"
 #include "rev_fft.cuh"
 #include "eq_os.cuh"
+
+int g_num_sms = 148;
+// MGB_COLC_PERSISTENT=1: the persistent bulk-copy-pipelined column pass (fs2::k_colC_p) instead of
+// one tile per CTA.  Measured slower (336 vs 437 steps/s), kept off for A/B runs.
+bool g_colc_persistent = false;
 
 struct ConvGeom {
   int M, off, logN;
@@ -450,6 +457,14 @@ struct Conv2 {
   }
   template <class Ep>
   static void colC(const float2* Bb, const Ep& ep, int out_rows, int rev, int B, cudaStream_t st) {
+    if constexpr (N1 == 512) {
+      if (g_colc_persistent) {  // persistent, bulk-copy-pipelined column pass (fs2::k_colC_p)
+        const int ntiles = B * fs2::GP<N1>::TILES_PER_NODE;
+        mgb_launch(fs2::k_colC_p<N1, Ep>, dim3(ntiles < g_num_sms ? ntiles : g_num_sms), dim3(G::NT),
+                   fs2::GP<N1>::SMEM, st, Bb, ep, 1.f / (float)G::N, out_rows, ntiles);
+        return;
+      }
+    }
     if constexpr (C64) {
       mgb_launch(fs2::k_colC64<Ep>, dim3(dim3(N2 / fs2::C64::TC, B)), dim3(fs2::C64::NT), fs2::C64::SMEM, st, Bb, ep,
                  1.f / (float)G::N, out_rows, rev);
@@ -476,6 +491,12 @@ struct Conv2 {
       cudaFuncSetAttribute(fs2::k_colC<N1, EpFwd>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
       cudaFuncSetAttribute(fs2::k_colC<N1, EpGx>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
       cudaFuncSetAttribute(fs2::k_colC<N1, EpGh>, cudaFuncAttributeMaxDynamicSharedMemorySize, sc);
+    }
+    if constexpr (N1 == 512) {
+      const int sp = (int)fs2::GP<N1>::SMEM;
+      cudaFuncSetAttribute(fs2::k_colC_p<N1, EpFwd>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp);
+      cudaFuncSetAttribute(fs2::k_colC_p<N1, EpGx>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp);
+      cudaFuncSetAttribute(fs2::k_colC_p<N1, EpGh>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp);
     }
     cudaFuncSetAttribute(fs2::k_rowH<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWH_SMEM);
     cudaFuncSetAttribute(fs2::k_rowF<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWF_SMEM);
@@ -601,6 +622,11 @@ int conv_bwd_dispatch(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cu
 }  // namespace
 
 int mgb_conv_init() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const char* e = getenv("MGB_COLC_PERSISTENT");
+  g_colc_persistent = e ? atoi(e) != 0 : false;
 #define X(l, a) Conv2<a>::attrs();
   MGB_CONV_SIZES(X)
 #undef X

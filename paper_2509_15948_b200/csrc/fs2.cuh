@@ -457,4 +457,136 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent column pass with bulk-async (TMA engine) tile staging.
+//
+// One CTA per SM walks the (node, column block) tiles t = blockIdx.x + k*gridDim.x.
+// A tile (N1 rows x TC columns of the complex input, TC*8-byte row segments 8 KB
+// apart) is copied global -> shared memory by cp.async.bulk (one 128-byte segment
+// per instruction, issued by warp 0, completion counted in bytes on an mbarrier)
+// into one of two stages; the next tile's copy is in flight while the CTA
+// transforms the current one, so the load latency that dominated the
+// one-tile-per-CTA kernels (ncu: long_scoreboard 40-60 % of stalls at 34-45 % of
+// DRAM bandwidth) overlaps the math.  A stage doubles as the transform's exchange
+// buffer once its tile is in registers.
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int N1>
+struct GP {
+  using g = G<N1>;
+  static constexpr int TILES_PER_NODE = N2 / g::TC;
+  static constexpr int TILE = N1 * g::TC;                       // float2 per tile
+  static constexpr int STAGE = ((g::TC * g::PITCH > TILE ? g::TC * g::PITCH : TILE) + 15) / 16 * 16;
+  static constexpr size_t SMEM = 2 * (size_t)STAGE * sizeof(float2);
+};
+
+// warp 0: stage tile t of Bb (rows n1 < rows) into st, completion on bar
+template <int N1>
+__device__ __forceinline__ void stage_tile(const float2* __restrict__ Bb, int t, int rows, float2* st,
+                                           unsigned long long* bar, int lane) {
+  using g = G<N1>;
+  const int b = t / GP<N1>::TILES_PER_NODE, col0 = (t % GP<N1>::TILES_PER_NODE) * g::TC;
+  if (lane == 0) mbar_expect_tx(bar, (unsigned)(rows * g::TC * sizeof(float2)));
+  __syncwarp();
+  const float2* src = Bb + (long long)b * g::N + col0;
+  for (int r = lane; r < rows; r += 32) bulk_g2s(st + r * g::TC, src + (long long)r * N2, g::TC * sizeof(float2), bar);
+}
+
+template <int N1, class Ep>
+__global__ void __launch_bounds__(G<N1>::NT, 1) k_colC_p(const float2* __restrict__ Bb, Ep ep, float scale, int out_rows,
+                                                        int ntiles) {
+  using g = G<N1>;
+  using gp = GP<N1>;
+  constexpr int Q = g::Q, P = g::P, TC = g::TC, B8 = Q < 8 ? Q : 8;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* stage = reinterpret_cast<float2*>(smraw);
+  __shared__ __align__(8) unsigned long long bar[2];
+  __shared__ double red[32];
+  const int c = threadIdx.x % TC, j = threadIdx.x / TC, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  mgb_pdl_entry();
+  int t = blockIdx.x;
+  if (warp == 0 && t < ntiles) stage_tile<N1>(Bb, t, N1, stage, &bar[0], lane);
+  for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
+    const int s = k & 1;
+    float2* cur = stage + s * gp::STAGE;
+    // the other stage was last read in iteration k-1, which ended with a barrier
+    if (warp == 0 && t + (int)gridDim.x < ntiles)
+      stage_tile<N1>(Bb, t + gridDim.x, N1, stage + (s ^ 1) * gp::STAGE, &bar[s ^ 1], lane);
+    const int b = t / gp::TILES_PER_NODE, cb = t % gp::TILES_PER_NODE, col = cb * TC + c;
+    const typename Ep::Ctx ctx = ep.prepare(b);
+    typename Ep::Raw raw[2][B8];
+#pragma unroll
+    for (int i = 0; i < B8; ++i) {
+      const int n1 = j + P * i;
+      raw[0][i] = ep.fetch(ctx, b, (long long)n1 * N2 + col, n1 < out_rows);
+    }
+    mbar_wait(&bar[s], (k >> 1) & 1);
+    float2 v[Q];
+#pragma unroll
+    for (int m = 0; m < Q; ++m) v[m] = cur[(j + P * m) * TC + c];
+    __syncthreads();  // every thread holds its column values: the stage becomes the exchange buffer
+    col_fft<N1, true>(v, cur, c, j);
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int m0 = 0; m0 < Q; m0 += B8) {
+      const int cr = (m0 / B8) & 1;
+      if (m0 + B8 < Q) {
+#pragma unroll
+        for (int i = 0; i < B8; ++i) {
+          const int n1 = j + P * (m0 + B8 + i);
+          raw[cr ^ 1][i] = ep.fetch(ctx, b, (long long)n1 * N2 + col, n1 < out_rows);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < B8; ++i) {
+        const int n1 = j + P * (m0 + i);
+        if (n1 < out_rows) {
+          float2 y = v[m0 + i];
+          y.x *= scale;
+          y.y *= scale;
+          ep.finish(ctx, b, (long long)n1 * N2 + col, y, raw[cr][i], a0, a1);
+        }
+      }
+    }
+    if (Ep::kAccum) {
+      const double t0 = block_sum((double)a0, red);
+      __syncthreads();
+      const double t1 = block_sum((double)a1, red);
+      if (threadIdx.x == 0) ep.commit(b, cb, t0, t1);
+    }
+    // the stage's generic-proxy accesses (exchange) are ordered before the async-proxy
+    // (bulk copy) writes that refill it in iteration k+1
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();  // stage s is free for the copy issued at the top of iteration k+1
+  }
+}
+
 }  // namespace fs2
