@@ -347,7 +347,11 @@ def main():
             songs = {"value": len(res) / float(sw.item()) * 3600.0, "unit": "songs/hour", "songs": len(res),
                      "wall_s": float(sw.item()), "recipe": "desk (pkg/README.md:54-58): console 600, 12 hybrid "
                      "rounds x 50 fine-tune, 57,000-sample segments, 4 eval segments, tau_rel 0.02",
-                     "concurrent_per_gpu": args.song_concurrency, "tracks": [r["tracks"] for r in res], "trials": [r["trials"] for r in res]}
+                     "concurrent_per_gpu": args.song_concurrency, "tracks": [r["tracks"] for r in res],
+                     "trials": [r["trials"] for r in res],
+                     "gathered": {"songs": len(res), "graph_json_bytes": sum(len(r["graph_json"]) for r in res),
+                                  "what": "final .mixgraph.json + PruneReport + survivors + ledger per song, "
+                                          "one gather_object to rank 0 (NCCL when N > 1)"}}
     # BASELINE config 1 (4 tracks + 1 subgroup, L = 132,300): launch-bound, CUDA-graph replays
     cfg1 = time_config(dev, 4, 1, 132_300, rank, render, steps=200, warmup=max(3, args.warmup))
     lay = eng.layout

@@ -93,16 +93,36 @@ def desk_prune_config(seed, iterations=12):
                        train=TrainConfig(segment_seconds=seg, warmup_seconds=1.0, seed=seed))
 
 
+def report_dict(rep) -> dict:
+    """A PruneReport (mg/pruning.py:72-91) as plain JSON-able values, plus its derived ratio."""
+    out = asdict(rep)
+    out["pruning_ratio"] = rep.pruning_ratio
+    return out
+
+
+def song_result(spec, graph, params, state, rep, search_s) -> dict:
+    """What one song's search hands to rank 0: the final ``.mixgraph.json`` bytes (the
+    reference writer's exact format, mg/graph.py:276-293), the PruneReport, the
+    surviving-processor mask and the trial ledger (mg/cli.py:128-182 writes the same
+    artefacts per song)."""
+    from .graph import serialize
+    return {"song": spec.index, "tracks": spec.tracks, "subgroups": spec.subgroups, "search_s": search_s,
+            "trials": rep.trial_count, "pruning_ratio": rep.pruning_ratio, "console_loss": rep.console_loss,
+            "final_loss": rep.final_loss, "report": report_dict(rep),
+            "alive": [bool(a) for a in state.alive],
+            "ledger": [(r.iteration, r.mode, [int(c) for c in r.candidates], float(r.loss), bool(r.accepted))
+                       for r in state.ledger],
+            "graph_json": serialize(graph, params).decode("utf-8")}
+
+
 def search_song(spec, graph, params, stems, target, iterations=12, device="cuda"):
-    """One song's full pruning search (``prune_song``) with the desk recipe; a JSON-able summary."""
+    """One song's full pruning search (``prune_song``) with the desk recipe; its JSON-able result."""
     from .optimizer import Session
     from .pruning import prune_song
     t0 = time.perf_counter()
-    _, _, _, rep, _ = prune_song(graph, params, Session(stems, target), desk_prune_config(spec.index, iterations),
-                                 device=device)
-    return {"song": spec.index, "tracks": spec.tracks, "subgroups": spec.subgroups,
-            "search_s": time.perf_counter() - t0, "trials": rep.trial_count,
-            "pruning_ratio": rep.pruning_ratio, "console_loss": rep.console_loss, "final_loss": rep.final_loss}
+    g, p, state, rep, _ = prune_song(graph, params, Session(stems, target), desk_prune_config(spec.index, iterations),
+                                     device=device)
+    return song_result(spec, g, p, state, rep, time.perf_counter() - t0)
 
 
 def search_songs(specs, mine, inputs, concurrent=1, iterations=12, device="cuda"):
@@ -172,5 +192,6 @@ def spec_dict(spec):
     return asdict(spec)
 
 
-__all__ = ["SongSpec", "song_costs", "assign_lpt", "desk_specs", "run_rank", "gather_results",
+__all__ = ["SongSpec", "song_costs", "assign_lpt", "desk_specs", "run_rank", "gather_results", "song_result",
+           "report_dict",
            "songs_per_hour", "spec_dict", "desk_prune_config", "search_song", "search_songs", "DESK_SEGMENT", "np"]
