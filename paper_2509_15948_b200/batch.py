@@ -1,0 +1,318 @@
+"""Several songs' consoles trained as ONE device program.
+
+A desk-recipe search trains on 57,000-sample segments, where one level launch
+of one song fills only part of the 148 SMs.  Here the consoles of G songs are
+joined into a disjoint union: node ids are offset per song, and level k of
+the union schedule is the union of every song's level k of the console
+sequence ``iecnsgdrmecnsgdro`` (mg/scheduler.py:135-154; a pruned song simply
+contributes nothing to a stage it lost), so each level type is ONE launch
+over all songs' nodes, the output level has one row per song.  Each song keeps
+its own loss (one MRSTFT per song), its own segment stream (its RNG draws its
+own offsets, mg/optimizer.py:97-105) and its own parameters; the optimiser is
+one fused AdamW over the union's flat vector (AdamW is elementwise, and songs
+in lock-step share the step count t and the sparsity weight).
+
+Every level kernel computes a node's rows independently of which other nodes
+share the launch (grids are (per-row blocks) x rows), so a song trained in a
+union makes bit-for-bit the updates it makes alone (GPU test).
+
+``prune_songs_lockstep`` runs G searches through ``pruning.prune_song_steps``
+(the single copy of the reference's search control flow): trials run per song,
+and whenever every search has reached its next train() (the console fit, each
+round's fine-tune: the same step counts for all songs of a recipe) the requests
+are served together by one ``BatchTrainEngine``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from ._lib import check, lib
+from .engine import (F32, F64, LossPlan, ParamLayout, RenderPlan, capture_graph, current_stream, ensure_device,
+                     host_wait, on_stream, own_stream, ptr, stream_ptr)
+from .graph import PROCESSOR_TYPES, MixGraph, ParamStore
+from .optimizer import NonFiniteLoss, SongTooShort, _EngineCfg, _graph_min_steps, make_optimizer
+from .schedule import CONSOLE_SEQUENCE, Schedule, plan_indices, schedule_console
+
+
+class SongUnion:
+    """Disjoint union of console graphs with the stage-merged console schedule."""
+
+    def __init__(self, graphs):
+        self.graphs = list(graphs)
+        types, edges = [], []
+        self.node_off, self.in_off, self.proc_off = [], [], []
+        n_in = n_proc = 0
+        stages = [[] for _ in CONSOLE_SEQUENCE]
+        for g in self.graphs:
+            off = len(types)
+            self.node_off.append(off)
+            self.in_off.append(n_in)
+            self.proc_off.append(n_proc)
+            n_in += len(g.nodes_of_type("i"))
+            n_proc += len(g.processor_nodes())
+            types.extend(g.node_types)
+            edges.extend((a + off, b + off) for a, b in g.edges)
+            sch = schedule_console(g)  # NotAConsole for anything but a console or its prunings
+            pos = 0
+            for step, tag in enumerate(sch.type_sequence):
+                while CONSOLE_SEQUENCE[pos] != tag:
+                    pos += 1
+                stages[pos].extend(v + off for v in sch.subsets[step])
+                pos += 1
+        self.n_in, self.n_proc = n_in, n_proc
+        self.graph = MixGraph("".join(types), tuple(edges))
+        seq = "".join(t for t, sub in zip(CONSOLE_SEQUENCE, stages) if sub)
+        self.schedule = plan_indices(self.graph, Schedule(seq, [sub for sub in stages if sub]))
+        self.layout = ParamLayout(self.graph)
+        # per type: the union bank rows of each song (songs appear in node-id order)
+        self.rows = {t: [len(g.nodes_of_type(t)) for g in self.graphs] for t in PROCESSOR_TYPES}
+
+    def pack(self, params_list) -> np.ndarray:
+        banks = {t: np.concatenate([np.asarray(p.params[t], dtype=np.float64).reshape(-1, self.layout_cols(t))
+                                    for p in params_list], axis=0) for t in PROCESSOR_TYPES}
+        raw = np.concatenate([np.asarray(p.raw_weights, dtype=np.float64) for p in params_list])
+        return self.layout.pack(ParamStore(banks, raw))
+
+    def unpack_into(self, flat: np.ndarray, params_list) -> None:
+        parts = self.layout.split(flat)
+        for t in PROCESSOR_TYPES:
+            o = 0
+            for p, n in zip(params_list, self.rows[t]):
+                p.params[t] = parts[t][o:o + n].copy()
+                o += n
+        o = 0
+        for p, g in zip(params_list, self.graphs):
+            n = len(g.processor_nodes())
+            p.raw_weights = parts["w"][o:o + n].copy()
+            o += n
+
+    @staticmethod
+    def layout_cols(t):
+        from .graph import PARAM_COUNTS
+        return PARAM_COUNTS[t]
+
+
+class BatchTrainEngine:
+    """``train_step`` (mg/optimizer.py:140-186) for G songs at once on a ``SongUnion``."""
+
+    def __init__(self, union: SongUnion, L: int, cfg, device="cuda"):
+        self.device = dev = ensure_device(device)
+        self.union, self.cfg, self.L = union, cfg, int(L)
+        self.ws = int(cfg.warmup_len)
+        G = self.G = len(union.graphs)
+        lay = self.layout = union.layout
+        self.params = torch.zeros(lay.n, dtype=F64, device=dev)
+        self.grads = torch.zeros(lay.n, dtype=F64, device=dev)
+        self.m = torch.zeros(lay.n, dtype=F64, device=dev)
+        self.v = torch.zeros(lay.n, dtype=F64, device=dev)
+        self.plan = RenderPlan(union.graph, union.schedule, self.L, dev, self.params, self.grads, lay, backward=True)
+        assert self.plan.n_out == G
+        self.losses = [LossPlan(cfg.loss, self.L - self.ws, dev) for _ in range(G)]
+        self.targets = torch.zeros((G, 2, self.L), dtype=F32, device=dev)
+        self.scalars = torch.zeros(8, dtype=F64, device=dev)
+        self.vals = torch.zeros((G, 4), dtype=F64, device=dev)  # per song: loss, L_a, L_g, L_p
+        self.guard = torch.zeros((), dtype=F64, device=dev)     # sum of the songs' losses
+        self.halt = torch.zeros((), dtype=F64, device=dev)
+        self.sparsity = torch.zeros(G, dtype=F64, device=dev)
+        self.plan.greg.fill_(float(cfg.loss.gain_staging_weight))
+        # song of every gain-staging slot (plan.reg: the e/r/d level rows in level order)
+        owner = []
+        sched = union.schedule
+        bounds = np.asarray(union.node_off + [union.graph.num_nodes])
+        for s in range(1, len(sched.subsets)):
+            if sched.type_sequence[s] in "erd":
+                owner.extend(int(np.searchsorted(bounds, v, side="right") - 1) for v in sched.subsets[s])
+        self.reg_owner = torch.tensor(owner if owner else [0], dtype=torch.int64, device=dev)
+        self.reg_song = torch.zeros(G, dtype=F64, device=dev)
+        self.t = 0
+        self.side = own_stream(dev, "side")
+        self._graph = None
+        self._ring = torch.zeros((64, 8), dtype=F64).pin_memory()
+        self._ring_ev = [None] * 64
+
+    def load_params(self, params_list):
+        self.params.copy_(torch.from_numpy(self.union.pack(params_list)))
+
+    def store_params(self, params_list):
+        self.union.unpack_into(self.params.cpu().numpy(), params_list)
+
+    def _body(self):
+        L, ws, G = self.L, self.ws, self.G
+        plan = self.plan
+        Ld = lib()
+        main, side = current_stream(), self.side
+        prepared = plan.prepare(side)
+        with on_stream(side):
+            plan.dYs[:, :, :ws].zero_()
+            for i, lp in enumerate(self.losses):
+                lp.target(ptr(self.targets, (2 * i) * L + ws), ptr(self.targets, (2 * i + 1) * L + ws))
+            tev = torch.cuda.Event()
+            tev.record(side)
+        plan.forward(use_mask=False, prepared=prepared, norms=side)
+        main.wait_event(tev)
+        for i, lp in enumerate(self.losses):
+            lp.forward(ptr(plan.ys, (2 * i) * L + ws), ptr(plan.ys, (2 * i + 1) * L + ws))
+        main.wait_stream(side)
+        side.wait_stream(main)
+        with on_stream(side):  # loss assembly per song (read by the optimiser only)
+            self.reg_song.zero_()
+            self.reg_song.index_add_(0, self.reg_owner[: plan.reg.numel()], plan.reg)
+            lay, u = self.layout, self.union
+            for i, g in enumerate(u.graphs):
+                n = len(g.processor_nodes())
+                if n:
+                    check(Ld.mgb_sparsity(ptr(self.params, lay.w_off + u.proc_off[i]), n,
+                                          ptr(self.sparsity, i), stream_ptr()), "mgb_sparsity")
+            la = torch.stack([lp.loss for lp in self.losses])
+            ap = self.scalars[7]
+            total = la + self.reg_song * float(self.cfg.loss.gain_staging_weight) + \
+                torch.where(ap > 0, ap * self.sparsity, torch.zeros_like(self.sparsity))
+            torch.stack([total, la, self.reg_song, self.sparsity], dim=1, out=self.vals)
+            torch.sum(total, dim=0, out=self.guard)
+        for i, lp in enumerate(self.losses):
+            lp.backward(ptr(plan.ys, (2 * i) * L + ws), ptr(plan.ys, (2 * i + 1) * L + ws),
+                        ptr(plan.dYs, (2 * i) * L + ws), ptr(plan.dYs, (2 * i + 1) * L + ws))
+        plan.backward(side)
+        main.wait_stream(side)
+        check(Ld.mgb_adamw_step(ptr(self.params), ptr(self.grads), ptr(self.m), ptr(self.v), lay.n,
+                                lay.off["d"], lay.rows["d"], lay.w_off, lay.P, ptr(plan.gw), None,
+                                ptr(self.scalars), ptr(self.guard), ptr(self.halt), stream_ptr()),
+              "mgb_adamw_step")
+
+    def _set_scalars(self, alpha_p):
+        c = self.cfg
+        self.t += 1
+        b1, b2 = c.betas
+        i = self.t % 64
+        if self._ring_ev[i] is not None:
+            host_wait(self._ring_ev[i])
+        self._ring[i].copy_(torch.tensor([c.lr, b1, b2, c.eps, c.weight_decay, 1.0 - b1 ** self.t,
+                                          1.0 - b2 ** self.t, float(alpha_p)], dtype=F64))
+        self.scalars.copy_(self._ring[i], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ring_ev[i] = ev
+
+    def step_async(self, alpha_p=0.0, use_graph=True):
+        self._set_scalars(alpha_p)
+        if not use_graph:
+            self._body()
+            return
+        if self._graph is None:
+            s = own_stream(self.device, "warm")
+            s.wait_stream(current_stream())
+            with torch.cuda.stream(s):
+                snap = [x.clone() for x in (self.params, self.m, self.v, self.halt)]
+                self._body()
+                for x, y in zip((self.params, self.m, self.v, self.halt), snap):
+                    x.copy_(y)
+            current_stream().wait_stream(s)
+            current_stream().synchronize()
+            self._graph = capture_graph(self._body, self.device)
+        self._graph.replay()
+
+
+def train_batch(reqs, device="cuda"):
+    """Serve several ``pruning.TrainRequest``s (one per song, same step count and
+    hyper-parameters) with one ``BatchTrainEngine``: each step draws every song's
+    segment offset from its own RNG, copies the segments into the union's input
+    rows, and replays the union step.  Same per-song semantics as ``optimizer.train``
+    (histories, parameters written back, fresh AdamW state per call, NonFiniteLoss)."""
+    import time
+    cfg = reqs[0].cfg
+    for r in reqs[1:]:
+        if (r.cfg.steps, r.cfg.segment_len, r.cfg.warmup_len, r.cfg.lr, r.cfg.betas, r.cfg.eps,
+                r.cfg.weight_decay, r.cfg.loss) != (cfg.steps, cfg.segment_len, cfg.warmup_len, cfg.lr, cfg.betas,
+                                                     cfg.eps, cfg.weight_decay, cfg.loss):
+            raise ValueError("batched train requests must share steps, segment length and hyper-parameters")
+    if cfg.steps <= 0:
+        return
+    seg = cfg.segment_len
+    for r in reqs:
+        if r.session.length < seg:
+            raise SongTooShort(f"song has {r.session.length} samples, segment needs {seg}")
+    dev = ensure_device(device)
+    union = SongUnion([r.graph for r in reqs])
+    eng = BatchTrainEngine(union, seg, _EngineCfg(make_optimizer(None, cfg), cfg), device=dev)
+    eng.load_params([r.params for r in reqs])
+    sessions = [r.session.on_device(dev) for r in reqs]
+    k_off = union.in_off
+    rng_states = [r.rng.bit_generator.state for r in reqs]
+    vals = torch.zeros((cfg.steps, eng.G, 4), dtype=F64, device=dev)
+    use_graph = cfg.steps >= _graph_min_steps()
+    t0 = time.perf_counter()
+    for step in range(cfg.steps):
+        for i, (r, (st, tg)) in enumerate(zip(reqs, sessions)):
+            off = int(r.rng.integers(0, r.session.length - seg + 1))
+            k = st.shape[0]
+            eng.plan.stems[k_off[i]:k_off[i] + k].copy_(st[..., off:off + seg])
+            eng.targets[i].copy_(tg[..., off:off + seg])
+        alphas = {r.alpha_p_fn(step) if r.alpha_p_fn else 0.0 for r in reqs}
+        if len(alphas) != 1:
+            raise ValueError("batched songs must share the sparsity weight of every step")
+        eng.step_async(alphas.pop(), use_graph=use_graph)
+        vals[step].copy_(eng.vals)
+    host_wait(torch.cuda.current_stream())
+    host = vals.cpu().numpy()
+    wall = (time.perf_counter() - t0) / cfg.steps
+    bad = [next((k for k in range(cfg.steps) if not np.isfinite(host[k, i, 0])), None) for i in range(eng.G)]
+    if any(b is not None for b in bad):
+        # a non-finite loss stopped the whole union at its first occurrence; the reference
+        # stops only the failing song: let the caller rerun these songs one at a time
+        for r, st in zip(reqs, rng_states):
+            r.rng.bit_generator.state = st
+        raise BatchNonFinite([i for i, b in enumerate(bad) if b is not None])
+    eng.store_params([r.params for r in reqs])
+    for i, r in enumerate(reqs):
+        for v in host[:, i]:
+            r.history.append({"loss": float(v[0]), "L_a": float(v[1]), "L_g": float(v[2]), "L_p": float(v[3]),
+                              "step": len(r.history), "wall_s": wall})
+
+
+class BatchNonFinite(NonFiniteLoss):
+    def __init__(self, songs):
+        super().__init__(f"non-finite loss in batched songs {songs}")
+        self.songs = songs
+
+
+def prune_songs_lockstep(jobs, device="cuda"):
+    """Run several ``prune_song`` searches in lock-step; ``jobs`` = list of
+    (graph, params, session, PruneConfig).  Returns each search's
+    (graph, params, state, report, history), identical to running them one by one."""
+    from .pruning import prune_song, prune_song_steps, run_train_request
+    gens = [prune_song_steps(g, p, s, c, None, device) for g, p, s, c in jobs]
+    out = [None] * len(gens)
+    reqs = {}
+    for i, gen in enumerate(gens):
+        try:
+            reqs[i] = next(gen)
+        except StopIteration as done:
+            out[i] = done.value
+    while reqs:
+        ids = sorted(reqs)
+        try:
+            if len(ids) == 1:
+                run_train_request(reqs[ids[0]], device)
+            else:
+                train_batch([reqs[i] for i in ids], device)
+        except BatchNonFinite:
+            # rare: rerun each of these searches on its own (the reference's per-song semantics)
+            for i in ids:
+                g, p, s, c = jobs[i]
+                try:
+                    out[i] = prune_song(g, p, s, c, device=device)
+                except NonFiniteLoss as e:
+                    out[i] = e
+            return out
+        for i in ids:
+            try:
+                reqs[i] = gens[i].send(None)
+            except StopIteration as done:
+                out[i] = done.value
+                del reqs[i]
+    return out
+
+
+__all__ = ["SongUnion", "BatchTrainEngine", "train_batch", "prune_songs_lockstep", "BatchNonFinite"]

@@ -358,7 +358,11 @@ class RenderPlan:
                 lv.struct = None
                 lv.keep = [in_rows, seg_t]
             self.levels.append(lv)
-        self.y = self.outs[nsteps - 1][0]  # (2, L) output node
+        # the output level: one row for a graph, one per song for a union of song consoles
+        # (batch.SongBatch); ys (n_out, 2, L), y its first row
+        self.ys = self.outs[nsteps - 1]
+        self.n_out = len(schedule.subsets[nsteps - 1])
+        self.y = self.ys[0]
         # processor index -> position of its level in self.levels (incremental re-render)
         self.proc_level = np.zeros(max(self.P, 1), dtype=np.int64)
         for i, s in enumerate(range(1, nsteps)):
@@ -366,7 +370,8 @@ class RenderPlan:
                 self.proc_level[np.asarray(schedule.plans[s].weight_idx, dtype=np.int64)] = i
 
         # ---- backward gradient routing
-        self.dY = torch.zeros((2, L), dtype=F32, device=dev) if backward else None
+        self.dYs = torch.zeros((self.n_out, 2, L), dtype=F32, device=dev) if backward else None
+        self.dY = self.dYs[0] if backward else None
         if backward:
             consumers = {}
             for s in range(1, nsteps):
@@ -374,7 +379,7 @@ class RenderPlan:
                 seg = plan.segments if plan.segments is not None else np.arange(len(plan.gather))
                 for i, g in enumerate(plan.gather):
                     consumers.setdefault(tuple(g), []).append((s, int(seg[i])))
-            gptr = {(nsteps - 1, 0): ptr(self.dY)}
+            gptr = {(nsteps - 1, r): ptr(self.dYs, r * 2 * L) for r in range(self.n_out)}
             fan_bufs = {}
             for s in range(nsteps - 2, 0, -1):
                 tag = schedule.type_sequence[s]

@@ -125,6 +125,32 @@ def search_song(spec, graph, params, stems, target, iterations=12, device="cuda"
     return song_result(spec, g, p, state, rep, time.perf_counter() - t0)
 
 
+def search_songs_lockstep(specs, mine, inputs, group=4, iterations=12, device="cuda"):
+    """This rank's songs in groups of ``group`` searched in lock-step (batch.prune_songs_lockstep):
+    trials per song, every console fit and fine-tune of a group as ONE batched device program
+    over the disjoint union of the group's consoles.  Songs are grouped costliest-first so a
+    group's consoles are of similar size.  Same results as searching the songs one by one."""
+    from .batch import prune_songs_lockstep
+    from .optimizer import Session
+    order = sorted(mine, key=lambda i: (-song_costs([specs[i]])[0], i))
+    out = {}
+    for g0 in range(0, len(order), group):
+        ids = order[g0:g0 + group]
+        t0 = time.perf_counter()
+        jobs = []
+        for i in ids:
+            graph, params, stems, target = inputs[i]
+            jobs.append((graph, params, Session(stems, target), desk_prune_config(specs[i].index, iterations)))
+        res = prune_songs_lockstep(jobs, device=device)
+        dt = (time.perf_counter() - t0) / len(ids)
+        for i, r in zip(ids, res):
+            if isinstance(r, BaseException):
+                raise r
+            g, p, state, rep, _ = r
+            out[i] = song_result(specs[i], g, p, state, rep, dt)
+    return [out[i] for i in mine]
+
+
 def search_songs(specs, mine, inputs, concurrent=1, iterations=12, device="cuda"):
     """Run this rank's songs, ``concurrent`` at a time on one GPU.
 
@@ -193,5 +219,6 @@ def spec_dict(spec):
 
 
 __all__ = ["SongSpec", "song_costs", "assign_lpt", "desk_specs", "run_rank", "gather_results", "song_result",
+           "search_songs_lockstep",
            "report_dict",
            "songs_per_hour", "spec_dict", "desk_prune_config", "search_song", "search_songs", "DESK_SEGMENT", "np"]

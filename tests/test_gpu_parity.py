@@ -463,3 +463,59 @@ def test_nonfinite_loss_stops_the_run_where_the_reference_does(dev):
         np.testing.assert_array_equal(p_fail.params[t], p_ok.params[t])
     np.testing.assert_array_equal(p_fail.raw_weights, p_ok.raw_weights)
     assert [h["loss"] for h in hist] == [h["loss"] for h in hist2]
+
+
+def test_batched_training_of_several_songs_equals_training_each_alone(dev):
+    """Multi-song batching: three songs' consoles (one pruned) trained as
+    one disjoint-union device program make bit-for-bit the updates each makes alone."""
+    import bench
+    from paper_2509_15948_b200.batch import train_batch
+    from paper_2509_15948_b200.common import rng_for
+    from paper_2509_15948_b200.graph import bypass_remove
+    from paper_2509_15948_b200.optimizer import Session, TrainConfig, train
+    from paper_2509_15948_b200.pruning import TrainRequest
+    from paper_2509_15948_b200.scheduler import execute_batched
+
+    def render(graph, tparams, stems):
+        return execute_batched(graph, tparams, stems, device=dev)[0].cpu().numpy()
+
+    songs = []
+    for i, (k, s) in enumerate(((4, 1), (6, 2), (3, 1))):
+        graph, params, stems, target = bench.make_inputs(40 + i, k, s, 70_000, render)
+        if i == 1:
+            procs = graph.processor_nodes()
+            graph, params = bypass_remove(graph, params, set(procs[::4]))
+        songs.append((graph, params, Session(stems, target)))
+    cfg = TrainConfig(segment_seconds=57_000 / 30000, steps=6, seed=0)
+    alone = []
+    for i, (g, p, sess) in enumerate(songs):
+        q, hist = p.copy(), []
+        train(g, q, sess, cfg, rng=rng_for(i, "train-segments"), history=hist, alpha_p_fn=lambda s: 1e-4 * s)
+        alone.append((q, hist))
+    reqs = [TrainRequest(g, p.copy(), sess, cfg, rng_for(i, "train-segments"), [], lambda s: 1e-4 * s)
+            for i, (g, p, sess) in enumerate(songs)]
+    train_batch(reqs, device=dev)
+    for (q, hist), r in zip(alone, reqs):
+        for t in "gsecnrd":
+            np.testing.assert_array_equal(r.params.params[t], q.params[t])
+        np.testing.assert_array_equal(r.params.raw_weights, q.raw_weights)
+        assert [h["loss"] for h in r.history] == [h["loss"] for h in hist]
+
+
+def test_lockstep_song_searches_equal_sequential(dev):
+    """Whole desk-recipe searches run in lock-step (every console fit and fine-tune of the
+    group as one batched program) give the sequential searches' results: trials, ledgers,
+    surviving sets, final .mixgraph.json bytes and losses."""
+    import bench
+    from paper_2509_15948_b200.scheduler import execute_batched
+    from paper_2509_15948_b200.songs import SongSpec, search_songs, search_songs_lockstep
+
+    def render(graph, tparams, stems):
+        return execute_batched(graph, tparams, stems, device=dev)[0].cpu().numpy()
+
+    specs = [SongSpec(index=i, tracks=k, subgroups=1, length=132_300) for i, k in enumerate((4, 5, 3))]
+    inputs = {i: bench.make_inputs(20 + i, s.tracks, s.subgroups, s.length, render) for i, s in enumerate(specs)}
+    seq = search_songs(specs, [0, 1, 2], inputs, concurrent=1, iterations=3, device=dev)
+    lock = search_songs_lockstep(specs, [0, 1, 2], inputs, group=3, iterations=3, device=dev)
+    keys = ("song", "tracks", "trials", "pruning_ratio", "console_loss", "final_loss", "alive", "ledger", "graph_json")
+    assert [{k: r[k] for k in keys} for r in lock] == [{k: r[k] for k in keys} for r in seq]
