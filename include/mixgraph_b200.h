@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define MGB_ABI_VERSION 3
+#define MGB_ABI_VERSION 4
 
 /* One homogeneous schedule level (Algorithm 1 step) of B same-type nodes.
  * Replaces processors.KERNELS[tag](u, p) + drywet_wrap(ybar, u, w)
@@ -116,6 +116,14 @@ int mgb_weights(const double* raw, const double* mask, double* w, int P, void* s
  * out[s] = sum_{i in [seg_off[s], seg_off[s+1])} in_rows[i], each row (2,L). */
 int mgb_bus_sum(const float* const* in_rows, const int* seg_off, float* out, int S, int L, void* stream);
 
+/* Segment gather for a training step (mg/optimizer.py:97-105 sample_segment):
+ * dst[r][0:len] = src[r][song_off[row_song[r]] : + len] for r < rows; src, dst
+ * and row_song are device arrays of rows entries, song_off a device array of
+ * per-song sample offsets (rewritten between steps; a captured step replays with
+ * the new values).  Used by the batched multi-song trainer. */
+int mgb_gather_rows(const float* const* src, float* const* dst, const int* row_song, const long long* song_off,
+                    int rows, int len, void* stream);
+
 /* Batched complex FFT, natural order, unnormalised except for `scale`.
  * in/out: batch x 2^log2n complex64; tmp: batch x 2^log2n (only for log2n > 13). */
 int mgb_fft(const void* in, void* out, void* tmp, int batch, int log2n, int inverse, float scale, void* stream);
@@ -149,12 +157,19 @@ typedef struct MgbLoss {
   MgbLossRes res[8];
   int Ls;                       /* scored length */
   double group_w[4];            /* [lr/2, lr/2, mid, side] */
-  double* stats;                /* [n_res*4*4] fp64: tnorm, slog, sdiff2, sc (per res, group) */
-  double* loss;                 /* device scalar: L_a */
+  double* stats;                /* [batch][n_res*4*4] fp64: tnorm, slog, sdiff2, sc (per res, group) */
+  double* loss;                 /* device [batch]: L_a per signal */
+  int batch;                    /* signals per call (0 or 1: one); the per-signal buffers of every
+                                   resolution (tmel, tlog, mel, part, gframes) hold batch copies,
+                                   signal-major */
+  long long sig_stride;         /* floats from one signal's left channel to the next signal's (input,
+                                   target and gradient pointers alike; batch > 1 only) */
 } MgbLoss;
 
 /* Target spectra for a (2, Ls) target whose channels start at tgt_l / tgt_r
- * (prepare_target, mg/losses.py:130-140). */
+ * (prepare_target, mg/losses.py:130-140).  With batch > 1 the three calls below
+ * process batch independent signals (songs) at once: signal q's pointers are the
+ * given ones plus q * sig_stride. */
 int mgb_mrstft_target(const MgbLoss* loss, const float* tgt_l, const float* tgt_r, void* stream);
 /* L_a for the (2, Ls) estimate; writes *loss->loss (mg/losses.py:143-170). */
 int mgb_mrstft_forward(const MgbLoss* loss, const float* y_l, const float* y_r, void* stream);

@@ -44,6 +44,7 @@ class MgbLoss(ctypes.Structure):
     _fields_ = [
         ("n_res", c_int), ("res", MgbLossRes * 8), ("Ls", c_int),
         ("group_w", c_double * 4), ("stats", c_void_p), ("loss", c_void_p),
+        ("batch", c_int), ("sig_stride", c_longlong),
     ]
 
 
@@ -56,7 +57,7 @@ class DeviceError(RuntimeError):
 
 
 _lib = None
-ABI_VERSION = 3  # MGB_ABI_VERSION in include/mixgraph_b200.h
+ABI_VERSION = 4  # MGB_ABI_VERSION in include/mixgraph_b200.h
 
 
 def lib():
@@ -93,13 +94,14 @@ def lib():
                                  c_longlong, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p]
     L.mgb_sparsity.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
+    L.mgb_gather_rows.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]
     L.mgb_stream_create.argtypes = []
     L.mgb_stream_create.restype = c_void_p
     L.mgb_stream_destroy.argtypes = [c_void_p]
     for name in ("mgb_init", "mgb_level_forward", "mgb_level_backward", "mgb_level_forward_phase",
                  "mgb_level_backward_phase", "mgb_weights", "mgb_bus_sum",
                  "mgb_fft", "mgb_mrstft_target", "mgb_mrstft_forward", "mgb_mrstft_backward",
-                 "mgb_adamw_step", "mgb_sparsity", "mgb_stream_destroy"):
+                 "mgb_adamw_step", "mgb_sparsity", "mgb_stream_destroy", "mgb_gather_rows"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -108,7 +110,7 @@ def lib():
 EXPORTED = ("mgb_abi_version", "mgb_init", "mgb_level_workspace", "mgb_level_forward",
             "mgb_level_backward", "mgb_level_forward_phase", "mgb_level_backward_phase", "mgb_launch_count", "mgb_weights", "mgb_bus_sum", "mgb_fft", "mgb_mrstft_target",
             "mgb_mrstft_forward", "mgb_mrstft_backward", "mgb_adamw_step", "mgb_sparsity",
-            "mgb_stream_create", "mgb_stream_destroy")
+            "mgb_stream_create", "mgb_stream_destroy", "mgb_gather_rows")
 
 
 def check(rc, what):

@@ -25,6 +25,8 @@ are served together by one ``BatchTrainEngine``.
 
 from __future__ import annotations
 
+import time
+
 import numpy as np
 import torch
 
@@ -109,7 +111,8 @@ class BatchTrainEngine:
         self.v = torch.zeros(lay.n, dtype=F64, device=dev)
         self.plan = RenderPlan(union.graph, union.schedule, self.L, dev, self.params, self.grads, lay, backward=True)
         assert self.plan.n_out == G
-        self.losses = [LossPlan(cfg.loss, self.L - self.ws, dev) for _ in range(G)]
+        # one MRSTFT call set for all songs (signals 2L apart in ys / targets / dYs)
+        self.lossp = LossPlan(cfg.loss, self.L - self.ws, dev, batch=G, sig_stride=2 * self.L)
         self.targets = torch.zeros((G, 2, self.L), dtype=F32, device=dev)
         self.scalars = torch.zeros(8, dtype=F64, device=dev)
         self.vals = torch.zeros((G, 4), dtype=F64, device=dev)  # per song: loss, L_a, L_g, L_p
@@ -129,8 +132,30 @@ class BatchTrainEngine:
         self.t = 0
         self.side = own_stream(dev, "side")
         self._graph = None
-        self._ring = torch.zeros((64, 8), dtype=F64).pin_memory()
+        self._ring = torch.zeros((64, 8 + G), dtype=F64).pin_memory()
         self._ring_ev = [None] * 64
+        self.song_off = torch.zeros(G, dtype=torch.int64, device=dev)
+        self.gather = None  # (src ptrs, dst ptrs, row song, rows): set_sessions
+
+    def set_sessions(self, sessions):
+        """Device sessions (stems (K_i, 2, T_i), target (2, T_i)) per song: every step
+        gathers each song's segment at its offset (song_off) into the union's inputs."""
+        L, u = self.L, self.union
+        src, dst, song = [], [], []
+        for i, (st, tg) in enumerate(sessions):
+            T = st.shape[-1]
+            for k in range(st.shape[0]):
+                for c in range(2):
+                    src.append(ptr(st, (k * 2 + c) * T))
+                    dst.append(ptr(self.plan.stems, ((u.in_off[i] + k) * 2 + c) * L))
+                    song.append(i)
+            for c in range(2):
+                src.append(ptr(tg, c * T))
+                dst.append(ptr(self.targets, (i * 2 + c) * L))
+                song.append(i)
+        self._sessions = sessions  # keep the source buffers alive
+        t = [torch.tensor(np.asarray(a, dtype=np.int64), device=self.device) for a in (src, dst)]
+        self.gather = (t[0], t[1], torch.tensor(song, dtype=torch.int32, device=self.device), len(src))
 
     def load_params(self, params_list):
         self.params.copy_(torch.from_numpy(self.union.pack(params_list)))
@@ -143,17 +168,19 @@ class BatchTrainEngine:
         plan = self.plan
         Ld = lib()
         main, side = current_stream(), self.side
+        if self.gather is not None:
+            src, dst, song, rows = self.gather
+            check(Ld.mgb_gather_rows(ptr(src), ptr(dst), ptr(song), ptr(self.song_off), rows, L, stream_ptr()),
+                  "mgb_gather_rows")
         prepared = plan.prepare(side)
         with on_stream(side):
             plan.dYs[:, :, :ws].zero_()
-            for i, lp in enumerate(self.losses):
-                lp.target(ptr(self.targets, (2 * i) * L + ws), ptr(self.targets, (2 * i + 1) * L + ws))
+            self.lossp.target(ptr(self.targets, ws), ptr(self.targets, L + ws))
             tev = torch.cuda.Event()
             tev.record(side)
         plan.forward(use_mask=False, prepared=prepared, norms=side)
         main.wait_event(tev)
-        for i, lp in enumerate(self.losses):
-            lp.forward(ptr(plan.ys, (2 * i) * L + ws), ptr(plan.ys, (2 * i + 1) * L + ws))
+        self.lossp.forward(ptr(plan.ys, ws), ptr(plan.ys, L + ws))
         main.wait_stream(side)
         side.wait_stream(main)
         with on_stream(side):  # loss assembly per song (read by the optimiser only)
@@ -165,15 +192,13 @@ class BatchTrainEngine:
                 if n:
                     check(Ld.mgb_sparsity(ptr(self.params, lay.w_off + u.proc_off[i]), n,
                                           ptr(self.sparsity, i), stream_ptr()), "mgb_sparsity")
-            la = torch.stack([lp.loss for lp in self.losses])
+            la = self.lossp.loss
             ap = self.scalars[7]
             total = la + self.reg_song * float(self.cfg.loss.gain_staging_weight) + \
                 torch.where(ap > 0, ap * self.sparsity, torch.zeros_like(self.sparsity))
             torch.stack([total, la, self.reg_song, self.sparsity], dim=1, out=self.vals)
             torch.sum(total, dim=0, out=self.guard)
-        for i, lp in enumerate(self.losses):
-            lp.backward(ptr(plan.ys, (2 * i) * L + ws), ptr(plan.ys, (2 * i + 1) * L + ws),
-                        ptr(plan.dYs, (2 * i) * L + ws), ptr(plan.dYs, (2 * i + 1) * L + ws))
+        self.lossp.backward(ptr(plan.ys, ws), ptr(plan.ys, L + ws), ptr(plan.dYs, ws), ptr(plan.dYs, L + ws))
         plan.backward(side)
         main.wait_stream(side)
         check(Ld.mgb_adamw_step(ptr(self.params), ptr(self.grads), ptr(self.m), ptr(self.v), lay.n,
@@ -181,22 +206,28 @@ class BatchTrainEngine:
                                 ptr(self.scalars), ptr(self.guard), ptr(self.halt), stream_ptr()),
               "mgb_adamw_step")
 
-    def _set_scalars(self, alpha_p):
+    def _set_scalars(self, alpha_p, offsets=None):
+        """Per-step [lr, b1, b2, eps, wd, c1, c2, alpha_p] and the songs' segment offsets
+        -> device, through a ring of pinned slots."""
         c = self.cfg
         self.t += 1
         b1, b2 = c.betas
         i = self.t % 64
         if self._ring_ev[i] is not None:
             host_wait(self._ring_ev[i])
-        self._ring[i].copy_(torch.tensor([c.lr, b1, b2, c.eps, c.weight_decay, 1.0 - b1 ** self.t,
-                                          1.0 - b2 ** self.t, float(alpha_p)], dtype=F64))
-        self.scalars.copy_(self._ring[i], non_blocking=True)
+        row = self._ring[i].numpy()
+        row[:8] = (c.lr, b1, b2, c.eps, c.weight_decay, 1.0 - b1 ** self.t, 1.0 - b2 ** self.t, float(alpha_p))
+        if offsets is not None:
+            row[8:] = offsets  # exact in float64 (< 2^53)
+        self.scalars.copy_(self._ring[i, :8], non_blocking=True)
+        if offsets is not None:
+            self.song_off.copy_(self._ring[i, 8:], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
         self._ring_ev[i] = ev
 
-    def step_async(self, alpha_p=0.0, use_graph=True):
-        self._set_scalars(alpha_p)
+    def step_async(self, alpha_p=0.0, use_graph=True, offsets=None):
+        self._set_scalars(alpha_p, offsets)
         if not use_graph:
             self._body()
             return
@@ -214,13 +245,17 @@ class BatchTrainEngine:
         self._graph.replay()
 
 
+# a batched train() call replays a captured step when it is at least this long (one capture
+# serves all songs of the batch; the 50-step fine-tunes of the desk recipe qualify)
+BATCH_GRAPH_MIN_STEPS = 10
+
+
 def train_batch(reqs, device="cuda"):
     """Serve several ``pruning.TrainRequest``s (one per song, same step count and
     hyper-parameters) with one ``BatchTrainEngine``: each step draws every song's
     segment offset from its own RNG, copies the segments into the union's input
     rows, and replays the union step.  Same per-song semantics as ``optimizer.train``
     (histories, parameters written back, fresh AdamW state per call, NonFiniteLoss)."""
-    import time
     cfg = reqs[0].cfg
     for r in reqs[1:]:
         if (r.cfg.steps, r.cfg.segment_len, r.cfg.warmup_len, r.cfg.lr, r.cfg.betas, r.cfg.eps,
@@ -237,22 +272,17 @@ def train_batch(reqs, device="cuda"):
     union = SongUnion([r.graph for r in reqs])
     eng = BatchTrainEngine(union, seg, _EngineCfg(make_optimizer(None, cfg), cfg), device=dev)
     eng.load_params([r.params for r in reqs])
-    sessions = [r.session.on_device(dev) for r in reqs]
-    k_off = union.in_off
+    eng.set_sessions([r.session.on_device(dev) for r in reqs])
     rng_states = [r.rng.bit_generator.state for r in reqs]
     vals = torch.zeros((cfg.steps, eng.G, 4), dtype=F64, device=dev)
-    use_graph = cfg.steps >= _graph_min_steps()
+    use_graph = cfg.steps >= BATCH_GRAPH_MIN_STEPS
     t0 = time.perf_counter()
     for step in range(cfg.steps):
-        for i, (r, (st, tg)) in enumerate(zip(reqs, sessions)):
-            off = int(r.rng.integers(0, r.session.length - seg + 1))
-            k = st.shape[0]
-            eng.plan.stems[k_off[i]:k_off[i] + k].copy_(st[..., off:off + seg])
-            eng.targets[i].copy_(tg[..., off:off + seg])
+        offs = [int(r.rng.integers(0, r.session.length - seg + 1)) for r in reqs]
         alphas = {r.alpha_p_fn(step) if r.alpha_p_fn else 0.0 for r in reqs}
         if len(alphas) != 1:
             raise ValueError("batched songs must share the sparsity weight of every step")
-        eng.step_async(alphas.pop(), use_graph=use_graph)
+        eng.step_async(alphas.pop(), use_graph=use_graph, offsets=offs)
         vals[step].copy_(eng.vals)
     host_wait(torch.cuda.current_stream())
     host = vals.cpu().numpy()
@@ -277,21 +307,149 @@ class BatchNonFinite(NonFiniteLoss):
         self.songs = songs
 
 
-def prune_songs_lockstep(jobs, device="cuda"):
+class BatchEvalEngine:
+    """Pruning trials of several songs in one device program: ``eval_loss``
+    (mg/pruning.py:115-123) of every song of a ``SongUnion`` at once, each song with
+    its own mask, parameters and eval set (same segment count and length for all
+    songs of a recipe).  One render plan per eval segment over the union, one MRSTFT
+    per (segment, song) against device-resident target spectra.  Renders are
+    incremental like ``engine.EvalEngine``'s: a trial starts at the first level where
+    any song's mask changed; per-row kernels make each song's loss bit-identical to
+    its own ``EvalEngine``."""
+
+    def __init__(self, union: SongUnion, eval_sets, device="cuda"):
+        self.device = dev = ensure_device(device)
+        self.union = union
+        es0 = eval_sets[0]
+        self.nseg, self.ws = len(es0.segments), int(es0.warmup_len)
+        L = self.L = np.asarray(es0.segments[0][0]).shape[-1]
+        for es in eval_sets:
+            if (len(es.segments), int(es.warmup_len), np.asarray(es.segments[0][0]).shape[-1], es.loss_cfg) != \
+                    (self.nseg, self.ws, L, es0.loss_cfg):
+                raise ValueError("batched eval sets must share segment count, length, warm-up and loss")
+        lay = self.layout = union.layout
+        self.params = torch.zeros(lay.n, dtype=F64, device=dev)
+        self._packed = None
+        self._prep_dirty = True
+        self.plans, self.losses, self._last = [], [], []
+        for j in range(self.nseg):
+            plan = RenderPlan(union.graph, union.schedule, L, dev, self.params, None, lay, backward=False)
+            for i, es in enumerate(eval_sets):
+                st = torch.as_tensor(np.asarray(es.segments[j][0]), dtype=F32).to(dev)
+                plan.stems[union.in_off[i]:union.in_off[i] + st.shape[0]].copy_(st)
+            self.plans.append(plan)
+            G, ws = len(eval_sets), self.ws
+            # targets laid out like the union's output rows (G, 2, L), scored part at ws
+            t = torch.zeros((G, 2, L), dtype=F32, device=dev)
+            for i, es in enumerate(eval_sets):
+                t[i, :, ws:].copy_(torch.as_tensor(np.asarray(es.segments[j][1]), dtype=F32))
+            lp = LossPlan(es0.loss_cfg, L - ws, dev, backward=False, batch=G, sig_stride=2 * L)
+            lp.target(ptr(t, ws), ptr(t, L + ws))
+            self.losses.append((lp, t))
+            self._last.append(None)
+        self.acc = torch.zeros((self.nseg, len(union.graphs)), dtype=F64, device=dev)
+        self.acc_host = torch.zeros(self.acc.shape, dtype=F64).pin_memory()
+        self.mask_host = torch.ones(max(lay.P, 1), dtype=F64).pin_memory()
+
+    def load_params(self, params_list):
+        packed = self.union.pack(params_list)
+        if self._packed is not None and np.array_equal(packed, self._packed):
+            return
+        self._packed = packed.copy()
+        self.params.copy_(torch.from_numpy(packed))
+        self._prep_dirty = True
+
+    def losses_for(self, masks):
+        """Per-song mean eval loss for per-song masks (a list, one mask per song)."""
+        u = self.union
+        m = np.ones(max(self.layout.P, 1))
+        for i, mk in enumerate(masks):
+            m[u.proc_off[i]:u.proc_off[i] + len(mk)] = mk
+        self.mask_host.copy_(torch.from_numpy(m))
+        L, ws = self.L, self.ws
+        if self._prep_dirty:
+            for plan in self.plans:
+                plan.prepare()
+        for j, plan in enumerate(self.plans):
+            plan.mask.copy_(self.mask_host, non_blocking=True)
+            start = 0
+            if not self._prep_dirty and self._last[j] is not None:
+                changed = np.nonzero(m != self._last[j])[0]
+                start = int(plan.proc_level[changed].min()) if changed.size else len(plan.levels)
+            plan.forward(use_mask=True, prepared=True, norms=None, start=start)
+            self._last[j] = m.copy()
+            lp = self.losses[j][0]
+            lp.forward(ptr(plan.ys, ws), ptr(plan.ys, L + ws))
+            self.acc[j].copy_(lp.loss)
+        self._prep_dirty = False
+        self.acc_host.copy_(self.acc, non_blocking=True)
+        host_wait(current_stream())
+        a = self.acc_host.numpy()
+        out = []
+        for i in range(len(u.graphs)):
+            total = 0.0
+            for j in range(self.nseg):  # per-segment float() then mean, as mg/pruning.py:120-123
+                total += float(a[j, i])
+            out.append(total / self.nseg)
+        return out
+
+
+def prune_songs_lockstep(jobs, device="cuda", batch_trials=True):
     """Run several ``prune_song`` searches in lock-step; ``jobs`` = list of
-    (graph, params, session, PruneConfig).  Returns each search's
-    (graph, params, state, report, history), identical to running them one by one."""
-    from .pruning import prune_song, prune_song_steps, run_train_request
+    (graph, params, session, PruneConfig).  Each search is ``pruning.prune_song_steps``
+    (the reference's control flow, one copy); its train requests are served together by
+    one ``train_batch`` once every search has reached one, and its trials together by a
+    ``BatchEvalEngine`` over the songs' current graphs (a song whose pass has ended
+    keeps its last graph and mask in the union until the next round, so the union is
+    rebuilt once per round).  Returns each search's (graph, params, state, report,
+    history), identical to running them one by one."""
+    from .pruning import EvalRequest, eval_loss, prune_song, prune_song_steps, run_train_request
     gens = [prune_song_steps(g, p, s, c, None, device) for g, p, s, c in jobs]
     out = [None] * len(gens)
-    reqs = {}
-    for i, gen in enumerate(gens):
+    reqs, last_eval = {}, {}
+
+    def advance(i, value):
         try:
-            reqs[i] = next(gen)
+            reqs[i] = gens[i].send(value) if value is not _START else next(gens[i])
+            if isinstance(reqs[i], EvalRequest):
+                last_eval[i] = reqs[i]
         except StopIteration as done:
             out[i] = done.value
+            reqs.pop(i, None)
+            last_eval.pop(i, None)
+
+    for i in range(len(gens)):
+        advance(i, _START)
+    beval, bkey, loaded, trained = None, None, None, 0
     while reqs:
+        evals = sorted(i for i, r in reqs.items() if isinstance(r, EvalRequest))
+        if evals:
+            if not batch_trials or len(evals) == 1 and len(last_eval) == 1:
+                for i in evals:
+                    r = reqs[i]
+                    advance(i, eval_loss(r.graph, r.params, r.mask, r.eval_set))
+                continue
+            ids = sorted(last_eval)
+            key = tuple((i, id(last_eval[i].graph), id(last_eval[i].eval_set)) for i in ids)
+            t0 = time.perf_counter()
+            if key != bkey:
+                beval = BatchEvalEngine(SongUnion([last_eval[i].graph for i in ids]),
+                                        [last_eval[i].eval_set for i in ids], device)
+                bkey = key
+                PHASE_S["trial_engine_build"] += time.perf_counter() - t0
+            pkey = (bkey, tuple(id(last_eval[i].params) for i in ids), trained)
+            if pkey != loaded:  # parameters change only in training: no repack per trial
+                beval.load_params([last_eval[i].params for i in ids])
+                loaded = pkey
+            losses = beval.losses_for([last_eval[i].mask for i in ids])
+            PHASE_S["trials"] += time.perf_counter() - t0
+            PHASE_S["trial_slots"] += 1
+            for k, i in enumerate(ids):
+                if i in evals:
+                    advance(i, losses[k])
+            continue
         ids = sorted(reqs)
+        t0 = time.perf_counter()
         try:
             if len(ids) == 1:
                 run_train_request(reqs[ids[0]], device)
@@ -306,13 +464,18 @@ def prune_songs_lockstep(jobs, device="cuda"):
                 except NonFiniteLoss as e:
                     out[i] = e
             return out
+        trained += 1
+        PHASE_S["train"] += time.perf_counter() - t0
         for i in ids:
-            try:
-                reqs[i] = gens[i].send(None)
-            except StopIteration as done:
-                out[i] = done.value
-                del reqs[i]
+            advance(i, None)
     return out
 
 
-__all__ = ["SongUnion", "BatchTrainEngine", "train_batch", "prune_songs_lockstep", "BatchNonFinite"]
+_START = object()
+
+# wall seconds per phase of prune_songs_lockstep (tools/songs_bench.py reports them)
+PHASE_S = {"train": 0.0, "trials": 0.0, "trial_engine_build": 0.0, "trial_slots": 0, "host_other": 0.0}
+
+
+__all__ = ["SongUnion", "BatchTrainEngine", "BatchEvalEngine", "train_batch", "prune_songs_lockstep",
+           "BatchNonFinite"]

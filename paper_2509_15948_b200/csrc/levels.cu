@@ -324,3 +324,31 @@ extern "C" int mgb_bus_sum(const float* const* in_rows, const int* seg_off, floa
   MGB_CHECK_LAUNCH();
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Segment gather (mg/optimizer.py:97-105 sample_segment, on device): row r of the
+// output is src[r][song_off[row_song[r]] : + len].  One launch copies a step's
+// segments of every stem channel and target channel of every song of a batch,
+// reading the per-song offsets from device memory (so a captured step replays
+// with new offsets).
+__global__ void __launch_bounds__(256) k_gather_rows(const float* const* __restrict__ src, float* const* __restrict__ dst,
+                                                     const int* __restrict__ row_song,
+                                                     const long long* __restrict__ song_off, int len) {
+  mgb_pdl_entry();
+  const int r = blockIdx.y;
+  const float* s = src[r] + song_off[row_song[r]];
+  float* d = dst[r];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x)
+    d[i] = __ldg(s + i);
+}
+
+extern "C" int mgb_gather_rows(const float* const* src, float* const* dst, const int* row_song,
+                               const long long* song_off, int rows, int len, void* stream) {
+  if (rows <= 0 || len <= 0) return 0;
+  if (!src || !dst || !row_song || !song_off) return 1;
+  int bx = (len + 255) / 256;
+  if (bx > 64) bx = 64;
+  mgb_launch(k_gather_rows, dim3(bx, rows), dim3(256), 0, (cudaStream_t)stream, src, dst, row_song, song_off, len);
+  MGB_CHECK_LAUNCH();
+  return 0;
+}

@@ -202,14 +202,30 @@ __device__ __forceinline__ void mags_inplace(float2* S, int tt) {
   __syncthreads();
 }
 
+// Several signals (songs) per call: signal q = blockIdx.y starts sig_stride floats after
+// signal q-1 (input, target and gradient alike); every per-signal buffer of a
+// resolution is batch x its single-signal size, signal-major.
+__device__ __forceinline__ size_t mel_elems(const MgbLossRes& r) { return (size_t)4 * r.frames * r.n_mels; }
+
 // mode 0: target (write tmel, tlog, part[.,g,0] = sum mel^2)
 // mode 1: estimate (write mel, part[.,g,0] = sum |dlog|, part[.,g,1] = sum (mel - tmel)^2)
 // FPC frames per CTA; within a frame, T/4 threads per group g walk the mel bands.
 template <int N>
 __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(MgbLossRes r, const float* __restrict__ xl,
-                                                      const float* __restrict__ xr, int Ls, int mode) {
+                                                      const float* __restrict__ xr, int Ls, int mode,
+                                                      long long sig_stride) {
   mgb_pdl_entry();
   using C = FC<N, 16>;
+  {
+    const int sq = blockIdx.y;
+    xl += sq * sig_stride;
+    xr += sq * sig_stride;
+    const size_t me = sq * mel_elems(r);
+    r.tmel += me;
+    r.tlog += me;
+    r.mel += me;
+    r.part += (size_t)sq * r.frames * 12;
+  }
   constexpr int T = C::T, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double red[2][C::NT];
@@ -283,19 +299,20 @@ __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(
 __global__ void k_mr_finalize(MgbLoss L, int mode) {
   mgb_pdl_entry();
   __shared__ double red[32];
-  const int ri = blockIdx.x >> 2, g = blockIdx.x & 3;
+  const int ri = blockIdx.x >> 2, g = blockIdx.x & 3, sq = blockIdx.y;
   const MgbLossRes& r = L.res[ri];
+  const double* part = r.part + (size_t)sq * r.frames * 12;
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll 4
   for (int f = threadIdx.x; f < r.frames; f += blockDim.x) {  // (loads of several frames in flight)
-    s0 += __ldg(r.part + ((size_t)f * 4 + g) * 3 + 0);
-    s1 += __ldg(r.part + ((size_t)f * 4 + g) * 3 + 1);
+    s0 += __ldg(part + ((size_t)f * 4 + g) * 3 + 0);
+    s1 += __ldg(part + ((size_t)f * 4 + g) * 3 + 1);
   }
   s0 = block_sum(s0, red);
   __syncthreads();
   s1 = block_sum(s1, red);
   if (threadIdx.x == 0) {
-    double* st = L.stats + ((size_t)ri * 4 + g) * 4;
+    double* st = L.stats + (size_t)sq * L.n_res * 16 + ((size_t)ri * 4 + g) * 4;
     if (mode == 0) {
       st[0] = fmax(sqrt(s0), 1e-12);
     } else {
@@ -309,14 +326,15 @@ __global__ void k_mr_finalize(MgbLoss L, int mode) {
 // L_a = sum over (res, group) of w_g (slog / frames + dn / tnorm), in a fixed order
 __global__ void k_mr_total(MgbLoss L) {
   mgb_pdl_entry();
-  if (threadIdx.x) return;
+  const int sq = threadIdx.x;
+  if (sq >= (L.batch > 1 ? L.batch : 1)) return;
   double tot = 0.0;
   for (int ri = 0; ri < L.n_res; ++ri)
     for (int g = 0; g < 4; ++g) {
-      const double* st = L.stats + ((size_t)ri * 4 + g) * 4;
+      const double* st = L.stats + (size_t)sq * L.n_res * 16 + ((size_t)ri * 4 + g) * 4;
       tot += L.group_w[g] * (st[1] / (double)L.res[ri].frames + st[3] / st[0]);
     }
-  *L.loss = tot;
+  L.loss[sq] = tot;
 }
 
 // backward: dmel, frame spectrum recomputed, d|X| through the CSC projection,
@@ -328,6 +346,17 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
                                                                        const float* __restrict__ xr, int Ls) {
   mgb_pdl_entry();
   using C = FC<N, 8>;
+  {
+    const int sq = blockIdx.y;
+    xl += sq * L.sig_stride;
+    xr += sq * L.sig_stride;
+    const size_t me = sq * mel_elems(r);
+    r.tmel += me;
+    r.tlog += me;
+    r.mel += me;
+    r.gframes += (size_t)sq * r.frames * 2 * N;
+    stats += (size_t)sq * L.n_res * 16;
+  }
   constexpr int T = C::T, NB = C::NB, PER = (NB + T - 1) / T;
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ float dmel[C::FPC][4][128];
@@ -423,9 +452,11 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
 // position t + n/2, plus the reflect-pad adjoint near both ends (gather, no atomics)
 __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ gl, float* __restrict__ gr) {
   mgb_pdl_entry();
-  const int Ls = L.Ls;
+  const int Ls = L.Ls, sq = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= Ls) return;
+  gl += sq * L.sig_stride;
+  gr += sq * L.sig_stride;
   double al = 0.0, ar = 0.0;
   for (int ri = 0; ri < L.n_res; ++ri) {
     const MgbLossRes& r = L.res[ri];
@@ -443,7 +474,7 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
       for (int f = flo; f <= fhi; ++f) {
         const int o = p - (f << lh);
         if (o < 0 || o >= n) continue;
-        const float* gfp = r.gframes + ((size_t)f << (ln + 1));
+        const float* gfp = r.gframes + (size_t)sq * r.frames * 2 * n + ((size_t)f << (ln + 1));
         al += __ldg(gfp + o);
         ar += __ldg(gfp + n + o);
       }
@@ -453,10 +484,14 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
   gr[t] = (float)ar;
 }
 
+inline int nbatch(const MgbLoss& L) { return L.batch > 1 ? L.batch : 1; }
+
 template <int N>
-int launch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, int mode, cudaStream_t st) {
+int launch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, int mode, int nb, long long stride,
+               cudaStream_t st) {
   using C = FC<N, 16>;
-  mgb_launch(k_mr_fwd<N>, dim3((r.frames + C::FPC - 1) / C::FPC), dim3(C::NT), C::SMEM, st, r, xl, xr, Ls, mode);
+  mgb_launch(k_mr_fwd<N>, dim3((r.frames + C::FPC - 1) / C::FPC, nb), dim3(C::NT), C::SMEM, st, r, xl, xr, Ls, mode,
+             stride);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -465,19 +500,21 @@ template <int N>
 int launch_bwd(const MgbLossRes& r, const double* stats, const MgbLoss& L, const float* xl, const float* xr,
                int Ls, cudaStream_t st) {
   using C = FC<N, 8>;
-  mgb_launch(k_mr_bwd<N>, dim3((r.frames + C::FPC - 1) / C::FPC), dim3(C::NT), C::SMEM, st, r, stats, L, xl, xr, Ls);
+  mgb_launch(k_mr_bwd<N>, dim3((r.frames + C::FPC - 1) / C::FPC, nbatch(L)), dim3(C::NT), C::SMEM, st, r, stats, L, xl,
+             xr, Ls);
   MGB_CHECK_LAUNCH();
   return 0;
 }
 
-int dispatch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, int mode, cudaStream_t st) {
+int dispatch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, int mode, int nb, long long stride,
+                 cudaStream_t st) {
   switch (r.n_fft) {
-    case 256: return launch_fwd<256>(r, xl, xr, Ls, mode, st);
-    case 512: return launch_fwd<512>(r, xl, xr, Ls, mode, st);
-    case 1024: return launch_fwd<1024>(r, xl, xr, Ls, mode, st);
-    case 2048: return launch_fwd<2048>(r, xl, xr, Ls, mode, st);
-    case 4096: return launch_fwd<4096>(r, xl, xr, Ls, mode, st);
-    case 8192: return launch_fwd<8192>(r, xl, xr, Ls, mode, st);
+    case 256: return launch_fwd<256>(r, xl, xr, Ls, mode, nb, stride, st);
+    case 512: return launch_fwd<512>(r, xl, xr, Ls, mode, nb, stride, st);
+    case 1024: return launch_fwd<1024>(r, xl, xr, Ls, mode, nb, stride, st);
+    case 2048: return launch_fwd<2048>(r, xl, xr, Ls, mode, nb, stride, st);
+    case 4096: return launch_fwd<4096>(r, xl, xr, Ls, mode, nb, stride, st);
+    case 8192: return launch_fwd<8192>(r, xl, xr, Ls, mode, nb, stride, st);
     default: return 1;
   }
 }
@@ -497,6 +534,7 @@ int dispatch_bwd(const MgbLossRes& r, const double* stats, const MgbLoss& L, con
 
 int check_loss(const MgbLoss* L) {
   if (!L || L->n_res <= 0 || L->n_res > 8 || L->Ls <= 0) return 1;
+  if (L->batch > 1024 || (L->batch > 1 && L->sig_stride < L->Ls)) return 1;
   for (int i = 0; i < L->n_res; ++i) {
     const MgbLossRes& r = L->res[i];
     if (r.n_mels > 128 || r.n_fft / 2 >= L->Ls) return 1;
@@ -577,9 +615,11 @@ int mgb_loss_init() {
 extern "C" int mgb_mrstft_target(const MgbLoss* L, const float* tl, const float* tr, void* stream) {
   if (int rc = check_loss(L)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) { return dispatch_fwd(L->res[i], tl, tr, L->Ls, 0, s); }))
+  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) {
+        return dispatch_fwd(L->res[i], tl, tr, L->Ls, 0, nbatch(*L), L->sig_stride, s);
+      }))
     return rc;
-  mgb_launch(k_mr_finalize, dim3(4 * L->n_res), dim3(1024), 0, st, *L, 0);
+  mgb_launch(k_mr_finalize, dim3(4 * L->n_res, nbatch(*L)), dim3(1024), 0, st, *L, 0);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -587,11 +627,13 @@ extern "C" int mgb_mrstft_target(const MgbLoss* L, const float* tl, const float*
 extern "C" int mgb_mrstft_forward(const MgbLoss* L, const float* yl, const float* yr, void* stream) {
   if (int rc = check_loss(L)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) { return dispatch_fwd(L->res[i], yl, yr, L->Ls, 1, s); }))
+  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) {
+        return dispatch_fwd(L->res[i], yl, yr, L->Ls, 1, nbatch(*L), L->sig_stride, s);
+      }))
     return rc;
-  mgb_launch(k_mr_finalize, dim3(4 * L->n_res), dim3(1024), 0, st, *L, 1);
+  mgb_launch(k_mr_finalize, dim3(4 * L->n_res, nbatch(*L)), dim3(1024), 0, st, *L, 1);
   MGB_CHECK_LAUNCH();
-  mgb_launch(k_mr_total, dim3(1), dim3(32), 0, st, *L);
+  mgb_launch(k_mr_total, dim3(1), dim3((nbatch(*L) + 31) / 32 * 32), 0, st, *L);
   MGB_CHECK_LAUNCH();
   return 0;
 }
@@ -604,7 +646,7 @@ extern "C" int mgb_mrstft_backward(const MgbLoss* L, const float* yl, const floa
         return dispatch_bwd(L->res[i], L->stats + (size_t)i * 16, *L, yl, yr, L->Ls, s);
       }))
     return rc;
-  mgb_launch(k_mr_ola, dim3((L->Ls + 255) / 256), dim3(256), 0, st, *L, gl, gr);
+  mgb_launch(k_mr_ola, dim3((L->Ls + 255) / 256, nbatch(*L)), dim3(256), 0, st, *L, gl, gr);
   MGB_CHECK_LAUNCH();
   return 0;
 }

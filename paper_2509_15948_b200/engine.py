@@ -507,10 +507,28 @@ class RenderPlan:
 # loss plan
 
 
-class LossPlan:
-    """Device MRSTFT (mg/losses.py:104-170) for a fixed scored length Ls."""
+_proj_dev = {}
 
-    def __init__(self, cfg, Ls: int, device):
+
+def projection_device(device, n, cfg):
+    """The banded mel x A-weight tables of one resolution on a device (immutable, shared)."""
+    key = (str(device), n, cfg.sample_rate, cfg.mel_bins, float(cfg.mel_fmax), bool(cfg.a_weighting))
+    hit = _proj_dev.get(key)
+    if hit is None:
+        tabs = projection_sparse(n, cfg.sample_rate, cfg.mel_bins, float(cfg.mel_fmax), bool(cfg.a_weighting))
+        hit = _proj_dev[key] = [torch.from_numpy(a).to(device) for a in tabs]
+    return hit
+
+
+class LossPlan:
+    """Device MRSTFT (mg/losses.py:104-170) for a fixed scored length Ls.
+
+    ``backward=False`` (a trial's forward-only loss) skips the frame-adjoint buffers.
+    ``batch`` > 1: that many independent signals (songs) per call, signal q's input,
+    target and gradient pointers ``sig_stride`` floats after signal q-1's; ``loss``
+    is then a (batch,) vector."""
+
+    def __init__(self, cfg, Ls: int, device, backward: bool = True, batch: int = 1, sig_stride: int = 0):
         self.device = ensure_device(device)
         dev = self.device
         self.cfg = cfg
@@ -532,26 +550,31 @@ class LossPlan:
         for i, v in enumerate(gw):
             st.group_w[i] = v
         self._keep = []
-        self.stats = torch.zeros(len(sizes) * 16, dtype=F64, device=dev)
-        self.loss = torch.zeros((), dtype=F64, device=dev)
+        nb = max(1, int(batch))
+        if nb > 1 and sig_stride < Ls:
+            raise ValueError("batched loss: sig_stride must be at least the scored length")
+        st.batch, st.sig_stride = nb, int(sig_stride) if nb > 1 else 0
+        self.batch = nb
+        self.stats = torch.zeros(nb * len(sizes) * 16, dtype=F64, device=dev)
+        self.loss = torch.zeros((nb,) if nb > 1 else (), dtype=F64, device=dev)
         st.stats, st.loss = ptr(self.stats), ptr(self.loss)
         for i, n in enumerate(sizes):
             hop = n // 4
             frames = 1 + Ls // hop
-            tabs = projection_sparse(n, cfg.sample_rate, cfg.mel_bins, float(cfg.mel_fmax),
-                                     bool(cfg.a_weighting))
-            dt = [torch.from_numpy(a).to(dev) for a in tabs]
+            dt = projection_device(dev, n, cfg)
             nm = cfg.mel_bins
-            tmel = torch.zeros((4, frames, nm), dtype=F64, device=dev)
-            tlog = torch.zeros_like(tmel)
-            mel = torch.zeros_like(tmel)
-            part = torch.zeros((frames, 4, 3), dtype=F64, device=dev)
-            gfr = torch.zeros((frames, 2, n), dtype=F32, device=dev)
+            # every element is written (target / forward kernels) before it is read
+            tmel = torch.empty((nb, 4, frames, nm), dtype=F64, device=dev)
+            tlog = torch.empty_like(tmel)
+            mel = torch.empty_like(tmel)
+            part = torch.empty((nb, frames, 4, 3), dtype=F64, device=dev)
+            gfr = torch.empty((nb, frames, 2, n), dtype=F32, device=dev) if backward else None
             r = st.res[i]
             r.n_fft, r.hop, r.frames, r.n_mels = n, hop, frames, nm
             (r.band_start, r.band_len, r.band_off, r.band_w,
              r.bin_start, r.bin_len, r.bin_band, r.bin_w) = [ptr(t) for t in dt]
-            r.tmel, r.tlog, r.mel, r.part, r.gframes = ptr(tmel), ptr(tlog), ptr(mel), ptr(part), ptr(gfr)
+            r.tmel, r.tlog, r.mel, r.part = ptr(tmel), ptr(tlog), ptr(mel), ptr(part)
+            r.gframes = ptr(gfr) if gfr is not None else None
             self._keep += dt + [tmel, tlog, mel, part, gfr]
         self.struct = st
 
@@ -563,6 +586,8 @@ class LossPlan:
               "mrstft forward")
 
     def backward(self, yl_ptr, yr_ptr, gl_ptr, gr_ptr):
+        if not self.struct.res[0].gframes:
+            raise RuntimeError("LossPlan built with backward=False")
         check(lib().mgb_mrstft_backward(ctypes.byref(self.struct), yl_ptr, yr_ptr, gl_ptr, gr_ptr,
                                         stream_ptr()), "mrstft backward")
 
@@ -787,7 +812,7 @@ class EvalEngine:
                 plan.set_stems(st)
                 self.plans.append(plan)
             self.seg_stems.append(st)
-            lp = LossPlan(loss_cfg, L - self.ws, dev)
+            lp = LossPlan(loss_cfg, L - self.ws, dev, backward=False)
             t = torch.as_tensor(np.asarray(target), dtype=F32).to(dev).contiguous()
             lp.target(ptr(t, 0), ptr(t, t.shape[-1]))
             self.losses.append((lp, t))

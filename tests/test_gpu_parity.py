@@ -519,3 +519,28 @@ def test_lockstep_song_searches_equal_sequential(dev):
     lock = search_songs_lockstep(specs, [0, 1, 2], inputs, group=3, iterations=3, device=dev)
     keys = ("song", "tracks", "trials", "pruning_ratio", "console_loss", "final_loss", "alive", "ledger", "graph_json")
     assert [{k: r[k] for k in keys} for r in lock] == [{k: r[k] for k in keys} for r in seq]
+
+
+def test_batched_mrstft_equals_per_signal_calls(dev):
+    """MgbLoss.batch > 1 (several songs' losses in one call set): every signal's loss and
+    gradient equal the single-signal calls bit for bit."""
+    from paper_2509_15948_b200.engine import LossPlan, ptr
+    from paper_2509_15948_b200.losses import LossConfig
+    rng = np.random.default_rng(11)
+    G, L, ws = 3, 70_000, 30_000
+    y = torch.tensor(0.3 * rng.standard_normal((G, 2, L)), dtype=torch.float32, device=dev)
+    t = torch.tensor(0.3 * rng.standard_normal((G, 2, L)), dtype=torch.float32, device=dev)
+    cfg = LossConfig()
+    bl = LossPlan(cfg, L - ws, dev, batch=G, sig_stride=2 * L)
+    gb = torch.zeros((G, 2, L), dtype=torch.float32, device=dev)
+    bl.target(ptr(t, ws), ptr(t, L + ws))
+    bl.forward(ptr(y, ws), ptr(y, L + ws))
+    bl.backward(ptr(y, ws), ptr(y, L + ws), ptr(gb, ws), ptr(gb, L + ws))
+    for i in range(G):
+        lp = LossPlan(cfg, L - ws, dev)
+        g1 = torch.zeros((2, L), dtype=torch.float32, device=dev)
+        lp.target(ptr(t[i], ws), ptr(t[i], L + ws))
+        lp.forward(ptr(y[i], ws), ptr(y[i], L + ws))
+        lp.backward(ptr(y[i], ws), ptr(y[i], L + ws), ptr(g1, ws), ptr(g1, L + ws))
+        assert float(bl.loss[i]) == float(lp.loss)
+        assert torch.equal(gb[i], g1)

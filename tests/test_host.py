@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     L = ctypes.CDLL(_lib.LIB_PATH)
     for s in _declared_symbols():
         assert hasattr(L, s), s
-    assert L.mgb_abi_version() == 3
+    assert L.mgb_abi_version() == 4
     lib = _lib.lib()
     # workspace queries are host-only arithmetic
     assert lib.mgb_level_workspace(b"g", 4, 1000) > 0

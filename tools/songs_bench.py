@@ -26,7 +26,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2509_15948_b200.scheduler import execute_batched  # noqa: E402
-from paper_2509_15948_b200.songs import assign_lpt, desk_specs, gather_results, search_songs, song_costs  # noqa: E402
+from paper_2509_15948_b200.songs import (assign_lpt, desk_specs, gather_results, search_songs,  # noqa: E402
+                                         search_songs_lockstep, song_costs)
 
 
 def main():
@@ -35,6 +36,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--iterations", type=int, default=12)
     ap.add_argument("--concurrent", type=int, default=1, help="songs in flight per GPU (threads + streams)")
+    ap.add_argument("--lockstep", type=int, default=0,
+                    help="search songs in lock-step groups of this size (batched training), 0 = off")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -58,7 +61,12 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    results = search_songs(specs, mine, inputs, concurrent=args.concurrent, iterations=args.iterations, device=dev)
+    if args.lockstep:
+        results = search_songs_lockstep(specs, mine, inputs, group=args.lockstep, iterations=args.iterations,
+                                        device=dev)
+    else:
+        results = search_songs(specs, mine, inputs, concurrent=args.concurrent, iterations=args.iterations,
+                               device=dev)
     torch.cuda.synchronize()
     wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if dist is not None:
@@ -69,9 +77,12 @@ def main():
         print(json.dumps({"metric": "songs searched/hour (config 5 desk recipe)",
                           "value": len(merged) / w * 3600.0, "unit": "songs/hour", "n_gpus": world,
                           "songs": len(merged), "wall_s": w, "iterations": args.iterations, "concurrent": args.concurrent,
+                          "lockstep": args.lockstep,
+                          "lockstep_phase_s": __import__("paper_2509_15948_b200.batch", fromlist=["PHASE_S"]).PHASE_S,
                           "max_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
                           "reserved_gb": torch.cuda.memory_reserved(dev) / 1e9,
-                          "per_song": merged}))
+                          "per_song": [{k: v for k, v in r.items() if k not in ("graph_json", "ledger", "alive")}
+                                       for r in merged]}))
     if dist is not None:
         dist.destroy_process_group()
 
