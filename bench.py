@@ -48,7 +48,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--song-concurrency", type=int, default=4,
-                    help="songs searched concurrently per GPU (host threads + CUDA streams)")
+                    help="songs searched concurrently per GPU (host threads + CUDA streams), with --song-lockstep 0")
+    ap.add_argument("--song-lockstep", type=int, default=8,
+                    help="songs per GPU searched in lock-step groups of this size: each group's training steps and "
+                         "trials run as one batched device program (0: threads instead)")
     ap.add_argument("--songs", type=int, default=8,
                     help="config-5 desk-recipe pruning searches per GPU for songs/hour (0: skip)")
     ap.add_argument("--tracks", type=int, default=K_TRACKS)
@@ -328,7 +331,8 @@ def main():
     # config 5: full pruning searches (desk recipe), this rank's LPT share of songs*world songs
     songs = None
     if args.songs > 0:
-        from paper_2509_15948_b200.songs import assign_lpt, desk_specs, gather_results, search_songs, song_costs
+        from paper_2509_15948_b200.songs import (assign_lpt, desk_specs, gather_results, search_songs,
+                                                 search_songs_lockstep, song_costs)
         specs = desk_specs(args.songs * world, seed=0)
         mine = assign_lpt(song_costs(specs), world)[rank]
         inputs = {i: make_inputs(1000 + specs[i].index, specs[i].tracks, specs[i].subgroups, specs[i].length,
@@ -337,7 +341,10 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = search_songs(specs, mine, inputs, concurrent=args.song_concurrency, device=dev)
+        if args.song_lockstep > 0:
+            res = search_songs_lockstep(specs, mine, inputs, group=args.song_lockstep, device=dev)
+        else:
+            res = search_songs(specs, mine, inputs, concurrent=args.song_concurrency, device=dev)
         torch.cuda.synchronize()
         sw = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
@@ -347,7 +354,10 @@ def main():
             songs = {"value": len(res) / float(sw.item()) * 3600.0, "unit": "songs/hour", "songs": len(res),
                      "wall_s": float(sw.item()), "recipe": "desk (pkg/README.md:54-58): console 600, 12 hybrid "
                      "rounds x 50 fine-tune, 57,000-sample segments, 4 eval segments, tau_rel 0.02",
-                     "concurrent_per_gpu": args.song_concurrency, "tracks": [r["tracks"] for r in res],
+                     "mode": (f"lock-step groups of {args.song_lockstep} (one batched device program per group "
+                              "for training and for trials)") if args.song_lockstep > 0 else
+                             f"{args.song_concurrency} songs in flight (threads + streams)",
+                     "tracks": [r["tracks"] for r in res],
                      "trials": [r["trials"] for r in res],
                      "gathered": {"songs": len(res), "graph_json_bytes": sum(len(r["graph_json"]) for r in res),
                                   "what": "final .mixgraph.json + PruneReport + survivors + ledger per song, "
