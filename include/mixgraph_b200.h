@@ -196,6 +196,25 @@ int mgb_adamw_step(double* p, double* g, double* m, double* v, long long n, long
                    long long w_off, int P, const double* gw, const double* mask, const double* step_scalars,
                    const double* loss_guard, double* halt, void* stream);
 
+/* ---- post-hoc song metrics (mg/metrics.py:45-112, mg/cli.py:55-63) --------- */
+
+/* Workspace bytes of mgb_song_metrics for (L, seg). */
+size_t mgb_metrics_workspace(int L, int seg);
+
+/* Metrics of a rendered match yh against its target y, both (2, L) float32:
+ *  seg_stats [L/seg][10] float64: per seg-sample segment (split_segments), for y
+ *            then yh: sum mid^2, max|mid|, sum side^2, sum l^2, sum r^2;
+ *  dots      [5] float64: s.s, s_hat.s, alpha = (s_hat.s)/(s.s), sum (alpha s)^2,
+ *            sum (s_hat - alpha s)^2 over the 2L samples (si_sdr);
+ *  bark_y, bark_yh [L/seg][n_bands] float64: log10(sum of |rfft(mid)|^2 over the
+ *            bins of Zwicker band j + 1e-12), bark_edges (device, n_bands + 1 Hz)
+ *            at sample rate sr (feature_bark_spectrum; the non-power-of-two rfft by
+ *            Bluestein on the float32 FFT).
+ * Segments require L >= seg; with L < seg only dots is written. */
+int mgb_song_metrics(const float* y, const float* yh, int L, int seg, const double* bark_edges, int n_bands,
+                     double sr, double* seg_stats, double* dots, double* bark_y, double* bark_yh, void* ws,
+                     size_t ws_bytes, void* stream);
+
 /* sum over the P effective weights' sigmoid (sparsity term, mg/losses.py:181-183) */
 int mgb_sparsity(const double* raw, int P, double* out, void* stream);
 

@@ -95,13 +95,17 @@ def lib():
                                  c_void_p]
     L.mgb_sparsity.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
     L.mgb_gather_rows.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]
+    L.mgb_metrics_workspace.argtypes = [c_int, c_int]
+    L.mgb_metrics_workspace.restype = c_size_t
+    L.mgb_song_metrics.argtypes = [c_void_p, c_void_p, c_int, c_int, c_void_p, c_int, c_double, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
     L.mgb_stream_create.argtypes = []
     L.mgb_stream_create.restype = c_void_p
     L.mgb_stream_destroy.argtypes = [c_void_p]
     for name in ("mgb_init", "mgb_level_forward", "mgb_level_backward", "mgb_level_forward_phase",
                  "mgb_level_backward_phase", "mgb_weights", "mgb_bus_sum",
                  "mgb_fft", "mgb_mrstft_target", "mgb_mrstft_forward", "mgb_mrstft_backward",
-                 "mgb_adamw_step", "mgb_sparsity", "mgb_stream_destroy", "mgb_gather_rows"):
+                 "mgb_adamw_step", "mgb_sparsity", "mgb_stream_destroy", "mgb_gather_rows", "mgb_song_metrics"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -110,7 +114,8 @@ def lib():
 EXPORTED = ("mgb_abi_version", "mgb_init", "mgb_level_workspace", "mgb_level_forward",
             "mgb_level_backward", "mgb_level_forward_phase", "mgb_level_backward_phase", "mgb_launch_count", "mgb_weights", "mgb_bus_sum", "mgb_fft", "mgb_mrstft_target",
             "mgb_mrstft_forward", "mgb_mrstft_backward", "mgb_adamw_step", "mgb_sparsity",
-            "mgb_stream_create", "mgb_stream_destroy", "mgb_gather_rows")
+            "mgb_stream_create", "mgb_stream_destroy", "mgb_gather_rows", "mgb_metrics_workspace",
+            "mgb_song_metrics")
 
 
 def check(rc, what):

@@ -100,13 +100,14 @@ def report_dict(rep) -> dict:
     return out
 
 
-def song_result(spec, graph, params, state, rep, search_s) -> dict:
+def song_result(spec, graph, params, state, rep, search_s, metrics=None) -> dict:
     """What one song's search hands to rank 0: the final ``.mixgraph.json`` bytes (the
     reference writer's exact format, mg/graph.py:276-293), the PruneReport, the
-    surviving-processor mask and the trial ledger (mg/cli.py:128-182 writes the same
-    artefacts per song)."""
+    surviving-processor mask, the trial ledger and the match metrics row (mg/cli.py:128-182
+    writes the same artefacts per song)."""
     from .graph import serialize
     return {"song": spec.index, "tracks": spec.tracks, "subgroups": spec.subgroups, "search_s": search_s,
+            "metrics": metrics,
             "trials": rep.trial_count, "pruning_ratio": rep.pruning_ratio, "console_loss": rep.console_loss,
             "final_loss": rep.final_loss, "report": report_dict(rep),
             "alive": [bool(a) for a in state.alive],
@@ -122,7 +123,15 @@ def search_song(spec, graph, params, stems, target, iterations=12, device="cuda"
     t0 = time.perf_counter()
     g, p, state, rep, _ = prune_song(graph, params, Session(stems, target), desk_prune_config(spec.index, iterations),
                                      device=device)
-    return song_result(spec, g, p, state, rep, time.perf_counter() - t0)
+    return song_result(spec, g, p, state, rep, time.perf_counter() - t0, match_metrics(spec, g, p, stems, target, device))
+
+
+def match_metrics(spec, graph, params, stems, target, device="cuda"):
+    """The final graph rendered over the whole session and scored against the target on the
+    device (mg/cli.py:164-170: match.wav + metrics.csv per song)."""
+    from .metrics import render_match, song_metrics
+    match = render_match(graph, params, stems, device=device)
+    return song_metrics(f"song{spec.index:03d}", target, match, 30_000, device=device)
 
 
 def search_songs_lockstep(specs, mine, inputs, group=4, iterations=12, device="cuda"):
@@ -147,7 +156,9 @@ def search_songs_lockstep(specs, mine, inputs, group=4, iterations=12, device="c
             if isinstance(r, BaseException):
                 raise r
             g, p, state, rep, _ = r
-            out[i] = song_result(specs[i], g, p, state, rep, dt)
+            _, _, stems, target = inputs[i]
+            out[i] = song_result(specs[i], g, p, state, rep, dt,
+                                 match_metrics(specs[i], g, p, stems, target, device))
     return [out[i] for i in mine]
 
 

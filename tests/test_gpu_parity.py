@@ -517,7 +517,8 @@ def test_lockstep_song_searches_equal_sequential(dev):
     inputs = {i: bench.make_inputs(20 + i, s.tracks, s.subgroups, s.length, render) for i, s in enumerate(specs)}
     seq = search_songs(specs, [0, 1, 2], inputs, concurrent=1, iterations=3, device=dev)
     lock = search_songs_lockstep(specs, [0, 1, 2], inputs, group=3, iterations=3, device=dev)
-    keys = ("song", "tracks", "trials", "pruning_ratio", "console_loss", "final_loss", "alive", "ledger", "graph_json")
+    keys = ("song", "tracks", "trials", "pruning_ratio", "console_loss", "final_loss", "alive", "ledger", "graph_json",
+            "metrics")
     assert [{k: r[k] for k in keys} for r in lock] == [{k: r[k] for k in keys} for r in seq]
 
 

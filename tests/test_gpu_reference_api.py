@@ -153,3 +153,36 @@ def test_reference_eval_loss_with_device_kernels(dev, monkeypatch):
         monkeypatch.setitem(RP.KERNELS, tag, fn)
     got = RPr.eval_loss(graph, params, mask, es)
     np.testing.assert_allclose(got, want, rtol=1e-5)
+
+
+def test_song_metrics_match_the_reference(dev):
+    """Post-hoc metrics on the device (mg/metrics.py:45-112, mg/cli.py:55-63) against the
+    reference's own functions on the same float32 signals: SI-SDR, the MIR feature
+    distances over two 8-second segments, and the L_a of the match."""
+    from mixgraph import metrics as RM
+    from mixgraph.losses import mrstft as rmrstft
+    from paper_2509_15948_b200 import metrics as M
+    rng = np.random.default_rng(3)
+    L = 2 * 240_000 + 1_000
+    t = np.arange(L) / 30000.0
+    base = np.stack([np.sin(2 * np.pi * 220 * t), 0.7 * np.sin(2 * np.pi * 331 * t + 0.3)])
+    target = (0.3 * base + 0.05 * rng.standard_normal((2, L))).astype(np.float32)
+    match = (0.27 * base + 0.02 * np.roll(base, 40, axis=1) + 0.05 * rng.standard_normal((2, L))).astype(np.float32)
+    tg, mt = target.astype(np.float64), match.astype(np.float64)
+    assert abs(M.si_sdr(target, match) - RM.si_sdr(tg, mt)) < 1e-9
+    got = M.mir_distances(target, match)
+    errs = {}
+    for f in M.FEATURES:
+        want = RM.mir_distance(tg, mt, f)
+        errs[f] = abs(got[f] - want)
+    print("metrics |device - reference| (log10 units):", {k: f"{v:.2e}" for k, v in errs.items()})
+    assert max(errs[f] for f in ("rms", "cf", "sw", "si")) < 1e-9
+    assert errs["bs"] < 1e-6  # float32 Bluestein FFT of a 240,000-point segment (measured 6e-8)
+    row = M.song_metrics("s", target, match, 30000)
+    from mixgraph import engine as E
+    la = float(E.value_of(rmrstft(mt[:, 30000:], tg[:, 30000:])))
+    np.testing.assert_allclose(row["L_a"], la, rtol=1e-5)
+    for f in M.FEATURES:
+        assert abs(row[f"d_{f}"] - got[f]) == 0.0
+    with pytest.raises(M.TooShort):
+        M.mir_distances(target[:, :1000], match[:, :1000])
