@@ -101,6 +101,9 @@ int mgb_level_backward_phase(const MgbLevel* level, int phase, void* stream);
  * at capture). */
 long long mgb_launch_count(void);
 
+/* cudaMemsetAsync(ptr, 0, bytes) on the stream (not a kernel; e.g. the warm-up part of dL/dy). */
+int mgb_zero(void* ptr, size_t bytes, void* stream);
+
 /* A new non-blocking CUDA stream on the current device, owned by the caller
  * (NULL on failure); mgb_stream_destroy releases it.  Concurrent song searches
  * give every host thread its own streams (torch hands out pooled streams, which
@@ -214,6 +217,14 @@ size_t mgb_metrics_workspace(int L, int seg);
 int mgb_song_metrics(const float* y, const float* yh, int L, int seg, const double* bark_edges, int n_bands,
                      double sr, double* seg_stats, double* dots, double* bark_y, double* bark_yh, void* ws,
                      size_t ws_bytes, void* stream);
+
+/* Loss assembly of n signals (songs) (mg/optimizer.py:156-162):
+ * vals[q] = [L_a + gain_w * L_g + (alpha_p > 0 ? alpha_p * L_p : 0), L_a, L_g, L_p] with
+ * L_a = la[q], L_g = sum of reg[reg_off[q] .. reg_off[q+1]) (reg_off NULL: 0), L_p =
+ * sparsity[q], alpha_p = step_scalars[7]; guard (may be NULL) = sum of the totals (the
+ * mgb_adamw_step loss guard).  n <= 1024. */
+int mgb_loss_assembly(const double* la, const double* reg, const int* reg_off, const double* sparsity,
+                      const double* step_scalars, double gain_w, int n, double* vals, double* guard, void* stream);
 
 /* sum over the P effective weights' sigmoid (sparsity term, mg/losses.py:181-183) */
 int mgb_sparsity(const double* raw, int P, double* out, void* stream);

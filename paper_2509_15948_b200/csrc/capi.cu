@@ -103,6 +103,11 @@ static std::atomic<long long> g_mgb_launches{0};
 void mgb_count_launch() { g_mgb_launches.fetch_add(1, std::memory_order_relaxed); }
 extern "C" long long mgb_launch_count(void) { return g_mgb_launches.load(std::memory_order_relaxed); }
 
+extern "C" int mgb_zero(void* ptr, size_t bytes, void* stream) {
+  if (!bytes) return 0;
+  return cudaMemsetAsync(ptr, 0, bytes, (cudaStream_t)stream) == cudaSuccess ? 0 : 2;
+}
+
 extern "C" void* mgb_stream_create(void) {
   cudaStream_t s = nullptr;
   if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;

@@ -1,7 +1,7 @@
 // Multi-resolution STFT loss (mg/losses.py:104-170), forward and backward.
 //
 // Per resolution n (hop n/4, reflect pad n/2, periodic Hann), a few frames
-// per CTA: both output channels ride one complex float64 FFT (left + i*right),
+// per CTA: both output channels ride one complex float32 FFT (left + i*right),
 // done as register radix-8 Stockham stages with shared-memory exchanges; the four groups [L, R, L+R, L-R] are separated from the
 // spectrum by linearity; |X| x (A-weight * HTK mel) is applied as a banded
 // (CSR) product; log-mel L1 and spectral-convergence partial sums are reduced

@@ -297,6 +297,7 @@ class RenderPlan:
         n_reg = sum(len(schedule.subsets[s]) for s in range(1, nsteps)
                     if schedule.type_sequence[s] in "erd")
         self.reg = torch.zeros(max(n_reg, 1), dtype=F64, device=dev)
+        self.n_reg = n_reg
         self._keep = []  # device tensors referenced by raw pointers
 
         def row_ptr(step, row):
@@ -626,6 +627,7 @@ class TrainEngine:
         self.vals = torch.zeros(4, dtype=F64, device=dev)        # loss, L_a, L_g, L_p
         self.vals_host = torch.zeros(4, dtype=F64).pin_memory()
         self.sparsity = torch.zeros((), dtype=F64, device=dev)
+        self.reg_off = torch.tensor([0, self.plan.n_reg], dtype=I32, device=dev)  # all reg rows: one signal
         self.plan.greg.fill_(float(cfg.loss.gain_staging_weight))
         self.t = 0
         self.use_graph = use_graph
@@ -657,7 +659,9 @@ class TrainEngine:
         # level backward; the loss backward writes the rest), then the target spectra
         prepared = plan.prepare(side)
         with on_stream(side):
-            plan.dY[:, :ws].zero_()
+            if ws:  # the warm-up part of dL/dy (the loss backward writes the rest)
+                check(Ld.mgb_zero(ptr(plan.dY), 4 * ws, stream_ptr()), "mgb_zero")
+                check(Ld.mgb_zero(ptr(plan.dY, L), 4 * ws, stream_ptr()), "mgb_zero")
             lp.target(ptr(self.target, ws), ptr(self.target, L + ws))
             tev = torch.cuda.Event()
             tev.record(side)
@@ -670,14 +674,13 @@ class TrainEngine:
         # from the loss forward into the backward sweep
         side.wait_stream(main)
         with on_stream(side):
-            reg = plan.reg_total()
+            sp = stream_ptr()
             if P:
-                check(Ld.mgb_sparsity(ptr(self.params, self.layout.w_off), P, ptr(self.sparsity), stream_ptr()),
+                check(Ld.mgb_sparsity(ptr(self.params, self.layout.w_off), P, ptr(self.sparsity), sp),
                       "mgb_sparsity")
-            ap = self.scalars[7]
-            total = lp.loss + reg * float(self.cfg.loss.gain_staging_weight) + \
-                torch.where(ap > 0, ap * self.sparsity, torch.zeros_like(ap))
-            torch.stack([total, lp.loss, reg, self.sparsity], out=self.vals)
+            check(Ld.mgb_loss_assembly(ptr(lp.loss), ptr(plan.reg), ptr(self.reg_off), ptr(self.sparsity),
+                                       ptr(self.scalars), float(self.cfg.loss.gain_staging_weight), 1,
+                                       ptr(self.vals), None, sp), "mgb_loss_assembly")
         lp.backward(ptr(y, ws), ptr(y, L + ws), ptr(plan.dY, ws), ptr(plan.dY, L + ws))
         plan.backward(side)
         main.wait_stream(side)
