@@ -47,6 +47,7 @@ class SongUnion:
         self.node_off, self.in_off, self.proc_off = [], [], []
         n_in = n_proc = 0
         stages = [[] for _ in CONSOLE_SEQUENCE]
+        schedules = {}  # a graph repeated in the union (eval segments) is scheduled once
         for g in self.graphs:
             off = len(types)
             self.node_off.append(off)
@@ -56,7 +57,9 @@ class SongUnion:
             n_proc += len(g.processor_nodes())
             types.extend(g.node_types)
             edges.extend((a + off, b + off) for a, b in g.edges)
-            sch = schedule_console(g)  # NotAConsole for anything but a console or its prunings
+            sch = schedules.get(id(g))
+            if sch is None:  # NotAConsole for anything but a console or its prunings
+                sch = schedules[id(g)] = schedule_console(g)
             pos = 0
             for step, tag in enumerate(sch.type_sequence):
                 while CONSOLE_SEQUENCE[pos] != tag:
@@ -309,50 +312,51 @@ class BatchNonFinite(NonFiniteLoss):
 
 class BatchEvalEngine:
     """Pruning trials of several songs in one device program: ``eval_loss``
-    (mg/pruning.py:115-123) of every song of a ``SongUnion`` at once, each song with
-    its own mask, parameters and eval set (same segment count and length for all
-    songs of a recipe).  One render plan per eval segment over the union, one MRSTFT
-    per (segment, song) against device-resident target spectra.  Renders are
-    incremental like ``engine.EvalEngine``'s: a trial starts at the first level where
-    any song's mask changed; per-row kernels make each song's loss bit-identical to
-    its own ``EvalEngine``."""
+    (mg/pruning.py:115-123) of every song at once, each song with its own graph,
+    mask, parameters and eval set (same segment count and length for all songs of
+    a recipe).  The unit of the union is a (segment, song) pair: every eval segment
+    of every song is its own copy of the song's console in ONE render plan (SURVEY
+    §8f rank 1 (iii): all eval segments in one launch per level type), and ONE
+    batched MRSTFT scores all of them against device-resident target spectra.
+    Renders are incremental like ``engine.EvalEngine``'s: a trial starts at the
+    first level where any unit's mask changed; per-row kernels make each song's
+    loss bit-identical to its own ``EvalEngine``."""
 
-    def __init__(self, union: SongUnion, eval_sets, device="cuda"):
+    def __init__(self, graphs, eval_sets, device="cuda"):
         self.device = dev = ensure_device(device)
-        self.union = union
         es0 = eval_sets[0]
+        self.G = G = len(graphs)
         self.nseg, self.ws = len(es0.segments), int(es0.warmup_len)
         L = self.L = np.asarray(es0.segments[0][0]).shape[-1]
         for es in eval_sets:
             if (len(es.segments), int(es.warmup_len), np.asarray(es.segments[0][0]).shape[-1], es.loss_cfg) != \
                     (self.nseg, self.ws, L, es0.loss_cfg):
                 raise ValueError("batched eval sets must share segment count, length, warm-up and loss")
+        # unit u = j * G + i: segment j of song i
+        self.union = union = SongUnion([g for _ in range(self.nseg) for g in graphs])
         lay = self.layout = union.layout
         self.params = torch.zeros(lay.n, dtype=F64, device=dev)
         self._packed = None
         self._prep_dirty = True
-        self.plans, self.losses, self._last = [], [], []
-        for j in range(self.nseg):
-            plan = RenderPlan(union.graph, union.schedule, L, dev, self.params, None, lay, backward=False)
-            for i, es in enumerate(eval_sets):
-                st = torch.as_tensor(np.asarray(es.segments[j][0]), dtype=F32).to(dev)
-                plan.stems[union.in_off[i]:union.in_off[i] + st.shape[0]].copy_(st)
-            self.plans.append(plan)
-            G, ws = len(eval_sets), self.ws
-            # targets laid out like the union's output rows (G, 2, L), scored part at ws
-            t = torch.zeros((G, 2, L), dtype=F32, device=dev)
-            for i, es in enumerate(eval_sets):
-                t[i, :, ws:].copy_(torch.as_tensor(np.asarray(es.segments[j][1]), dtype=F32))
-            lp = LossPlan(es0.loss_cfg, L - ws, dev, backward=False, batch=G, sig_stride=2 * L)
-            lp.target(ptr(t, ws), ptr(t, L + ws))
-            self.losses.append((lp, t))
-            self._last.append(None)
-        self.acc = torch.zeros((self.nseg, len(union.graphs)), dtype=F64, device=dev)
-        self.acc_host = torch.zeros(self.acc.shape, dtype=F64).pin_memory()
+        self._last = None
+        self.plan = plan = RenderPlan(union.graph, union.schedule, L, dev, self.params, None, lay, backward=False)
+        U, ws = G * self.nseg, self.ws
+        t = torch.zeros((U, 2, L), dtype=F32, device=dev)  # targets laid out like the output rows
+        for i, es in enumerate(eval_sets):
+            for j, (st, tg) in enumerate(es.device_segments(dev)):  # uploaded once per search
+                u = j * G + i
+                plan.stems[union.in_off[u]:union.in_off[u] + st.shape[0]].copy_(st)
+                t[u, :, ws:].copy_(tg)
+        self.lossp = LossPlan(es0.loss_cfg, L - ws, dev, backward=False, batch=U, sig_stride=2 * L) if U > 1 else \
+            LossPlan(es0.loss_cfg, L - ws, dev, backward=False)
+        self.lossp.target(ptr(t, ws), ptr(t, L + ws))
+        self._targets = t
+        self.acc = torch.zeros(U, dtype=F64, device=dev)
+        self.acc_host = torch.zeros(U, dtype=F64).pin_memory()
         self.mask_host = torch.ones(max(lay.P, 1), dtype=F64).pin_memory()
 
     def load_params(self, params_list):
-        packed = self.union.pack(params_list)
+        packed = self.union.pack([p for _ in range(self.nseg) for p in params_list])
         if self._packed is not None and np.array_equal(packed, self._packed):
             return
         self._packed = packed.copy()
@@ -363,33 +367,32 @@ class BatchEvalEngine:
         """Per-song mean eval loss for per-song masks (a list, one mask per song)."""
         u = self.union
         m = np.ones(max(self.layout.P, 1))
-        for i, mk in enumerate(masks):
-            m[u.proc_off[i]:u.proc_off[i] + len(mk)] = mk
+        for j in range(self.nseg):
+            for i, mk in enumerate(masks):
+                o = u.proc_off[j * self.G + i]
+                m[o:o + len(mk)] = mk
         self.mask_host.copy_(torch.from_numpy(m))
-        L, ws = self.L, self.ws
+        L, ws, plan = self.L, self.ws, self.plan
         if self._prep_dirty:
-            for plan in self.plans:
-                plan.prepare()
-        for j, plan in enumerate(self.plans):
-            plan.mask.copy_(self.mask_host, non_blocking=True)
-            start = 0
-            if not self._prep_dirty and self._last[j] is not None:
-                changed = np.nonzero(m != self._last[j])[0]
-                start = int(plan.proc_level[changed].min()) if changed.size else len(plan.levels)
-            plan.forward(use_mask=True, prepared=True, norms=None, start=start)
-            self._last[j] = m.copy()
-            lp = self.losses[j][0]
-            lp.forward(ptr(plan.ys, ws), ptr(plan.ys, L + ws))
-            self.acc[j].copy_(lp.loss)
+            plan.prepare()
+        plan.mask.copy_(self.mask_host, non_blocking=True)
+        start = 0
+        if not self._prep_dirty and self._last is not None:
+            changed = np.nonzero(m != self._last)[0]
+            start = int(plan.proc_level[changed].min()) if changed.size else len(plan.levels)
+        plan.forward(use_mask=True, prepared=True, norms=None, start=start)
+        self._last = m
+        self.lossp.forward(ptr(plan.ys, ws), ptr(plan.ys, L + ws))
+        self.acc.copy_(self.lossp.loss)
         self._prep_dirty = False
         self.acc_host.copy_(self.acc, non_blocking=True)
         host_wait(current_stream())
         a = self.acc_host.numpy()
         out = []
-        for i in range(len(u.graphs)):
+        for i in range(self.G):
             total = 0.0
             for j in range(self.nseg):  # per-segment float() then mean, as mg/pruning.py:120-123
-                total += float(a[j, i])
+                total += float(a[j * self.G + i])
             out.append(total / self.nseg)
         return out
 
@@ -424,7 +427,7 @@ def prune_songs_lockstep(jobs, device="cuda", batch_trials=True):
     while reqs:
         evals = sorted(i for i, r in reqs.items() if isinstance(r, EvalRequest))
         if evals:
-            if not batch_trials or len(evals) == 1 and len(last_eval) == 1:
+            if not batch_trials:
                 for i in evals:
                     r = reqs[i]
                     advance(i, eval_loss(r.graph, r.params, r.mask, r.eval_set))
@@ -433,7 +436,7 @@ def prune_songs_lockstep(jobs, device="cuda", batch_trials=True):
             key = tuple((i, id(last_eval[i].graph), id(last_eval[i].eval_set)) for i in ids)
             t0 = time.perf_counter()
             if key != bkey:
-                beval = BatchEvalEngine(SongUnion([last_eval[i].graph for i in ids]),
+                beval = BatchEvalEngine([last_eval[i].graph for i in ids],
                                         [last_eval[i].eval_set for i in ids], device)
                 bkey = key
                 PHASE_S["trial_engine_build"] += time.perf_counter() - t0
