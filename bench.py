@@ -52,7 +52,9 @@ def parse():
     ap.add_argument("--song-lockstep", type=int, default=8,
                     help="songs per GPU searched in lock-step groups of this size: each group's training steps and "
                          "trials run as one batched device program (0: threads instead)")
-    ap.add_argument("--songs", type=int, default=8,
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the BASELINE config 3 and 4 sub-lines (tools/configs_bench.py)")
+    ap.add_argument("--songs", type=int, default=32,
                     help="config-5 desk-recipe pruning searches per GPU for songs/hour (0: skip)")
     ap.add_argument("--tracks", type=int, default=K_TRACKS)
     ap.add_argument("--subgroups", type=int, default=S_GROUPS)
@@ -364,6 +366,22 @@ def main():
                                           "one gather_object to rank 0 (NCCL when N > 1)"}}
     # BASELINE config 1 (4 tracks + 1 subgroup, L = 132,300): launch-bound, CUDA-graph replays
     cfg1 = time_config(dev, 4, 1, 132_300, rank, render, steps=200, warmup=max(3, args.warmup))
+    # BASELINE configs 3 (c/n-heavy, 32 trk, 1,323,000 samples) and 4 (e/r-heavy, 6-resolution loss)
+    secondary = None
+    if not args.no_secondary:
+        import importlib.util
+        spec_ = importlib.util.spec_from_file_location("configs_bench", os.path.join(ROOT, "tools", "configs_bench.py"))
+        cb = importlib.util.module_from_spec(spec_)
+        spec_.loader.exec_module(cb)
+        secondary = {}
+        for cid in (3, 4):
+            r = cb.run(cid, 10, dev)
+            secondary[f"config{cid}"] = {k: r[k] for k in ("chains", "tracks", "subgroups", "length", "processors",
+                                                           "steps_per_s", "ms_per_step", "step_roofline")}
+            for k in ("scan_ns_per_sample_row", "fft"):
+                if k in r and (k != "fft" or cid == 4):
+                    secondary[f"config{cid}"][k] = r[k]
+            torch.cuda.empty_cache()
     lay = eng.layout
     # per step: its segment and the 8 step scalars in, the 4 metrics out (params move once per run)
     h2d = stems.nbytes + target.nbytes + 8 * 8
@@ -414,6 +432,7 @@ def main():
                     "final param read-back",
                     "train_step_sync": sync_val},
             "config1": cfg1,
+            "configs34": secondary,
             "eval_trial_ms": trial_ms,
             "songs_per_hour": songs,
             "gpu_launches": eng.launches_per_step() * args.steps,
