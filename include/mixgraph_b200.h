@@ -152,7 +152,8 @@ typedef struct MgbLossRes {
   double* tlog;                 /* (4, frames, n_mels) log(target mel + 1e-7) */
   double* mel;                  /* (4, frames, n_mels) estimate mel (fwd -> bwd) */
   double* part;                 /* (frames, 4, 3) per-frame partial sums */
-  float* gframes;               /* (frames, 2, n_fft) backward frame adjoints */
+  float* gframes;               /* (frames, 2, n_fft): the forward's frame spectra, then the backward's
+                                   frame adjoints; NULL for a forward-only loss */
 } MgbLossRes;
 
 typedef struct MgbLoss {
@@ -176,7 +177,10 @@ typedef struct MgbLoss {
 int mgb_mrstft_target(const MgbLoss* loss, const float* tgt_l, const float* tgt_r, void* stream);
 /* L_a for the (2, Ls) estimate; writes *loss->loss (mg/losses.py:143-170). */
 int mgb_mrstft_forward(const MgbLoss* loss, const float* y_l, const float* y_r, void* stream);
-/* dL_a/dy * scale into g_l, g_r (Ls each, overwritten). */
+/* dL_a/dy into g_l, g_r (Ls each, overwritten).  Must follow mgb_mrstft_forward on the
+ * same estimate: the forward leaves each frame's spectrum in gframes (when gframes is
+ * set) and its mel / stats, the backward reads them and overwrites gframes with the
+ * frame adjoints. */
 int mgb_mrstft_backward(const MgbLoss* loss, const float* y_l, const float* y_r, float* g_l, float* g_r,
                         void* stream);
 

@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(
     r.tlog += me;
     r.mel += me;
     r.part += (size_t)sq * r.frames * 12;
+    if (r.gframes) r.gframes += (size_t)sq * r.frames * 2 * N;
   }
   constexpr int T = C::T, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -243,6 +244,12 @@ __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(
   float2 v[C::V];
   load_frame<N, 16>(v, xl, xr, Ls, r.hop, f, valid, tt);
   frame_fft<N, 16, false>(v, S, tt);  // (its barriers publish the band tables)
+  if (mode != 0 && r.gframes && valid) {
+    // the estimate's frame spectrum, kept for the backward (which overwrites the slot
+    // with the frame's adjoint): the backward does not transform the frame again
+    float2* gs = reinterpret_cast<float2*>(r.gframes + (size_t)f * 2 * N);
+    for (int t = tt; t < N; t += T) gs[t] = S[pd16(t)];
+  }
   mags_inplace<N, 16>(S, tt);
   const float* md = reinterpret_cast<const float*>(S);
   const int g = tt & 3;  // items idx = tt + T i: group idx % 4 (fixed per thread), band idx / 4
@@ -337,7 +344,7 @@ __global__ void k_mr_total(MgbLoss L) {
   L.loss[sq] = tot;
 }
 
-// backward: dmel, frame spectrum recomputed, d|X| through the CSC projection,
+// backward: dmel, the frame spectrum the forward kept, d|X| through the CSC projection,
 // dX per group -> packed Hermitian adjoint of both channels, one inverse FFT,
 // windowed frame adjoints to gframes (float32) for the overlap-add gather.
 template <int N>
@@ -366,8 +373,11 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
   float2* S = reinterpret_cast<float2*>(smraw) + q * C::PADN;
   const int nm = r.n_mels;
   float2 v[C::V];
-  // the frame's global loads go out first; the dmel prologue's loads overlap them
-  load_frame<N, 8>(v, xl, xr, Ls, r.hop, f, valid, tt);
+  // the frame spectrum of the forward pass (natural order) -> S
+  if (valid) {
+    const float2* gs = reinterpret_cast<const float2*>(r.gframes + (size_t)f * 2 * N);
+    for (int t = tt; t < N; t += T) S[pd16(t)] = gs[t];
+  }
   if (valid) {
     for (int idx = tt; idx < 4 * nm; idx += T) {
       const int g = idx / nm, j = idx % nm;
@@ -390,7 +400,7 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
       dmel[q][g][j] = (float)(L.group_w[g] * v);
     }
   }
-  frame_fft<N, 8, false>(v, S, tt);  // (its barriers also publish dmel)
+  __syncthreads();  // publishes the spectrum and dmel
   float2 dl[PER], dr[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
