@@ -406,7 +406,7 @@ def prune_songs_lockstep(jobs, device="cuda", batch_trials=True):
     keeps its last graph and mask in the union until the next round, so the union is
     rebuilt once per round).  Returns each search's (graph, params, state, report,
     history), identical to running them one by one."""
-    from .pruning import EvalRequest, eval_loss, prune_song, prune_song_steps, run_train_request
+    from .pruning import EvalRequest, eval_losses, prune_song, prune_song_steps, run_train_request
     gens = [prune_song_steps(g, p, s, c, None, device) for g, p, s, c in jobs]
     out = [None] * len(gens)
     reqs, last_eval = {}, {}
@@ -430,7 +430,7 @@ def prune_songs_lockstep(jobs, device="cuda", batch_trials=True):
             if not batch_trials:
                 for i in evals:
                     r = reqs[i]
-                    advance(i, eval_loss(r.graph, r.params, r.mask, r.eval_set))
+                    advance(i, eval_losses(r.graph, r.params, r.masks, r.eval_set))
                 continue
             ids = sorted(last_eval)
             key = tuple((i, id(last_eval[i].graph), id(last_eval[i].eval_set)) for i in ids)
@@ -449,7 +449,7 @@ def prune_songs_lockstep(jobs, device="cuda", batch_trials=True):
             PHASE_S["trial_slots"] += 1
             for k, i in enumerate(ids):
                 if i in evals:
-                    advance(i, losses[k])
+                    advance(i, [losses[k]])
             continue
         ids = sorted(reqs)
         t0 = time.perf_counter()
@@ -463,7 +463,7 @@ def prune_songs_lockstep(jobs, device="cuda", batch_trials=True):
             for i in ids:
                 g, p, s, c = jobs[i]
                 try:
-                    out[i] = prune_song(g, p, s, c, device=device)
+                    out[i] = prune_song(g, p, s, c, device=device, speculate=1)
                 except NonFiniteLoss as e:
                     out[i] = e
             return out

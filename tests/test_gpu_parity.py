@@ -545,3 +545,28 @@ def test_batched_mrstft_equals_per_signal_calls(dev):
         lp.backward(ptr(y[i], ws), ptr(y[i], L + ws), ptr(g1, ws), ptr(g1, L + ws))
         assert float(bl.loss[i]) == float(lp.loss)
         assert torch.equal(gb[i], g1)
+
+
+def test_speculative_bruteforce_trials_make_the_same_decisions(dev):
+    """brute-force trials requested four per device render under
+    the reject assumption give the sequential search's ledger, survivors and graph."""
+    import bench
+    from paper_2509_15948_b200.graph import serialize
+    from paper_2509_15948_b200.optimizer import Session
+    from paper_2509_15948_b200.pruning import prune_song
+    from paper_2509_15948_b200.scheduler import execute_batched
+    from paper_2509_15948_b200.songs import desk_prune_config
+
+    def render(graph, tparams, stems):
+        return execute_batched(graph, tparams, stems, device=dev)[0].cpu().numpy()
+
+    graph, params, stems, target = bench.make_inputs(31, 5, 2, 132_300, render)
+    cfg = desk_prune_config(3, iterations=4)  # hybrid: round 4 is brute force
+    outs = [prune_song(graph, params, Session(stems, target), cfg, device=dev, speculate=s) for s in (1, 4)]
+    (g1, p1, s1, r1, _), (g4, p4, s4, r4, _) = outs
+    led = lambda st: [(r.iteration, r.mode, r.candidates, r.loss, r.accepted) for r in st.ledger]  # noqa: E731
+    assert led(s1) == led(s4)
+    assert any(r.mode == "bruteforce" for r in s1.ledger)
+    np.testing.assert_array_equal(s1.alive, s4.alive)
+    assert serialize(g1, p1) == serialize(g4, p4)
+    assert r1.final_loss == r4.final_loss

@@ -225,8 +225,11 @@ def _fake_train(graph, params, session, cfg, *args, rng=None, history=None, alph
     return history
 
 
-@pytest.mark.parametrize("mode", ["hybrid", "bruteforce", "drywet"])
-def test_prune_song_control_flow_matches_reference(monkeypatch, mode):
+@pytest.mark.parametrize("mode,speculate", [("hybrid", 1), ("bruteforce", 1), ("drywet", 1), ("hybrid", 4),
+                                            ("bruteforce", 3)])
+def test_prune_song_control_flow_matches_reference(monkeypatch, mode, speculate):
+    """Also with speculative brute-force batches (``speculate`` trials requested per
+    render under the reject assumption): the same ledger as the reference's sequential loop."""
     from paper_2509_15948_b200 import console as ours
     from paper_2509_15948_b200 import graph as og
     from paper_2509_15948_b200 import pruning as op
@@ -236,6 +239,13 @@ def test_prune_song_control_flow_matches_reference(monkeypatch, mode):
     for mod in (op, Pr):
         monkeypatch.setattr(mod, "eval_loss", _fake_eval)
         monkeypatch.setattr(mod, "train", _fake_train)
+    requests = []
+
+    def fake_losses(g, p, masks, es, schedule=None):
+        requests.append(len(masks))
+        return [_fake_eval(g, p, m, es) for m in masks]
+
+    monkeypatch.setattr(op, "eval_losses", fake_losses)
     mo, mr = _both_manifests(6, 2)
     go, zo = ours.build_console(mo)
     gr, zr = Co.build_console(mr)
@@ -246,7 +256,9 @@ def test_prune_song_control_flow_matches_reference(monkeypatch, mode):
               eval_segments=2, eval_segment_seconds=1.2, sparsity_ramp_steps=7)
     tc = dict(segment_seconds=1.2, warmup_seconds=1.0, seed=3)
     out_o = op.prune_song(go, ours.init_params(zo, 4), Session(stems, target),
-                          op.PruneConfig(**kw, train=TrainConfig(**tc)), device="cpu")
+                          op.PruneConfig(**kw, train=TrainConfig(**tc)), device="cpu", speculate=speculate)
+    if speculate > 1 and mode != "drywet":
+        assert max(requests) == speculate  # brute-force trials were requested in batches
     out_r = Pr.prune_song(gr, Co.init_params(zr, 4), RO.Session(stems, target),
                           Pr.PruneConfig(**kw, train=RO.TrainConfig(**tc)))
     (g_o, p_o, s_o, rep_o, _), (g_r, p_r, s_r, rep_r, _) = out_o, out_r
