@@ -87,7 +87,7 @@ ConvWs carve_into(A& a, char tag, int B, int L) {
     w.aux = w.aux2 = nullptr;
     w.offs = nullptr;
     w.Hs = a.template take<float2>((size_t)B * EOS_N);
-    w.pspec = a.template take<float2>((size_t)B * eos_nblk(L) * EOS_N);
+    w.pspec = a.template take<float2>((size_t)B * eos_nchunk(L, B) * 2 * EOS_N);  // D park + C accumulator per CTA
     w.csum = a.template take<float2>((size_t)B * EOS_N);
     return w;
   }
@@ -718,8 +718,8 @@ int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st) {
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
     const int nb = eos_nblk(L);
-    mgb_launch(k_eqos_bwd, dim3(dim3(nb, B)), dim3(EOS_NT), kEosSmem1, st, lv->u_rows, lv->gy_rows, lv->ybar, w.Hs, lv->widx, lv->w,
-                                                       lv->greg, w.stats, lv->gu, w.part, w.pspec, L, nb);
+    mgb_launch(k_eqos_bwd, dim3(dim3(eos_nchunk(L, B), B)), dim3(EOS_NT), kEosSmem1, st, lv->u_rows, lv->gy_rows,
+               lv->ybar, w.Hs, lv->widx, lv->w, lv->greg, w.stats, lv->gu, w.part, w.pspec, L, nb, eos_per(L, B));
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -734,11 +734,11 @@ int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st) {
   MgbArena a{(char*)lv->ws, 0};
   const ConvWs w = carve_into(a, tag, B, L);
   // dL/dw from the backward prologue's per-CTA partials (phase 1)
-  mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, tag == 'e' ? eos_nblk(L) : conv_dw_nblk(g), lv->widx,
-             lv->w, lv->gw);
+  mgb_launch(k_dw_finalize, dim3(B), dim3(256), 0, st, w.part, tag == 'e' ? eos_nchunk(L, B) : conv_dw_nblk(g),
+             lv->widx, lv->w, lv->gw);
   MGB_CHECK_LAUNCH();
   if (tag == 'e') {
-    mgb_launch(k_eqos_csum, dim3(dim3(EOS_N / 256, B)), dim3(256), 0, st, w.pspec, eos_nblk(L), w.csum);
+    mgb_launch(k_eqos_csum, dim3(dim3(EOS_N / 256, B)), dim3(256), 0, st, w.pspec, eos_nchunk(L, B), w.csum);
     MGB_CHECK_LAUNCH();
     mgb_launch(k_eqos_gh, dim3(B), dim3(EOS_NT), kEosSmem1, st, w.csum, w.ghbuf);
     MGB_CHECK_LAUNCH();

@@ -34,6 +34,12 @@ constexpr int EOS_SM = 32 * 16 * EOS_S2P;            // 8704 float2 >= 8192
 constexpr int kEosSmem1 = EOS_SM * 8;
 
 int eos_nblk(int L) { return (L + EOS_HOP - 1) / EOS_HOP; }
+// backward blocks per CTA: about two CTAs per SM over the level (B nodes)
+int eos_per(int L, int B) {
+  const int n = eos_nblk(L) * B, per = (n + 2 * 148 - 1) / (2 * 148);
+  return per < 1 ? 1 : per;
+}
+int eos_nchunk(int L, int B) { return (eos_nblk(L) + eos_per(L, B) - 1) / eos_per(L, B); }
 
 // natural order (thread t holds x[t + 256 m]) -> spectrum in (t, r) order:
 // v[s*16 + ka] = X[k1 + 32 kb + 512 ka], k1 = (t >> 4) + 16 s, kb = t & 15
@@ -216,15 +222,25 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
                                                      const double* __restrict__ greg,
                                                      const double* __restrict__ stats, float* __restrict__ gu,
                                                      double* __restrict__ part, float2* __restrict__ pspec,
-                                                     int L, int nblk) {
+                                                     int L, int nblk, int per) {
   mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* S = reinterpret_cast<float2*>(dsm);
   __shared__ double red[32];
-  const int blk = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
+  // a CTA handles `per` consecutive blocks of one node: its D park and its C
+  // accumulator are two 8192-point slots of its own (L2-resident across the blocks),
+  // and its dL/dw partial is one slot
+  const int chunk = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
   const float* u = u_rows[b];
   const float* gy = gy_rows[b];
   const float* yb = ybar + (size_t)b * 2 * L;
+  float2* dpark = pspec + ((size_t)b * gridDim.x + chunk) * 2 * EOS_N + t;
+  float2* cacc = dpark + EOS_N;
+  float fw = 0.f;
+  const int blk_end = min(nblk, (chunk + 1) * per);
+#pragma unroll 1
+  for (int blk = chunk * per; blk < blk_end; ++blk) {
+  const bool first = blk == chunk * per;
   const long long n0 = (long long)blk * EOS_HOP, w0 = n0 - EOS_OFF;
   const double wv = w ? w[widx[b]] : 1.0;
   const bool bypass = wv == 0.0;
@@ -250,20 +266,27 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
       v[m0 + q] = make_float2(fmaf(cy, my, wf * g[q].x), fmaf(cy, my, wf * g[q].y));
     }
   }
-  float2* ps = pspec + ((size_t)b * nblk + blk) * EOS_N + t;
-  // pass 0: D = FFT(d) (parked in this block's pspec slot), gx = IDFT(D conj H) -> gu;
-  // pass 1: Xm = FFT(x masked to the block), C = conj(D) Xm -> pspec.  One copy of the
-  // forward-transform code serves both passes (instruction-cache footprint).
+  // pass 0: D = FFT(d) (parked in the CTA's D slot), gx = IDFT(D conj H) -> gu;
+  // pass 1: Xm = FFT(x masked to the block), C += conj(D) Xm in the CTA's C slot.  One
+  // copy of the forward-transform code serves both passes (instruction-cache footprint).
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
     eos_fft(v, S);
     if (pass == 1) {
 #pragma unroll
-      for (int r = 0; r < 32; ++r) ps[r * 256] = cmulc(v[r], ps[r * 256]);
+      for (int r = 0; r < 32; ++r) {
+        const float2 c = cmulc(v[r], dpark[r * 256]);
+        if (first) {
+          cacc[r * 256] = c;
+        } else {
+          const float2 a = cacc[r * 256];
+          cacc[r * 256] = make_float2(a.x + c.x, a.y + c.y);
+        }
+      }
       break;
     }
 #pragma unroll
-    for (int r = 0; r < 32; ++r) ps[r * 256] = v[r];
+    for (int r = 0; r < 32; ++r) dpark[r * 256] = v[r];
     float* go = gu ? gu + (size_t)b * 2 * L : nullptr;  // null: input gradient not requested (no gx transform)
     if (go) {
       const float2* H = Hs + (size_t)b * EOS_N + t;
@@ -275,7 +298,6 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
       }
       eos_ifft(v, S);
     }
-    float fw = 0.f;
 #pragma unroll
     for (int m0 = 0; m0 < EOS_HOP / 256 + 1; m0 += 5) {  // window indices i < HOP: m <= 24
       float4 gq[5];
@@ -305,8 +327,6 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
         }
       }
     }
-    const double tw = block_sum((double)fw, red);
-    if (t == 0) part[((size_t)b * kMaxParts + blk) * 4 + 2] = tw;
     // pass 1 input: x masked to the block
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
@@ -316,18 +336,21 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
                                                                 : make_float2(0.f, 0.f);
     }
   }
+  }
+  const double tw = block_sum((double)fw, red);
+  if (t == 0) part[((size_t)b * kMaxParts + chunk) * 4 + 2] = tw;
 }
 
-// Csum[b][slot] = sum over blocks of C (float64, fixed order), one thread per slot
-__global__ void __launch_bounds__(256) k_eqos_csum(const float2* __restrict__ pspec, int nblk,
+// Csum[b][slot] = sum over the backward CTAs' C accumulators (float64, fixed order)
+__global__ void __launch_bounds__(256) k_eqos_csum(const float2* __restrict__ pspec, int nchunk,
                                                    float2* __restrict__ csum) {
   mgb_pdl_entry();
   const int b = blockIdx.y, slot = blockIdx.x * 256 + threadIdx.x;
-  const float2* ps = pspec + (size_t)b * nblk * EOS_N + slot;
+  const float2* ps = pspec + (size_t)b * nchunk * 2 * EOS_N + EOS_N + slot;
   double re = 0.0, im = 0.0;
 #pragma unroll 8
-  for (int q = 0; q < nblk; ++q) {
-    const float2 c = __ldg(ps + (size_t)q * EOS_N);
+  for (int q = 0; q < nchunk; ++q) {
+    const float2 c = __ldg(ps + (size_t)q * 2 * EOS_N);
     re += c.x;
     im += c.y;
   }
