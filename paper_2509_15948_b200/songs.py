@@ -68,8 +68,9 @@ def run_rank(specs, mine, run_song):
 
 
 def gather_results(results, rank, world, dist=None):
-    """Collect every rank's result list on rank 0 (one gather at the very end)."""
-    if world == 1 or dist is None:
+    """Collect every rank's result list on rank 0 (one gather at the very end; NCCL's
+    gather_object when the process group is NCCL, also for a single rank)."""
+    if dist is None or not dist.is_initialized():
         return results
     box = [None] * world if rank == 0 else None
     dist.gather_object(results, box, dst=0)
