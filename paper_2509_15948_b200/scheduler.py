@@ -18,25 +18,25 @@ from .schedule import (CONSOLE_SEQUENCE, GREEDY_TIE_ORDER, LengthMismatch, NotAC
 
 
 def _check_sources(graph, sources):
-    if torch.is_tensor(sources):
-        src = sources
-    elif isinstance(sources, (list, tuple)):
-        lengths = {np.asarray(s).shape[-1] if not torch.is_tensor(s) else s.shape[-1] for s in sources}
-        if len(lengths) > 1:
-            raise LengthMismatch(f"sources have mixed lengths {sorted(lengths)}")
-        src = torch.stack([torch.as_tensor(np.asarray(s)) if not torch.is_tensor(s) else s for s in sources])
-    else:
-        src = torch.as_tensor(np.asarray(sources))
+    """mg/scheduler.py:207-215: the source count, then equal lengths (same errors)."""
     k = len(graph.nodes_of_type("i"))
-    if src.shape[0] != k:
-        raise LengthMismatch(f"graph has {k} inputs, got {src.shape[0]} sources")
-    return src
+    n = sources.shape[0] if (torch.is_tensor(sources) or isinstance(sources, np.ndarray)) else len(sources)
+    if n != k:
+        raise LengthMismatch(f"graph has {k} inputs, got {n} sources")
+    if torch.is_tensor(sources):
+        return sources
+    if isinstance(sources, (list, tuple)):
+        lengths = {np.asarray(s).shape[-1] if not torch.is_tensor(s) else s.shape[-1] for s in sources}
+        if len(lengths) != 1:
+            raise LengthMismatch(f"sources have mixed lengths {sorted(lengths)}")
+        return torch.stack([torch.as_tensor(np.asarray(s)) if not torch.is_tensor(s) else s for s in sources])
+    return torch.as_tensor(np.asarray(sources))
 
 
 def execute_batched(graph, params, sources, schedule=None, mask=None, device="cuda"):
     """Render the graph through its schedule; returns (y (2, L), reg) on the device."""
+    src = _check_sources(graph, sources)  # host checks first: the reference's errors on any device
     dev = ensure_device(device)
-    src = _check_sources(graph, sources)
     L = src.shape[-1]
     if schedule is None:
         schedule = schedule_greedy(graph)

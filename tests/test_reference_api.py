@@ -272,3 +272,22 @@ def test_prune_song_control_flow_matches_reference(monkeypatch, mode, speculate)
     for f in ("console_loss", "final_loss", "la_min", "tolerance", "mode", "console_counts", "pruned_counts",
               "trial_count"):
         assert getattr(rep_o, f) == getattr(rep_r, f), f
+
+
+def test_source_errors_match_reference():
+    """execute_batched's input errors (mg/scheduler.py:207-215) are raised before any device
+    work, with the reference's exception class and message."""
+    from paper_2509_15948_b200 import console as ours
+    from paper_2509_15948_b200.scheduler import execute_batched
+    _, Co, _, S, *_ = _ref()
+    mo, mr = _both_manifests(3, 1)
+    go, zo = ours.build_console(mo)
+    gr, zr = Co.build_console(mr)
+    cases = [np.zeros((2, 2, 100)), [np.zeros((2, 100)), np.zeros((2, 100)), np.zeros((2, 90))]]
+    for src in cases:
+        errs = []
+        for fn, g, z in ((execute_batched, go, zo), (S.execute_batched, gr, zr)):
+            with pytest.raises(Exception) as e:
+                fn(g, z, src)
+            errs.append((type(e.value).__name__, str(e.value)))
+        assert errs[0] == errs[1], errs
