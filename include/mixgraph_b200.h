@@ -110,6 +110,9 @@ int mgb_zero(void* ptr, size_t bytes, void* stream);
  * two threads could share while one of them is capturing a CUDA graph). */
 void* mgb_stream_create(void);
 int mgb_stream_destroy(void* stream);
+/* The same with a priority: level > 0 the device's greatest, < 0 the least, 0 default
+ * (a step's critical-path stream high, its side streams low; graph captures keep it). */
+void* mgb_stream_create_priority(int level);
 
 /* Effective dry/wet weights w = sigmoid(raw) * mask (mg/scheduler.py:218-222).
  * mask may be NULL. */

@@ -104,6 +104,8 @@ def lib():
                                    c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
     L.mgb_stream_create.argtypes = []
     L.mgb_stream_create.restype = c_void_p
+    L.mgb_stream_create_priority.argtypes = [c_int]
+    L.mgb_stream_create_priority.restype = c_void_p
     L.mgb_stream_destroy.argtypes = [c_void_p]
     for name in ("mgb_init", "mgb_level_forward", "mgb_level_backward", "mgb_level_forward_phase",
                  "mgb_level_backward_phase", "mgb_weights", "mgb_bus_sum",
@@ -117,7 +119,7 @@ def lib():
 EXPORTED = ("mgb_abi_version", "mgb_init", "mgb_level_workspace", "mgb_level_forward",
             "mgb_level_backward", "mgb_level_forward_phase", "mgb_level_backward_phase", "mgb_launch_count", "mgb_weights", "mgb_bus_sum", "mgb_fft", "mgb_mrstft_target",
             "mgb_mrstft_forward", "mgb_mrstft_backward", "mgb_adamw_step", "mgb_sparsity",
-            "mgb_stream_create", "mgb_stream_destroy", "mgb_gather_rows", "mgb_metrics_workspace",
+            "mgb_stream_create", "mgb_stream_destroy", "mgb_stream_create_priority", "mgb_gather_rows", "mgb_metrics_workspace",
             "mgb_song_metrics", "mgb_loss_assembly", "mgb_zero")
 
 

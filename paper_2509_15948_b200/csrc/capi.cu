@@ -103,14 +103,24 @@ static std::atomic<long long> g_mgb_launches{0};
 void mgb_count_launch() { g_mgb_launches.fetch_add(1, std::memory_order_relaxed); }
 extern "C" long long mgb_launch_count(void) { return g_mgb_launches.load(std::memory_order_relaxed); }
 
+extern "C" void* mgb_stream_create_priority(int level);
+
 extern "C" int mgb_zero(void* ptr, size_t bytes, void* stream) {
   if (!bytes) return 0;
   return cudaMemsetAsync(ptr, 0, bytes, (cudaStream_t)stream) == cudaSuccess ? 0 : 2;
 }
 
-extern "C" void* mgb_stream_create(void) {
+extern "C" void* mgb_stream_create(void) { return mgb_stream_create_priority(0); }
+
+// level > 0: the device's greatest priority (the critical path of a step: its
+// kernels' CTAs are scheduled first when side-stream work competes for SMs);
+// level < 0: the least; 0: default.  Captured kernels keep their stream's priority.
+extern "C" void* mgb_stream_create_priority(int level) {
+  int least = 0, greatest = 0;
+  if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return nullptr;
+  const int prio = level > 0 ? greatest : (level < 0 ? least : 0);
   cudaStream_t s = nullptr;
-  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio) != cudaSuccess) return nullptr;
   return (void*)s;
 }
 

@@ -12,6 +12,8 @@
 // reflect-pad adjoint) across all resolutions into dL/dy, without atomics.
 // The frame transforms run in float32, magnitudes are projected, logged and reduced
 // in float64 (precision note at the frame FFT below).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "mgb_internal.h"
 #include "regfft.cuh"
@@ -579,7 +581,13 @@ int side_init() {
   if (g_side_ok[dev]) return 0;
   if (cudaEventCreateWithFlags(&g_fork[dev], cudaEventDisableTiming) != cudaSuccess) return 2;
   for (int i = 0; i < kSide; ++i) {
-    if (cudaStreamCreateWithFlags(&g_side[dev][i], cudaStreamNonBlocking) != cudaSuccess) return 2;
+    // MGB_STREAM_PRIORITY=1: the resolutions (on the step's critical path) at the
+    // greatest priority (a captured launch keeps its stream's priority)
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    const char* e = getenv("MGB_STREAM_PRIORITY");
+    const int prio = (e && atoi(e) == 1) ? greatest : 0;  // opt-in (measured slower)
+    if (cudaStreamCreateWithPriority(&g_side[dev][i], cudaStreamNonBlocking, prio) != cudaSuccess) return 2;
     if (cudaEventCreateWithFlags(&g_join[dev][i], cudaEventDisableTiming) != cudaSuccess) return 2;
   }
   g_side_ok[dev] = true;

@@ -21,6 +21,7 @@ on one stream and captured once into a CUDA graph per graph version.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -153,6 +154,9 @@ def host_wait(obj) -> None:
 
 
 _own_streams = {}
+# stream priority per role with MGB_STREAM_PRIORITY=1: the captured step's critical path
+# high, its side work low.  Off by default: measured 442 vs 446 steps/s.
+_ROLE_PRIORITY = {"capture": 1, "side": -1, "main": 1}
 
 
 def own_stream(device, role: str) -> torch.cuda.Stream:
@@ -165,8 +169,9 @@ def own_stream(device, role: str) -> torch.cuda.Stream:
     key = (threading.get_ident(), idx, role)
     s = _own_streams.get(key)
     if s is None:
+        prio = _ROLE_PRIORITY.get(role, 0) if os.environ.get("MGB_STREAM_PRIORITY", "0") == "1" else 0
         with torch.cuda.device(idx):
-            raw = lib().mgb_stream_create()
+            raw = lib().mgb_stream_create_priority(prio)
         if not raw:
             raise _lib.DeviceError("mgb_stream_create failed")
         s = _own_streams[key] = torch.cuda.ExternalStream(raw, device=torch.device("cuda", idx))
