@@ -227,11 +227,12 @@ int mgb_song_metrics(const float* y, const float* yh, int L, int seg, const doub
 
 /* Loss assembly of n signals (songs) (mg/optimizer.py:156-162):
  * vals[q] = [L_a + gain_w * L_g + (alpha_p > 0 ? alpha_p * L_p : 0), L_a, L_g, L_p] with
- * L_a = la[q], L_g = sum of reg[reg_off[q] .. reg_off[q+1]) (reg_off NULL: 0), L_p =
- * sparsity[q], alpha_p = step_scalars[7]; guard (may be NULL) = sum of the totals (the
- * mgb_adamw_step loss guard).  n <= 1024. */
-int mgb_loss_assembly(const double* la, const double* reg, const int* reg_off, const double* sparsity,
-                      const double* step_scalars, double gain_w, int n, double* vals, double* guard, void* stream);
+ * L_a = la[q], L_g = sum of reg[reg_idx[i]] for i in [reg_off[q], reg_off[q+1]) (reg_idx NULL:
+ * reg[i]; reg_off NULL: 0), L_p = sparsity[q], alpha_p = step_scalars[7]; guard (may be NULL)
+ * = sum of the totals (the mgb_adamw_step loss guard).  n <= 1024. */
+int mgb_loss_assembly(const double* la, const double* reg, const int* reg_off, const int* reg_idx,
+                      const double* sparsity, const double* step_scalars, double gain_w, int n, double* vals,
+                      double* guard, void* stream);
 
 /* sum over the P effective weights' sigmoid (sparsity term, mg/losses.py:181-183) */
 int mgb_sparsity(const double* raw, int P, double* out, void* stream);

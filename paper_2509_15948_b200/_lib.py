@@ -96,8 +96,8 @@ def lib():
     L.mgb_sparsity.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
     L.mgb_gather_rows.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]
     L.mgb_zero.argtypes = [c_void_p, c_size_t, c_void_p]
-    L.mgb_loss_assembly.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p,
-                                    c_void_p, c_void_p]
+    L.mgb_loss_assembly.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
+                                    c_void_p, c_void_p, c_void_p]
     L.mgb_metrics_workspace.argtypes = [c_int, c_int]
     L.mgb_metrics_workspace.restype = c_size_t
     L.mgb_song_metrics.argtypes = [c_void_p, c_void_p, c_int, c_int, c_void_p, c_int, c_double, c_void_p, c_void_p,

@@ -130,8 +130,11 @@ class BatchTrainEngine:
         for s in range(1, len(sched.subsets)):
             if sched.type_sequence[s] in "erd":
                 owner.extend(int(np.searchsorted(bounds, v, side="right") - 1) for v in sched.subsets[s])
-        self.reg_owner = torch.tensor(owner if owner else [0], dtype=torch.int64, device=dev)
-        self.reg_song = torch.zeros(G, dtype=F64, device=dev)
+        # the gain-staging rows of each song, in level order: (offsets, row indices)
+        order = sorted(range(len(owner)), key=lambda i: (owner[i], i))
+        counts = np.bincount(np.asarray(owner, dtype=np.int64), minlength=G) if owner else np.zeros(G, np.int64)
+        self.reg_off = torch.tensor(np.concatenate([[0], np.cumsum(counts)]).astype(np.int32), device=dev)
+        self.reg_idx = torch.tensor(order if order else [0], dtype=torch.int32, device=dev)
         self.t = 0
         self.side = own_stream(dev, "side")
         self._graph = None
@@ -187,20 +190,17 @@ class BatchTrainEngine:
         main.wait_stream(side)
         side.wait_stream(main)
         with on_stream(side):  # loss assembly per song (read by the optimiser only)
-            self.reg_song.zero_()
-            self.reg_song.index_add_(0, self.reg_owner[: plan.reg.numel()], plan.reg)
             lay, u = self.layout, self.union
+            sp = stream_ptr()
             for i, g in enumerate(u.graphs):
                 n = len(g.processor_nodes())
                 if n:
-                    check(Ld.mgb_sparsity(ptr(self.params, lay.w_off + u.proc_off[i]), n,
-                                          ptr(self.sparsity, i), stream_ptr()), "mgb_sparsity")
-            la = self.lossp.loss
-            ap = self.scalars[7]
-            total = la + self.reg_song * float(self.cfg.loss.gain_staging_weight) + \
-                torch.where(ap > 0, ap * self.sparsity, torch.zeros_like(self.sparsity))
-            torch.stack([total, la, self.reg_song, self.sparsity], dim=1, out=self.vals)
-            torch.sum(total, dim=0, out=self.guard)
+                    check(Ld.mgb_sparsity(ptr(self.params, lay.w_off + u.proc_off[i]), n, ptr(self.sparsity, i), sp),
+                          "mgb_sparsity")
+            check(Ld.mgb_loss_assembly(ptr(self.lossp.loss), ptr(plan.reg), ptr(self.reg_off), ptr(self.reg_idx),
+                                       ptr(self.sparsity), ptr(self.scalars),
+                                       float(self.cfg.loss.gain_staging_weight), G, ptr(self.vals), ptr(self.guard),
+                                       sp), "mgb_loss_assembly")
         self.lossp.backward(ptr(plan.ys, ws), ptr(plan.ys, L + ws), ptr(plan.dYs, ws), ptr(plan.dYs, L + ws))
         plan.backward(side)
         main.wait_stream(side)

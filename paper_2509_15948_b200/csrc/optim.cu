@@ -108,7 +108,8 @@ __global__ void k_sparsity(const double* __restrict__ raw, int P, double* __rest
 // L = L_a + w_g * sum(reg) + alpha_p * sum sigma(raw)  (mg/optimizer.py:156-162), one
 // signal per thread q: reg rows [reg_off[q], reg_off[q+1]), in row order
 __global__ void k_loss_assembly(const double* __restrict__ la, const double* __restrict__ reg,
-                                const int* __restrict__ reg_off, const double* __restrict__ sparsity,
+                                const int* __restrict__ reg_off, const int* __restrict__ reg_idx,
+                                const double* __restrict__ sparsity,
                                 const double* __restrict__ sc, double gain_w, int n, double* __restrict__ vals,
                                 double* __restrict__ guard) {
   mgb_pdl_entry();
@@ -117,7 +118,7 @@ __global__ void k_loss_assembly(const double* __restrict__ la, const double* __r
   if (q < n) {
     double r = 0.0;
     const int r0 = reg_off ? reg_off[q] : 0, r1 = reg_off ? reg_off[q + 1] : 0;
-    for (int i = r0; i < r1; ++i) r += reg[i];
+    for (int i = r0; i < r1; ++i) r += reg[reg_idx ? reg_idx[i] : i];
     const double ap = sc[7];
     double total = la[q] + r * gain_w;
     if (ap > 0.0) total += ap * sparsity[q];
@@ -137,13 +138,13 @@ __global__ void k_loss_assembly(const double* __restrict__ la, const double* __r
 
 }  // namespace
 
-extern "C" int mgb_loss_assembly(const double* la, const double* reg, const int* reg_off, const double* sparsity,
-                                 const double* step_scalars, double gain_w, int n, double* vals, double* guard,
-                                 void* stream) {
+extern "C" int mgb_loss_assembly(const double* la, const double* reg, const int* reg_off, const int* reg_idx,
+                                 const double* sparsity, const double* step_scalars, double gain_w, int n, double* vals,
+                                 double* guard, void* stream) {
   if (n <= 0 || n > 1024 || !la || !sparsity || !step_scalars || !vals) return 1;
   if (reg_off && !reg) return 1;
-  mgb_launch(k_loss_assembly, dim3(1), dim3((n + 31) / 32 * 32), 0, (cudaStream_t)stream, la, reg, reg_off, sparsity,
-             step_scalars, gain_w, n, vals, guard);
+  mgb_launch(k_loss_assembly, dim3(1), dim3((n + 31) / 32 * 32), 0, (cudaStream_t)stream, la, reg, reg_off, reg_idx,
+             sparsity, step_scalars, gain_w, n, vals, guard);
   MGB_CHECK_LAUNCH();
   return 0;
 }

@@ -683,7 +683,7 @@ class TrainEngine:
             if P:
                 check(Ld.mgb_sparsity(ptr(self.params, self.layout.w_off), P, ptr(self.sparsity), sp),
                       "mgb_sparsity")
-            check(Ld.mgb_loss_assembly(ptr(lp.loss), ptr(plan.reg), ptr(self.reg_off), ptr(self.sparsity),
+            check(Ld.mgb_loss_assembly(ptr(lp.loss), ptr(plan.reg), ptr(self.reg_off), None, ptr(self.sparsity),
                                        ptr(self.scalars), float(self.cfg.loss.gain_staging_weight), 1,
                                        ptr(self.vals), None, sp), "mgb_loss_assembly")
         lp.backward(ptr(y, ws), ptr(y, L + ws), ptr(plan.dY, ws), ptr(plan.dY, L + ws))
