@@ -423,7 +423,7 @@ def prune_songs_lockstep(jobs, device="cuda", batch_trials=True):
 
     for i in range(len(gens)):
         advance(i, _START)
-    beval, bkey, loaded, trained = None, None, None, 0
+    engines, trained = {}, 0  # per eval-set shape: (engine key, engine, loaded-params key)
     while reqs:
         evals = sorted(i for i, r in reqs.items() if isinstance(r, EvalRequest))
         if evals:
@@ -432,45 +432,67 @@ def prune_songs_lockstep(jobs, device="cuda", batch_trials=True):
                     r = reqs[i]
                     advance(i, eval_losses(r.graph, r.params, r.masks, r.eval_set))
                 continue
-            ids = sorted(last_eval)
-            key = tuple((i, id(last_eval[i].graph), id(last_eval[i].eval_set)) for i in ids)
-            t0 = time.perf_counter()
-            if key != bkey:
-                beval = BatchEvalEngine([last_eval[i].graph for i in ids],
-                                        [last_eval[i].eval_set for i in ids], device)
-                bkey = key
-                PHASE_S["trial_engine_build"] += time.perf_counter() - t0
-            pkey = (bkey, tuple(id(last_eval[i].params) for i in ids), trained)
-            if pkey != loaded:  # parameters change only in training: no repack per trial
-                beval.load_params([last_eval[i].params for i in ids])
-                loaded = pkey
-            losses = beval.losses_for([last_eval[i].mask for i in ids])
-            PHASE_S["trials"] += time.perf_counter() - t0
-            PHASE_S["trial_slots"] += 1
-            for k, i in enumerate(ids):
-                if i in evals:
-                    advance(i, [losses[k]])
+            # songs whose eval sets share a shape form one union (every song of one recipe)
+            groups = {}
+            for i in sorted(last_eval):
+                es = last_eval[i].eval_set
+                shape = (len(es.segments), np.shape(es.segments[0][0])[-1], int(es.warmup_len), es.loss_cfg)
+                groups.setdefault(shape, []).append(i)
+            for shape, ids in groups.items():
+                if not any(i in evals for i in ids):
+                    continue
+                key = tuple((i, id(last_eval[i].graph), id(last_eval[i].eval_set)) for i in ids)
+                t0 = time.perf_counter()
+                ekey, beval, loaded = engines.get(shape, (None, None, None))
+                if key != ekey:
+                    beval = BatchEvalEngine([last_eval[i].graph for i in ids],
+                                            [last_eval[i].eval_set for i in ids], device)
+                    ekey, loaded = key, None
+                    PHASE_S["trial_engine_build"] += time.perf_counter() - t0
+                pkey = (tuple(id(last_eval[i].params) for i in ids), trained)
+                if pkey != loaded:  # parameters change only in training: no repack per trial
+                    beval.load_params([last_eval[i].params for i in ids])
+                    loaded = pkey
+                engines[shape] = (ekey, beval, loaded)
+                losses = beval.losses_for([last_eval[i].mask for i in ids])
+                PHASE_S["trials"] += time.perf_counter() - t0
+                PHASE_S["trial_slots"] += 1
+                for k, i in enumerate(ids):
+                    if i in evals:
+                        advance(i, [losses[k]])
             continue
-        ids = sorted(reqs)
+        # every pending search waits on a train(): requests with the same step count,
+        # hyper-parameters and sparsity schedule run as one batch
+        batches = {}
+        for i in sorted(reqs):
+            r = reqs[i]
+            c = r.cfg
+            alphas = tuple(r.alpha_p_fn(s) if r.alpha_p_fn else 0.0 for s in range(c.steps))
+            batches.setdefault((c.steps, c.segment_len, c.warmup_len, c.lr, tuple(c.betas), c.eps,
+                                c.weight_decay, c.loss, alphas), []).append(i)
         t0 = time.perf_counter()
-        try:
-            if len(ids) == 1:
-                run_train_request(reqs[ids[0]], device)
-            else:
-                train_batch([reqs[i] for i in ids], device)
-        except BatchNonFinite:
-            # rare: rerun each of these searches on its own (the reference's per-song semantics)
+        for ids in batches.values():
+            try:
+                if len(ids) == 1:
+                    run_train_request(reqs[ids[0]], device)
+                else:
+                    train_batch([reqs[i] for i in ids], device)
+            except NonFiniteLoss:
+                # rare: rerun these searches one by one from the start (the reference's
+                # per-song semantics: only a failing song stops)
+                for i in ids:
+                    g, p, s, c = jobs[i]
+                    try:
+                        out[i] = prune_song(g, p, s, c, device=device, speculate=1)
+                    except NonFiniteLoss as e:
+                        out[i] = e
+                    reqs.pop(i, None)
+                    last_eval.pop(i, None)
+                continue
+            trained += 1
             for i in ids:
-                g, p, s, c = jobs[i]
-                try:
-                    out[i] = prune_song(g, p, s, c, device=device, speculate=1)
-                except NonFiniteLoss as e:
-                    out[i] = e
-            return out
-        trained += 1
+                advance(i, None)
         PHASE_S["train"] += time.perf_counter() - t0
-        for i in ids:
-            advance(i, None)
     return out
 
 

@@ -570,3 +570,34 @@ def test_speculative_bruteforce_trials_make_the_same_decisions(dev):
     np.testing.assert_array_equal(s1.alive, s4.alive)
     assert serialize(g1, p1) == serialize(g4, p4)
     assert r1.final_loss == r4.final_loss
+
+
+def test_lockstep_with_mixed_recipes_equals_one_by_one(dev):
+    """prune_songs_lockstep groups what it can batch: songs whose train() calls differ in
+    step count, or whose eval sets differ in shape, run in separate batches, and every
+    search still equals its own prune_song."""
+    import bench
+    from paper_2509_15948_b200.batch import prune_songs_lockstep
+    from paper_2509_15948_b200.graph import serialize
+    from paper_2509_15948_b200.optimizer import Session
+    from paper_2509_15948_b200.pruning import prune_song
+    from paper_2509_15948_b200.scheduler import execute_batched
+    from paper_2509_15948_b200.songs import desk_prune_config
+
+    def render(graph, tparams, stems):
+        return execute_batched(graph, tparams, stems, device=dev)[0].cpu().numpy()
+
+    jobs = []
+    for i, (k, ft, segs) in enumerate(((4, 5, 2), (3, 8, 2), (4, 5, 3))):
+        graph, params, stems, target = bench.make_inputs(60 + i, k, 1, 132_300, render)
+        cfg = desk_prune_config(i, iterations=2)
+        cfg.console_steps, cfg.finetune_steps, cfg.eval_segments = 20, ft, segs
+        jobs.append((graph, params, Session(stems, target), cfg))
+    lock = prune_songs_lockstep(jobs, device=dev)
+    for (g, p, s, c), r in zip(jobs, lock):
+        g1, p1, st1, rep1, _ = prune_song(g, p, s, c, device=dev, speculate=1)
+        g2, p2, st2, rep2, _ = r
+        assert serialize(g1, p1) == serialize(g2, p2)
+        assert [(x.candidates, x.loss, x.accepted) for x in st1.ledger] == \
+            [(x.candidates, x.loss, x.accepted) for x in st2.ledger]
+        assert rep1.final_loss == rep2.final_loss
