@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--concurrent", type=int, default=1, help="songs in flight per GPU (threads + streams)")
     ap.add_argument("--lockstep", type=int, default=0,
                     help="search songs in lock-step groups of this size (batched training), 0 = off")
+    ap.add_argument("--group-threads", type=int, default=1, help="lock-step groups in flight (host threads)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -63,7 +64,7 @@ def main():
     t0 = time.perf_counter()
     if args.lockstep:
         results = search_songs_lockstep(specs, mine, inputs, group=args.lockstep, iterations=args.iterations,
-                                        device=dev)
+                                        device=dev, threads=args.group_threads)
     else:
         results = search_songs(specs, mine, inputs, concurrent=args.concurrent, iterations=args.iterations,
                                device=dev)
