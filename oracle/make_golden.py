@@ -83,6 +83,17 @@ def main():
         t.backward(val)
         mr[f"{name}_loss"] = np.asarray(E.value_of(val))
         mr[f"{name}_grad"] = yb.grad
+    # short scored signals: the 4096- and 8192-point frames' reflect pads span several
+    # reflections (mg/engine.py:640-645)
+    y_hat, tgt = mrstft_inputs()
+    for name, ls in (("short1000", 1000), ("short3000", 3000)):
+        cfg = Lo.LossConfig(fft_sizes=(256, 512, 1024, 2048, 4096, 8192))
+        t = E.Tape()
+        yb = t.leaf(y_hat[:, :ls].copy())
+        val = Lo.mrstft(yb, tgt[:, :ls].copy(), cfg)
+        t.backward(val)
+        mr[f"{name}_loss"] = np.asarray(E.value_of(val))
+        mr[f"{name}_grad"] = yb.grad
     np.savez_compressed(os.path.join(OUT, "mrstft.npz"), **mr)
 
     # 4. one full train_step on a small console (K=2, S=1)

@@ -473,13 +473,16 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
   for (int ri = 0; ri < L.n_res; ++ri) {
     const MgbLossRes& r = L.res[ri];
     const int n = r.n_fft, pad = n / 2, lh = __ffs(r.hop) - 1, ln = __ffs(n) - 1;
-    int P[3];
-    int np = 0;
-    P[np++] = t + pad;
-    if (t >= 1 && t <= pad) P[np++] = pad - t;
-    if (t >= Ls - 1 - pad && t <= Ls - 2) P[np++] = 2 * (Ls - 1) - t + pad;
-    for (int qi = 0; qi < np; ++qi) {
-      const int p = P[qi];
+    // every padded position whose reflect-pad source is t: q = +-t (mod 2(Ls-1)) in
+    // [-pad, Ls + pad) -- one or two positions when pad < Ls - 1, more when the pad
+    // spans several reflections (the reference's index-map branch, mg/engine.py:640-645)
+    const int period = 2 * (Ls - 1);
+    for (int cls = 0; cls < 2; ++cls) {
+      if (cls == 1 && (t == 0 || t == Ls - 1)) break;  // -t is the +t class
+      const int base = cls ? -t : t, num = -pad - base;
+      const int k0 = num <= 0 ? -((-num) / period) : (num + period - 1) / period;
+    for (int q = base + k0 * period; q < Ls + pad; q += period) {
+      const int p = q + pad;
       int fhi = p >> lh;
       if (fhi > r.frames - 1) fhi = r.frames - 1;
       const int flo = (p - n + 1 <= 0) ? 0 : ((p - n + r.hop) >> lh);  // ceil((p - n + 1) / hop)
@@ -490,6 +493,7 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
         al += __ldg(gfp + o);
         ar += __ldg(gfp + n + o);
       }
+    }
     }
   }
   gl[t] = (float)al;
@@ -545,11 +549,11 @@ int dispatch_bwd(const MgbLossRes& r, const double* stats, const MgbLoss& L, con
 }
 
 int check_loss(const MgbLoss* L) {
-  if (!L || L->n_res <= 0 || L->n_res > 8 || L->Ls <= 0) return 1;
+  if (!L || L->n_res <= 0 || L->n_res > 8 || L->Ls <= 1) return 1;
   if (L->batch > 1024 || (L->batch > 1 && L->sig_stride < L->Ls)) return 1;
   for (int i = 0; i < L->n_res; ++i) {
     const MgbLossRes& r = L->res[i];
-    if (r.n_mels > 128 || r.n_fft / 2 >= L->Ls) return 1;
+    if (r.n_mels > 128) return 1;
   }
   return 0;
 }

@@ -545,8 +545,8 @@ class LossPlan:
         for n in sizes:
             if n & (n - 1) or not 256 <= n <= 8192:
                 raise NotImplementedError(f"fft size {n}: power of two in [256, 8192] required")
-            if n // 2 >= Ls:
-                raise NotImplementedError(f"scored length {Ls} too short for fft size {n}")
+        if Ls < 2:
+            raise ValueError("the scored length must be at least 2 samples")
         if cfg.mel_bins > 128:
             raise NotImplementedError("mel_bins <= 128")
         st = MgbLoss()

@@ -79,6 +79,26 @@ def test_mrstft_matches_reference_golden(dev, name, sizes):
     assert normrel(yt.grad.cpu().numpy(), yo.grad.numpy()) < 1e-4
 
 
+@pytest.mark.parametrize("name,ls", [("short1000", 1000), ("short3000", 3000)])
+def test_mrstft_short_signals_match_reference_golden(dev, name, ls):
+    """Scored signals shorter than the 4096/8192-point frames' reflect pad: the pad spans
+    several reflections (mg/engine.py:640-645), in the forward and in the adjoint."""
+    from paper_2509_15948_b200.losses import LossConfig, mrstft
+    gm = golden("mrstft.npz")
+    y_hat, tgt = mrstft_inputs()
+    yt = torch.tensor(y_hat[:, :ls].astype(np.float32), device=dev, requires_grad=True)
+    val = mrstft(yt, tgt[:, :ls].astype(np.float32), LossConfig(fft_sizes=(256, 512, 1024, 2048, 4096, 8192)))
+    val.backward()
+    from oracle import mixgraph_oracle as O
+    yo = torch.tensor(y_hat[:, :ls].astype(np.float32).astype(np.float64), requires_grad=True)
+    ov = O.mrstft(yo, tgt[:, :ls].astype(np.float32).astype(np.float64),
+                  O.LossConfig(fft_sizes=(256, 512, 1024, 2048, 4096, 8192)))
+    ov.backward()
+    np.testing.assert_allclose(float(val.detach()), float(ov.detach()), rtol=1e-5)
+    np.testing.assert_allclose(float(val.detach()), float(gm[f"{name}_loss"]), rtol=1e-3)
+    assert normrel(yt.grad.cpu().numpy(), yo.grad.numpy()) < 1e-4
+
+
 def _step_setup():
     from paper_2509_15948_b200.console import build_console, init_params
     from workloads import SynthSpec, make_stems_f32, manifest_for

@@ -136,3 +136,15 @@ def test_oracle_config1_step_matches_reference():
     O.train_step(graph, p, raw, stems, target, 30000, O.LossConfig(), opt)
     for t in "gsecnr":
         np.testing.assert_allclose(p[t], gs[f"after_{t}"], rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("name,ls", [("short1000", 1000), ("short3000", 3000)])
+def test_oracle_mrstft_short_signals_match_reference(name, ls):
+    """Scored signals shorter than the frames' reflect pad (mg/engine.py:640-645)."""
+    gm = golden("mrstft.npz")
+    y_hat, tgt = mrstft_inputs()
+    yt = torch.tensor(y_hat[:, :ls].copy(), requires_grad=True)
+    val = O.mrstft(yt, tgt[:, :ls].copy(), O.LossConfig(fft_sizes=(256, 512, 1024, 2048, 4096, 8192)))
+    val.backward()
+    np.testing.assert_allclose(float(val.detach()), float(gm[f"{name}_loss"]), rtol=1e-12)
+    assert normrel(yt.grad.numpy(), gm[f"{name}_grad"]) < 1e-10
