@@ -194,13 +194,14 @@ def _oracle_render(graph, params, src, mask=None):
     return y.numpy(), float(reg)
 
 
-@pytest.mark.parametrize("seed", range(4))
-def test_execute_batched_matches_oracle_on_random_consoles(dev, seed):
+@pytest.mark.parametrize("seed,L", [(0, 5000), (1, 5000), (2, 5000), (3, 5000), (4, 4999), (5, 8193), (6, 1231)])
+def test_execute_batched_matches_oracle_on_random_consoles(dev, seed, L):
+    """Random consoles and prunings; odd lengths take the scalar (non-float4) row paths."""
     from paper_2509_15948_b200.schedule import schedule_console
     from paper_2509_15948_b200.scheduler import execute_batched
     rng = np.random.default_rng(seed + 100)
     graph, params = _random_console(rng, kmax=5, prune=rng.uniform(0, 0.8))
-    src = (0.3 * rng.standard_normal((len(graph.nodes_of_type("i")), 2, 5000))).astype(np.float32)
+    src = (0.3 * rng.standard_normal((len(graph.nodes_of_type("i")), 2, L))).astype(np.float32)
     y, reg = execute_batched(graph, params, src, schedule_console(graph))
     yo, rego = _oracle_render(graph, params, src)
     assert normrel(y.cpu().numpy(), yo) < 1e-5
@@ -621,3 +622,39 @@ def test_lockstep_with_mixed_recipes_equals_one_by_one(dev):
         assert [(x.candidates, x.loss, x.accepted) for x in st1.ledger] == \
             [(x.candidates, x.loss, x.accepted) for x in st2.ledger]
         assert rep1.final_loss == rep2.final_loss
+
+
+@pytest.mark.parametrize("L", [4999, 6151])
+def test_train_step_gradients_at_odd_lengths_match_oracle(dev, L):
+    """A full forward + backward at lengths that are not multiples of 4 (scalar row paths in
+    every streaming kernel) and shorter than one 8192-sample scan chunk.  (Below ~3,000
+    samples a delay node whose taps all fall past the signal has a wet output of pure FFT
+    rounding noise, and the gain-staging term's 1/||ybar|| turns that noise into O(100)
+    gradients that differ between any two implementations, the reference and its own
+    float64 restatement included.)"""
+    from oracle import mixgraph_oracle as O
+    from paper_2509_15948_b200.console import build_console, init_params
+    from paper_2509_15948_b200.engine import TrainEngine
+    from paper_2509_15948_b200.optimizer import TrainConfig, _EngineCfg, make_optimizer
+    from workloads import SynthSpec, make_stems_f32, manifest_for
+    ws = 1000
+    spec = SynthSpec(tracks=3, subgroups=1, duration_seconds=L / 30000)
+    stems = make_stems_f32(spec, 9, L)
+    graph, zeros = build_console(manifest_for(spec))
+    params = init_params(zeros, 0)
+    rng = np.random.default_rng(L)
+    target = (0.3 * rng.standard_normal((2, L))).astype(np.float32)
+    cfg = TrainConfig(segment_seconds=L / 30000, warmup_seconds=ws / 30000, steps=1)
+    eng = TrainEngine(graph, L, _EngineCfg(make_optimizer(params, cfg), cfg), device=dev, use_graph=False)
+    eng.load_params(params)
+    eng.plan.set_stems(stems)
+    eng.target.copy_(torch.as_tensor(target))
+    vals, grads, gw, y = eng.grads_only()
+    args = (graph, {t: v.copy() for t, v in params.params.items()}, params.raw_weights.copy(),
+            stems.astype(np.float64), target.astype(np.float64), ws, O.LossConfig())
+    ov, og, oy = O.render_loss_and_grads(*args)
+    _, ogd, _ = O.render_loss_and_grads(*args, loss_point=y.astype(np.float64))
+    assert normrel(y, oy) < 1e-5
+    np.testing.assert_allclose(vals["L_a"], ov["L_a"], rtol=1e-5)
+    for t in "gsecnrd":
+        assert normrel(grads[t], ogd[t], floor=1e-6) < 1e-4, t
