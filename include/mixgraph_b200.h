@@ -101,6 +101,10 @@ int mgb_level_backward_phase(const MgbLevel* level, int phase, void* stream);
  * at capture). */
 long long mgb_launch_count(void);
 
+/* Profiling: *dst = the GPU's global nanosecond timer when the stream reaches this point
+ * (a one-thread kernel; usable inside a captured CUDA graph, where timing events are not). */
+int mgb_timestamp(unsigned long long* dst, void* stream);
+
 /* cudaMemsetAsync(ptr, 0, bytes) on the stream (not a kernel; e.g. the warm-up part of dL/dy). */
 int mgb_zero(void* ptr, size_t bytes, void* stream);
 

@@ -96,6 +96,7 @@ def lib():
     L.mgb_sparsity.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
     L.mgb_gather_rows.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]
     L.mgb_zero.argtypes = [c_void_p, c_size_t, c_void_p]
+    L.mgb_timestamp.argtypes = [c_void_p, c_void_p]
     L.mgb_loss_assembly.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
                                     c_void_p, c_void_p, c_void_p]
     L.mgb_metrics_workspace.argtypes = [c_int, c_int]
@@ -110,7 +111,7 @@ def lib():
     for name in ("mgb_init", "mgb_level_forward", "mgb_level_backward", "mgb_level_forward_phase",
                  "mgb_level_backward_phase", "mgb_weights", "mgb_bus_sum",
                  "mgb_fft", "mgb_mrstft_target", "mgb_mrstft_forward", "mgb_mrstft_backward",
-                 "mgb_adamw_step", "mgb_sparsity", "mgb_stream_destroy", "mgb_gather_rows", "mgb_song_metrics", "mgb_loss_assembly", "mgb_zero"):
+                 "mgb_adamw_step", "mgb_sparsity", "mgb_stream_destroy", "mgb_gather_rows", "mgb_song_metrics", "mgb_loss_assembly", "mgb_zero", "mgb_timestamp"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -120,7 +121,7 @@ EXPORTED = ("mgb_abi_version", "mgb_init", "mgb_level_workspace", "mgb_level_for
             "mgb_level_backward", "mgb_level_forward_phase", "mgb_level_backward_phase", "mgb_launch_count", "mgb_weights", "mgb_bus_sum", "mgb_fft", "mgb_mrstft_target",
             "mgb_mrstft_forward", "mgb_mrstft_backward", "mgb_adamw_step", "mgb_sparsity",
             "mgb_stream_create", "mgb_stream_destroy", "mgb_stream_create_priority", "mgb_gather_rows", "mgb_metrics_workspace",
-            "mgb_song_metrics", "mgb_loss_assembly", "mgb_zero")
+            "mgb_song_metrics", "mgb_loss_assembly", "mgb_zero", "mgb_timestamp")
 
 
 def check(rc, what):

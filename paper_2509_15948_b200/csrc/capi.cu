@@ -105,6 +105,17 @@ extern "C" long long mgb_launch_count(void) { return g_mgb_launches.load(std::me
 
 extern "C" void* mgb_stream_create_priority(int level);
 
+__global__ void k_timestamp(unsigned long long* dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
+
+extern "C" int mgb_timestamp(unsigned long long* dst, void* stream) {
+  k_timestamp<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
 extern "C" int mgb_zero(void* ptr, size_t bytes, void* stream) {
   if (!bytes) return 0;
   return cudaMemsetAsync(ptr, 0, bytes, (cudaStream_t)stream) == cudaSuccess ? 0 : 2;
