@@ -1,3 +1,4 @@
+# songs/hour of one lock-step group (tools/songs_bench.py) with its phase split, and a cProfile of the same run
 mkdir -p gpurun_out/songs
 N=${N:-8}
 timeout 600 python tools/songs_bench.py --songs $N --lockstep 8 > gpurun_out/songs/prof.json 2> gpurun_out/songs/prof.err
