@@ -1,5 +1,4 @@
 """d-bank gradient of a short console step, device vs the oracle, largest differences by tap (degenerate delay case)."""
-"""d-bank gradient of a short train step, device vs oracle, by tap and part."""
 import os
 import sys
 
