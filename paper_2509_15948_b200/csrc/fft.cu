@@ -14,6 +14,8 @@
 // stereo rows: the two real channels ride one complex transform
 // (z = left + i*right), and the per-channel spectra are separated with the
 // Hermitian pairing X_l[k] = (Z[k] + conj Z[-k])/2, X_r[k] = (Z[k] - conj Z[-k])/2i.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "tables.cuh"
 #include "mgb_internal.h"
@@ -83,8 +85,11 @@ int mgb_init_device(cudaStream_t st) {
   MGB_CHECK_LAUNCH();
   mgb_launch(k_init_fs_twiddles, dim3(dim3(2048 / 256, MGB_FS_LMAX - MGB_FS_LMIN + 1)), dim3(256), 0, st);
   MGB_CHECK_LAUNCH();
-  mgb_launch(k_init_eq_table, dim3(dim3((MGB_EQ_LEN + 255) / 256, MGB_EQ_BINS)), dim3(256), 0, st);
-  MGB_CHECK_LAUNCH();
+  const char* mm = getenv("MGB_EQ_FIR_MM");  // the table of the (off by default) product-form EQ FIR
+  if (mm && atoi(mm) != 0) {
+    mgb_launch(k_init_eq_table, dim3(dim3((MGB_EQ_LEN + 255) / 256, MGB_EQ_BINS)), dim3(256), 0, st);
+    MGB_CHECK_LAUNCH();
+  }
   return 0;
 }
 
