@@ -46,11 +46,6 @@ int g_num_sms = 148;
 // MGB_COLC_PERSISTENT=1: the persistent bulk-copy-pipelined column pass (fs2::k_colC_p) instead of
 // one tile per CTA.  Measured slower (336 vs 437 steps/s), kept off for A/B runs.
 bool g_colc_persistent = false;
-// EQ FIR synthesis / adjoint as float64 matrix products against a cosine table
-// (MGB_EQ_FIR_MM=1) instead of per-lane rotation recurrences: measured slower (FIR
-// synthesis 0.289 vs 0.236 ms per config-2 step: one output per thread leaves the
-// products shared-memory bound), kept off for A/B runs
-bool g_eq_fir_mm = false;
 
 struct ConvGeom {
   int M, off, logN;
@@ -76,7 +71,6 @@ struct ConvWs {
   float* aux2;                 // r: dexpo (B,2,313,193)
   int* offs;                   // d: (B,2,20) quantised delays
   float2 *Hs, *pspec, *csum;   // e (overlap-save): 8192-pt FIR spectra, per-block / summed dh cross spectra
-  double* xexp;                // e: exp(p) per node (forward phase 1 -> backward phase 2)
 };
 
 template <class A>
@@ -84,7 +78,6 @@ ConvWs carve_into(A& a, char tag, int B, int L) {
   const ConvGeom g = geom(tag, L);
   ConvWs w;
   w.Hs = w.pspec = w.csum = nullptr;
-  w.xexp = nullptr;
   if (tag == 'e') {  // overlap-save path: no four-step buffers
     w.Ax = w.Ah = w.X = w.H = w.Bo = nullptr;
     w.hbuf = a.template take<float2>((size_t)B * g.M);
@@ -96,7 +89,6 @@ ConvWs carve_into(A& a, char tag, int B, int L) {
     w.Hs = a.template take<float2>((size_t)B * EOS_N);
     w.pspec = a.template take<float2>((size_t)B * eos_nchunk(L, B) * 2 * EOS_N);  // D park + C accumulator per CTA
     w.csum = a.template take<float2>((size_t)B * EOS_N);
-    w.xexp = a.template take<double>((size_t)B * MGB_EQ_BINS);
     return w;
   }
   const size_t BN = (size_t)B * g.N;
@@ -635,8 +627,6 @@ int mgb_conv_init() {
   cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   const char* e = getenv("MGB_COLC_PERSISTENT");
   g_colc_persistent = e ? atoi(e) != 0 : false;
-  const char* e2 = getenv("MGB_EQ_FIR_MM");
-  g_eq_fir_mm = e2 ? atoi(e2) != 0 : false;
 #define X(l, a) Conv2<a>::attrs();
   MGB_CONV_SIZES(X)
 #undef X
@@ -665,14 +655,7 @@ int mgb_conv_prepare(const MgbLevel* lv, cudaStream_t st) {
   MgbArena a{(char*)lv->ws, 0};
   const ConvWs w = carve_into(a, tag, B, L);
   if (tag == 'e') {
-    if (g_eq_fir_mm) {
-      mgb_launch(k_eq_exp, dim3(dim3(MGB_EQ_BINS / 256, B)), dim3(256), 0, st, lv->bank, lv->prow, w.xexp);
-      MGB_CHECK_LAUNCH();
-      mgb_launch(k_eq_fir_mm, dim3(dim3((MGB_EQ_LEN + EQF_TT - 1) / EQF_TT, (B + EQF_TN - 1) / EQF_TN)), dim3(256), 0,
-                 st, (const double*)w.xexp, B, w.hbuf);
-    } else {
-      mgb_launch(k_eq_fir, dim3(dim3((MGB_EQ_LEN + 31) / 32, B)), dim3(256), 0, st, lv->bank, lv->prow, w.hbuf);
-    }
+    mgb_launch(k_eq_fir, dim3(dim3((MGB_EQ_LEN + 31) / 32, B)), dim3(256), 0, st, lv->bank, lv->prow, w.hbuf);
     MGB_CHECK_LAUNCH();
     mgb_launch(k_eqos_hspec, dim3(B), dim3(EOS_NT), kEosSmem1, st, w.hbuf, w.Hs);
     MGB_CHECK_LAUNCH();
@@ -759,13 +742,7 @@ int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st) {
     MGB_CHECK_LAUNCH();
     mgb_launch(k_eqos_gh, dim3(B), dim3(EOS_NT), kEosSmem1, st, w.csum, w.ghbuf);
     MGB_CHECK_LAUNCH();
-    if (g_eq_fir_mm) {
-      mgb_launch(k_eq_fir_bwd_mm, dim3(dim3(MGB_EQ_BINS / EQF_TT, (B + EQF_TN - 1) / EQF_TN)), dim3(256), 0, st,
-                 (const double*)w.xexp, lv->prow, B, w.ghbuf, g.M, lv->gbank);
-    } else {
-      mgb_launch(k_eq_fir_bwd, dim3(dim3(MGB_EQ_BINS / 32, B)), dim3(256), 0, st, lv->bank, lv->prow, w.ghbuf, g.M,
-                 lv->gbank);
-    }
+    mgb_launch(k_eq_fir_bwd, dim3(dim3(MGB_EQ_BINS / 32, B)), dim3(256), 0, st, lv->bank, lv->prow, w.ghbuf, g.M, lv->gbank);
   } else if (tag == 'r') {
     if (int rc = conv_firgrad_dispatch(lv, w, g, st)) return rc;
     mgb_launch(k_rev_bwd_frames_fft, dim3(dim3((MGB_REV_FRAMES + RV_F - 1) / RV_F, B)), dim3(RV_NT), kRevFftSmem, st, 

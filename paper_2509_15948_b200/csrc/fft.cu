@@ -14,8 +14,6 @@
 // stereo rows: the two real channels ride one complex transform
 // (z = left + i*right), and the per-channel spectra are separated with the
 // Hermitian pairing X_l[k] = (Z[k] + conj Z[-k])/2, X_r[k] = (Z[k] - conj Z[-k])/2i.
-#include <stdlib.h>
-
 #include "common.cuh"
 #include "tables.cuh"
 #include "mgb_internal.h"
@@ -27,19 +25,6 @@ __device__ float2 g_fs_hi[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
 // FIR-synthesis tables (float64): the symmetric Hann of n = 2047 (EQ); cos(2 pi j / n) and Hann of n = 39 (colour)
 __device__ double g_hann2047[MGB_EQ_LEN];
 __device__ double g_cos39[MGB_COLOR_LEN], g_hann39[MGB_COLOR_LEN];
-// the EQ FIR synthesis as a matrix (16.8 MB): g_eq_cos[k][t'] = s_k cos(2 pi k ((t' + 1024) mod n) / n)
-// hann_sym(n)[t'], s_0 = 1/n, s_k = 2/n (n = 2047): centred FIR = exp(p) @ g_eq_cos, and the
-// FIR adjoint d p_k = exp(p_k) (dh @ g_eq_cos^T)_k
-__device__ double g_eq_cos[MGB_EQ_BINS][MGB_EQ_LEN];
-
-__global__ void k_init_eq_table() {
-  const int k = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= MGB_EQ_LEN) return;
-  const long long arg = ((long long)k * ((t + 1024) % MGB_EQ_LEN)) % MGB_EQ_LEN;  // exact reduction
-  const double sk = (k == 0 ? 1.0 : 2.0) / (double)MGB_EQ_LEN;
-  const double hann = 0.5 - 0.5 * cospi(2.0 * t / (double)(MGB_EQ_LEN - 1));
-  g_eq_cos[k][t] = sk * cospi(2.0 * (double)arg / (double)MGB_EQ_LEN) * hann;
-}
 
 __global__ void k_init_fir_tables() {
   mgb_pdl_entry();
@@ -85,11 +70,6 @@ int mgb_init_device(cudaStream_t st) {
   MGB_CHECK_LAUNCH();
   mgb_launch(k_init_fs_twiddles, dim3(dim3(2048 / 256, MGB_FS_LMAX - MGB_FS_LMIN + 1)), dim3(256), 0, st);
   MGB_CHECK_LAUNCH();
-  const char* mm = getenv("MGB_EQ_FIR_MM");  // the table of the (off by default) product-form EQ FIR
-  if (mm && atoi(mm) != 0) {
-    mgb_launch(k_init_eq_table, dim3(dim3((MGB_EQ_LEN + 255) / 256, MGB_EQ_BINS)), dim3(256), 0, st);
-    MGB_CHECK_LAUNCH();
-  }
   return 0;
 }
 

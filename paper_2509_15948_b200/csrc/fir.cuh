@@ -77,86 +77,6 @@ __global__ void __launch_bounds__(256) k_eq_fir_bwd(const double* __restrict__ b
   }
 }
 
-// The same two transforms as small float64 matrix products against the precomputed
-// g_eq_cos table (one DFMA per term instead of a serial rotation recurrence with three
-// more float64 operations per term): a CTA computes an EQF_TN x EQF_TT tile, K staged
-// through shared memory in EQF_TK chunks, two accumulators per thread.
-constexpr int EQF_TN = 8, EQF_TT = 32, EQF_TK = 64;
-
-// X[b][k] = exp(p[b][k]) once per node (the tiles of k_eq_fir_mm / k_eq_fir_bwd_mm read it)
-__global__ void __launch_bounds__(256) k_eq_exp(const double* __restrict__ bank, const int* __restrict__ prow,
-                                                double* __restrict__ X) {
-  mgb_pdl_entry();
-  const int b = blockIdx.y, k = blockIdx.x * 256 + threadIdx.x;
-  X[(size_t)b * MGB_EQ_BINS + k] = exp(bank[(size_t)prow[b] * MGB_EQ_BINS + k]);
-}
-
-// H[b][t'] = sum_k X[b][k] g_eq_cos[k][t']   (both channels)
-__global__ void __launch_bounds__(256) k_eq_fir_mm(const double* __restrict__ X, int B, float2* __restrict__ H) {
-  mgb_pdl_entry();
-  __shared__ double sA[EQF_TN][EQF_TK];
-  __shared__ double sT[EQF_TK][EQF_TT];
-  const int tx = threadIdx.x % EQF_TT, ty = threadIdx.x / EQF_TT;  // tap, node within the tile
-  const int t = blockIdx.x * EQF_TT + tx, b = blockIdx.y * EQF_TN + ty;
-  double a0 = 0.0, a1 = 0.0;
-  for (int k0 = 0; k0 < MGB_EQ_BINS; k0 += EQF_TK) {
-    for (int i = threadIdx.x; i < EQF_TN * EQF_TK; i += 256) {
-      const int r = i / EQF_TK, c = i % EQF_TK, bb = blockIdx.y * EQF_TN + r;
-      sA[r][c] = bb < B ? X[(size_t)bb * MGB_EQ_BINS + k0 + c] : 0.0;
-    }
-    for (int i = threadIdx.x; i < EQF_TK * EQF_TT; i += 256) {
-      const int r = i / EQF_TT, c = i % EQF_TT, tt = blockIdx.x * EQF_TT + c;
-      sT[r][c] = tt < MGB_EQ_LEN ? g_eq_cos[k0 + r][tt] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int k = 0; k < EQF_TK; k += 2) {
-      a0 = fma(sA[ty][k], sT[k][tx], a0);
-      a1 = fma(sA[ty][k + 1], sT[k + 1][tx], a1);
-    }
-    __syncthreads();
-  }
-  if (b < B && t < MGB_EQ_LEN) {
-    const float c = (float)(a0 + a1);
-    H[(size_t)b * MGB_EQ_LEN + t] = make_float2(c, c);
-  }
-}
-
-// d p[b][k] = X[b][k] sum_t' (dh_l + dh_r)[b][t'] g_eq_cos[k][t']
-__global__ void __launch_bounds__(256) k_eq_fir_bwd_mm(const double* __restrict__ X, const int* __restrict__ prow,
-                                                       int B, const float2* __restrict__ GH, int M,
-                                                       double* __restrict__ gbank) {
-  mgb_pdl_entry();
-  __shared__ double sD[EQF_TN][EQF_TK];
-  __shared__ double sT[EQF_TT][EQF_TK + 1];  // [bin][tap], padded against bank conflicts
-  const int tx = threadIdx.x % EQF_TT, ty = threadIdx.x / EQF_TT;  // bin, node within the tile
-  const int k = blockIdx.x * EQF_TT + tx, b = blockIdx.y * EQF_TN + ty;
-  double a0 = 0.0, a1 = 0.0;
-  for (int t0 = 0; t0 < MGB_EQ_LEN; t0 += EQF_TK) {
-    for (int i = threadIdx.x; i < EQF_TN * EQF_TK; i += 256) {
-      const int r = i / EQF_TK, c = i % EQF_TK, bb = blockIdx.y * EQF_TN + r, tt = t0 + c;
-      double v = 0.0;
-      if (bb < B && tt < MGB_EQ_LEN) {
-        const float2 g = GH[(size_t)bb * M + tt];
-        v = (double)g.x + (double)g.y;
-      }
-      sD[r][c] = v;
-    }
-    for (int i = threadIdx.x; i < EQF_TT * EQF_TK; i += 256) {
-      const int r = i / EQF_TK, c = i % EQF_TK, kk = blockIdx.x * EQF_TT + r, tt = t0 + c;
-      sT[r][c] = tt < MGB_EQ_LEN ? g_eq_cos[kk][tt] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int c = 0; c < EQF_TK; c += 2) {
-      a0 = fma(sD[ty][c], sT[tx][c], a0);
-      a1 = fma(sD[ty][c + 1], sT[tx][c + 1], a1);
-    }
-    __syncthreads();
-  }
-  if (b < B) gbank[(size_t)prow[b] * MGB_EQ_BINS + k] = (a0 + a1) * X[(size_t)b * MGB_EQ_BINS + k];
-}
-
 // ---------------------------------------------------------------------------
 // Reverb FIR synthesis
 

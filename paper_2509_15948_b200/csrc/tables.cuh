@@ -23,4 +23,3 @@ extern __device__ float2 g_rev_spec[2][MGB_REV_FRAMES][MGB_REV_BINS];
 extern __device__ float g_rev_inv_wss[MGB_REV_LEN];
 extern __device__ double g_hann2047[MGB_EQ_LEN];
 extern __device__ double g_cos39[MGB_COLOR_LEN], g_hann39[MGB_COLOR_LEN];
-extern __device__ double g_eq_cos[MGB_EQ_BINS][MGB_EQ_LEN];
