@@ -210,8 +210,8 @@ extern __device__ float2 g_fs_hi[MGB_FS_LMAX - MGB_FS_LMIN + 1][2048];
 template <int LOGN>
 __device__ __forceinline__ float2 fs_twiddle(int e, bool inv) {
   static_assert(LOGN >= MGB_FS_LMIN && LOGN <= MGB_FS_LMAX, "four-step size");
-  const float2 a = g_fs_lo[LOGN - MGB_FS_LMIN][e & 2047];
-  const float2 b = g_fs_hi[LOGN - MGB_FS_LMIN][e >> 11];
+  const float2 a = __ldg(&g_fs_lo[LOGN - MGB_FS_LMIN][e & 2047]);  // read-only path: loads may be hoisted
+  const float2 b = __ldg(&g_fs_hi[LOGN - MGB_FS_LMIN][e >> 11]);
   float2 w = cmul(a, b);
   if (inv) w.y = -w.y;
   return w;

@@ -22,6 +22,21 @@ namespace {
 
 constexpr double LOG_EPS = 1e-7;
 
+// log(x) for x > 0 (normal): x = m 2^e with m in [0.75, 1.5), e ln 2 in float64 and log m
+// in float32 (|log m| < 0.41: absolute error below 6e-8, far under the float32 STFT's
+// own rounding of the mel values); the loss's L1 log terms use it for the estimate and
+// the target alike
+__device__ __forceinline__ double log_mel(double x) {
+  const long long b = __double_as_longlong(x);
+  int e = (int)((b >> 52) & 0x7ff) - 1023;
+  double m = __longlong_as_double((b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);  // [1, 2)
+  if (m >= 1.5) {
+    m *= 0.5;
+    ++e;
+  }
+  return (double)e * 0.69314718055994530942 + (double)logf((float)m);
+}
+
 __device__ __forceinline__ long long reflect_idx(long long i, long long n) {
   if (n == 1) return 0;
   const long long period = 2 * (n - 1);
@@ -45,6 +60,15 @@ __device__ __forceinline__ long long reflect_idx(long long i, long long n) {
 
 __device__ __forceinline__ int pd16(int i) { return i + (i >> 4); }  // 8-byte slots, 1 pad per 16
 
+// asynchronous 8-byte global -> shared copies (no registers held while in flight)
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all8() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // plans: V = 16 values per thread (radix-16 stages, used by the forward) or
 // V = 8 (radix-8 stages, the backward: shorter per-bin unrolls, less register
 // pressure next to the adjoint work)
@@ -62,22 +86,28 @@ template <> struct FP<2048, 8> { static constexpr int T = 256, R1 = 8, R2 = 8, R
 template <> struct FP<4096, 8> { static constexpr int T = 512, R1 = 8, R2 = 8, R3 = 8, R4 = 8, R5 = 1; };
 template <> struct FP<8192, 8> { static constexpr int T = 1024, R1 = 8, R2 = 8, R3 = 8, R4 = 8, R5 = 2; };
 
-template <int N, int VV>
+// CTA shape: NT threads, FPC = NT / T frames of N points per CTA; the frame buffers
+// of a CTA always hold NT * V points (the same dynamic shared memory for every N
+// of one multi-resolution launch)
+template <int N, int VV, int NTT>
 struct FC {
   using P = FP<N, VV>;
   static constexpr int T = P::T, V = N / T;
-  static constexpr int FPC = T >= 256 ? 1 : 256 / T;  // frames per CTA (CTA = max(256, T) threads)
-  static constexpr int NT = T * FPC;
+  static_assert(NTT % T == 0, "CTA smaller than one frame");
+  static constexpr int FPC = NTT / T;  // frames per CTA
+  static constexpr int NT = NTT;
   static constexpr int NB = N / 2 + 1;
   static constexpr int PADN = N + N / 16;              // padded frame buffer (float2)
   static constexpr size_t SMEM = sizeof(float2) * PADN * FPC;
 };
+template <int NT, int VV>
+constexpr size_t frames_smem() { return sizeof(float2) * (size_t)NT * VV * 17 / 16; }
 
 // One Stockham stage over this thread's butterflies j = tt + T i (i < V/R):
 // inputs v[i*R + m] = x[j + m N/R]; outputs y[(j/NS) NS R + j%NS + m NS] -> S
 template <int N, int VV, int R, int NS, bool INV>
 __device__ __forceinline__ void st_stage(float2* v, float2* S, int tt) {
-  constexpr int T = FC<N, VV>::T, V = FC<N, VV>::V;
+  constexpr int T = FP<N, VV>::T, V = N / T;
 #pragma unroll
   for (int i = 0; i < V / R; ++i) {
     const int j = tt + T * i, k = j % NS;
@@ -86,14 +116,14 @@ __device__ __forceinline__ void st_stage(float2* v, float2* S, int tt) {
       // w^m for m = 1..R-1: table values at m = 1 and every 4th m, products in between
       // (<= 3 roundings from a table value; a quarter of the table loads)
       const int e1 = k * (MGB_TW_N / (NS * R));
-      float2 w1 = g_tw32[e1 & (MGB_TW_N - 1)], wm = w1;
+      float2 w1 = __ldg(&g_tw32[e1 & (MGB_TW_N - 1)]), wm = w1;
       if (INV) w1.y = -w1.y;
       wm = w1;
 #pragma unroll
       for (int m = 1; m < R; ++m) {
         if (m > 1) {
           if (m % 4 == 0) {
-            wm = g_tw32[(e1 * m) & (MGB_TW_N - 1)];
+            wm = __ldg(&g_tw32[(e1 * m) & (MGB_TW_N - 1)]);
             if (INV) wm.y = -wm.y;
           } else {
             wm = cmul(wm, w1);
@@ -112,7 +142,7 @@ __device__ __forceinline__ void st_stage(float2* v, float2* S, int tt) {
 // gather the inputs of a radix-R stage from S
 template <int N, int VV, int R>
 __device__ __forceinline__ void st_gather(float2* v, const float2* S, int tt) {
-  constexpr int T = FC<N, VV>::T, V = FC<N, VV>::V;
+  constexpr int T = FP<N, VV>::T, V = N / T;
 #pragma unroll
   for (int i = 0; i < V / R; ++i)
 #pragma unroll
@@ -150,32 +180,55 @@ __device__ __forceinline__ void frame_fft(float2* v, float2* S, int tt) {
   }
 }
 
+// cos / sin of 2 pi m / 16 (m = 0..15): the window at t + m N/R is the one at t
+// rotated by a constant angle
+__device__ __forceinline__ float cos16(int m) {
+  constexpr float c[16] = {1.f, 0.92387953251f, 0.70710678119f, 0.38268343237f, 0.f, -0.38268343237f,
+                           -0.70710678119f, -0.92387953251f, -1.f, -0.92387953251f, -0.70710678119f,
+                           -0.38268343237f, 0.f, 0.38268343237f, 0.70710678119f, 0.92387953251f};
+  return c[m & 15];
+}
+__device__ __forceinline__ float sin16(int m) { return cos16(m - 4); }
+
+// periodic Hann window 0.5 - 0.5 cos(2 pi t / N) at t = t0 + m N / R (m < R, R | 16)
+template <int R>
+__device__ __forceinline__ float hann_at(float c0, float s0, int m) {
+  const int k = m * (16 / R);
+  return 0.5f - 0.5f * (c0 * cos16(k) - s0 * sin16(k));
+}
+
 // windowed, reflect-padded frame f of (xl + i xr) into the first stage's inputs
 template <int N, int VV>
 __device__ __forceinline__ void load_frame(float2* v, const float* __restrict__ xl, const float* __restrict__ xr,
                                            int Ls, int hop, int f, bool valid, int tt) {
-  constexpr int T = FC<N, VV>::T, V = FC<N, VV>::V, R = FP<N, VV>::R1;
+  constexpr int T = FP<N, VV>::T, V = N / T, R = FP<N, VV>::R1;
+  static_assert(16 % R == 0, "");
+  const long long base = (long long)f * hop - N / 2;
+  const bool interior = base >= 0 && base + N <= Ls;  // no reflected sample (most frames)
 #pragma unroll
-  for (int i = 0; i < V / R; ++i)
+  for (int i = 0; i < V / R; ++i) {
+    float s0, c0;
+    sincospif(2.f * (float)(tt + T * i) / (float)N, &s0, &c0);
 #pragma unroll
     for (int m = 0; m < R; ++m) {
       const int t = tt + T * i + m * (N / R);
       float2 z = make_float2(0.f, 0.f);
       if (valid) {
-        long long idx = (long long)f * hop + t - N / 2;
-        if (idx < 0 || idx >= Ls) idx = reflect_idx(idx, Ls);
-        const float win = 0.5f - 0.5f * cospif(2.f * (float)t / (float)N);  // periodic Hann
+        long long idx = base + t;
+        if (!interior && (idx < 0 || idx >= Ls)) idx = reflect_idx(idx, Ls);
+        const float win = hann_at<R>(c0, s0, m);
         z = make_float2(__ldg(xl + idx) * win, __ldg(xr + idx) * win);
       }
       v[i * R + m] = z;
     }
+  }
 }
 
 // spectrum in S (natural, padded) -> the 4 group magnitudes as float32,
 // md[g*NB + k] over the start of the same buffer (all reads precede the barrier)
 template <int N, int VV>
 __device__ __forceinline__ void mags_inplace(float2* S, int tt) {
-  constexpr int T = FC<N, VV>::T, NB = FC<N, VV>::NB, PER = (NB + T - 1) / T;
+  constexpr int T = FP<N, VV>::T, NB = N / 2 + 1, PER = (NB + T - 1) / T;
   float m[PER][4];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
@@ -212,12 +265,11 @@ __device__ __forceinline__ size_t mel_elems(const MgbLossRes& r) { return (size_
 // mode 0: target (write tmel, tlog, part[.,g,0] = sum mel^2)
 // mode 1: estimate (write mel, part[.,g,0] = sum |dlog|, part[.,g,1] = sum (mel - tmel)^2)
 // FPC frames per CTA; within a frame, T/4 threads per group g walk the mel bands.
-template <int N>
-__global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(MgbLossRes r, const float* __restrict__ xl,
-                                                      const float* __restrict__ xr, int Ls, int mode,
-                                                      long long sig_stride) {
-  mgb_pdl_entry();
-  using C = FC<N, 16>;
+template <int N, int NT>
+__device__ __forceinline__ void mr_fwd_body(MgbLossRes r, const float* __restrict__ xl, const float* __restrict__ xr,
+                                            int Ls, int mode, long long sig_stride, int blk, unsigned char* smraw,
+                                            double (*red)[NT], int* bst, int* blen, int* boff) {
+  using C = FC<N, 16, NT>;
   {
     const int sq = blockIdx.y;
     xl += sq * sig_stride;
@@ -230,13 +282,10 @@ __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(
     if (r.gframes) r.gframes += (size_t)sq * r.frames * 2 * N;
   }
   constexpr int T = C::T, NB = C::NB;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ double red[2][C::NT];
   const int q = threadIdx.x / T, tt = threadIdx.x % T;
-  const int f = blockIdx.x * C::FPC + q;
+  const int f = blk * C::FPC + q;
   const bool valid = f < r.frames;
   float2* S = reinterpret_cast<float2*>(smraw) + q * C::PADN;
-  __shared__ int bst[128], blen[128], boff[128];  // band tables (n_mels <= 128)
   const int nm = r.n_mels;
   for (int i = threadIdx.x; i < nm; i += C::NT) {
     bst[i] = r.band_start[i];
@@ -256,12 +305,60 @@ __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(
   const float* md = reinterpret_cast<const float*>(S);
   const int g = tt & 3;  // items idx = tt + T i: group idx % 4 (fixed per thread), band idx / 4
   double a0 = 0.0, a1 = 0.0;
-  if (valid) {
+  // one (group, band) item: its mel value -> the log terms and partial sums
+  auto item = [&](int j, double mel, double tl, double tm) {
+    const size_t o = ((size_t)g * r.frames + f) * nm + j;
+    if (mode == 0) {
+      r.tmel[o] = mel;
+      r.tlog[o] = log_mel(mel + LOG_EPS);
+      a0 += mel * mel;
+    } else {
+      r.mel[o] = mel;
+      const double dlog = log_mel(mel + LOG_EPS) - tl;
+      const double dm = mel - tm;
+      a0 += fabs(dlog);
+      a1 += dm * dm;
+    }
+  };
+  if constexpr (T >= 128) {
+    // long bands (up to 133 bins at 4096 points): every item is split in two halves
+    // summed by lanes l and l ^ 4 (idx2 = tt + T i over 8 nm half-items: half = bit 2 of
+    // tt, band = idx2 >> 3), so a thread's bands come from the low, middle and high
+    // ranges; lane (i & 1) == half finishes the item (logs shared by both lanes)
+    const int h = (tt >> 2) & 1;
+    const int iters = (8 * nm + T - 1) / T;  // the same for every lane (shuffles below)
+    for (int i = 0; i < iters; ++i) {
+      const int j = (tt >> 3) + (T / 8) * i;
+      const bool ok = valid && j < nm;
+      double m0 = 0.0, m1 = 0.0, tl = 0.0, tm = 0.0;
+      if (ok) {
+        const bool fin = (i & 1) == h;
+        if (mode != 0 && fin) {
+          const size_t o = ((size_t)g * r.frames + f) * nm + j;
+          tl = r.tlog[o];
+          tm = r.tmel[o];
+        }
+        const int len = blen[j], half = (len + 1) >> 1;
+        const int k0 = bst[j] + (h ? half : 0), n = h ? len - half : half;
+        const float* mg = md + g * NB + k0;
+        const double* bw = r.band_w + boff[j] + (h ? half : 0);
+        int k = 0;
+        for (; k + 1 < n; k += 2) {
+          m0 = fma((double)mg[k], __ldg(bw + k), m0);
+          m1 = fma((double)mg[k + 1], __ldg(bw + k + 1), m1);
+        }
+        if (k < n) m0 = fma((double)mg[k], __ldg(bw + k), m0);
+      }
+      const double part = m0 + m1;
+      const double other = __shfl_xor_sync(0xffffffffu, part, 4);
+      if (ok && (i & 1) == h) item(j, h ? other + part : part + other, tl, tm);
+    }
+  } else if (valid) {
     for (int idx = tt; idx < 4 * nm; idx += T) {
       const int j = idx >> 2;
-      const size_t o = ((size_t)g * r.frames + f) * nm + j;
       double tl = 0.0, tm = 0.0;
       if (mode != 0) {  // issued ahead of the band sum
+        const size_t o = ((size_t)g * r.frames + f) * nm + j;
         tl = r.tlog[o];
         tm = r.tmel[o];
       }
@@ -275,18 +372,7 @@ __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(
         m1 = fma((double)mg[i + 1], __ldg(bw + i + 1), m1);
       }
       if (i < len) m0 = fma((double)mg[i], __ldg(bw + i), m0);
-      const double mel = m0 + m1;
-      if (mode == 0) {
-        r.tmel[o] = mel;
-        r.tlog[o] = log(mel + LOG_EPS);
-        a0 += mel * mel;
-      } else {
-        r.mel[o] = mel;
-        const double dlog = log(mel + LOG_EPS) - tl;
-        const double dm = mel - tm;
-        a0 += fabs(dlog);
-        a1 += dm * dm;
-      }
+      item(j, m0 + m1, tl, tm);
     }
   }
   red[0][threadIdx.x] = a0;
@@ -301,6 +387,54 @@ __global__ void __launch_bounds__(FC<N, 16>::NT, 1024 / FC<N, 16>::NT) k_mr_fwd(
     r.part[((size_t)f * 4 + g) * 3 + 0] = t0;
     r.part[((size_t)f * 4 + g) * 3 + 1] = t1;
   }
+}
+
+// The resolutions of one call share a launch: CTA blockIdx.x walks the group's
+// resolutions in order (each takes ceil(frames / FPC) CTAs); sizes NLO..NHI are
+// compiled in, every CTA holds NT * 16 points (the same shared memory for each N).
+struct MrGroup {
+  unsigned mask;  // bit i: resolution i is in this launch
+};
+
+template <int NT, int VV>
+__device__ __forceinline__ int group_cta(const MgbLoss& L, MrGroup G, int& blk) {
+  int last = 31 - __clz(G.mask);
+  for (int k = 0; k < last; ++k) {
+    if (!((G.mask >> k) & 1u)) continue;
+    const MgbLossRes& r = L.res[k];
+    const int fpc = NT * VV / r.n_fft;
+    const int nb = (r.frames + fpc - 1) / fpc;
+    if (blk < nb) return k;
+    blk -= nb;
+  }
+  return last;
+}
+
+template <int NT, int NLO, int NHI>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_mr_fwd(MgbLoss L, MrGroup G, const float* __restrict__ xl,
+                                                          const float* __restrict__ xr, int mode) {
+  mgb_pdl_entry();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double red[2][NT];
+  __shared__ int bst[128], blen[128], boff[128];  // band tables (n_mels <= 128)
+  int blk = blockIdx.x;
+  const int ri = group_cta<NT, 16>(L, G, blk);
+  const MgbLossRes& r = L.res[ri];
+#define MR_FWD_CASE(n)                                                                                   \
+  case n:                                                                                                \
+    if constexpr (n >= NLO && n <= NHI)                                                                  \
+      mr_fwd_body<n, NT>(r, xl, xr, L.Ls, mode, L.batch > 1 ? L.sig_stride : 0, blk, smraw, red, bst, blen, \
+                         boff);                                                                          \
+    break;
+  switch (r.n_fft) {
+    MR_FWD_CASE(256)
+    MR_FWD_CASE(512)
+    MR_FWD_CASE(1024)
+    MR_FWD_CASE(2048)
+    MR_FWD_CASE(4096)
+    MR_FWD_CASE(8192)
+  }
+#undef MR_FWD_CASE
 }
 
 // stats layout per (res, group): [tnorm, slog, sdiff2, dn]
@@ -349,16 +483,12 @@ __global__ void k_mr_total(MgbLoss L) {
 // backward: dmel, the frame spectrum the forward kept, d|X| through the CSC projection,
 // dX per group -> packed Hermitian adjoint of both channels, one inverse FFT,
 // windowed frame adjoints to gframes (float32) for the overlap-add gather.
-template <int N>
-__global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(MgbLossRes r, const double* __restrict__ stats,
-                                                                       MgbLoss L, const float* __restrict__ xl,
-                                                                       const float* __restrict__ xr, int Ls) {
-  mgb_pdl_entry();
-  using C = FC<N, 8>;
+template <int N, int NT>
+__device__ __forceinline__ void mr_bwd_body(MgbLossRes r, const double* __restrict__ stats, const MgbLoss& L, int blk,
+                                            unsigned char* smraw, float (*dmel)[4][128]) {
+  using C = FC<N, 8, NT>;
   {
     const int sq = blockIdx.y;
-    xl += sq * L.sig_stride;
-    xr += sq * L.sig_stride;
     const size_t me = sq * mel_elems(r);
     r.tmel += me;
     r.tlog += me;
@@ -367,41 +497,71 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
     stats += (size_t)sq * L.n_res * 16;
   }
   constexpr int T = C::T, NB = C::NB, PER = (NB + T - 1) / T;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ float dmel[C::FPC][4][128];
   const int q = threadIdx.x / T, tt = threadIdx.x % T;
-  const int f = blockIdx.x * C::FPC + q;
+  const int f = blk * C::FPC + q;
   const bool valid = f < r.frames;
   float2* S = reinterpret_cast<float2*>(smraw) + q * C::PADN;
   const int nm = r.n_mels;
   float2 v[C::V];
-  // the frame spectrum of the forward pass (natural order) -> S
+  // the frame spectrum of the forward pass (natural order) -> S by asynchronous copies
+  // that overlap the dmel loop
   if (valid) {
     const float2* gs = reinterpret_cast<const float2*>(r.gframes + (size_t)f * 2 * N);
-    for (int t = tt; t < N; t += T) S[pd16(t)] = gs[t];
+#pragma unroll
+    for (int i = 0; i < C::V; ++i) cp_async8(S + pd16(tt + i * T), gs + tt + i * T);
   }
   if (valid) {
-    for (int idx = tt; idx < 4 * nm; idx += T) {
-      const int g = idx / nm, j = idx % nm;
-      const size_t o = ((size_t)g * r.frames + f) * nm + j;
-      const double mel = r.mel[o], tm = r.tmel[o];
-      // sign of the log difference = sign(mel - tmel) (log is monotonic); the logs are
-      // only evaluated when rounding could decide it
-      const double dm = mel - tm;
-      double sg;
-      if (fabs(dm) > 1e-12 * fmax(fabs(mel), fabs(tm))) {
-        sg = dm > 0.0 ? 1.0 : -1.0;
-      } else {
-        const double dlog = log(mel + LOG_EPS) - r.tlog[o];
-        sg = (dlog > 0.0) ? 1.0 : (dlog < 0.0 ? -1.0 : 0.0);
-      }
+    // dmel = w_g sg / (frames (mel + eps)) + w_g (mel - tmel) / (dn tn): the difference
+    // in float64, the quotients in float32 (dmel is float32)
+    float c1[4], c2[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
       const double* st = stats + (size_t)g * 4;
-      const double dn = st[3], tn = st[0];
-      double v = sg / ((double)r.frames * (mel + LOG_EPS));
-      if (dn > 0.0) v += dm / (dn * tn);
-      dmel[q][g][j] = (float)(L.group_w[g] * v);
+      c1[g] = __fdividef((float)L.group_w[g], (float)r.frames);
+      c2[g] = st[3] > 0.0 ? __fdividef((float)L.group_w[g], (float)(st[3] * st[0])) : 0.f;
+    }
+    int g = 0, j = tt;  // (g, j) = divmod(idx, nm), stepped without divisions
+    while (j >= nm) j -= nm, ++g;
+    constexpr int U = 3;  // items per round: their loads issued together
+    for (int idx0 = tt; idx0 < 4 * nm; idx0 += U * T) {
+      double mel[U], tm[U];
+      int gs_[U], js_[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        gs_[u] = g;
+        js_[u] = j;
+        mel[u] = tm[u] = 0.0;
+        if (idx0 + u * T < 4 * nm) {
+          const size_t o = ((size_t)g * r.frames + f) * nm + j;
+          mel[u] = r.mel[o];
+          tm[u] = r.tmel[o];
+        }
+        j += T;
+        while (j >= nm) j -= nm, ++g;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (idx0 + u * T >= 4 * nm) break;
+        const int gu = gs_[u], ju = js_[u];
+        // sign of the log difference = sign(mel - tmel) (log is monotonic); the logs are
+        // only evaluated when rounding could decide it
+        const double dm = mel[u] - tm[u];
+        float sg;
+        if (fabs(dm) > 1e-12 * fmax(fabs(mel[u]), fabs(tm[u]))) {
+          sg = dm > 0.0 ? 1.f : -1.f;
+        } else {
+          const double dlog = log_mel(mel[u] + LOG_EPS) - r.tlog[((size_t)gu * r.frames + f) * nm + ju];
+          sg = (dlog > 0.0) ? 1.f : (dlog < 0.0 ? -1.f : 0.f);
+        }
+        float cg1 = c1[0], cg2 = c2[0];
+#pragma unroll
+        for (int gg = 1; gg < 4; ++gg)
+          if (gu == gg) cg1 = c1[gg], cg2 = c2[gg];
+        dmel[q][gu][ju] = __fdividef(sg * cg1, (float)(mel[u] + LOG_EPS)) + cg2 * (float)dm;
+      }
     }
   }
+  cp_async_wait_all8();
   __syncthreads();  // publishes the spectrum and dmel
   float2 dl[PER], dr[PER];
 #pragma unroll
@@ -416,14 +576,30 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
       X[1] = make_float2(d.y, -d.x);
       X[2] = make_float2(X[0].x + X[1].x, X[0].y + X[1].y);
       X[3] = make_float2(X[0].x - X[1].x, X[0].y - X[1].y);
-      const int b0 = r.bin_start[k], bl = r.bin_len[k];
+      const int b0 = __ldg(r.bin_start + k), bl = __ldg(r.bin_len + k);
+      float dmg[4] = {0.f, 0.f, 0.f, 0.f};
+      // the bin's (band, weight) entries, once for all 4 groups (a bin sits in at most
+      // two or three overlapping mel bands: the first three unrolled, loads together)
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        if (e < bl) {
+          const int band = __ldg(r.bin_band + b0 + e);
+          const float w = (float)__ldg(r.bin_w + b0 + e);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) dmg[g] = fmaf(dmel[q][g][band], w, dmg[g]);
+        }
+      }
+      for (int e = 3; e < bl; ++e) {
+        const int band = __ldg(r.bin_band + b0 + e);
+        const float w = (float)__ldg(r.bin_w + b0 + e);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) dmg[g] = fmaf(dmel[q][g][band], w, dmg[g]);
+      }
       float2 dX[4];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        double dm = 0.0;
-        for (int e = 0; e < bl; ++e) dm = fma((double)dmel[q][g][r.bin_band[b0 + e]], r.bin_w[b0 + e], dm);
-        const float mag = sqrtf(X[g].x * X[g].x + X[g].y * X[g].y);
-        const float sc = mag == 0.f ? 0.f : (float)dm / mag;
+        const float m2 = X[g].x * X[g].x + X[g].y * X[g].y;
+        const float sc = m2 == 0.f ? 0.f : dmg[g] * rsqrtf(m2);
         dX[g] = make_float2(sc * X[g].x, sc * X[g].y);
       }
       dl[i] = make_float2(dX[0].x + dX[2].x + dX[3].x, dX[0].y + dX[2].y + dX[3].y);
@@ -452,24 +628,47 @@ __global__ void __launch_bounds__(FC<N, 8>::NT, 1024 / FC<N, 8>::NT) k_mr_bwd(Mg
   frame_fft<N, 8, true>(v, S, tt);
   if (!valid) return;
   float* gf = r.gframes + (size_t)f * 2 * N;
-  for (int t = tt; t < N; t += T) {
-    const float win = 0.5f - 0.5f * cospif(2.f * (float)t / (float)N);
+  float s0, c0;
+  sincospif(2.f * (float)tt / (float)N, &s0, &c0);
+  static_assert(16 % C::V == 0, "");
+#pragma unroll
+  for (int i = 0; i < C::V; ++i) {  // t = tt + i T = tt + i N / V
+    const int t = tt + i * T;
+    const float win = hann_at<C::V>(c0, s0, i);
     const float2 z = S[pd16(t)];
     gf[t] = z.x * win;
     gf[N + t] = z.y * win;
   }
 }
 
+template <int NT, int NLO, int NHI>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_mr_bwd(MgbLoss L, MrGroup G) {
+  mgb_pdl_entry();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ float dmel[NT * 8 / NLO][4][128];
+  int blk = blockIdx.x;
+  const int ri = group_cta<NT, 8>(L, G, blk);
+  const MgbLossRes& r = L.res[ri];
+#define MR_BWD_CASE(n)                                                           \
+  case n:                                                                        \
+    if constexpr (n >= NLO && n <= NHI) mr_bwd_body<n, NT>(r, L.stats + (size_t)ri * 16, L, blk, smraw, dmel); \
+    break;
+  switch (r.n_fft) {
+    MR_BWD_CASE(256)
+    MR_BWD_CASE(512)
+    MR_BWD_CASE(1024)
+    MR_BWD_CASE(2048)
+    MR_BWD_CASE(4096)
+    MR_BWD_CASE(8192)
+  }
+#undef MR_BWD_CASE
+}
+
 // dL/dy[t] = sum over resolutions of the frame adjoints covering the padded
 // position t + n/2, plus the reflect-pad adjoint near both ends (gather, no atomics)
-__global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ gl, float* __restrict__ gr) {
-  mgb_pdl_entry();
-  const int Ls = L.Ls, sq = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= Ls) return;
-  gl += sq * L.sig_stride;
-  gr += sq * L.sig_stride;
-  double al = 0.0, ar = 0.0;
+__device__ __forceinline__ void ola_sample(const MgbLoss& L, int sq, int t, double& al, double& ar) {
+  const int Ls = L.Ls;
+  al = 0.0, ar = 0.0;
   for (int ri = 0; ri < L.n_res; ++ri) {
     const MgbLossRes& r = L.res[ri];
     const int n = r.n_fft, pad = n / 2, lh = __ffs(r.hop) - 1, ln = __ffs(n) - 1;
@@ -481,20 +680,51 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
       if (cls == 1 && (t == 0 || t == Ls - 1)) break;  // -t is the +t class
       const int base = cls ? -t : t, num = -pad - base;
       const int k0 = num <= 0 ? -((-num) / period) : (num + period - 1) / period;
-    for (int q = base + k0 * period; q < Ls + pad; q += period) {
-      const int p = q + pad;
-      int fhi = p >> lh;
-      if (fhi > r.frames - 1) fhi = r.frames - 1;
-      const int flo = (p - n + 1 <= 0) ? 0 : ((p - n + r.hop) >> lh);  // ceil((p - n + 1) / hop)
-      for (int f = flo; f <= fhi; ++f) {
-        const int o = p - (f << lh);
-        if (o < 0 || o >= n) continue;
-        const float* gfp = r.gframes + (size_t)sq * r.frames * 2 * n + ((size_t)f << (ln + 1));
-        al += __ldg(gfp + o);
-        ar += __ldg(gfp + n + o);
+      for (int q = base + k0 * period; q < Ls + pad; q += period) {
+        const int p = q + pad;
+        int fhi = p >> lh;
+        if (fhi > r.frames - 1) fhi = r.frames - 1;
+        const int flo = (p - n + 1 <= 0) ? 0 : ((p - n + r.hop) >> lh);  // ceil((p - n + 1) / hop)
+        for (int f = flo; f <= fhi; ++f) {
+          const int o = p - (f << lh);
+          if (o < 0 || o >= n) continue;
+          const float* gfp = r.gframes + (size_t)sq * r.frames * 2 * n + ((size_t)f << (ln + 1));
+          al += __ldg(gfp + o);
+          ar += __ldg(gfp + n + o);
+        }
       }
     }
+  }
+}
+
+// One sample per thread.  Away from both ends (no reflected position) only q = t
+// contributes: the frames covering t + n/2, without the reflection-class search.
+__global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ gl, float* __restrict__ gr,
+                                                int pad_max) {
+  mgb_pdl_entry();
+  const int Ls = L.Ls, sq = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Ls) return;
+  gl += sq * L.sig_stride;
+  gr += sq * L.sig_stride;
+  double al = 0.0, ar = 0.0;
+  if (t > pad_max && t < Ls - 2 - pad_max) {
+    for (int ri = 0; ri < L.n_res; ++ri) {
+      const MgbLossRes& r = L.res[ri];
+      const int n = r.n_fft, lh = __ffs(r.hop) - 1, ln = __ffs(n) - 1;
+      const int p = t + n / 2;
+      int fhi = p >> lh;
+      if (fhi > r.frames - 1) fhi = r.frames - 1;
+      const int flo = (p - n + 1 <= 0) ? 0 : ((p - n + r.hop) >> lh);
+      const float* gb = r.gframes + (size_t)sq * r.frames * 2 * n + p;
+      for (int f = flo; f <= fhi; ++f) {
+        const float* gfp = gb + ((size_t)f << (ln + 1)) - (f << lh);
+        al += __ldg(gfp);
+        ar += __ldg(gfp + n);
+      }
     }
+  } else {
+    ola_sample(L, sq, t, al, ar);
   }
   gl[t] = (float)al;
   gr[t] = (float)ar;
@@ -502,50 +732,62 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
 
 inline int nbatch(const MgbLoss& L) { return L.batch > 1 ? L.batch : 1; }
 
-template <int N>
-int launch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, int mode, int nb, long long stride,
-               cudaStream_t st) {
-  using C = FC<N, 16>;
-  mgb_launch(k_mr_fwd<N>, dim3((r.frames + C::FPC - 1) / C::FPC, nb), dim3(C::NT), C::SMEM, st, r, xl, xr, Ls, mode,
-             stride);
+// kernels of a call: every resolution with n <= 4096 in one launch, an 8192-point one alone
+constexpr int kFwdNT = 256, kBwdNT = 512;
+#define MR_FWD_SMALL k_mr_fwd<kFwdNT, 256, 4096>
+#define MR_FWD_BIG k_mr_fwd<512, 8192, 8192>
+#define MR_BWD_SMALL k_mr_bwd<kBwdNT, 256, 4096>
+#define MR_BWD_BIG k_mr_bwd<1024, 8192, 8192>
+
+// the launch groups of a call: group 0 = the resolutions up to 4096 points (may be
+// empty), then one group per 8192-point resolution
+int make_groups(const MgbLoss& L, MrGroup* G) {
+  int ng = 0;
+  unsigned small = 0;
+  for (int i = 0; i < L.n_res; ++i) {
+    if (L.res[i].n_fft <= 4096) small |= 1u << i;
+  }
+  if (small) G[ng++].mask = small;
+  for (int i = 0; i < L.n_res; ++i) {
+    if (L.res[i].n_fft > 4096) G[ng++].mask = 1u << i;
+  }
+  return ng;
+}
+
+int group_ctas(const MgbLoss& L, const MrGroup& G, int nt, int vv) {
+  int n = 0;
+  for (int k = 0; k < L.n_res; ++k) {
+    if (!((G.mask >> k) & 1u)) continue;
+    const MgbLossRes& r = L.res[k];
+    const int fpc = nt * vv / r.n_fft;
+    n += (r.frames + fpc - 1) / fpc;
+  }
+  return n;
+}
+
+int first_n(const MgbLoss& L, const MrGroup& G) { return L.res[__builtin_ctz(G.mask)].n_fft; }
+
+int launch_fwd(const MgbLoss& L, const MrGroup& G, const float* xl, const float* xr, int mode, cudaStream_t st) {
+  if (first_n(L, G) <= 4096) {
+    mgb_launch(MR_FWD_SMALL, dim3(group_ctas(L, G, kFwdNT, 16), nbatch(L)), dim3(kFwdNT), frames_smem<kFwdNT, 16>(),
+               st, L, G, xl, xr, mode);
+  } else {
+    mgb_launch(MR_FWD_BIG, dim3(group_ctas(L, G, 512, 16), nbatch(L)), dim3(512), frames_smem<512, 16>(), st, L, G,
+               xl, xr, mode);
+  }
   MGB_CHECK_LAUNCH();
   return 0;
 }
 
-template <int N>
-int launch_bwd(const MgbLossRes& r, const double* stats, const MgbLoss& L, const float* xl, const float* xr,
-               int Ls, cudaStream_t st) {
-  using C = FC<N, 8>;
-  mgb_launch(k_mr_bwd<N>, dim3((r.frames + C::FPC - 1) / C::FPC, nbatch(L)), dim3(C::NT), C::SMEM, st, r, stats, L, xl,
-             xr, Ls);
+int launch_bwd(const MgbLoss& L, const MrGroup& G, cudaStream_t st) {
+  if (first_n(L, G) <= 4096) {
+    mgb_launch(MR_BWD_SMALL, dim3(group_ctas(L, G, kBwdNT, 8), nbatch(L)), dim3(kBwdNT), frames_smem<kBwdNT, 8>(), st,
+               L, G);
+  } else {
+    mgb_launch(MR_BWD_BIG, dim3(group_ctas(L, G, 1024, 8), nbatch(L)), dim3(1024), frames_smem<1024, 8>(), st, L, G);
+  }
   MGB_CHECK_LAUNCH();
   return 0;
-}
-
-int dispatch_fwd(const MgbLossRes& r, const float* xl, const float* xr, int Ls, int mode, int nb, long long stride,
-                 cudaStream_t st) {
-  switch (r.n_fft) {
-    case 256: return launch_fwd<256>(r, xl, xr, Ls, mode, nb, stride, st);
-    case 512: return launch_fwd<512>(r, xl, xr, Ls, mode, nb, stride, st);
-    case 1024: return launch_fwd<1024>(r, xl, xr, Ls, mode, nb, stride, st);
-    case 2048: return launch_fwd<2048>(r, xl, xr, Ls, mode, nb, stride, st);
-    case 4096: return launch_fwd<4096>(r, xl, xr, Ls, mode, nb, stride, st);
-    case 8192: return launch_fwd<8192>(r, xl, xr, Ls, mode, nb, stride, st);
-    default: return 1;
-  }
-}
-
-int dispatch_bwd(const MgbLossRes& r, const double* stats, const MgbLoss& L, const float* xl, const float* xr,
-                 int Ls, cudaStream_t st) {
-  switch (r.n_fft) {
-    case 256: return launch_bwd<256>(r, stats, L, xl, xr, Ls, st);
-    case 512: return launch_bwd<512>(r, stats, L, xl, xr, Ls, st);
-    case 1024: return launch_bwd<1024>(r, stats, L, xl, xr, Ls, st);
-    case 2048: return launch_bwd<2048>(r, stats, L, xl, xr, Ls, st);
-    case 4096: return launch_bwd<4096>(r, stats, L, xl, xr, Ls, st);
-    case 8192: return launch_bwd<8192>(r, stats, L, xl, xr, Ls, st);
-    default: return 1;
-  }
 }
 
 int check_loss(const MgbLoss* L) {
@@ -554,15 +796,17 @@ int check_loss(const MgbLoss* L) {
   for (int i = 0; i < L->n_res; ++i) {
     const MgbLossRes& r = L->res[i];
     if (r.n_mels > 128) return 1;
+    if (r.n_fft < 256 || r.n_fft > 8192 || (r.n_fft & (r.n_fft - 1))) return 1;
   }
   return 0;
 }
 
-template <int N>
 int loss_attrs() {
   int rc = 0;
-  rc |= cudaFuncSetAttribute(k_mr_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC<N, 16>::SMEM);
-  rc |= cudaFuncSetAttribute(k_mr_bwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC<N, 8>::SMEM);
+  rc |= cudaFuncSetAttribute(MR_FWD_SMALL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)frames_smem<kFwdNT, 16>());
+  rc |= cudaFuncSetAttribute(MR_FWD_BIG, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)frames_smem<512, 16>());
+  rc |= cudaFuncSetAttribute(MR_BWD_SMALL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)frames_smem<kBwdNT, 8>());
+  rc |= cudaFuncSetAttribute(MR_BWD_BIG, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)frames_smem<1024, 8>());
   return rc;
 }
 
@@ -629,17 +873,15 @@ int fork_res(int n, cudaStream_t st, F fn) {
 int mgb_loss_init() {
   if (side_init()) return 2;
   // smem attributes set eagerly (outside any stream capture)
-  int rc = loss_attrs<256>() | loss_attrs<512>() | loss_attrs<1024>() | loss_attrs<2048>() | loss_attrs<4096>() |
-           loss_attrs<8192>();
-  return rc ? 2 : 0;
+  return loss_attrs() ? 2 : 0;
 }
 
 extern "C" int mgb_mrstft_target(const MgbLoss* L, const float* tl, const float* tr, void* stream) {
   if (int rc = check_loss(L)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) {
-        return dispatch_fwd(L->res[i], tl, tr, L->Ls, 0, nbatch(*L), L->sig_stride, s);
-      }))
+  MrGroup G[8];
+  const int ng = make_groups(*L, G);
+  if (int rc = fork_res(ng, st, [&](int i, cudaStream_t s) { return launch_fwd(*L, G[i], tl, tr, 0, s); }))
     return rc;
   mgb_launch(k_mr_finalize, dim3(4 * L->n_res, nbatch(*L)), dim3(1024), 0, st, *L, 0);
   MGB_CHECK_LAUNCH();
@@ -649,9 +891,9 @@ extern "C" int mgb_mrstft_target(const MgbLoss* L, const float* tl, const float*
 extern "C" int mgb_mrstft_forward(const MgbLoss* L, const float* yl, const float* yr, void* stream) {
   if (int rc = check_loss(L)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) {
-        return dispatch_fwd(L->res[i], yl, yr, L->Ls, 1, nbatch(*L), L->sig_stride, s);
-      }))
+  MrGroup G[8];
+  const int ng = make_groups(*L, G);
+  if (int rc = fork_res(ng, st, [&](int i, cudaStream_t s) { return launch_fwd(*L, G[i], yl, yr, 1, s); }))
     return rc;
   mgb_launch(k_mr_finalize, dim3(4 * L->n_res, nbatch(*L)), dim3(1024), 0, st, *L, 1);
   MGB_CHECK_LAUNCH();
@@ -664,11 +906,13 @@ extern "C" int mgb_mrstft_backward(const MgbLoss* L, const float* yl, const floa
                                    void* stream) {
   if (int rc = check_loss(L)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (int rc = fork_res(L->n_res, st, [&](int i, cudaStream_t s) {
-        return dispatch_bwd(L->res[i], L->stats + (size_t)i * 16, *L, yl, yr, L->Ls, s);
-      }))
+  MrGroup G[8];
+  const int ng = make_groups(*L, G);
+  if (int rc = fork_res(ng, st, [&](int i, cudaStream_t s) { return launch_bwd(*L, G[i], s); }))
     return rc;
-  mgb_launch(k_mr_ola, dim3((L->Ls + 255) / 256, nbatch(*L)), dim3(256), 0, st, *L, gl, gr);
+  int pad_max = 0;
+  for (int i = 0; i < L->n_res; ++i) pad_max = pad_max > L->res[i].n_fft / 2 ? pad_max : L->res[i].n_fft / 2;
+  mgb_launch(k_mr_ola, dim3((L->Ls + 255) / 256, nbatch(*L)), dim3(256), 0, st, *L, gl, gr, pad_max);
   MGB_CHECK_LAUNCH();
   return 0;
 }
