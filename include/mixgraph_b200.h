@@ -155,9 +155,9 @@ typedef struct MgbLossRes {
   const int* bin_len;           /* [n_bins] */
   const int* bin_band;          /* transposed (CSC) band indices */
   const double* bin_w;          /* transposed weights */
-  double* tmel;                 /* (4, frames, n_mels) target mel */
-  double* tlog;                 /* (4, frames, n_mels) log(target mel + 1e-7) */
-  double* mel;                  /* (4, frames, n_mels) estimate mel (fwd -> bwd) */
+  double* tmel;                 /* (frames, n_mels, 4 groups) target mel */
+  double* tlog;                 /* (frames, n_mels, 4) log(target mel + 1e-7) */
+  double* mel;                  /* (frames, n_mels, 4) estimate mel (fwd -> bwd) */
   double* part;                 /* (frames, 4, 3) per-frame partial sums */
   float* gframes;               /* (frames, 2, n_fft): the forward's frame spectra, then the backward's
                                    frame adjoints; NULL for a forward-only loss */

@@ -103,6 +103,29 @@ struct FC {
 template <int NT, int VV>
 constexpr size_t frames_smem() { return sizeof(float2) * (size_t)NT * VV * 17 / 16; }
 
+// barrier over the T threads of frame q of the CTA: the warp's when a frame fits in one
+// warp, a named barrier per frame when it spans several, the CTA's when it is the whole
+// CTA.  Frames proceed independently (no convoy behind the slowest frame of the CTA).
+template <int T, int NT>
+__device__ __forceinline__ void frame_sync(int q) {
+  if constexpr (T <= 32) {
+    __syncwarp();
+  } else if constexpr (T >= NT) {
+    __syncthreads();
+  } else {
+    // constant barrier ids (ptxas reserves only the ids it sees: NT / T + 1 per CTA)
+    static_assert(NT / T <= 8, "named barriers 1..8");
+    switch (q) {
+#define MR_BAR(i)                                                            \
+  case i:                                                                    \
+    if constexpr (i < NT / T) asm volatile("bar.sync %0, %1;\n" ::"n"(i + 1), "n"(T) : "memory"); \
+    break;
+      MR_BAR(0) MR_BAR(1) MR_BAR(2) MR_BAR(3) MR_BAR(4) MR_BAR(5) MR_BAR(6) MR_BAR(7)
+#undef MR_BAR
+    }
+  }
+}
+
 // One Stockham stage over this thread's butterflies j = tt + T i (i < V/R):
 // inputs v[i*R + m] = x[j + m N/R]; outputs y[(j/NS) NS R + j%NS + m NS] -> S
 template <int N, int VV, int R, int NS, bool INV>
@@ -150,33 +173,33 @@ __device__ __forceinline__ void st_gather(float2* v, const float2* S, int tt) {
 }
 
 // all stages after the first stage's inputs are in v; result (natural order) in S.
-// Contains __syncthreads: every thread of the CTA must call it.
-template <int N, int VV, bool INV>
-__device__ __forceinline__ void frame_fft(float2* v, float2* S, int tt) {
+// Contains frame barriers: every thread of frame q must call it.
+template <int N, int VV, bool INV, int NT>
+__device__ __forceinline__ void frame_fft(float2* v, float2* S, int tt, int q) {
   using P = FP<N, VV>;
   st_stage<N, VV, P::R1, 1, INV>(v, S, tt);
-  __syncthreads();
+  frame_sync<P::T, NT>(q);
   st_gather<N, VV, P::R2>(v, S, tt);
-  __syncthreads();
+  frame_sync<P::T, NT>(q);
   st_stage<N, VV, P::R2, P::R1, INV>(v, S, tt);
-  __syncthreads();
+  frame_sync<P::T, NT>(q);
   if constexpr (P::R3 > 1) {
     st_gather<N, VV, P::R3>(v, S, tt);
-    __syncthreads();
+    frame_sync<P::T, NT>(q);
     st_stage<N, VV, P::R3, P::R1 * P::R2, INV>(v, S, tt);
-    __syncthreads();
+    frame_sync<P::T, NT>(q);
   }
   if constexpr (P::R4 > 1) {
     st_gather<N, VV, P::R4>(v, S, tt);
-    __syncthreads();
+    frame_sync<P::T, NT>(q);
     st_stage<N, VV, P::R4, P::R1 * P::R2 * P::R3, INV>(v, S, tt);
-    __syncthreads();
+    frame_sync<P::T, NT>(q);
   }
   if constexpr (P::R5 > 1) {
     st_gather<N, VV, P::R5>(v, S, tt);
-    __syncthreads();
+    frame_sync<P::T, NT>(q);
     st_stage<N, VV, P::R5, P::R1 * P::R2 * P::R3 * P::R4, INV>(v, S, tt);
-    __syncthreads();
+    frame_sync<P::T, NT>(q);
   }
 }
 
@@ -226,8 +249,8 @@ __device__ __forceinline__ void load_frame(float2* v, const float* __restrict__ 
 
 // spectrum in S (natural, padded) -> the 4 group magnitudes as float32,
 // md[g*NB + k] over the start of the same buffer (all reads precede the barrier)
-template <int N, int VV>
-__device__ __forceinline__ void mags_inplace(float2* S, int tt) {
+template <int N, int VV, int NT>
+__device__ __forceinline__ void mags_inplace(float2* S, int tt, int q) {
   constexpr int T = FP<N, VV>::T, NB = N / 2 + 1, PER = (NB + T - 1) / T;
   float m[PER][4];
 #pragma unroll
@@ -244,7 +267,7 @@ __device__ __forceinline__ void mags_inplace(float2* S, int tt) {
       m[i][3] = sqrtf((a.x - bb.x) * (a.x - bb.x) + (a.y - bb.y) * (a.y - bb.y));
     }
   }
-  __syncthreads();
+  frame_sync<FP<N, VV>::T, NT>(q);
   float* md = reinterpret_cast<float*>(S);
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
@@ -254,7 +277,7 @@ __device__ __forceinline__ void mags_inplace(float2* S, int tt) {
       for (int g = 0; g < 4; ++g) md[g * NB + k] = m[i][g];
     }
   }
-  __syncthreads();
+  frame_sync<FP<N, VV>::T, NT>(q);
 }
 
 // Several signals (songs) per call: signal q = blockIdx.y starts sig_stride floats after
@@ -292,22 +315,24 @@ __device__ __forceinline__ void mr_fwd_body(MgbLossRes r, const float* __restric
     blen[i] = r.band_len[i];
     boff[i] = r.band_off[i];
   }
+  __syncthreads();  // publishes the band tables (the frames' barriers below are their own)
   float2 v[C::V];
   load_frame<N, 16>(v, xl, xr, Ls, r.hop, f, valid, tt);
-  frame_fft<N, 16, false>(v, S, tt);  // (its barriers publish the band tables)
+  frame_fft<N, 16, false, NT>(v, S, tt, q);
   if (mode != 0 && r.gframes && valid) {
     // the estimate's frame spectrum, kept for the backward (which overwrites the slot
     // with the frame's adjoint): the backward does not transform the frame again
     float2* gs = reinterpret_cast<float2*>(r.gframes + (size_t)f * 2 * N);
-    for (int t = tt; t < N; t += T) gs[t] = S[pd16(t)];
+#pragma unroll
+    for (int i = 0; i < C::V; ++i) gs[tt + i * T] = S[pd16(tt + i * T)];
   }
-  mags_inplace<N, 16>(S, tt);
+  mags_inplace<N, 16, NT>(S, tt, q);
   const float* md = reinterpret_cast<const float*>(S);
   const int g = tt & 3;  // items idx = tt + T i: group idx % 4 (fixed per thread), band idx / 4
   double a0 = 0.0, a1 = 0.0;
   // one (group, band) item: its mel value -> the log terms and partial sums
   auto item = [&](int j, double mel, double tl, double tm) {
-    const size_t o = ((size_t)g * r.frames + f) * nm + j;
+    const size_t o = ((size_t)f * nm + j) * 4 + g;
     if (mode == 0) {
       r.tmel[o] = mel;
       r.tlog[o] = log_mel(mel + LOG_EPS);
@@ -334,7 +359,7 @@ __device__ __forceinline__ void mr_fwd_body(MgbLossRes r, const float* __restric
       if (ok) {
         const bool fin = (i & 1) == h;
         if (mode != 0 && fin) {
-          const size_t o = ((size_t)g * r.frames + f) * nm + j;
+          const size_t o = ((size_t)f * nm + j) * 4 + g;
           tl = r.tlog[o];
           tm = r.tmel[o];
         }
@@ -358,7 +383,7 @@ __device__ __forceinline__ void mr_fwd_body(MgbLossRes r, const float* __restric
       const int j = idx >> 2;
       double tl = 0.0, tm = 0.0;
       if (mode != 0) {  // issued ahead of the band sum
-        const size_t o = ((size_t)g * r.frames + f) * nm + j;
+        const size_t o = ((size_t)f * nm + j) * 4 + g;
         tl = r.tlog[o];
         tm = r.tmel[o];
       }
@@ -377,7 +402,7 @@ __device__ __forceinline__ void mr_fwd_body(MgbLossRes r, const float* __restric
   }
   red[0][threadIdx.x] = a0;
   red[1][threadIdx.x] = a1;
-  __syncthreads();
+  frame_sync<T, NT>(q);
   if (valid && tt < 4) {  // fixed-order sum over the T/4 threads of (frame, group)
     double t0 = 0.0, t1 = 0.0;
     for (int i = threadIdx.x; i < (q + 1) * T; i += 4) {
@@ -485,7 +510,7 @@ __global__ void k_mr_total(MgbLoss L) {
 // windowed frame adjoints to gframes (float32) for the overlap-add gather.
 template <int N, int NT>
 __device__ __forceinline__ void mr_bwd_body(MgbLossRes r, const double* __restrict__ stats, const MgbLoss& L, int blk,
-                                            unsigned char* smraw, float (*dmel)[4][128]) {
+                                            unsigned char* smraw, float4 (*dmel)[128]) {
   using C = FC<N, 8, NT>;
   {
     const int sq = blockIdx.y;
@@ -513,36 +538,29 @@ __device__ __forceinline__ void mr_bwd_body(MgbLossRes r, const double* __restri
   if (valid) {
     // dmel = w_g sg / (frames (mel + eps)) + w_g (mel - tmel) / (dn tn): the difference
     // in float64, the quotients in float32 (dmel is float32)
-    float c1[4], c2[4];
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const double* st = stats + (size_t)g * 4;
-      c1[g] = __fdividef((float)L.group_w[g], (float)r.frames);
-      c2[g] = st[3] > 0.0 ? __fdividef((float)L.group_w[g], (float)(st[3] * st[0])) : 0.f;
-    }
-    int g = 0, j = tt;  // (g, j) = divmod(idx, nm), stepped without divisions
-    while (j >= nm) j -= nm, ++g;
+    // items idx = tt + T i: group g = idx % 4 (fixed per thread: T is a multiple of 4),
+    // band idx / 4; the (frame, band, group) layout makes the loads contiguous
+    const int g = tt & 3;
+    const double* st = stats + (size_t)g * 4;
+    const float cg1 = __fdividef((float)L.group_w[g], (float)r.frames);
+    const float cg2 = st[3] > 0.0 ? __fdividef((float)L.group_w[g], (float)(st[3] * st[0])) : 0.f;
+    const double* mrow = r.mel + (size_t)f * nm * 4;
+    const double* trow = r.tmel + (size_t)f * nm * 4;
     constexpr int U = 3;  // items per round: their loads issued together
     for (int idx0 = tt; idx0 < 4 * nm; idx0 += U * T) {
       double mel[U], tm[U];
-      int gs_[U], js_[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        gs_[u] = g;
-        js_[u] = j;
         mel[u] = tm[u] = 0.0;
         if (idx0 + u * T < 4 * nm) {
-          const size_t o = ((size_t)g * r.frames + f) * nm + j;
-          mel[u] = r.mel[o];
-          tm[u] = r.tmel[o];
+          mel[u] = mrow[idx0 + u * T];
+          tm[u] = trow[idx0 + u * T];
         }
-        j += T;
-        while (j >= nm) j -= nm, ++g;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (idx0 + u * T >= 4 * nm) break;
-        const int gu = gs_[u], ju = js_[u];
+        const int idx = idx0 + u * T;
+        if (idx >= 4 * nm) break;
         // sign of the log difference = sign(mel - tmel) (log is monotonic); the logs are
         // only evaluated when rounding could decide it
         const double dm = mel[u] - tm[u];
@@ -550,25 +568,23 @@ __device__ __forceinline__ void mr_bwd_body(MgbLossRes r, const double* __restri
         if (fabs(dm) > 1e-12 * fmax(fabs(mel[u]), fabs(tm[u]))) {
           sg = dm > 0.0 ? 1.f : -1.f;
         } else {
-          const double dlog = log_mel(mel[u] + LOG_EPS) - r.tlog[((size_t)gu * r.frames + f) * nm + ju];
+          const double dlog = log_mel(mel[u] + LOG_EPS) - r.tlog[(size_t)f * nm * 4 + idx];
           sg = (dlog > 0.0) ? 1.f : (dlog < 0.0 ? -1.f : 0.f);
         }
-        float cg1 = c1[0], cg2 = c2[0];
-#pragma unroll
-        for (int gg = 1; gg < 4; ++gg)
-          if (gu == gg) cg1 = c1[gg], cg2 = c2[gg];
-        dmel[q][gu][ju] = __fdividef(sg * cg1, (float)(mel[u] + LOG_EPS)) + cg2 * (float)dm;
+        reinterpret_cast<float*>(dmel[q])[idx] = __fdividef(sg * cg1, (float)(mel[u] + LOG_EPS)) + cg2 * (float)dm;
       }
     }
   }
   cp_async_wait_all8();
-  __syncthreads();  // publishes the spectrum and dmel
-  float2 dl[PER], dr[PER];
+  frame_sync<T, NT>(q);  // publishes the spectrum and dmel
+  // bin k's adjoint from S[k] and S[N - k], written back to the same two slots: no other
+  // thread of the frame reads them, so no barrier between the reads and the writes
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int k = tt + i * T;
-    dl[i] = dr[i] = make_float2(0.f, 0.f);
-    if (k < NB && valid) {
+    if (k >= NB) break;
+    float2 dl = make_float2(0.f, 0.f), dr = dl;
+    if (valid) {
       const float2 zk = S[pd16(k)], zp = S[pd16((N - k) & (N - 1))];
       float2 X[4];
       X[0] = make_float2(0.5f * (zk.x + zp.x), 0.5f * (zk.y - zp.y));
@@ -585,15 +601,21 @@ __device__ __forceinline__ void mr_bwd_body(MgbLossRes r, const double* __restri
         if (e < bl) {
           const int band = __ldg(r.bin_band + b0 + e);
           const float w = (float)__ldg(r.bin_w + b0 + e);
-#pragma unroll
-          for (int g = 0; g < 4; ++g) dmg[g] = fmaf(dmel[q][g][band], w, dmg[g]);
+          const float4 d = dmel[q][band];  // the band's 4 groups in one 16-byte load
+          dmg[0] = fmaf(d.x, w, dmg[0]);
+          dmg[1] = fmaf(d.y, w, dmg[1]);
+          dmg[2] = fmaf(d.z, w, dmg[2]);
+          dmg[3] = fmaf(d.w, w, dmg[3]);
         }
       }
       for (int e = 3; e < bl; ++e) {
         const int band = __ldg(r.bin_band + b0 + e);
         const float w = (float)__ldg(r.bin_w + b0 + e);
-#pragma unroll
-        for (int g = 0; g < 4; ++g) dmg[g] = fmaf(dmel[q][g][band], w, dmg[g]);
+        const float4 d = dmel[q][band];
+        dmg[0] = fmaf(d.x, w, dmg[0]);
+        dmg[1] = fmaf(d.y, w, dmg[1]);
+        dmg[2] = fmaf(d.z, w, dmg[2]);
+        dmg[3] = fmaf(d.w, w, dmg[3]);
       }
       float2 dX[4];
 #pragma unroll
@@ -602,30 +624,23 @@ __device__ __forceinline__ void mr_bwd_body(MgbLossRes r, const double* __restri
         const float sc = m2 == 0.f ? 0.f : dmg[g] * rsqrtf(m2);
         dX[g] = make_float2(sc * X[g].x, sc * X[g].y);
       }
-      dl[i] = make_float2(dX[0].x + dX[2].x + dX[3].x, dX[0].y + dX[2].y + dX[3].y);
-      dr[i] = make_float2(dX[1].x + dX[2].x - dX[3].x, dX[1].y + dX[2].y - dX[3].y);
+      dl = make_float2(dX[0].x + dX[2].x + dX[3].x, dX[0].y + dX[2].y + dX[3].y);
+      dr = make_float2(dX[1].x + dX[2].x - dX[3].x, dX[1].y + dX[2].y - dX[3].y);
+    }
+    // P[k] = Hl[k] + i Hr[k]; Hc[k] = dXc/2 (0<k<N/2), Hc[N-k] = conj(dXc)/2, Hc[0]/Hc[N/2] = Re dXc
+    if (k == 0 || k == N / 2) {
+      S[pd16(k)] = make_float2(dl.x, dr.x);
+    } else {
+      const float2 hl = make_float2(0.5f * dl.x, 0.5f * dl.y);
+      const float2 hr = make_float2(0.5f * dr.x, 0.5f * dr.y);
+      S[pd16(k)] = make_float2(hl.x - hr.y, hl.y + hr.x);          // hl + i hr
+      S[pd16(N - k)] = make_float2(hl.x + hr.y, -hl.y + hr.x);     // conj(hl) + i conj(hr)
     }
   }
-  __syncthreads();
-  // P[k] = Hl[k] + i Hr[k]; Hc[k] = dXc/2 (0<k<N/2), Hc[N-k] = conj(dXc)/2, Hc[0]/Hc[N/2] = Re dXc
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int k = tt + i * T;
-    if (k < NB) {
-      if (k == 0 || k == N / 2) {
-        S[pd16(k)] = make_float2(dl[i].x, dr[i].x);
-      } else {
-        const float2 hl = make_float2(0.5f * dl[i].x, 0.5f * dl[i].y);
-        const float2 hr = make_float2(0.5f * dr[i].x, 0.5f * dr[i].y);
-        S[pd16(k)] = make_float2(hl.x - hr.y, hl.y + hr.x);          // hl + i hr
-        S[pd16(N - k)] = make_float2(hl.x + hr.y, -hl.y + hr.x);     // conj(hl) + i conj(hr)
-      }
-    }
-  }
-  __syncthreads();
+  frame_sync<T, NT>(q);
   st_gather<N, 8, FP<N, 8>::R1>(v, S, tt);
-  __syncthreads();
-  frame_fft<N, 8, true>(v, S, tt);
+  frame_sync<T, NT>(q);
+  frame_fft<N, 8, true, NT>(v, S, tt, q);
   if (!valid) return;
   float* gf = r.gframes + (size_t)f * 2 * N;
   float s0, c0;
@@ -645,7 +660,7 @@ template <int NT, int NLO, int NHI>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_mr_bwd(MgbLoss L, MrGroup G) {
   mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ float dmel[NT * 8 / NLO][4][128];
+  __shared__ float4 dmel[NT * 8 / NLO][128];  // [frame][band]: the 4 groups' dmel
   int blk = blockIdx.x;
   const int ri = group_cta<NT, 8>(L, G, blk);
   const MgbLossRes& r = L.res[ri];

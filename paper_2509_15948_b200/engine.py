@@ -570,7 +570,7 @@ class LossPlan:
             dt = projection_device(dev, n, cfg)
             nm = cfg.mel_bins
             # every element is written (target / forward kernels) before it is read
-            tmel = torch.empty((nb, 4, frames, nm), dtype=F64, device=dev)
+            tmel = torch.empty((nb, frames, nm, 4), dtype=F64, device=dev)  # (frame, band, group)
             tlog = torch.empty_like(tmel)
             mel = torch.empty_like(tmel)
             part = torch.empty((nb, frames, 4, 3), dtype=F64, device=dev)
