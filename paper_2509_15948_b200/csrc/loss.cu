@@ -724,6 +724,7 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
   gr += sq * L.sig_stride;
   double al = 0.0, ar = 0.0;
   if (t > pad_max && t < Ls - 2 - pad_max) {
+#pragma unroll 3
     for (int ri = 0; ri < L.n_res; ++ri) {
       const MgbLossRes& r = L.res[ri];
       const int n = r.n_fft, lh = __ffs(r.hop) - 1, ln = __ffs(n) - 1;
@@ -732,10 +733,25 @@ __global__ void __launch_bounds__(256) k_mr_ola(MgbLoss L, float* __restrict__ g
       if (fhi > r.frames - 1) fhi = r.frames - 1;
       const int flo = (p - n + 1 <= 0) ? 0 : ((p - n + r.hop) >> lh);
       const float* gb = r.gframes + (size_t)sq * r.frames * 2 * n + p;
-      for (int f = flo; f <= fhi; ++f) {
-        const float* gfp = gb + ((size_t)f << (ln + 1)) - (f << lh);
-        al += __ldg(gfp);
-        ar += __ldg(gfp + n);
+      if (fhi - flo == 3) {  // hop = n / 4: four covering frames, loads issued together
+        float a[4], c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float* gfp = gb + ((size_t)(flo + k) << (ln + 1)) - ((flo + k) << lh);
+          a[k] = __ldg(gfp);
+          c[k] = __ldg(gfp + n);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          al += a[k];
+          ar += c[k];
+        }
+      } else {
+        for (int f = flo; f <= fhi; ++f) {
+          const float* gfp = gb + ((size_t)f << (ln + 1)) - (f << lh);
+          al += __ldg(gfp);
+          ar += __ldg(gfp + n);
+        }
       }
     }
   } else {
