@@ -65,6 +65,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all8() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -247,6 +251,27 @@ __device__ __forceinline__ void load_frame(float2* v, const float* __restrict__ 
   }
 }
 
+// the same from a CTA's staged sample window (frame q of the CTA starts q hop samples in)
+template <int N, int VV>
+__device__ __forceinline__ void load_frame_win(float2* v, const float* wl, const float* wr, int off, int tt) {
+  constexpr int T = FP<N, VV>::T, V = N / T, R = FP<N, VV>::R1;
+#pragma unroll
+  for (int i = 0; i < V / R; ++i) {
+    float s0, c0;
+    sincospif(2.f * (float)(tt + T * i) / (float)N, &s0, &c0);
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      const int t = off + tt + T * i + m * (N / R);
+      const float win = hann_at<R>(c0, s0, m);
+      v[i * R + m] = make_float2(wl[t] * win, wr[t] * win);
+    }
+  }
+}
+
+// samples of the window shared by a forward CTA's frames (N <= 1024: FPC >= 4 frames
+// overlapping 4x, staged once instead of read once per frame)
+constexpr int kFwdWin = 1792;  // (FPC - 1) N / 4 + N = 4 NT + 3 N / 4 at NT = 256, N <= 1024
+
 // spectrum in S (natural, padded) -> the 4 group magnitudes as float32,
 // md[g*NB + k] over the start of the same buffer (all reads precede the barrier)
 template <int N, int VV, int NT>
@@ -315,9 +340,28 @@ __device__ __forceinline__ void mr_fwd_body(MgbLossRes r, const float* __restric
     blen[i] = r.band_len[i];
     boff[i] = r.band_off[i];
   }
-  __syncthreads();  // publishes the band tables (the frames' barriers below are their own)
   float2 v[C::V];
-  load_frame<N, 16>(v, xl, xr, Ls, r.hop, f, valid, tt);
+  constexpr bool kWin = C::FPC >= 4 && (C::FPC - 1) * (N / 4) + N <= kFwdWin;
+  if (kWin && r.hop * 4 == N) {
+    // the CTA's frames blk FPC .. + FPC - 1 cover one window of W samples: staged by
+    // asynchronous 4-byte copies (reflect-padded per sample), then read from shared memory
+    constexpr int W = kWin ? (C::FPC - 1) * (N / 4) + N : 1;
+    float* wl = reinterpret_cast<float*>(smraw + frames_smem<NT, 16>());
+    float* wr = wl + kFwdWin;
+    const long long w0 = (long long)blk * C::FPC * (N / 4) - N / 2;
+    for (int i = threadIdx.x; i < W; i += NT) {
+      long long idx = w0 + i;
+      if (idx < 0 || idx >= Ls) idx = reflect_idx(idx, Ls);
+      cp_async4(wl + i, xl + idx);
+      cp_async4(wr + i, xr + idx);
+    }
+    cp_async_wait_all8();
+    __syncthreads();  // publishes the window and the band tables
+    load_frame_win<N, 16>(v, wl, wr, q * (N / 4), tt);
+  } else {
+    __syncthreads();  // publishes the band tables (the frames' barriers below are their own)
+    load_frame<N, 16>(v, xl, xr, Ls, r.hop, f, valid, tt);
+  }
   frame_fft<N, 16, false, NT>(v, S, tt, q);
   if (mode != 0 && r.gframes && valid) {
     // the estimate's frame spectrum, kept for the backward (which overwrites the slot
@@ -765,6 +809,8 @@ inline int nbatch(const MgbLoss& L) { return L.batch > 1 ? L.batch : 1; }
 
 // kernels of a call: every resolution with n <= 4096 in one launch, an 8192-point one alone
 constexpr int kFwdNT = 256, kBwdNT = 512;
+// frame buffers + the staged two-channel sample window
+constexpr size_t kFwdSmem = frames_smem<kFwdNT, 16>() + 2 * sizeof(float) * kFwdWin;
 #define MR_FWD_SMALL k_mr_fwd<kFwdNT, 256, 4096>
 #define MR_FWD_BIG k_mr_fwd<512, 8192, 8192>
 #define MR_BWD_SMALL k_mr_bwd<kBwdNT, 256, 4096>
@@ -800,7 +846,7 @@ int first_n(const MgbLoss& L, const MrGroup& G) { return L.res[__builtin_ctz(G.m
 
 int launch_fwd(const MgbLoss& L, const MrGroup& G, const float* xl, const float* xr, int mode, cudaStream_t st) {
   if (first_n(L, G) <= 4096) {
-    mgb_launch(MR_FWD_SMALL, dim3(group_ctas(L, G, kFwdNT, 16), nbatch(L)), dim3(kFwdNT), frames_smem<kFwdNT, 16>(),
+    mgb_launch(MR_FWD_SMALL, dim3(group_ctas(L, G, kFwdNT, 16), nbatch(L)), dim3(kFwdNT), kFwdSmem,
                st, L, G, xl, xr, mode);
   } else {
     mgb_launch(MR_FWD_BIG, dim3(group_ctas(L, G, 512, 16), nbatch(L)), dim3(512), frames_smem<512, 16>(), st, L, G,
@@ -834,7 +880,7 @@ int check_loss(const MgbLoss* L) {
 
 int loss_attrs() {
   int rc = 0;
-  rc |= cudaFuncSetAttribute(MR_FWD_SMALL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)frames_smem<kFwdNT, 16>());
+  rc |= cudaFuncSetAttribute(MR_FWD_SMALL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
   rc |= cudaFuncSetAttribute(MR_FWD_BIG, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)frames_smem<512, 16>());
   rc |= cudaFuncSetAttribute(MR_BWD_SMALL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)frames_smem<kBwdNT, 8>());
   rc |= cudaFuncSetAttribute(MR_BWD_BIG, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)frames_smem<1024, 8>());
