@@ -116,6 +116,9 @@ __device__ __forceinline__ void frame_sync(int q) {
     __syncwarp();
   } else if constexpr (T >= NT) {
     __syncthreads();
+  } else if constexpr (NT >= 512) {
+    // (at most two such CTAs per SM: the barrier id from a register, no dispatch)
+    asm volatile("bar.sync %0, %1;\n" ::"r"(q + 1), "n"(T) : "memory");
   } else {
     // constant barrier ids (ptxas reserves only the ids it sees: NT / T + 1 per CTA)
     static_assert(NT / T <= 8, "named barriers 1..8");
