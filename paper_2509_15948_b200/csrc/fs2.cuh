@@ -160,6 +160,16 @@ __device__ __forceinline__ void row_fft_compact(float2 (&v)[32], float2* T, int 
   }
 }
 
+// epilogues with a prefetch(ctx, n, b) hook (kPrefetch = true)
+template <class Ep, class = void>
+struct ep_prefetch {
+  static constexpr bool value = false;
+};
+template <class Ep>
+struct ep_prefetch<Ep, decltype(void(Ep::kPrefetch))> {
+  static constexpr bool value = Ep::kPrefetch;
+};
+
 // ---------------------------------------------------------------------------
 // column pass, forward: A[b][k1*N2 + n2] = w_N^{k1 n2} FFT_{N1}(x[. * N2 + n2])
 template <int N1, class Ld>
@@ -237,6 +247,13 @@ __global__ void __launch_bounds__(G<N1>::NT, 512 / G<N1>::NT) k_colC(const float
   for (int i = 0; i < B8; ++i) {
     const int n1 = j + P * i;
     raw[0][i] = ep.fetch(ctx, b, (long long)n1 * N2 + col, n1 < out_rows);
+  }
+  if constexpr (ep_prefetch<Ep>::value) {  // the later batches' inputs towards L2 meanwhile
+#pragma unroll
+    for (int m = B8; m < Q; ++m) {
+      const int n1 = j + P * m;
+      if (n1 < out_rows) ep.prefetch(ctx, (long long)n1 * N2 + col, b);
+    }
   }
   col_fft<N1, true>(v, sm, c, j);
   float a0 = 0.f, a1 = 0.f;
