@@ -304,7 +304,6 @@ struct EpFwd {
 
 struct EpGx {
   static constexpr bool kAccum = false;
-  static constexpr bool kPrefetch = true;
   typedef NoCtx Ctx;
   typedef float2 Raw;
   float* gu;
