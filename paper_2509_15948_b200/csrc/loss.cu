@@ -1,17 +1,20 @@
 // Multi-resolution STFT loss (mg/losses.py:104-170), forward and backward.
 //
-// Per resolution n (hop n/4, reflect pad n/2, periodic Hann), a few frames
+// Per resolution n (hop n/4, reflect pad n/2, periodic Hann), several frames
 // per CTA: both output channels ride one complex float32 FFT (left + i*right),
-// done as register radix-8 Stockham stages with shared-memory exchanges; the four groups [L, R, L+R, L-R] are separated from the
-// spectrum by linearity; |X| x (A-weight * HTK mel) is applied as a banded
-// (CSR) product; log-mel L1 and spectral-convergence partial sums are reduced
-// per frame (float64) and combined by a one-CTA finalize.
-// Backward recomputes the frame spectrum, forms dmel, d|X| (CSC), dX, packs
-// the two channels' Hermitian adjoint spectra into one inverse FFT, and
-// writes per-frame adjoints; a gather kernel overlap-adds them (with the
-// reflect-pad adjoint) across all resolutions into dL/dy, without atomics.
-// The frame transforms run in float32, magnitudes are projected, logged and reduced
-// in float64 (precision note at the frame FFT below).
+// done as register radix-16 (forward) / radix-8 (backward) Stockham stages with
+// shared-memory exchanges and per-frame barriers; the four groups [L, R, L+R,
+// L-R] are separated from the spectrum by linearity; |X| x (A-weight * HTK mel)
+// is applied as a banded (CSR) product; log-mel L1 and spectral-convergence
+// partial sums are reduced per frame (float64) and combined by a finalize.
+// Every resolution up to 4096 points shares one launch (CTAs hold the same
+// number of points whatever n); an 8192-point resolution gets its own.
+// The forward keeps each frame's spectrum; the backward forms dmel, d|X| (CSC),
+// dX, packs the two channels' Hermitian adjoint spectra in place into one
+// inverse FFT and writes per-frame adjoints; a gather kernel overlap-adds them
+// (with the reflect-pad adjoint) across all resolutions into dL/dy, without
+// atomics.  The frame transforms run in float32, magnitudes are projected,
+// logged and reduced in float64 (precision note at the frame FFT below).
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -102,7 +105,6 @@ struct FC {
   static constexpr int NT = NTT;
   static constexpr int NB = N / 2 + 1;
   static constexpr int PADN = N + N / 16;              // padded frame buffer (float2)
-  static constexpr size_t SMEM = sizeof(float2) * PADN * FPC;
 };
 template <int NT, int VV>
 constexpr size_t frames_smem() { return sizeof(float2) * (size_t)NT * VV * 17 / 16; }
