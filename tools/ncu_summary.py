@@ -28,7 +28,10 @@ for tag in sys.argv[1:]:
         if key in h:
             i = h.index(key)
             print(f"   {key}: {v[i]} {rows[1][i]}")
-    src = list(csv.reader(gzip.open(f"gpurun_out/ncu_{tag}_src.csv.gz", "rt")))
+    try:
+        src = list(csv.reader(gzip.open(f"gpurun_out/ncu_{tag}_src.csv.gz", "rt")))
+    except FileNotFoundError:  # the hottest source lines are in ncu_<tag>_lines.txt instead
+        continue
     hdr, src = src[1], src[2:]
     src = [r for r in src if len(r) > 2 and r[2].isdigit()]
     tot = sum(int(r[2]) for r in src) or 1
