@@ -304,6 +304,7 @@ struct EpFwd {
 
 struct EpGx {
   static constexpr bool kAccum = false;
+  static constexpr int kBatch64 = 2;  // k_colC64: a batch of 8 spilled 116 bytes, 4 spilled 32, at the 128-register cap
   typedef NoCtx Ctx;
   typedef float2 Raw;
   float* gu;

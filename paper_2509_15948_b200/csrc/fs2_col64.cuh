@@ -26,6 +26,16 @@ struct C64 {
   __device__ static __forceinline__ int row(int j, int m) { return (j >> 1) + 32 * m + 1024 * (j & 1); }
 };
 
+// epilogue batch of the 2048-point inverse column pass: Ep::kBatch64 if declared, else 8
+template <class Ep, class = void>
+struct ep_batch64 {
+  static constexpr int value = 8;
+};
+template <class Ep>
+struct ep_batch64<Ep, decltype(void(Ep::kBatch64))> {
+  static constexpr int value = Ep::kBatch64;
+};
+
 template <bool INV>
 __device__ __forceinline__ void col_fft64(float2 (&v)[32], float2* sm, int c, int j) {
   rf::rdft<32, INV>(v);
@@ -108,7 +118,7 @@ __global__ void __launch_bounds__(C64::NT, 1) k_colC64(const float2* __restrict_
 #pragma unroll
   for (int m = 0; m < 32; ++m) v[m] = src[(long long)(j + 64 * m) * N2];
   const typename Ep::Ctx ctx = ep.prepare(b);
-  constexpr int B8 = 8;
+  constexpr int B8 = ep_batch64<Ep>::value;  // epilogue batch (register budget at 512 threads)
   typename Ep::Raw raw[2][B8];
 #pragma unroll
   for (int i = 0; i < B8; ++i) {
