@@ -319,7 +319,7 @@ def main():
     e2e_t = e2e_t[:1]
     e2e_val = world * args.e2e_steps / float(e2e_t.item())
     # one pruning trial (masked forward-only render + MRSTFT, mg/pruning.py:115-123) on the
-    # same clip (forward-only levels: no kept spectra, no gain-staging adjoints)
+    # same clip
     from paper_2509_15948_b200.engine import EvalEngine
     ev = EvalEngine(graph, [(stems, target)], WARMUP, cfg.loss, device=dev, params=params)
     mask = np.ones(eng.layout.P)
