@@ -158,7 +158,12 @@ def test_train_segments_equals_train_step_loop(dev):
     p_loop, p_pipe = params.copy(), params.copy()
     opt = make_optimizer(p_loop, cfg)
     loop = [train_step(graph, p_loop, s, cfg, opt) for s in segs]
-    pipe = train_segments(graph, p_pipe, segs, cfg, make_optimizer(p_pipe, cfg))
+    opt_pipe = make_optimizer(p_pipe, cfg)
+    pipe = train_segments(graph, p_pipe, segs, cfg, opt_pipe)
+    # the pipelined run reads the stems from its staging slots; the next train_step on the
+    # same engine must read its own input again
+    loop.append(train_step(graph, p_loop, segs[2], cfg, opt))
+    pipe.append(train_step(graph, p_pipe, segs[2], cfg, opt_pipe))
     assert len(pipe) == len(loop)
     for a, b in zip(loop, pipe):
         for key in ("loss", "L_a", "L_g", "L_p"):
