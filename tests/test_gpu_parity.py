@@ -548,16 +548,18 @@ def test_lockstep_song_searches_equal_sequential(dev):
     assert [{k: r[k] for k in keys} for r in lock] == [{k: r[k] for k in keys} for r in seq]
 
 
-def test_batched_mrstft_equals_per_signal_calls(dev):
+@pytest.mark.parametrize("sizes", [(512, 1024, 4096), (256, 512, 1024, 2048, 4096, 8192)])
+def test_batched_mrstft_equals_per_signal_calls(dev, sizes):
     """MgbLoss.batch > 1 (several songs' losses in one call set): every signal's loss and
-    gradient equal the single-signal calls bit for bit."""
+    gradient equal the single-signal calls bit for bit (six resolutions: the 8192-point
+    one in its own launch beside the merged launch of the others)."""
     from paper_2509_15948_b200.engine import LossPlan, ptr
     from paper_2509_15948_b200.losses import LossConfig
     rng = np.random.default_rng(11)
     G, L, ws = 3, 70_000, 30_000
     y = torch.tensor(0.3 * rng.standard_normal((G, 2, L)), dtype=torch.float32, device=dev)
     t = torch.tensor(0.3 * rng.standard_normal((G, 2, L)), dtype=torch.float32, device=dev)
-    cfg = LossConfig()
+    cfg = LossConfig(fft_sizes=sizes)
     bl = LossPlan(cfg, L - ws, dev, batch=G, sig_stride=2 * L)
     gb = torch.zeros((G, 2, L), dtype=torch.float32, device=dev)
     bl.target(ptr(t, ws), ptr(t, L + ws))
