@@ -46,6 +46,10 @@ int g_num_sms = 148;
 // MGB_COLC_PERSISTENT=1: the persistent bulk-copy-pipelined column pass (fs2::k_colC_p) instead of
 // one tile per CTA.  Measured slower (336 vs 437 steps/s), kept off for A/B runs.
 bool g_colc_persistent = false;
+// levels of at most this many nodes compute the FIR-gradient rows in backward phase 2
+// (MGB_SPLIT_FIR_B; measured: +2.2 % at config 1, slower at B = 16 where the GPU is saturated)
+int g_split_fir_b = 4;
+bool split_fir_rows(int B) { return B <= g_split_fir_b; }
 
 struct ConvGeom {
   int M, off, logN;
@@ -514,6 +518,8 @@ struct Conv2 {
     cudaFuncSetAttribute(fs2::k_rowH<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWH_SMEM);
     cudaFuncSetAttribute(fs2::k_rowF<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWF_SMEM);
     cudaFuncSetAttribute(fs2::k_rowG<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWG_SMEM);
+    cudaFuncSetAttribute(fs2::k_rowF<N1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWF_SMEM);
+    cudaFuncSetAttribute(fs2::k_rowP<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs2::ROWF_SMEM);
   }
 
   static int prep(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
@@ -547,7 +553,14 @@ struct Conv2 {
     const int g_rows = (int)((g.off + L + N2 - 1) / N2);
     colA(ld, w.Ax, g_rows < N1 ? g_rows : N1, 1, B, st);
     MGB_CHECK_LAUNCH();
-    mgb_launch(fs2::k_rowG<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWG_SMEM, st, w.Ax, w.X, w.H, w.Bo, w.Ah, 0);
+    if (split_fir_rows(B)) {
+      // narrow level (latency-bound): G = FFT(Ag) kept in Ah for the FIR gradient (phase 2,
+      // k_rowP, off the critical path), Bo = IFFT(G conj H)
+      mgb_launch(fs2::k_rowF<N1, true>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWF_SMEM, st, w.Ax, w.H, w.Ah, w.Bo, 0);
+    } else {
+      // wide level (the GPU is saturated): all three row transforms in one pass, Ah = the FIR rows
+      mgb_launch(fs2::k_rowG<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWG_SMEM, st, w.Ax, w.X, w.H, w.Bo, w.Ah, 0);
+    }
     MGB_CHECK_LAUNCH();
     if (lv->gu) {
       colC(w.Bo, EpGx{lv->gu, L}, N1, 1, B, st);
@@ -558,7 +571,11 @@ struct Conv2 {
 
   // FIR gradient dh = IFFT(G conj(X))[0:M] (backward phase 2: only the FIR adjoint reads it)
   static int fir_grad(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
-    const dim3 gc(N2 / G::TC, lv->B);
+    if (split_fir_rows(lv->B)) {  // the FIR rows from the kept G and X (see bwd)
+      const dim3 gr(G::ROW_CTAS, lv->B);
+      mgb_launch(fs2::k_rowP<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWF_SMEM, st, w.Ah, w.X, w.Ah, 1);
+      MGB_CHECK_LAUNCH();
+    }
     const int h_rows = (int)((g.M + N2 - 1) / N2);
     colC(w.Ah, EpGh{w.ghbuf, g.M}, h_rows < N1 ? h_rows : N1, 1, lv->B, st);
     MGB_CHECK_LAUNCH();
@@ -640,6 +657,8 @@ int mgb_conv_init() {
   cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   const char* e = getenv("MGB_COLC_PERSISTENT");
   g_colc_persistent = e ? atoi(e) != 0 : false;
+  const char* sf = getenv("MGB_SPLIT_FIR_B");
+  g_split_fir_b = sf ? atoi(sf) : 4;
 #define X(l, a) Conv2<a>::attrs();
   MGB_CONV_SIZES(X)
 #undef X

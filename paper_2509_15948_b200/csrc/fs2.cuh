@@ -349,7 +349,9 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowH(const float2* __restrict__
 // partner warp's staged H row and spectrum are read from its region.  The two
 // transforms share one code copy (pass loop); the duplicate warp of a
 // self-paired row computes along but stores nothing.
-template <int N1>
+// CONJ (the backward's input gradient): Ax = the column pass of dL/dy, X receives its row
+// spectrum G (kept for k_rowP), Bo = the inverse rows of G_l conj(H_l) + i G_r conj(H_r).
+template <int N1, bool CONJ = false>
 __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__ Ax, const float2* __restrict__ H,
                                                      float2* __restrict__ X, float2* __restrict__ Bo, int rev) {
   mgb_pdl_entry();
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowF(const float2* __restrict__
       float2 xl, xr, hl, hr;
       split_pair(v[ka], pA[kp], xl, xr);
       split_pair(sH[k], pH[kp], hl, hr);
-      const float2 y1 = cmul(xl, hl), y2 = cmul(xr, hr);
+      const float2 y1 = CONJ ? cmulc(xl, hl) : cmul(xl, hl), y2 = CONJ ? cmulc(xr, hr) : cmul(xr, hr);
       v[ka] = make_float2(y1.x - y2.y, -(y1.y + y2.x));  // conj: inverse via the forward code
     }
     __syncthreads();  // both warps done reading the spectra before sA is scratch again
@@ -474,6 +476,50 @@ __global__ void __launch_bounds__(2 * RP * 32) k_rowG(const float2* __restrict__
   }
 }
 
+
+// FIR-gradient rows (backward phase 2, off the critical path): B = conj-twiddled inverse
+// rows of A_l conj(O_l) + i A_r conj(O_r) for two kept row spectra (A = G from
+// k_rowF<N1, true>, O = X).  B may alias A: both warps of a row pair stage their rows in
+// shared memory and pass a barrier before either writes.
+template <int N1>
+__global__ void __launch_bounds__(2 * RP * 32) k_rowP(const float2* A, const float2* __restrict__ O, float2* B,
+                                                     int rev) {
+  mgb_pdl_entry();
+  using g = G<N1>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int w = threadIdx.x >> 5;
+  float2* sA = warp_region<ROWF_WARP>(smraw, w);  // A row, then the transpose scratch
+  float2* sO = sA + TBUF;                          // O row
+  const RowMap rm = row_map<N1>();
+  const bool self = rm.row == rm.prow;
+  float2* pA = self ? sA : warp_region<ROWF_WARP>(smraw, w ^ 1);
+  float2* pO = pA + TBUF;
+  const int bnode = rev ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
+  const long long base = (long long)bnode * g::N + (long long)rm.row * N2;
+  const int lane = rm.lane;
+  row_prefetch(sA, A + base, lane);
+  row_prefetch(sO, O + base, lane);
+  cp_async_wait_all();
+  __syncthreads();  // both warps' rows staged (and A read: B may overwrite it from here on)
+  float2 v[32];
+#pragma unroll
+  for (int ka = 0; ka < 32; ++ka) {
+    const int k = lane + 32 * ka, kp = partner_col(rm.row, k);
+    float2 al, ar, ol, orr;
+    split_pair(sA[k], pA[kp], al, ar);
+    split_pair(sO[k], pO[kp], ol, orr);
+    const float2 y1 = cmulc(al, ol), y2 = cmulc(ar, orr);
+    v[ka] = make_float2(y1.x - y2.y, -(y1.y + y2.x));  // conj: inverse via the forward code
+  }
+  __syncthreads();  // partner done reading sA before it is scratch
+  row_fft_compact(v, sA, lane);
+  if (!rm.active) return;
+#pragma unroll
+  for (int n = 0; n < 32; ++n) v[n].y = -v[n].y;
+  twiddle_run<g::LOGN, 32, true>(v, rm.row * lane, rm.row * 32);
+#pragma unroll
+  for (int n = 0; n < 32; ++n) B[base + lane + 32 * n] = v[n];
+}
 
 // ---------------------------------------------------------------------------
 // Persistent column pass with bulk-async (TMA engine) tile staging.
