@@ -50,6 +50,8 @@ bool g_colc_persistent = false;
 // (MGB_SPLIT_FIR_B; measured: +2.2 % at config 1, slower at B = 16 where the GPU is saturated)
 int g_split_fir_b = 4;
 bool split_fir_rows(int B) { return B <= g_split_fir_b; }
+// the EQ backward's FIR-gradient pass in phase 2: narrow levels with one block per CTA
+bool eos_split(int L, int B) { return B <= g_split_fir_b && eos_per(L, B) == 1; }
 
 struct ConvGeom {
   int M, off, logN;
@@ -669,6 +671,7 @@ int mgb_conv_init() {
   cudaFuncSetAttribute(k_eqos_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
   cudaFuncSetAttribute(k_eqos_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
   cudaFuncSetAttribute(k_eqos_gh, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
+  cudaFuncSetAttribute(k_eqos_bwd_c, cudaFuncAttributeMaxDynamicSharedMemorySize, kEosSmem1);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -751,7 +754,8 @@ int mgb_conv_backward(const MgbLevel* lv, cudaStream_t st) {
   if (tag == 'e') {
     const int nb = eos_nblk(L);
     mgb_launch(k_eqos_bwd, dim3(dim3(eos_nchunk(L, B), B)), dim3(EOS_NT), kEosSmem1, st, lv->u_rows, lv->gy_rows,
-               lv->ybar, w.Hs, lv->widx, lv->w, lv->greg, w.stats, lv->gu, w.part, w.pspec, L, nb, eos_per(L, B));
+               lv->ybar, w.Hs, lv->widx, lv->w, lv->greg, w.stats, lv->gu, w.part, w.pspec, L, nb, eos_per(L, B),
+               eos_split(L, B) ? 1 : 2);
     MGB_CHECK_LAUNCH();
     return 0;
   }
@@ -770,6 +774,10 @@ int mgb_conv_param_grad(const MgbLevel* lv, cudaStream_t st) {
              lv->widx, lv->w, lv->gw);
   MGB_CHECK_LAUNCH();
   if (tag == 'e') {
+    if (eos_split(L, B)) {  // the FIR-gradient pass phase 1 left out (narrow level)
+      mgb_launch(k_eqos_bwd_c, dim3(dim3(eos_nchunk(L, B), B)), dim3(EOS_NT), kEosSmem1, st, lv->u_rows, w.pspec, L);
+      MGB_CHECK_LAUNCH();
+    }
     mgb_launch(k_eqos_csum, dim3(dim3(EOS_N / 256, B)), dim3(256), 0, st, w.pspec, eos_nchunk(L, B), w.csum);
     MGB_CHECK_LAUNCH();
     mgb_launch(k_eqos_gh, dim3(B), dim3(EOS_NT), kEosSmem1, st, w.csum, w.ghbuf);

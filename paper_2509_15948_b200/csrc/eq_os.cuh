@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
                                                      const double* __restrict__ greg,
                                                      const double* __restrict__ stats, float* __restrict__ gu,
                                                      double* __restrict__ part, float2* __restrict__ pspec,
-                                                     int L, int nblk, int per) {
+                                                     int L, int nblk, int per, int passes) {
   mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* S = reinterpret_cast<float2*>(dsm);
@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
         }
       }
     }
+    if (passes == 1) break;  // the FIR-gradient pass runs in phase 2 (k_eqos_bwd_c)
     // pass 1 input: x masked to the block
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
@@ -339,6 +340,32 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd(const float* const* __re
   }
   const double tw = block_sum((double)fw, red);
   if (t == 0) part[((size_t)b * kMaxParts + chunk) * 4 + 2] = tw;
+}
+
+// The FIR-gradient pass of k_eqos_bwd on its own (narrow levels, one block per CTA:
+// backward phase 2, off the critical path): C = conj(D) FFT(x masked to the block),
+// D parked by phase 1 in the CTA's slot.
+__global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd_c(const float* const* __restrict__ u_rows,
+                                                       float2* __restrict__ pspec, int L) {
+  mgb_pdl_entry();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float2* S = reinterpret_cast<float2*>(dsm);
+  const int blk = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
+  const float* u = u_rows[b];
+  const float2* dpark = pspec + ((size_t)b * gridDim.x + blk) * 2 * EOS_N + t;
+  float2* cacc = const_cast<float2*>(dpark) + EOS_N;
+  const long long w0 = (long long)blk * EOS_HOP - EOS_OFF;
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int i = t + 256 * m;
+    const long long n = w0 + i;
+    v[m] = (i >= EOS_OFF && i < EOS_OFF + EOS_HOP && n < L) ? make_float2(__ldg(u + n), __ldg(u + L + n))
+                                                              : make_float2(0.f, 0.f);
+  }
+  eos_fft(v, S);
+#pragma unroll
+  for (int r = 0; r < 32; ++r) cacc[r * 256] = cmulc(v[r], dpark[r * 256]);
 }
 
 // Csum[b][slot] = sum over the backward CTAs' C accumulators (float64, fixed order)
