@@ -46,11 +46,14 @@ int g_num_sms = 148;
 // MGB_COLC_PERSISTENT=1: the persistent bulk-copy-pipelined column pass (fs2::k_colC_p) instead of
 // one tile per CTA.  Measured slower (336 vs 437 steps/s), kept off for A/B runs.
 bool g_colc_persistent = false;
-// levels of at most this many nodes compute the FIR-gradient rows in backward phase 2
-// (MGB_SPLIT_FIR_B; measured: +2.2 % at config 1, slower at B = 16 where the GPU is saturated)
+// Narrow levels move their FIR-gradient transform to backward phase 2 (side stream, off
+// the critical path): conv levels of at most g_split_rows (B x N1) rows, EQ levels of at
+// most g_split_fir_b nodes with one overlap-save block per backward CTA.  Measured
+// (MGB_SPLIT_ROWS / MGB_SPLIT_FIR_B): config 1 +7.7 %, config 2 +1.3 %; wide levels
+// (B = 16 at N1 = 512, B = 4 at N1 = 2048) are slower split: the GPU is saturated there.
+int g_split_rows = 2048;
 int g_split_fir_b = 4;
-bool split_fir_rows(int B) { return B <= g_split_fir_b; }
-// the EQ backward's FIR-gradient pass in phase 2: narrow levels with one block per CTA
+bool split_fir_rows(int B, int N1) { return (long long)B * N1 <= g_split_rows; }
 bool eos_split(int L, int B) { return B <= g_split_fir_b && eos_per(L, B) == 1; }
 
 struct ConvGeom {
@@ -555,7 +558,7 @@ struct Conv2 {
     const int g_rows = (int)((g.off + L + N2 - 1) / N2);
     colA(ld, w.Ax, g_rows < N1 ? g_rows : N1, 1, B, st);
     MGB_CHECK_LAUNCH();
-    if (split_fir_rows(B)) {
+    if (split_fir_rows(B, N1)) {
       // narrow level (latency-bound): G = FFT(Ag) kept in Ah for the FIR gradient (phase 2,
       // k_rowP, off the critical path), Bo = IFFT(G conj H)
       mgb_launch(fs2::k_rowF<N1, true>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWF_SMEM, st, w.Ax, w.H, w.Ah, w.Bo, 0);
@@ -573,7 +576,7 @@ struct Conv2 {
 
   // FIR gradient dh = IFFT(G conj(X))[0:M] (backward phase 2: only the FIR adjoint reads it)
   static int fir_grad(const MgbLevel* lv, const ConvWs& w, const ConvGeom& g, cudaStream_t st) {
-    if (split_fir_rows(lv->B)) {  // the FIR rows from the kept G and X (see bwd)
+    if (split_fir_rows(lv->B, N1)) {  // the FIR rows from the kept G and X (see bwd)
       const dim3 gr(G::ROW_CTAS, lv->B);
       mgb_launch(fs2::k_rowP<N1>, dim3(gr), dim3(2 * fs2::RP * 32), fs2::ROWF_SMEM, st, w.Ah, w.X, w.Ah, 1);
       MGB_CHECK_LAUNCH();
@@ -661,6 +664,8 @@ int mgb_conv_init() {
   g_colc_persistent = e ? atoi(e) != 0 : false;
   const char* sf = getenv("MGB_SPLIT_FIR_B");
   g_split_fir_b = sf ? atoi(sf) : 4;
+  const char* sr = getenv("MGB_SPLIT_ROWS");
+  g_split_rows = sr ? atoi(sr) : 2048;
 #define X(l, a) Conv2<a>::attrs();
   MGB_CONV_SIZES(X)
 #undef X
