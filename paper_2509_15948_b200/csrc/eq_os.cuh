@@ -352,8 +352,8 @@ __global__ void __launch_bounds__(EOS_NT, 2) k_eqos_bwd_c(const float* const* __
   float2* S = reinterpret_cast<float2*>(dsm);
   const int blk = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
   const float* u = u_rows[b];
-  const float2* dpark = pspec + ((size_t)b * gridDim.x + blk) * 2 * EOS_N + t;
-  float2* cacc = const_cast<float2*>(dpark) + EOS_N;
+  float2* dpark = pspec + ((size_t)b * gridDim.x + blk) * 2 * EOS_N + t;
+  float2* cacc = dpark + EOS_N;
   const long long w0 = (long long)blk * EOS_HOP - EOS_OFF;
   float2 v[32];
 #pragma unroll
