@@ -51,10 +51,16 @@ __global__ void __launch_bounds__(RV_NT) k_rev_frames_fft(const double* __restri
   mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* s = reinterpret_cast<float2*>(dsm);
+  __shared__ float win[MGB_REV_NFFT];  // periodic Hann(384) / 384
   const int m0 = blockIdx.x * RV_F, b = blockIdx.y;
   const double* p = bank + (size_t)prow[b] * 768;
-  for (int q = threadIdx.x; q < RV_F * (MGB_REV_PBINS + 1); q += RV_NT) {
-    const int f = q / (MGB_REV_PBINS + 1), k = q % (MGB_REV_PBINS + 1);
+  for (int i = threadIdx.x; i < MGB_REV_NFFT; i += RV_NT)
+    win[i] = (0.5f - 0.5f * cospif(2.f * (float)i / (float)MGB_REV_NFFT)) * (1.0f / (float)MGB_REV_NFFT);
+  // (f, k) = divmod(q, 193) stepped without divisions
+  int f = 0, k = threadIdx.x;
+  while (k >= MGB_REV_PBINS + 1) k -= MGB_REV_PBINS + 1, ++f;
+  for (int q = threadIdx.x; q < RV_F * (MGB_REV_PBINS + 1); q += RV_NT, k += RV_NT) {
+    while (k >= MGB_REV_PBINS + 1) k -= MGB_REV_PBINS + 1, ++f;
     const int m = m0 + f;
     float2 Z0 = make_float2(0.f, 0.f), Z1 = Z0;  // Z[k], Z[384-k]
     if (m < MGB_REV_FRAMES) {
@@ -74,16 +80,16 @@ __global__ void __launch_bounds__(RV_NT) k_rev_frames_fft(const double* __restri
       fr[(k2 >> 7) * RV_P + pidx<true>(k2 & 127)] = Z1;
     }
   }
-  dft384(s, true);
-  const float inv = 1.0f / (float)MGB_REV_NFFT;
-  for (int q = threadIdx.x; q < RV_F * MGB_REV_NFFT; q += RV_NT) {
-    const int f = q / MGB_REV_NFFT, i = q % MGB_REV_NFFT;
-    const int m = m0 + f;
+  dft384(s, true);  // (its barriers publish the window table)
+  int fo = 0, i = threadIdx.x;  // (fo, i) = divmod(q, 384), stepped
+  for (int q = threadIdx.x; q < RV_F * MGB_REV_NFFT; q += RV_NT, i += RV_NT) {
+    while (i >= MGB_REV_NFFT) i -= MGB_REV_NFFT, ++fo;
+    const int m = m0 + fo;
     if (m >= MGB_REV_FRAMES) continue;
-    const float2 z = s[f * RV_FRAME + (i % 3) * RV_P + pidx<true>(i / 3)];
-    const float win = (0.5f - 0.5f * cospif(2.f * (float)i / (float)MGB_REV_NFFT)) * inv;
-    frames[(((size_t)b * 2 + 0) * MGB_REV_FRAMES + m) * MGB_REV_NFFT + i] = z.x * win;
-    frames[(((size_t)b * 2 + 1) * MGB_REV_FRAMES + m) * MGB_REV_NFFT + i] = z.y * win;
+    const float2 z = s[fo * RV_FRAME + (i % 3) * RV_P + pidx<true>(i / 3)];
+    const float wv = win[i];
+    frames[(((size_t)b * 2 + 0) * MGB_REV_FRAMES + m) * MGB_REV_NFFT + i] = z.x * wv;
+    frames[(((size_t)b * 2 + 1) * MGB_REV_FRAMES + m) * MGB_REV_NFFT + i] = z.y * wv;
   }
 }
 
@@ -94,15 +100,20 @@ __global__ void __launch_bounds__(RV_NT) k_rev_bwd_frames_fft(const double* __re
   mgb_pdl_entry();
   extern __shared__ __align__(16) unsigned char dsm[];
   float2* s = reinterpret_cast<float2*>(dsm);
+  __shared__ float hann[MGB_REV_NFFT];  // periodic Hann(384)
   const int m0 = blockIdx.x * RV_F, m0f = m0, b = blockIdx.y;
   const float2* g = GH + (size_t)b * M;
-  for (int q = threadIdx.x; q < RV_F * MGB_REV_NFFT; q += RV_NT) {
-    const int f = q / MGB_REV_NFFT, i = q % MGB_REV_NFFT;
+  for (int i = threadIdx.x; i < MGB_REV_NFFT; i += RV_NT)
+    hann[i] = 0.5f - 0.5f * cospif(2.f * (float)i / (float)MGB_REV_NFFT);
+  __syncthreads();
+  int f = 0, i = threadIdx.x;  // (f, i) = divmod(q, 384), stepped
+  for (int q = threadIdx.x; q < RV_F * MGB_REV_NFFT; q += RV_NT, i += RV_NT) {
+    while (i >= MGB_REV_NFFT) i -= MGB_REV_NFFT, ++f;
     const int t = (m0 + f) * MGB_REV_HOP + i - MGB_REV_HOP;  // position in the sliced FIR
     float dm = 0.f, ds = 0.f;
     if (m0 + f < MGB_REV_FRAMES && t >= 0 && t < MGB_REV_LEN) {
       const float2 v = g[t];
-      const float iw = g_rev_inv_wss[t] * (0.5f - 0.5f * cospif(2.f * (float)i / (float)MGB_REV_NFFT));
+      const float iw = g_rev_inv_wss[t] * hann[i];
       dm = 0.5f * (v.x + v.y) * iw;
       ds = 0.5f * (v.x - v.y) * iw;
     }
