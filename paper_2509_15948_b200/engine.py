@@ -493,6 +493,8 @@ class RenderPlan:
         L = lib()
         sp = stream_ptr()
         main = current_stream()
+        sides = side if isinstance(side, (tuple, list)) else (side,)
+        n = 0
         for lv in reversed(self.levels):
             for src, off, buf in lv.fanouts:
                 check(L.mgb_bus_sum(ptr(src), ptr(off), ptr(buf), 1, self.L, sp), "fan-out sum")
@@ -502,8 +504,10 @@ class RenderPlan:
                 check(L.mgb_level_backward(ctypes.byref(lv.struct), sp), f"level {lv.tag} backward")
                 continue
             check(L.mgb_level_backward_phase(ctypes.byref(lv.struct), 1, sp), f"level {lv.tag} backward")
-            side.wait_stream(main)
-            with on_stream(side):
+            sd = sides[n % len(sides)]  # levels' parameter phases alternate over the side streams
+            n += 1
+            sd.wait_stream(main)
+            with on_stream(sd):
                 check(L.mgb_level_backward_phase(ctypes.byref(lv.struct), 2, stream_ptr()),
                       f"level {lv.tag} FIR adjoint")
 
@@ -639,6 +643,10 @@ class TrainEngine:
         self._graph = None
         self.d_rows = lay.rows["d"]
         self.side = own_stream(dev, "side")
+        # the levels' backward parameter phases alternate over two side streams, so the
+        # last levels' phases run side by side before the optimiser (config 1 +1.3 %,
+        # config 2 unchanged; MG_SIDE2=0: one side stream)
+        self.side2 = own_stream(dev, "side2") if os.environ.get("MG_SIDE2", "1") == "1" else None
         # sticky NonFiniteLoss flag of the current run (mgb_adamw_step); zeroed per run
         self.halt = torch.zeros((), dtype=F64, device=dev)
 
@@ -687,7 +695,11 @@ class TrainEngine:
                                        ptr(self.scalars), float(self.cfg.loss.gain_staging_weight), 1,
                                        ptr(self.vals), None, sp), "mgb_loss_assembly")
         lp.backward(ptr(y, ws), ptr(y, L + ws), ptr(plan.dY, ws), ptr(plan.dY, L + ws))
-        plan.backward(side)
+        if self.side2 is not None:
+            plan.backward((side, self.side2))
+            main.wait_stream(self.side2)
+        else:
+            plan.backward(side)
         main.wait_stream(side)
         lay = self.layout
         check(Ld.mgb_adamw_step(ptr(self.params), ptr(self.grads), ptr(self.m), ptr(self.v), lay.n,
