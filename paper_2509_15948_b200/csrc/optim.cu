@@ -5,6 +5,7 @@
 //   3. AdamW over the flat vector (banks + raw weights), fresh-state semantics
 //      are the caller's (moments zeroed at each train() call)
 //   4. unit-disk projection of every delay z
+// all in one pass (k_optim_step), with the sticky non-finite guard.
 // The AdamW arithmetic is written with explicit round-to-nearest ops so nvcc
 // does not contract it into FMAs: it reproduces numpy's operation order.
 #include "common.cuh"
@@ -12,37 +13,19 @@
 
 namespace {
 
-__global__ void k_raw_grad(const double* __restrict__ p, double* __restrict__ g, long long w_off, int P,
-                           const double* __restrict__ gw, const double* __restrict__ mask,
-                           const double* __restrict__ sc) {
-  mgb_pdl_entry();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
-  const double s = expit64(p[w_off + i]);
-  const double ds = s * (1.0 - s);
-  double v = gw[i] * (mask ? mask[i] : 1.0) * ds;
-  const double ap = sc[7];
-  if (ap > 0.0) v += ap * ds;
-  g[w_off + i] = v;
-}
-
-__global__ void k_delay_rule(const double* __restrict__ p, double* __restrict__ g, long long d_off, int rows) {
-  mgb_pdl_entry();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (row, channel, tap)
-  if (i >= rows * 40) return;
-  const int row = i / 40, c = (i / 20) % 2, m = i % 20;
-  const long long base = d_off + (long long)row * 880 + c * 440;
-  const double zr = p[base + m], zi = p[base + 20 + m];
-  const double gr = g[base + m], gi = g[base + 20 + m];
-  const double mag = hypot(gr, gi);
-  double sr = 0.0, si = 0.0;
-  if (mag > 0.0) { sr = gr / mag; si = gi / mag; }
-  const double zm = hypot(zr, zi);
-  double cr = 0.0, ci = 0.0;
-  if (zm > 0.0) { cr = zr / zm; ci = -zi / zm; }
-  const double k = 0.01 * (zm - 1.0);
-  g[base + m] = sr + k * cr;
-  g[base + 20 + m] = si + k * ci;
+__device__ __forceinline__ void adamw_update(double* __restrict__ p, double* __restrict__ m,
+                                             double* __restrict__ v, long long i, double gi, double lr,
+                                             double b1, double b2, double eps, double wd, double c1, double c2) {
+  double mi = m[i], vi = v[i], pi = p[i];
+  mi = __dadd_rn(mi, __dmul_rn(__dsub_rn(1.0, b1), __dsub_rn(gi, mi)));
+  vi = __dadd_rn(vi, __dmul_rn(__dsub_rn(1.0, b2), __dsub_rn(__dmul_rn(gi, gi), vi)));
+  const double mh = __ddiv_rn(mi, c1);
+  const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps);
+  const double upd = __dadd_rn(__ddiv_rn(mh, den), __dmul_rn(wd, pi));
+  pi = __dsub_rn(pi, __dmul_rn(lr, upd));
+  m[i] = mi;
+  v[i] = vi;
+  p[i] = pi;
 }
 
 // NonFiniteLoss (mg/optimizer.py:164-171): the reference raises at the first step whose
@@ -50,50 +33,67 @@ __global__ void k_delay_rule(const double* __restrict__ p, double* __restrict__ 
 // flag is sticky: once a step's loss is non-finite, that step and every later step of
 // the same run leave parameters and moments untouched (the host raises after reading
 // the per-step losses back, with the parameters as of the last finite step).
-__global__ void k_guard(const double* __restrict__ loss, double* __restrict__ halt) {
+//
+// The whole step in one pass (steps 1-4 of the header with the non-finite guard), the
+// same arithmetic as the separate kernels above: a thread owns whole delay taps (the
+// re/im pair of one z: rule, both AdamW updates, projection), a raw weight (its
+// gradient, then AdamW), or a plain parameter.  The updated gradients are written back
+// as the separate steps leave them.
+__global__ void k_optim_step(double* __restrict__ p, double* __restrict__ g, double* __restrict__ m,
+                             double* __restrict__ v, long long n, long long d_off, int d_rows, long long w_off,
+                             int P, const double* __restrict__ gw, const double* __restrict__ mask,
+                             const double* __restrict__ sc, const double* __restrict__ guard,
+                             double* __restrict__ halt) {
   mgb_pdl_entry();
-  if (!isfinite(*loss)) *halt = 1.0;
-}
-
-__device__ __forceinline__ bool halted(const double* guard, const double* halt) {
-  if (halt) return *halt != 0.0;
-  return guard && !isfinite(*guard);
-}
-
-__global__ void k_adamw(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
-                        double* __restrict__ v, long long n, const double* __restrict__ sc,
-                        const double* __restrict__ guard, const double* __restrict__ halt) {
-  mgb_pdl_entry();
-  if (halted(guard, halt)) return;
+  const bool nonfinite = guard && !isfinite(*guard);
+  // sticky flag: set by one thread; every thread decides from the flag's previous value
+  // and the loss itself, so the order of that write does not matter
+  const bool bad = nonfinite || (halt && *halt != 0.0);
+  if (halt && nonfinite && blockIdx.x == 0 && threadIdx.x == 0) *halt = 1.0;
   const double lr = sc[0], b1 = sc[1], b2 = sc[2], eps = sc[3], wd = sc[4], c1 = sc[5], c2 = sc[6];
+  const long long d_end = d_off + (long long)d_rows * 880;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const double gi = g[i];
-    double mi = m[i], vi = v[i], pi = p[i];
-    mi = __dadd_rn(mi, __dmul_rn(__dsub_rn(1.0, b1), __dsub_rn(gi, mi)));
-    vi = __dadd_rn(vi, __dmul_rn(__dsub_rn(1.0, b2), __dsub_rn(__dmul_rn(gi, gi), vi)));
-    const double mh = __ddiv_rn(mi, c1);
-    const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps);
-    const double upd = __dadd_rn(__ddiv_rn(mh, den), __dmul_rn(wd, pi));
-    pi = __dsub_rn(pi, __dmul_rn(lr, upd));
-    m[i] = mi;
-    v[i] = vi;
-    p[i] = pi;
+    if (i >= d_off && i < d_end) {
+      const int q = (int)((i - d_off) % 440);  // [20 z re | 20 z im | 400 colour bins] per channel
+      if (q < 20) {
+        const long long re = i, im = i + 20;
+        const double zr = p[re], zi = p[im], gr = g[re], gi = g[im];
+        const double mag = hypot(gr, gi);
+        double sr = 0.0, si = 0.0;
+        if (mag > 0.0) { sr = gr / mag; si = gi / mag; }
+        const double zm = hypot(zr, zi);
+        double cr = 0.0, ci = 0.0;
+        if (zm > 0.0) { cr = zr / zm; ci = -zi / zm; }
+        const double k = 0.01 * (zm - 1.0);
+        const double nr = sr + k * cr, ni = si + k * ci;
+        g[re] = nr;
+        g[im] = ni;
+        if (bad) continue;
+        adamw_update(p, m, v, re, nr, lr, b1, b2, eps, wd, c1, c2);
+        adamw_update(p, m, v, im, ni, lr, b1, b2, eps, wd, c1, c2);
+        const double pr = p[re], pim = p[im];
+        const double pm = __dsqrt_rn(__dadd_rn(__dmul_rn(pr, pr), __dmul_rn(pim, pim)));
+        const double s = pm > 1.0 ? 1.0 / pm : 1.0;
+        p[re] = pr * s;
+        p[im] = pim * s;
+        continue;
+      }
+      if (q < 40) continue;  // the im half of a tap: its re thread owns the pair
+    }
+    double gi;
+    if (i >= w_off && i < w_off + P) {
+      const int r = (int)(i - w_off);
+      const double sg = expit64(p[i]);
+      const double ds = sg * (1.0 - sg);
+      gi = gw[r] * (mask ? mask[r] : 1.0) * ds;
+      const double ap = sc[7];
+      if (ap > 0.0) gi += ap * ds;
+      g[i] = gi;
+    } else {
+      gi = g[i];
+    }
+    if (!bad) adamw_update(p, m, v, i, gi, lr, b1, b2, eps, wd, c1, c2);
   }
-}
-
-__global__ void k_project(double* __restrict__ p, long long d_off, int rows, const double* __restrict__ guard,
-                          const double* __restrict__ halt) {
-  mgb_pdl_entry();
-  if (halted(guard, halt)) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows * 40) return;
-  const int row = i / 40, c = (i / 20) % 2, mm = i % 20;
-  const long long base = d_off + (long long)row * 880 + c * 440;
-  const double re = p[base + mm], im = p[base + 20 + mm];
-  const double mag = __dsqrt_rn(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
-  const double s = mag > 1.0 ? 1.0 / mag : 1.0;
-  p[base + mm] = re * s;
-  p[base + 20 + mm] = im * s;
 }
 
 __global__ void k_sparsity(const double* __restrict__ raw, int P, double* __restrict__ out) {
@@ -156,25 +156,10 @@ extern "C" int mgb_adamw_step(double* p, double* g, double* m, double* v, long l
   cudaStream_t st = (cudaStream_t)stream;
   if (n <= 0) return 0;
   if (halt && !loss_guard) return 1;
-  if (halt) {
-    mgb_launch(k_guard, dim3(1), dim3(1), 0, st, loss_guard, halt);
-    MGB_CHECK_LAUNCH();
-  }
-  if (P > 0) {
-    mgb_launch(k_raw_grad, dim3((P + 255) / 256), dim3(256), 0, st, p, g, w_off, P, gw, mask, step_scalars);
-    MGB_CHECK_LAUNCH();
-  }
-  if (d_rows > 0) {
-    mgb_launch(k_delay_rule, dim3((d_rows * 40 + 255) / 256), dim3(256), 0, st, p, g, d_off, d_rows);
-    MGB_CHECK_LAUNCH();
-  }
   const int blocks = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
-  mgb_launch(k_adamw, dim3(blocks), dim3(256), 0, st, p, g, m, v, n, step_scalars, loss_guard, (const double*)halt);
+  mgb_launch(k_optim_step, dim3(blocks), dim3(256), 0, st, p, g, m, v, n, d_off, d_rows, w_off, P, gw, mask,
+             step_scalars, loss_guard, halt);
   MGB_CHECK_LAUNCH();
-  if (d_rows > 0) {
-    mgb_launch(k_project, dim3((d_rows * 40 + 255) / 256), dim3(256), 0, st, p, d_off, d_rows, loss_guard, (const double*)halt);
-    MGB_CHECK_LAUNCH();
-  }
   return 0;
 }
 

@@ -14,8 +14,10 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         data.append(dict(zip(hdr, r)))
-# one train step ends with the unit-disk projection (k_project, or k_adamw without delays)
-ends = [i for i, d in enumerate(data) if "k_project" in d["Kernel Name"]] or \
+# one train step ends with the optimiser pass (k_optim_step; k_project / k_adamw in
+# captures of earlier builds)
+ends = [i for i, d in enumerate(data) if "k_optim_step" in d["Kernel Name"]] or \
+    [i for i, d in enumerate(data) if "k_project" in d["Kernel Name"]] or \
     [i for i, d in enumerate(data) if "k_adamw" in d["Kernel Name"]]
 if len(ends) >= 2:
     step = data[ends[-2] + 1: ends[-1] + 1]

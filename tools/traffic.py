@@ -37,7 +37,8 @@ lst = list(launches.values())
 if level:  # --profile-level run: the last reps x per launches are the level's fwd+bwd repetitions
     step = lst[-reps * per:]
 else:
-    ends = [i for i, L in enumerate(lst) if "k_project" in L["name"]]
+    ends = [i for i, L in enumerate(lst) if "k_optim_step" in L["name"]] or \
+        [i for i, L in enumerate(lst) if "k_project" in L["name"]]
     step = lst[ends[-2] + 1: ends[-1] + 1] if len(ends) >= 2 else lst
 tot_b = sum(L.get("dram__bytes_read.sum", 0) + L.get("dram__bytes_write.sum", 0) for L in step)
 tot_t = sum(L.get("us", 0) for L in step)
